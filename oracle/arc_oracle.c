@@ -1,0 +1,513 @@
+/*
+ * arc_oracle.c — the CPU ORACLE for the EF21M + ARC-Top-K compression step.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2510_26709_b200/) never imports, links or calls it,
+ * and this file includes nothing from the product (no shared headers, tables
+ * or helpers).  Its only shared source is the text of the paper plus the
+ * readings written down in DESIGN.md §3 ("Readings").
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, "P:n" = line n):
+ *   EF21M, eq:ef21m-1..3, with the compressor C_local / C realised
+ *   by ARC-Top-K, Algorithm 1 alg:ar_topk:
+ *     reshape g -> G (m x n)                 z72habsd00111, Alg.1 l.2
+ *     V in R^{n x r}, vec(V) ~ N(0, I)       P:229-230,     Alg.1 l.3
+ *     P_i = (1/sqrt r) G_i V                 P:231-233,     Alg.1 l.4
+ *     P   = (1/N) sum_i P_i    (All-Reduce)  P:232,         Alg.1 l.5
+ *     Sigma = diag(P P^T), I = argtop_K      zn28373 P:236-237, Alg.1 l.6
+ *     C_local(G_i) = [G_i]_{I,:}             2zn20 P:241-243, Alg.1 l.7
+ *     C = (1/N) sum_i C_local (All-Reduce)   P:242, Alg.1 l.8
+ *
+ * Precision.  The selection I is an argtop (an integer decided by floating
+ * point), and h, g feed the next step's Sigma, so every value on that chain is
+ * computed in IEEE binary32 — the kernel's precision — with each operation
+ * rounded once (no FMA contraction: built with -ffp-contract=off), in the
+ * plain left-to-right order in which the formulas are written.  The places
+ * where the paper is silent (summation order, tie-break, generator, NaN) follow
+ * DESIGN.md §3; each is cited below as "[Rn]".
+ *
+ * The plain definitions are written out with plain loops; nothing is blocked,
+ * fused or reordered.  It is deliberately slow.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* Counter-based generator [R8]: Philox4x32-10 (Salmon et al., SC'11).        */
+/* ------------------------------------------------------------------------- */
+
+void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; round++) {
+        if (round > 0) {               /* key schedule: bump before rounds 2..10 */
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t prod0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t prod1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(prod0 >> 32), lo0 = (uint32_t)prod0;
+        uint32_t hi1 = (uint32_t)(prod1 >> 32), lo1 = (uint32_t)prod1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+static float bits_to_float(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+static uint32_t float_to_bits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+
+/* word -> uniform in (0,1): (x >> 9) * 2^-23 + 2^-24, both operations exact [R8]. */
+float orc_uniform(uint32_t x)
+{
+    float i = (float)(x >> 9);
+    return i * 0x1p-23f + 0x1p-24f;
+}
+
+/* Natural log of a positive normal float, built only from exactly specified
+ * operations (bit split, exact subtraction, explicit fmaf) [R8].  Coefficients:
+ * the classic Cephes logf set. */
+float orc_ln(float u)
+{
+    uint32_t b = float_to_bits(u);
+    int e = (int)(b >> 23) - 126;                       /* u = f * 2^e, f in [0.5,1) */
+    float f = bits_to_float((b & 0x007FFFFFu) | 0x3F000000u);
+    float x;
+    if (f < 0.707106781186547524f) {                    /* SQRTHF */
+        e = e - 1;
+        x = (f + f) - 1.0f;                              /* exact */
+    } else {
+        x = f - 1.0f;                                    /* exact (Sterbenz) */
+    }
+    float z = x * x;
+    float p = 7.0376836292e-2f;
+    p = fmaf(p, x, -1.1514610310e-1f);
+    p = fmaf(p, x, 1.1676998740e-1f);
+    p = fmaf(p, x, -1.2420140846e-1f);
+    p = fmaf(p, x, 1.4249322787e-1f);
+    p = fmaf(p, x, -1.6668057665e-1f);
+    p = fmaf(p, x, 2.0000714765e-1f);
+    p = fmaf(p, x, -2.4999993993e-1f);
+    p = fmaf(p, x, 3.3333331174e-1f);
+    float y = (p * x) * z;
+    float fe = (float)e;
+    y = fmaf(fe, -2.12194440e-4f, y);
+    y = fmaf(-0.5f, z, y);
+    float res = x + y;
+    res = fmaf(fe, 0.693359375f, res);
+    return res;
+}
+
+/* sin(pi/2 * f) and cos(pi/2 * f) for |f| <= 1/2: Taylor series of sin/cos at
+ * argument (pi/2) f, coefficients (pi/2)^k / k! rounded to float [R8]. */
+static float sin_quarter(float f)
+{
+    float f2 = f * f;
+    float p = 1.6044118478735982e-4f;
+    p = fmaf(p, f2, -4.6817541353186881e-3f);
+    p = fmaf(p, f2, 7.9692626246167046e-2f);
+    p = fmaf(p, f2, -6.4596409750624625e-1f);
+    p = fmaf(p, f2, 1.5707963267948966f);
+    return p * f;
+}
+static float cos_quarter(float f)
+{
+    float f2 = f * f;
+    float p = -2.5202042373060605e-5f;
+    p = fmaf(p, f2, 9.1926027483942659e-4f);
+    p = fmaf(p, f2, -2.0863480763352961e-2f);
+    p = fmaf(p, f2, 2.5366950790104802e-1f);
+    p = fmaf(p, f2, -1.2337005501361697f);
+    p = fmaf(p, f2, 1.0f);
+    return p;
+}
+
+/* sin(2 pi u), cos(2 pi u) for u in (0,1): 2 pi u = (pi/2)(k + f) with
+ * k = rint(4u), f = 4u - k, both exact; then a quadrant rotation [R8]. */
+void orc_sincos2pi(float u, float* s_out, float* c_out)
+{
+    float w = 4.0f * u;                 /* exact */
+    float kf = rintf(w);                /* exact; never a tie for u = (2i+1) 2^-24 */
+    float f = w - kf;                   /* exact */
+    float s = sin_quarter(f), c = cos_quarter(f);
+    int k = ((int)kf) & 3;
+    if (k == 0)      { *s_out = s;  *c_out = c;  }
+    else if (k == 1) { *s_out = c;  *c_out = -s; }
+    else if (k == 2) { *s_out = -s; *c_out = -c; }
+    else             { *s_out = -c; *c_out = s;  }
+}
+
+/* V_b in R^{n x r}, row-major (V[q*r + j]), vec(V) ~ N(0, I) — P:229-230, Alg.1
+ * l.3.  Entry (q, j) is drawn from Philox with key (lo32 seed, hi32 seed) and
+ * counter (q*R4 + j/4, b, lo32 t, hi32 t), R4 = ceil(r/4); the four words give
+ * two Box–Muller pairs (u0,u1) -> (z0,z1), (u2,u3) -> (z2,z3) [R8]. */
+void orc_gaussian_V(uint64_t seed, int64_t t, int32_t b, int64_t n, int32_t r, float* V)
+{
+    int64_t R4 = (r + 3) / 4;
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    for (int64_t q = 0; q < n; q++) {
+        for (int64_t jj = 0; jj < R4; jj++) {
+            uint32_t ctr[4] = { (uint32_t)(q * R4 + jj), (uint32_t)b,
+                                (uint32_t)(uint64_t)t, (uint32_t)((uint64_t)t >> 32) };
+            uint32_t x[4];
+            orc_philox4x32_10(ctr, key, x);
+            float z[4];
+            for (int pair = 0; pair < 2; pair++) {
+                float ua = orc_uniform(x[2 * pair]);
+                float ub = orc_uniform(x[2 * pair + 1]);
+                float rho = sqrtf(-2.0f * orc_ln(ua));
+                float sn, cs;
+                orc_sincos2pi(ub, &sn, &cs);
+                z[2 * pair] = rho * cs;
+                z[2 * pair + 1] = rho * sn;
+            }
+            for (int k = 0; k < 4; k++) {
+                int64_t j = 4 * jj + k;
+                if (j < r) V[q * r + j] = z[k];
+            }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Selection: I = argtop_K(Sigma), P:134 + P:237 [R5].                        */
+/* ------------------------------------------------------------------------- */
+
+/* Order key of a Sigma value: its binary32 bit pattern (Sigma >= +0, where
+ * unsigned bit order is numeric order); every NaN maps to the largest key [R15]. */
+uint32_t orc_sigma_key(float s)
+{
+    if (isnan(s)) return 0xFFFFFFFFu;
+    return float_to_bits(s);
+}
+
+typedef struct { uint32_t key; int64_t idx; } orc_keyed;
+
+static int cmp_desc_key_asc_idx(const void* a, const void* b)
+{
+    const orc_keyed* x = (const orc_keyed*)a;
+    const orc_keyed* y = (const orc_keyed*)b;
+    if (x->key != y->key) return (x->key > y->key) ? -1 : 1;
+    if (x->idx != y->idx) return (x->idx < y->idx) ? -1 : 1;
+    return 0;
+}
+static int cmp_i32(const void* a, const void* b)
+{
+    int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+    return (x > y) - (x < y);
+}
+
+/* The K rows with the largest Sigma (ties -> smaller index), returned in
+ * ascending row order. */
+void orc_argtop_k(const float* sigma, int64_t m, int64_t K, int32_t* sel)
+{
+    orc_keyed* a = (orc_keyed*)malloc((size_t)m * sizeof(orc_keyed));
+    for (int64_t p = 0; p < m; p++) { a[p].key = orc_sigma_key(sigma[p]); a[p].idx = p; }
+    qsort(a, (size_t)m, sizeof(orc_keyed), cmp_desc_key_asc_idx);
+    for (int64_t k = 0; k < K; k++) sel[k] = (int32_t)a[k].idx;
+    qsort(sel, (size_t)K, sizeof(int32_t), cmp_i32);
+    free(a);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Algorithm 1 (ARC-Top-K) on one m x n block, for all N nodes.               */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    int64_t offset;   /* first flat element of the block                          */
+    int64_t len;      /* flat elements in the block, (m-1) n < len <= m n [R14]   */
+    int64_t m, n;     /* the m x n view, row-major [R1]                           */
+    int64_t K;        /* rows kept, 1 <= K <= m (K = m for DENSE)                 */
+    int32_t kind;     /* 0 = ARC, 1 = DENSE (identity compressor) [R20]           */
+    int32_t pad_;
+} orc_block;
+
+/* Number of real columns in row p: rows are full except a short last row. */
+static int64_t row_len(int64_t len, int64_t n, int64_t p)
+{
+    int64_t rest = len - p * n;
+    return rest < n ? rest : n;
+}
+
+/*
+ * orc_arc_round — Algorithm 1 on N node-local m x n matrices.
+ *   G[i]      : node i's block as flat floats (len of them), read-only
+ *   V         : n x r projection (row-major)
+ *   exact     : 0 = Gaussian sketch (the paper); 1 = test mode, Sigma_p =
+ *               || (1/N) sum_i G_i[p,:] ||^2 exactly (the quantity the sketch
+ *               estimates, z72ena P:254-261)
+ * Outputs (each optional except sel):
+ *   P_nodes [N][m][r] : P_i = (1/sqrt r) G_i V
+ *   P_avg   [m][r]    : P   = (1/N) sum_i P_i
+ *   sigma   [m]       : Sigma = diag(P P^T)
+ *   sel     [K]       : I, ascending
+ *   C_local [N][K][n] : [G_i]_{I,:}, compact rows in I order, +0 in padding
+ *   C_glob  [K][n]    : (1/N) sum_i C_local_i
+ */
+void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int32_t r,
+                   const float* const* G, const float* V, int32_t exact,
+                   float* P_nodes, float* P_avg, float* sigma, int32_t* sel,
+                   float* C_local, float* C_glob)
+{
+    float* Pn = (float*)malloc((size_t)N * (size_t)m * (size_t)r * sizeof(float));
+    float* Pa = (float*)malloc((size_t)m * (size_t)r * sizeof(float));
+    float* Sg = (float*)calloc((size_t)m, sizeof(float));
+    const float inv_sqrt_r = 1.0f / sqrtf((float)r);       /* [R2] */
+    const float Nf = (float)N;
+
+    if (!exact) {
+        /* Alg.1 l.4: P_i = (1/sqrt r) G_i V; each entry a plain left-to-right
+         * sum over q [R9]. */
+        for (int32_t i = 0; i < N; i++) {
+            for (int64_t p = 0; p < m; p++) {
+                int64_t nv = row_len(len, n, p);
+                for (int32_t j = 0; j < r; j++) {
+                    float acc = 0.0f;
+                    for (int64_t q = 0; q < nv; q++)
+                        acc = acc + G[i][p * n + q] * V[q * r + j];
+                    Pn[((size_t)i * m + p) * r + j] = inv_sqrt_r * acc;
+                }
+            }
+        }
+        /* Alg.1 l.5: P = (1/N) sum_i P_i, the node sum in ascending node id [R9]. */
+        for (int64_t p = 0; p < m; p++) {
+            for (int32_t j = 0; j < r; j++) {
+                float s = Pn[(size_t)p * r + j];
+                for (int32_t i = 1; i < N; i++) s = s + Pn[((size_t)i * m + p) * r + j];
+                Pa[(size_t)p * r + j] = s / Nf;
+            }
+        }
+        /* Alg.1 l.6: Sigma = diag(P P^T): Sigma_p = sum_j P_pj^2 [R9]. */
+        for (int64_t p = 0; p < m; p++) {
+            float s = 0.0f;
+            for (int32_t j = 0; j < r; j++) s = s + Pa[(size_t)p * r + j] * Pa[(size_t)p * r + j];
+            Sg[p] = s;
+        }
+    } else {
+        for (int64_t p = 0; p < m; p++) {
+            int64_t nv = row_len(len, n, p);
+            float s = 0.0f;
+            for (int64_t q = 0; q < nv; q++) {
+                float a = G[0][p * n + q];
+                for (int32_t i = 1; i < N; i++) a = a + G[i][p * n + q];
+                float u = a / Nf;
+                s = s + u * u;
+            }
+            Sg[p] = s;
+        }
+    }
+    /* Alg.1 l.6: I = argtop_K(Sigma) */
+    orc_argtop_k(Sg, m, K, sel);
+
+    /* Alg.1 l.7-8: C_local(G_i) = [G_i]_{I,:};  C = (1/N) sum_i C_local(G_i). */
+    for (int64_t k = 0; k < K; k++) {
+        int64_t p = sel[k];
+        int64_t nv = row_len(len, n, p);
+        for (int64_t q = 0; q < n; q++) {
+            float a = 0.0f;
+            for (int32_t i = 0; i < N; i++) {
+                float c = (q < nv) ? G[i][p * n + q] : 0.0f;
+                if (C_local) C_local[((size_t)i * K + k) * n + q] = c;
+                a = (i == 0) ? c : a + c;
+            }
+            if (C_glob) C_glob[(size_t)k * n + q] = a / Nf;
+        }
+    }
+
+    if (P_nodes && !exact) memcpy(P_nodes, Pn, (size_t)N * m * r * sizeof(float));
+    if (P_avg && !exact) memcpy(P_avg, Pa, (size_t)m * r * sizeof(float));
+    if (sigma) memcpy(sigma, Sg, (size_t)m * sizeof(float));
+    free(Pn); free(Pa); free(Sg);
+}
+
+/* ------------------------------------------------------------------------- */
+/* One EF21M step (eq:ef21m-1, eq:ef21m-2) with ARC-Top-K,         */
+/* plus the replicated global tracker gbar = (1/N) sum_i g_i that             */
+/* eq:ef21m-3 consumes [R13].                                          */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    int32_t N;             /* nodes                                        */
+    int32_t r;             /* sketch width                                 */
+    int64_t d;             /* per-node vector length                       */
+    float eta;             /* EF21M momentum                               */
+    int32_t exact;         /* sketch mode (0 Gaussian, 1 exact, test only)  */
+    uint64_t seed;         /* shared base seed [R7]                         */
+    int32_t num_blocks;
+    int32_t pad_;
+    const orc_block* blocks;  /* tile [0, d) in order                      */
+} orc_cfg;
+
+/* debug outputs, each optional: V concatenated per ARC block ([n_b][r]);
+ * sigma per ARC block ([m_b]), both in block order. */
+int orc_step(const orc_cfg* cfg, int64_t t,
+             const float* const* grad, float* const* h, float* const* g, float* gbar,
+             int32_t* sel_out, float* values_out, float* V_out, float* sigma_out)
+{
+    const int32_t N = cfg->N;
+    const float eta = cfg->eta;
+    const float one_minus_eta = 1.0f - eta;
+
+    /* eq:ef21m-1: h_t = (1 - eta) h_{t-1} + eta grad */
+    for (int32_t i = 0; i < N; i++)
+        for (int64_t e = 0; e < cfg->d; e++)
+            h[i][e] = one_minus_eta * h[i][e] + eta * grad[i][e];
+
+    int64_t sel_pos = 0, val_pos = 0, V_pos = 0, sig_pos = 0;
+    for (int32_t b = 0; b < cfg->num_blocks; b++) {
+        const orc_block* B = &cfg->blocks[b];
+        const int64_t m = B->m, n = B->n, K = B->K, len = B->len;
+
+        /* residual Delta_i = h_t - g_{t-1}, the input of C_local in eq:ef21m-2 [R4] */
+        float** D = (float**)malloc((size_t)N * sizeof(float*));
+        for (int32_t i = 0; i < N; i++) {
+            D[i] = (float*)malloc((size_t)len * sizeof(float));
+            for (int64_t e = 0; e < len; e++) D[i][e] = h[i][B->offset + e] - g[i][B->offset + e];
+        }
+        int32_t* sel = (int32_t*)malloc((size_t)K * sizeof(int32_t));
+        float* Cl = (float*)malloc((size_t)N * K * n * sizeof(float));
+        float* Cg = (float*)malloc((size_t)K * n * sizeof(float));
+
+        if (B->kind == 0) {
+            float* V = (float*)malloc((size_t)n * cfg->r * sizeof(float));
+            orc_gaussian_V(cfg->seed, t, b, n, cfg->r, V);
+            float* sg = (float*)malloc((size_t)m * sizeof(float));
+            orc_arc_round(N, len, m, n, K, cfg->r, (const float* const*)D, V, cfg->exact,
+                          NULL, NULL, sg, sel, Cl, Cg);
+            if (V_out) memcpy(V_out + V_pos, V, (size_t)n * cfg->r * sizeof(float));
+            if (sigma_out) memcpy(sigma_out + sig_pos, sg, (size_t)m * sizeof(float));
+            V_pos += n * cfg->r;
+            sig_pos += m;
+            free(V); free(sg);
+        } else {
+            /* DENSE block: identity compressor, I = all rows [R20] */
+            for (int64_t k = 0; k < K; k++) {
+                sel[k] = (int32_t)k;
+                int64_t nv = row_len(len, n, k);
+                for (int64_t q = 0; q < n; q++) {
+                    float a = 0.0f;
+                    for (int32_t i = 0; i < N; i++) {
+                        float c = (q < nv) ? D[i][k * n + q] : 0.0f;
+                        Cl[((size_t)i * K + k) * n + q] = c;
+                        a = (i == 0) ? c : a + c;
+                    }
+                    Cg[(size_t)k * n + q] = a / (float)N;
+                }
+            }
+        }
+
+        /* eq:ef21m-2: g_t = g_{t-1} + C_local(h_t - g_{t-1}); rows outside I
+         * receive + 0 and are left as they are [R12].  gbar += C [R13]. */
+        for (int64_t k = 0; k < K; k++) {
+            int64_t p = sel[k];
+            int64_t nv = row_len(len, n, p);
+            for (int64_t q = 0; q < nv; q++) {
+                int64_t e = B->offset + p * n + q;
+                for (int32_t i = 0; i < N; i++) g[i][e] = g[i][e] + Cl[((size_t)i * K + k) * n + q];
+                gbar[e] = gbar[e] + Cg[(size_t)k * n + q];
+            }
+        }
+        if (sel_out) memcpy(sel_out + sel_pos, sel, (size_t)K * sizeof(int32_t));
+        if (values_out) memcpy(values_out + val_pos, Cg, (size_t)K * n * sizeof(float));
+        sel_pos += K;
+        val_pos += K * n;
+
+        for (int32_t i = 0; i < N; i++) free(D[i]);
+        free(D); free(sel); free(Cl); free(Cg);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Baseline: vanilla EF21M with per-node row Top-K (Table I row "Top-K",      */
+/* P:91): node i keeps the K rows of its own residual   */
+/* with the largest ||row||^2 (ties -> smaller index), and the global update  */
+/* is the average of the N differently supported sparse rows.                 */
+/* ------------------------------------------------------------------------- */
+
+/* sel_out: [N][sum K_b] per-node selections (ascending within block);
+ * values_out: [N][sum K_b n_b] per-node compact rows C_local_i. */
+int orc_step_topk(const orc_cfg* cfg, int64_t t,
+                  const float* const* grad, float* const* h, float* const* g, float* gbar,
+                  int32_t* sel_out, float* values_out)
+{
+    (void)t;
+    const int32_t N = cfg->N;
+    const float eta = cfg->eta;
+    const float one_minus_eta = 1.0f - eta;
+    for (int32_t i = 0; i < N; i++)
+        for (int64_t e = 0; e < cfg->d; e++)
+            h[i][e] = one_minus_eta * h[i][e] + eta * grad[i][e];
+
+    int64_t sumK = 0, sumKn = 0;
+    for (int32_t b = 0; b < cfg->num_blocks; b++) { sumK += cfg->blocks[b].K; sumKn += cfg->blocks[b].K * cfg->blocks[b].n; }
+
+    int64_t sel_pos = 0, val_pos = 0;
+    for (int32_t b = 0; b < cfg->num_blocks; b++) {
+        const orc_block* B = &cfg->blocks[b];
+        const int64_t m = B->m, n = B->n, K = B->K, len = B->len;
+        int32_t* sel = (int32_t*)malloc((size_t)N * K * sizeof(int32_t));
+        float* Cl = (float*)malloc((size_t)N * K * n * sizeof(float));
+        float* norms = (float*)malloc((size_t)m * sizeof(float));
+        for (int32_t i = 0; i < N; i++) {
+            /* node-local row norms of Delta_i = h - g */
+            for (int64_t p = 0; p < m; p++) {
+                int64_t nv = row_len(len, n, p);
+                float s = 0.0f;
+                for (int64_t q = 0; q < nv; q++) {
+                    int64_t e = B->offset + p * n + q;
+                    float dlt = h[i][e] - g[i][e];
+                    s = s + dlt * dlt;
+                }
+                norms[p] = s;
+            }
+            if (B->kind == 0) orc_argtop_k(norms, m, K, sel + (size_t)i * K);
+            else for (int64_t k = 0; k < K; k++) sel[(size_t)i * K + k] = (int32_t)k;
+            for (int64_t k = 0; k < K; k++) {
+                int64_t p = sel[(size_t)i * K + k];
+                int64_t nv = row_len(len, n, p);
+                for (int64_t q = 0; q < n; q++) {
+                    int64_t e = B->offset + p * n + q;
+                    Cl[((size_t)i * K + k) * n + q] = (q < nv) ? (h[i][e] - g[i][e]) : 0.0f;
+                }
+            }
+        }
+        /* merge: gbar += (1/N) C_local_j for j ascending; g_i += C_local_i */
+        for (int32_t i = 0; i < N; i++) {
+            for (int64_t k = 0; k < K; k++) {
+                int64_t p = sel[(size_t)i * K + k];
+                int64_t nv = row_len(len, n, p);
+                for (int64_t q = 0; q < nv; q++) {
+                    int64_t e = B->offset + p * n + q;
+                    float c = Cl[((size_t)i * K + k) * n + q];
+                    g[i][e] = g[i][e] + c;
+                    gbar[e] = gbar[e] + c / (float)N;
+                }
+            }
+            if (sel_out) memcpy(sel_out + (size_t)i * sumK + sel_pos, sel + (size_t)i * K, (size_t)K * sizeof(int32_t));
+            if (values_out) memcpy(values_out + (size_t)i * sumKn + val_pos, Cl + (size_t)i * K * n, (size_t)K * n * sizeof(float));
+        }
+        sel_pos += K;
+        val_pos += K * n;
+        free(sel); free(Cl); free(norms);
+    }
+    return 0;
+}
+
+/* Array forms of the generator's scalar functions (used by the exhaustive
+ * accuracy pins in tests/; a plain loop over the scalar function). */
+void orc_ln_array(const float* u, int64_t n, float* out)
+{
+    for (int64_t i = 0; i < n; i++) out[i] = orc_ln(u[i]);
+}
+void orc_sincos2pi_array(const float* u, int64_t n, float* s, float* c)
+{
+    for (int64_t i = 0; i < n; i++) orc_sincos2pi(u[i], &s[i], &c[i]);
+}
