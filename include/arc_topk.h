@@ -1,0 +1,173 @@
+/*
+ * arc_topk.h — C ABI of libarctopk.so: the EF21M + ARC-Top-K compression step
+ * on B200 (sm_100a).
+ *
+ * What one arc_topk_step computes (PAPER.md = arXiv 2510.26709 LaTeX, "P:n" =
+ * line n; readings R1..R21 are in DESIGN.md §3):
+ *   for every node i held by this GPU, every block b (an m_b x n_b row-major
+ *   view of the flat vector, R1):
+ *     h_i   <- (1-eta) h_i + eta grad_i                      eq:ef21m-1, P:325 (R11)
+ *     Delta_i = h_i - g_i                                     R4
+ *     V_b   ~ N(0, I), n_b x r, from (seed, t, b)             P:229-230, Alg.1 l.3 (R7, R8)
+ *     P_i   = (1/sqrt r) G_i V_b                              P:231-233, Alg.1 l.4 (R2)
+ *     P     = (1/N) sum_i P_i        (exchange #1)            P:232, Alg.1 l.5 (R3, R9, R21)
+ *     Sigma = diag(P P^T); I_b = argtop_{K_b}(Sigma)          zn28373 P:236-237, Alg.1 l.6 (R5, R15)
+ *     C_i   = [Delta_i]_{I_b,:}                               2zn20 P:241-243, Alg.1 l.7
+ *     g_i[I_b] <- g_i[I_b] + C_i                              eq:ef21m-2, P:326 (R12)
+ *     C     = (1/N) sum_i C_i        (exchange #2)            P:242, P:278 (index-free All-Reduce)
+ *     gbar[I_b] <- gbar[I_b] + C                              eq:ef21m-3 consumes gbar, P:327 (R13)
+ *   DENSE blocks (R20) skip the sketch: I_b = all rows.
+ *
+ * Conventions
+ *   - Device pointers unless a name ends in _host.  All base pointers 16-byte
+ *     aligned (torch's allocator gives 512); rows inside a block may be
+ *     unaligned (n % 4 != 0) and are handled.
+ *   - Every GPU call enqueues on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) and returns without blocking the host, except create
+ *     (when a comm is given), get_status and destroy, which synchronise.
+ *   - Ownership: the caller owns grad, h, g, gbar, the workspace, sel_out,
+ *     values_out, the stream and the NCCL communicator (borrowed; it must
+ *     outlive the context).  The library owns only the host context.
+ *   - Errors: validation failures return before anything is enqueued and leave
+ *     all state untouched.  ARC_ERR_CUDA / ARC_ERR_NCCL leave the state
+ *     undefined: destroy the context.  No call aborts or throws.
+ *   - SPMD: with G > 1 GPUs every rank calls create/step/destroy in the same
+ *     order with identical params (except rank) and t.
+ */
+#ifndef ARC_TOPK_H
+#define ARC_TOPK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ARC_TOPK_ABI_VERSION 1u
+#define ARC_MAX_NODES_LOCAL 16
+
+typedef struct arc_topk_ctx arc_topk_ctx;   /* opaque, library-owned */
+
+typedef enum {
+    ARC_OK = 0,
+    ARC_ERR_INVALID_ARG = 1,     /* bad pointer, size, layout or parameter   */
+    ARC_ERR_UNSUPPORTED = 2,     /* valid but not implemented on this build  */
+    ARC_ERR_PARAM_MISMATCH = 3,  /* ranks passed different params to create  */
+    ARC_ERR_CUDA = 4,            /* a CUDA runtime call failed               */
+    ARC_ERR_NCCL = 5,            /* an NCCL call failed / NCCL not loadable  */
+    ARC_ERR_NONFINITE = 6        /* get_status: a non-finite Sigma was seen  */
+} arc_status;
+
+typedef enum { ARC_BLOCK_ARC = 0, ARC_BLOCK_DENSE = 1 } arc_block_kind;
+
+typedef enum {
+    ARC_REDUCE_NCCL = 0,     /* exchange #2 = ncclAllReduce(sum): gbar within tolerance (G > 1) */
+    ARC_REDUCE_ORDERED = 1   /* exchange #2 = all-gather + ascending node-id sum: bit-exact gbar */
+} arc_reduce_mode;
+
+/* flags */
+#define ARC_FLAG_HOST_STAGING   0x1u  /* reserve device staging for arc_topk_step_host          */
+#define ARC_FLAG_DEBUG_SKETCH   0x2u  /* keep P_i for arc_topk_query(ARC_Q_P_NODES)              */
+#define ARC_FLAG_FORCE_EXCHANGE 0x4u  /* G == 1: run the G > 1 kernel sequence (tests)           */
+
+/* One block: the m x n row-major view of flat elements [offset, offset+len),
+ * (m-1) n < len <= m n (only the last row may be short, R14).  K rows kept,
+ * 1 <= K <= m; DENSE blocks require K == m.  Blocks must tile [0, d) in order. */
+typedef struct {
+    int64_t offset, len, m, n, K;
+    int32_t kind;        /* arc_block_kind */
+    int32_t reserved;    /* 0 */
+} arc_block;
+
+typedef struct {
+    uint32_t abi_version;   /* ARC_TOPK_ABI_VERSION                                   */
+    int32_t  N;             /* paper nodes in the job (all GPUs)                      */
+    int32_t  nodes_local;   /* nodes held by this GPU, 1..ARC_MAX_NODES_LOCAL;        */
+                            /* G = N / nodes_local GPUs; global node ids of this GPU  */
+                            /* are rank*nodes_local + [0, nodes_local)                */
+    int32_t  rank;          /* this GPU's rank in the communicator (0 when G == 1)    */
+    int64_t  d;             /* per-node vector length in floats                       */
+    int32_t  r;             /* sketch width, 1..32 (paper: 4)                         */
+    int32_t  num_blocks;    /* >= 1                                                   */
+    const arc_block* blocks;/* host array, copied at create                           */
+    float    eta;           /* EF21M momentum, 0 < eta <= 1                           */
+    int32_t  value_reduce;  /* arc_reduce_mode                                        */
+    uint64_t seed;          /* shared base seed (R7), identical on every rank         */
+    uint32_t flags;         /* ARC_FLAG_*                                             */
+    uint32_t reserved;      /* 0                                                      */
+} arc_topk_params;
+
+/* Bytes of device workspace `create` needs for these params (host-only call). */
+arc_status arc_topk_workspace_bytes(const arc_topk_params* params, size_t* bytes);
+
+/* Create a context.  workspace: >= arc_topk_workspace_bytes() device bytes,
+ * 256-byte aligned, owned by the caller, untouched by anyone else while the
+ * context lives.  nccl_comm: an ncclComm_t of G ranks (G = N/nodes_local) when
+ * G > 1 (borrowed, e.g. from torch's ProcessGroupNCCL); may be NULL when
+ * G == 1.  With G > 1, create all-gathers a hash of the params and returns
+ * ARC_ERR_PARAM_MISMATCH on every rank if any rank differs (synchronises). */
+arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm,
+                           void* workspace, size_t workspace_bytes,
+                           void* stream, arc_topk_ctx** out);
+
+/* One EF21M + ARC-Top-K step at iteration t (t keys the shared V, R7).
+ *   grad  : host array [nodes_local] of device pointers to d floats (read-only)
+ *   h, g  : host arrays [nodes_local] of device pointers to d floats (in/out)
+ *   gbar  : device, d floats (in/out), replicated on every rank
+ *   sel_out    : optional device int32[sum_b K_b]: I_b per block, ascending
+ *   values_out : optional device float[sum_b K_b n_b]: C = (1/N) sum_i C_i,
+ *                the compressed global rows in I order (+0 in padding)      */
+arc_status arc_topk_step(arc_topk_ctx* ctx, int64_t t,
+                         const float* const* grad, float* const* h, float* const* g,
+                         float* gbar, int32_t* sel_out, float* values_out, void* stream);
+
+/* Same step with the gradients in HOST memory (pinned for async copies): the
+ * call enqueues host->device copies of grad_host[i] (d floats each) into the
+ * workspace staging area (needs ARC_FLAG_HOST_STAGING), the step, and
+ * device->host copies of the selection and values into sel_host /
+ * values_host (each optional).  Returns after enqueueing. */
+arc_status arc_topk_step_host(arc_topk_ctx* ctx, int64_t t,
+                              const float* const* grad_host, float* const* h, float* const* g,
+                              float* gbar, int32_t* sel_host, float* values_host, void* stream);
+
+/* Debug read-back of the last step's intermediates (device dst, async). */
+typedef enum {
+    ARC_Q_V = 0,        /* float [sum_ARC n_b * r]       V_b row-major, blocks in order        */
+    ARC_Q_SIGMA = 1,    /* float [sum_ARC m_b]           Sigma per ARC block row               */
+    ARC_Q_SEL = 2,      /* int32 [sum_b K_b]             I_b                                   */
+    ARC_Q_P_NODES = 3   /* float [sum_ARC m_b][nodes_local][r]  P_i (needs DEBUG_SKETCH, or G>1) */
+} arc_query;
+arc_status arc_topk_query(arc_topk_ctx* ctx, int32_t what, void* dst, size_t bytes, void* stream);
+
+/* Sizes of the step's outputs. */
+arc_status arc_topk_sizes(const arc_topk_ctx* ctx, int64_t* sum_K, int64_t* sum_Kn,
+                          int64_t* sum_m_arc, int64_t* sum_nr_arc);
+
+/* Synchronises the context's last stream; reports ARC_ERR_NONFINITE if a
+ * non-finite Sigma was produced since the last call (flag cleared), or an
+ * asynchronous NCCL error.  flags (optional) receives the raw status word. */
+arc_status arc_topk_get_status(arc_topk_ctx* ctx, uint32_t* flags);
+
+/* Number of kernels one arc_topk_step launches (for bench accounting). */
+int32_t arc_topk_kernels_per_step(const arc_topk_ctx* ctx);
+
+/* Per-phase device timing (CUDA events recorded on the step's stream between
+ * the step's phases; off by default, and must stay off during graph capture).
+ * Phases: 0 S0 vgen, 1 S1 ef_sketch, 2 exchange #1 + S2 reduce, 3 S3 select,
+ * 4 S4 gather/EF, 5 exchange #2 + S6 scatter, 6 output copies.
+ * read_timing synchronises and returns the summed milliseconds of each phase
+ * over the timed steps since the last read (n_phases <= 7), then resets. */
+#define ARC_TIMING_PHASES 7
+arc_status arc_topk_set_timing(arc_topk_ctx* ctx, int32_t enable);
+arc_status arc_topk_read_timing(arc_topk_ctx* ctx, float* ms, int32_t n_phases, int32_t* steps);
+
+/* Frees the host context (synchronises first).  Never frees caller memory. */
+arc_status arc_topk_destroy(arc_topk_ctx* ctx);
+
+const char* arc_topk_status_string(arc_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARC_TOPK_H */

@@ -1,0 +1,18 @@
+"""B200-native EF21M + ARC-Top-K compression step (arXiv 2510.26709).
+
+Public surface:
+
+* :class:`ArcTopK` — one compression context (a C-ABI ``arc_topk_ctx``);
+  ``step()`` runs one EF21M + ARC-Top-K iteration on CUDA tensors.
+* :class:`Block`, :func:`flat_layout` — the m x n block views of the flat
+  gradient (per-tensor blocks P:130).
+
+Everything runs in ``libarctopk.so`` (hand-written sm_100a CUDA + NCCL).
+PyTorch supplies device memory, streams and the process group only.
+"""
+from __future__ import annotations
+
+from .api import ArcTopK, Block, flat_layout, nccl_comm_ptr, per_tensor_layout  # noqa: F401
+from .ledger import comm_entries  # noqa: F401
+
+__all__ = ["ArcTopK", "Block", "flat_layout", "per_tensor_layout", "nccl_comm_ptr", "comm_entries"]

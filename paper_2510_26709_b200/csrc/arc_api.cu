@@ -1,0 +1,664 @@
+// arc_api.cu — the C ABI of libarctopk.so (include/arc_topk.h): validation,
+// workspace layout, the tile scheduler for the streaming pass, NCCL plumbing
+// and the per-step launch sequence.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <new>
+#include <queue>
+#include <vector>
+
+#include "arc_internal.cuh"
+#include "nccl.h"   // types only (torch wheel's NCCL 2.28); functions are resolved with dlsym
+
+using namespace arc;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr int kMinTileRows = 8;
+constexpr int kMaxGrid = 8192;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// ---- NCCL, resolved at run time from the libnccl.so.2 torch already loaded ----
+struct Nccl {
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*commUserRank)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    bool ok = false;
+};
+
+bool load_nccl(Nccl& n) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) return false;
+    n.allGather = reinterpret_cast<decltype(n.allGather)>(dlsym(h, "ncclAllGather"));
+    n.allReduce = reinterpret_cast<decltype(n.allReduce)>(dlsym(h, "ncclAllReduce"));
+    n.commCount = reinterpret_cast<decltype(n.commCount)>(dlsym(h, "ncclCommCount"));
+    n.commUserRank = reinterpret_cast<decltype(n.commUserRank)>(dlsym(h, "ncclCommUserRank"));
+    n.commGetAsyncError = reinterpret_cast<decltype(n.commGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+    n.ok = n.allGather && n.allReduce && n.commCount && n.commUserRank && n.commGetAsyncError;
+    return n.ok;
+}
+
+// ---- derived layout -----------------------------------------------------------
+struct Plan {
+    int G = 1, L = 1;
+    bool exchange = false;       // run the G>1 sequence
+    bool keep_pnodes = false;
+    int M = 0;                   // sum of ARC m_b (global ARC rows)
+    int64_t sumK = 0, sumKn = 0, sum_nr = 0;
+    int max_nR4 = 0;
+    int max_tiles = 0;
+    std::vector<BlockDev> bdev;
+    // workspace offsets (bytes)
+    size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
+           o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
+           o_vals = 0, o_hash = 0, total = 0;
+};
+
+arc_status validate(const arc_topk_params* p) {
+    if (p == nullptr) return ARC_ERR_INVALID_ARG;
+    if (p->abi_version != ARC_TOPK_ABI_VERSION) return ARC_ERR_INVALID_ARG;
+    if (p->N < 1 || p->nodes_local < 1 || p->nodes_local > ARC_MAX_NODES_LOCAL) return ARC_ERR_INVALID_ARG;
+    if (p->N % p->nodes_local != 0) return ARC_ERR_INVALID_ARG;
+    const int G = p->N / p->nodes_local;
+    if (p->rank < 0 || p->rank >= G) return ARC_ERR_INVALID_ARG;
+    if (p->d < 1 || p->r < 1 || p->r > 32) return ARC_ERR_INVALID_ARG;
+    if (!(p->eta > 0.0f && p->eta <= 1.0f)) return ARC_ERR_INVALID_ARG;
+    if (p->value_reduce != ARC_REDUCE_NCCL && p->value_reduce != ARC_REDUCE_ORDERED) return ARC_ERR_INVALID_ARG;
+    if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
+    if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE)) return ARC_ERR_INVALID_ARG;
+    int64_t pos = 0, M = 0, sumK = 0;
+    for (int b = 0; b < p->num_blocks; ++b) {
+        const arc_block& B = p->blocks[b];
+        if (B.offset != pos) return ARC_ERR_INVALID_ARG;                  // tile [0, d) in order
+        if (B.m < 1 || B.n < 1 || B.len < 1) return ARC_ERR_INVALID_ARG;
+        if (B.m > INT32_MAX || B.n > INT32_MAX) return ARC_ERR_INVALID_ARG;
+        if (B.len > B.m * B.n || B.len <= (B.m - 1) * B.n) return ARC_ERR_INVALID_ARG;
+        if (B.K < 1 || B.K > B.m) return ARC_ERR_INVALID_ARG;
+        if (B.kind != ARC_BLOCK_ARC && B.kind != ARC_BLOCK_DENSE) return ARC_ERR_INVALID_ARG;
+        if (B.kind == ARC_BLOCK_DENSE && B.K != B.m) return ARC_ERR_INVALID_ARG;
+        if (B.reserved != 0) return ARC_ERR_INVALID_ARG;
+        pos += B.len;
+        if (B.kind == ARC_BLOCK_ARC) M += B.m;
+        sumK += B.K;
+    }
+    if (pos != p->d) return ARC_ERR_INVALID_ARG;
+    if (M > INT32_MAX || sumK > INT32_MAX) return ARC_ERR_INVALID_ARG;
+    return ARC_OK;
+}
+
+void make_plan(const arc_topk_params* p, Plan& pl) {
+    pl.L = p->nodes_local;
+    pl.G = p->N / p->nodes_local;
+    pl.exchange = pl.G > 1 || (p->flags & ARC_FLAG_FORCE_EXCHANGE);
+    pl.keep_pnodes = pl.exchange || (p->flags & ARC_FLAG_DEBUG_SKETCH);
+    pl.bdev.resize(p->num_blocks);
+    int64_t M = 0, sumK = 0, sumKn = 0, sum_nr = 0;
+    int max_tiles = 0;
+    const int R4 = (p->r + 3) / 4;
+    for (int b = 0; b < p->num_blocks; ++b) {
+        const arc_block& B = p->blocks[b];
+        BlockDev& D = pl.bdev[b];
+        D.off = B.offset;
+        D.len = B.len;
+        D.m = static_cast<int>(B.m);
+        D.n = static_cast<int>(B.n);
+        D.K = static_cast<int>(B.K);
+        D.kind = B.kind;
+        D.v_off = sum_nr;
+        D.row_base = static_cast<int>(M);
+        D.sel_base = static_cast<int>(sumK);
+        D.val_base = sumKn;
+        D.vec = (B.offset % 4 == 0) && (B.n % 4 == 0);
+        D.pad_ = 0;
+        if (B.kind == ARC_BLOCK_ARC) {
+            M += B.m;
+            sum_nr += B.n * p->r;
+            pl.max_nR4 = std::max<int64_t>(pl.max_nR4, B.n * R4);
+            max_tiles += static_cast<int>((B.m + kMinTileRows - 1) / kMinTileRows);
+        }
+        sumK += B.K;
+        sumKn += B.K * B.n;
+    }
+    pl.M = static_cast<int>(M);
+    pl.sumK = sumK;
+    pl.sumKn = sumKn;
+    pl.sum_nr = sum_nr;
+    pl.max_tiles = std::max(max_tiles, 1);
+
+    size_t off = 0;
+    auto take = [&](size_t bytes) { const size_t o = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o; };
+    pl.o_blocks = take(sizeof(BlockDev) * p->num_blocks);
+    pl.o_tiles = take(sizeof(Tile) * pl.max_tiles);
+    pl.o_cta = take(sizeof(int) * (kMaxGrid + 1));
+    pl.o_selrows = take(sizeof(SelRow) * sumK);
+    pl.o_V = take(sizeof(float) * sum_nr);
+    pl.o_sigma = take(sizeof(float) * std::max<int64_t>(M, 1));
+    pl.o_sel = take(sizeof(int32_t) * sumK);
+    pl.o_status = take(16);
+    pl.o_hash = take(sizeof(uint64_t) * (pl.G + 1));
+    const size_t pn = sizeof(float) * static_cast<size_t>(M) * pl.L * p->r;
+    pl.o_pnodes = pl.keep_pnodes ? take(pn) : 0;
+    if (pl.exchange) {
+        pl.o_xrecv = take(pn * pl.G);
+        const bool ordered = p->value_reduce == ARC_REDUCE_ORDERED;
+        pl.o_wire = take(sizeof(float) * sumKn * (ordered ? pl.L : 1));
+        pl.o_wire_all = ordered ? take(sizeof(float) * sumKn * pl.L * pl.G) : 0;
+    }
+    if (p->flags & ARC_FLAG_HOST_STAGING) {
+        pl.o_staging = take(sizeof(float) * static_cast<size_t>(p->d) * pl.L);
+        pl.o_vals = take(sizeof(float) * sumKn);
+    }
+    pl.total = off;
+}
+
+// ---- the tile scheduler: balance the streaming pass over the resident CTAs ----
+// Tiles are <= 64 rows of one ARC block (a row never spans two CTAs: its sums
+// are sequential, R9).  For a few candidate tile heights the tiles are placed
+// on CTAs longest-first onto the least-loaded CTA (LPT); the plan with the
+// smallest makespan wins.
+void plan_tiles(const Plan& pl, int resident, std::vector<Tile>& tiles, std::vector<int>& cta_begin, int& grid) {
+    struct Cand { int64_t makespan; std::vector<Tile> tiles; std::vector<int> begin; int grid; };
+    Cand best;
+    best.makespan = INT64_MAX;
+    int64_t work = 0;
+    for (const BlockDev& B : pl.bdev)
+        if (B.kind == ARC_BLOCK_ARC) work += static_cast<int64_t>(B.m) * (B.n + 8);
+    resident = std::max(1, std::min(resident, kMaxGrid));
+    for (int waves = 1; waves <= 12; ++waves) {
+        const double target = static_cast<double>(work) / (static_cast<double>(resident) * waves);
+        std::vector<Tile> ts;
+        std::vector<int64_t> cost;
+        for (size_t b = 0; b < pl.bdev.size(); ++b) {
+            const BlockDev& B = pl.bdev[b];
+            if (B.kind != ARC_BLOCK_ARC) continue;
+            int R = static_cast<int>(target / (B.n + 8));
+            R = std::max(kMinTileRows, std::min(kTileRows, R));
+            R = std::min(R, B.m);
+            const int nt = (B.m + R - 1) / R;
+            // spread the rows evenly over the block's tiles
+            for (int i = 0; i < nt; ++i) {
+                const int r0 = static_cast<int>(static_cast<int64_t>(B.m) * i / nt);
+                const int r1 = static_cast<int>(static_cast<int64_t>(B.m) * (i + 1) / nt);
+                ts.push_back(Tile{static_cast<int>(b), r0, r1 - r0});
+                cost.push_back(static_cast<int64_t>(r1 - r0 + 2) * (B.n + 8));
+            }
+        }
+        if (static_cast<int>(ts.size()) > pl.max_tiles) continue;
+        const int g = std::min<int>(resident, static_cast<int>(ts.size()));
+        std::vector<int> order(ts.size());
+        for (size_t i = 0; i < ts.size(); ++i) order[i] = static_cast<int>(i);
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost[x] > cost[y]; });
+        using Slot = std::pair<int64_t, int>;
+        std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+        for (int c = 0; c < g; ++c) heap.push({0, c});
+        std::vector<std::vector<int>> lists(g);
+        int64_t makespan = 0;
+        for (int idx : order) {
+            Slot s = heap.top();
+            heap.pop();
+            s.first += cost[idx];
+            makespan = std::max(makespan, s.first);
+            lists[s.second].push_back(idx);
+            heap.push(s);
+        }
+        if (makespan < best.makespan) {
+            Cand c;
+            c.makespan = makespan;
+            c.grid = g;
+            c.begin.push_back(0);
+            for (int k = 0; k < g; ++k) {
+                std::sort(lists[k].begin(), lists[k].end());
+                for (int idx : lists[k]) c.tiles.push_back(ts[idx]);
+                c.begin.push_back(static_cast<int>(c.tiles.size()));
+            }
+            best = std::move(c);
+        }
+    }
+    tiles = std::move(best.tiles);
+    cta_begin = std::move(best.begin);
+    grid = best.grid;
+}
+
+uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) { h ^= p[i]; h *= 1099511628211ull; }
+    return h;
+}
+
+uint64_t params_hash(const arc_topk_params* p) {
+    uint64_t h = 1469598103934665603ull;
+    h = fnv1a(h, &p->abi_version, sizeof p->abi_version);
+    h = fnv1a(h, &p->N, sizeof p->N);
+    h = fnv1a(h, &p->nodes_local, sizeof p->nodes_local);
+    h = fnv1a(h, &p->d, sizeof p->d);
+    h = fnv1a(h, &p->r, sizeof p->r);
+    h = fnv1a(h, &p->num_blocks, sizeof p->num_blocks);
+    h = fnv1a(h, p->blocks, sizeof(arc_block) * p->num_blocks);
+    h = fnv1a(h, &p->eta, sizeof p->eta);
+    h = fnv1a(h, &p->value_reduce, sizeof p->value_reduce);
+    h = fnv1a(h, &p->seed, sizeof p->seed);
+    const uint32_t f = p->flags & ~ARC_FLAG_HOST_STAGING;
+    h = fnv1a(h, &f, sizeof f);
+    return h;
+}
+
+}  // namespace
+
+struct arc_topk_ctx {
+    arc_topk_params p{};
+    std::vector<arc_block> blocks;
+    Plan pl;
+    Nccl nccl;
+    ncclComm_t comm = nullptr;
+    unsigned char* ws = nullptr;
+    int grid = 0, num_tiles = 0;
+    float ome = 0.f, c_r = 0.f, Nf = 0.f;
+    cudaStream_t last = nullptr;
+    // per-phase timing
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;   // (ARC_TIMING_PHASES + 1) per timed step
+    int timed_steps = 0;
+
+    template <class T> T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+};
+
+#define ARC_CUDA(call)                                     \
+    do {                                                   \
+        if ((call) != cudaSuccess) return ARC_ERR_CUDA;    \
+    } while (0)
+#define ARC_LAUNCHED()                                               \
+    do {                                                             \
+        if (cudaPeekAtLastError() != cudaSuccess) {                  \
+            (void)cudaGetLastError();                                \
+            return ARC_ERR_CUDA;                                     \
+        }                                                            \
+    } while (0)
+
+extern "C" {
+
+const char* arc_topk_status_string(arc_status s) {
+    switch (s) {
+        case ARC_OK: return "ok";
+        case ARC_ERR_INVALID_ARG: return "invalid argument";
+        case ARC_ERR_UNSUPPORTED: return "unsupported";
+        case ARC_ERR_PARAM_MISMATCH: return "parameters differ across ranks";
+        case ARC_ERR_CUDA: return "CUDA error";
+        case ARC_ERR_NCCL: return "NCCL error";
+        case ARC_ERR_NONFINITE: return "non-finite row importance";
+    }
+    return "unknown status";
+}
+
+arc_status arc_topk_workspace_bytes(const arc_topk_params* params, size_t* bytes) {
+    if (bytes == nullptr) return ARC_ERR_INVALID_ARG;
+    const arc_status v = validate(params);
+    if (v != ARC_OK) return v;
+    Plan pl;
+    make_plan(params, pl);
+    *bytes = pl.total;
+    return ARC_OK;
+}
+
+arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void* workspace, size_t workspace_bytes,
+                           void* stream, arc_topk_ctx** out) {
+    if (out == nullptr) return ARC_ERR_INVALID_ARG;
+    *out = nullptr;
+    const arc_status v = validate(params);
+    if (v != ARC_OK) return v;
+    if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) % kAlign) != 0) return ARC_ERR_INVALID_ARG;
+    arc_topk_ctx* c = new (std::nothrow) arc_topk_ctx();
+    if (c == nullptr) return ARC_ERR_INVALID_ARG;
+    c->p = *params;
+    c->blocks.assign(params->blocks, params->blocks + params->num_blocks);
+    c->p.blocks = c->blocks.data();
+    make_plan(&c->p, c->pl);
+    if (workspace_bytes < c->pl.total) { delete c; return ARC_ERR_INVALID_ARG; }
+    c->ws = static_cast<unsigned char*>(workspace);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    c->last = s;
+
+    const int G = c->pl.G;
+    if (G > 1) {
+        if (nccl_comm == nullptr) { delete c; return ARC_ERR_INVALID_ARG; }
+        if (!load_nccl(c->nccl)) { delete c; return ARC_ERR_NCCL; }
+        c->comm = static_cast<ncclComm_t>(nccl_comm);
+        int cnt = 0, rk = -1;
+        if (c->nccl.commCount(c->comm, &cnt) != ncclSuccess || c->nccl.commUserRank(c->comm, &rk) != ncclSuccess) {
+            delete c;
+            return ARC_ERR_NCCL;
+        }
+        if (cnt != G || rk != params->rank) { delete c; return ARC_ERR_INVALID_ARG; }
+    } else if (nccl_comm != nullptr) {
+        if (!load_nccl(c->nccl)) { delete c; return ARC_ERR_NCCL; }
+        c->comm = static_cast<ncclComm_t>(nccl_comm);
+    }
+
+    // static tables
+    std::vector<Tile> tiles;
+    std::vector<int> cta_begin;
+    plan_tiles(c->pl, ef_sketch_resident_ctas(c->p.r), tiles, cta_begin, c->grid);
+    c->num_tiles = static_cast<int>(tiles.size());
+    std::vector<SelRow> rows;
+    rows.reserve(static_cast<size_t>(c->pl.sumK));
+    for (int b = 0; b < c->p.num_blocks; ++b)
+        for (int64_t k = 0; k < c->blocks[b].K; ++k) rows.push_back(SelRow{b, static_cast<int>(k)});
+
+#define UPLOAD(off, vec) \
+    if (!(vec).empty()) ARC_CUDA(cudaMemcpyAsync(c->ws + (off), (vec).data(), sizeof((vec)[0]) * (vec).size(), cudaMemcpyHostToDevice, s))
+    do {
+        arc_status st = ARC_OK;
+        auto up = [&]() -> arc_status {
+            UPLOAD(c->pl.o_blocks, c->pl.bdev);
+            UPLOAD(c->pl.o_tiles, tiles);
+            UPLOAD(c->pl.o_cta, cta_begin);
+            UPLOAD(c->pl.o_selrows, rows);
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_status, 0, 16, s));
+            ARC_CUDA(cudaStreamSynchronize(s));
+            return ARC_OK;
+        };
+        st = up();
+        if (st != ARC_OK) { delete c; return st; }
+    } while (0);
+#undef UPLOAD
+
+    c->ome = 1.0f - c->p.eta;                       // R11, fp32
+    c->c_r = 1.0f / sqrtf(static_cast<float>(c->p.r));   // R2: fl(1 / sqrt_rn(r))
+    c->Nf = static_cast<float>(c->p.N);             // R3
+
+    if (G > 1) {   // every rank checks that all ranks passed identical params
+        const uint64_t mine = params_hash(&c->p);
+        uint64_t* dh = c->at<uint64_t>(c->pl.o_hash);
+        std::vector<uint64_t> all(G, 0);
+        if (cudaMemcpyAsync(dh + G, &mine, 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            c->nccl.allGather(dh + G, dh, 8, ncclUint8, c->comm, s) != ncclSuccess ||
+            cudaMemcpyAsync(all.data(), dh, 8 * G, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            delete c;
+            return ARC_ERR_NCCL;
+        }
+        for (uint64_t x : all)
+            if (x != mine) { delete c; return ARC_ERR_PARAM_MISMATCH; }
+    }
+    *out = c;
+    return ARC_OK;
+}
+
+static arc_status mark(arc_topk_ctx* c, int phase_edge, cudaStream_t s) {
+    if (!c->timing) return ARC_OK;
+    const size_t idx = static_cast<size_t>(c->timed_steps) * (ARC_TIMING_PHASES + 1) + phase_edge;
+    while (c->ev_pool.size() <= idx) {
+        cudaEvent_t e;
+        ARC_CUDA(cudaEventCreate(&e));
+        c->ev_pool.push_back(e);
+    }
+    ARC_CUDA(cudaEventRecord(c->ev_pool[idx], s));
+    return ARC_OK;
+}
+#define ARC_MARK(edge)                                          \
+    do {                                                        \
+        const arc_status ms_ = mark(c, (edge), s);              \
+        if (ms_ != ARC_OK) return ms_;                          \
+    } while (0)
+
+static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad, float* const* h, float* const* g,
+                           float* gbar, int32_t* sel_out, float* values_out, cudaStream_t s) {
+    const Plan& pl = c->pl;
+    const int L = pl.L;
+    NodePtrs np{};
+    for (int i = 0; i < L; ++i) {
+        if (grad[i] == nullptr || h[i] == nullptr || g[i] == nullptr) return ARC_ERR_INVALID_ARG;
+        np.grad[i] = grad[i];
+        np.h[i] = h[i];
+        np.g[i] = g[i];
+    }
+    c->last = s;
+    const BlockDev* blocks = c->at<BlockDev>(pl.o_blocks);
+    float* V = c->at<float>(pl.o_V);
+    float* sigma = c->at<float>(pl.o_sigma);
+    int32_t* sel = c->at<int32_t>(pl.o_sel);
+    unsigned* status = c->at<unsigned>(pl.o_status);
+    const SelRow* rows = c->at<SelRow>(pl.o_selrows);
+
+    ARC_MARK(0);
+    // S0
+    if (pl.M > 0) {
+        launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V, s);
+        ARC_LAUNCHED();
+    }
+    // S1 (+S2)
+    if (pl.M > 0) {
+        SketchLaunch a{};
+        a.blocks = blocks;
+        a.tiles = c->at<Tile>(pl.o_tiles);
+        a.cta_begin = c->at<int>(pl.o_cta);
+        a.num_tiles = c->num_tiles;
+        a.grid = c->grid;
+        a.nodes = np;
+        a.nodes_local = L;
+        a.N = c->p.N;
+        a.r = c->p.r;
+        a.eta = c->p.eta;
+        a.ome = c->ome;
+        a.c_r = c->c_r;
+        a.Nf = c->Nf;
+        a.V = V;
+        a.sigma = sigma;
+        a.pnodes = pl.keep_pnodes ? c->at<float>(pl.o_pnodes) : nullptr;
+        a.mode = pl.exchange ? 1 : 0;
+        a.status = status;
+        ARC_MARK(1);
+        launch_ef_sketch(a, s);
+        ARC_LAUNCHED();
+    } else {
+        ARC_MARK(1);
+    }
+    ARC_MARK(2);
+    // (DENSE blocks skip the sketch pass: k_gather_ef applies their momentum.)
+    // Exchange #1 + S2 for G > 1
+    if (pl.exchange && pl.M > 0) {
+        const size_t cnt = static_cast<size_t>(pl.M) * L * c->p.r;
+        float* xs = c->at<float>(pl.o_pnodes);
+        float* xr = c->at<float>(pl.o_xrecv);
+        if (c->comm != nullptr) {
+            if (c->nccl.allGather(xs, xr, cnt, ncclFloat32, c->comm, s) != ncclSuccess) return ARC_ERR_NCCL;
+        } else {
+            ARC_CUDA(cudaMemcpyAsync(xr, xs, cnt * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        }
+        launch_sketch_reduce(xr, pl.M, pl.G, L, c->p.r, c->Nf, sigma, status, s);
+        ARC_LAUNCHED();
+    }
+    ARC_MARK(3);
+    // S3
+    launch_select(blocks, c->p.num_blocks, sigma, sel, s);
+    ARC_LAUNCHED();
+    ARC_MARK(4);
+    // S4..S6
+    GatherLaunch ga{};
+    ga.blocks = blocks;
+    ga.rows = rows;
+    ga.num_rows = static_cast<int>(pl.sumK);
+    ga.sel = sel;
+    ga.nodes = np;
+    ga.nodes_local = L;
+    ga.eta = c->p.eta;
+    ga.ome = c->ome;
+    ga.Nf = c->Nf;
+    ga.sum_Kn = pl.sumKn;
+    if (!pl.exchange) {
+        ga.mode = 0;
+        ga.gbar = gbar;
+        ga.values = values_out;
+        launch_gather_ef(ga, s);
+        ARC_LAUNCHED();
+        ARC_MARK(5);
+    } else {
+        const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
+        float* wire = c->at<float>(pl.o_wire);
+        ga.mode = ordered ? 2 : 1;
+        ga.values = wire;
+        launch_gather_ef(ga, s);
+        ARC_LAUNCHED();
+        ARC_MARK(5);
+        const float* reduced = wire;
+        if (!ordered) {
+            if (c->comm != nullptr && pl.G > 1) {
+                if (c->nccl.allReduce(wire, wire, static_cast<size_t>(pl.sumKn), ncclFloat32, ncclSum, c->comm, s) != ncclSuccess)
+                    return ARC_ERR_NCCL;
+            }
+        } else {
+            float* all = c->at<float>(pl.o_wire_all);
+            const size_t cnt = static_cast<size_t>(pl.sumKn) * L;
+            if (c->comm != nullptr) {
+                if (c->nccl.allGather(wire, all, cnt, ncclFloat32, c->comm, s) != ncclSuccess) return ARC_ERR_NCCL;
+            } else {
+                ARC_CUDA(cudaMemcpyAsync(all, wire, cnt * sizeof(float), cudaMemcpyDeviceToDevice, s));
+            }
+            reduced = all;
+        }
+        ScatterLaunch sa{};
+        sa.blocks = blocks;
+        sa.rows = rows;
+        sa.num_rows = static_cast<int>(pl.sumK);
+        sa.sel = sel;
+        sa.wire = reduced;
+        sa.mode = ordered ? 1 : 0;
+        sa.nodes_total = c->p.N;
+        sa.sum_Kn = pl.sumKn;
+        sa.Nf = c->Nf;
+        sa.gbar = gbar;
+        sa.values = values_out;
+        launch_scatter(sa, s);
+        ARC_LAUNCHED();
+    }
+    ARC_MARK(6);
+    if (sel_out != nullptr)
+        ARC_CUDA(cudaMemcpyAsync(sel_out, sel, sizeof(int32_t) * pl.sumK, cudaMemcpyDeviceToDevice, s));
+    ARC_MARK(7);
+    if (c->timing) ++c->timed_steps;
+    return ARC_OK;
+}
+
+arc_status arc_topk_step(arc_topk_ctx* c, int64_t t, const float* const* grad, float* const* h, float* const* g,
+                         float* gbar, int32_t* sel_out, float* values_out, void* stream) {
+    if (c == nullptr || grad == nullptr || h == nullptr || g == nullptr || gbar == nullptr) return ARC_ERR_INVALID_ARG;
+    return run_step(c, t, grad, h, g, gbar, sel_out, values_out, static_cast<cudaStream_t>(stream));
+}
+
+arc_status arc_topk_step_host(arc_topk_ctx* c, int64_t t, const float* const* grad_host, float* const* h,
+                              float* const* g, float* gbar, int32_t* sel_host, float* values_host, void* stream) {
+    if (c == nullptr || grad_host == nullptr || h == nullptr || g == nullptr || gbar == nullptr) return ARC_ERR_INVALID_ARG;
+    if (!(c->p.flags & ARC_FLAG_HOST_STAGING)) return ARC_ERR_INVALID_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int L = c->pl.L;
+    const float* dgrad[ARC_MAX_NODES_LOCAL];
+    float* stage = c->at<float>(c->pl.o_staging);
+    for (int i = 0; i < L; ++i) {
+        if (grad_host[i] == nullptr) return ARC_ERR_INVALID_ARG;
+        float* dst = stage + static_cast<size_t>(i) * c->p.d;
+        ARC_CUDA(cudaMemcpyAsync(dst, grad_host[i], sizeof(float) * c->p.d, cudaMemcpyHostToDevice, s));
+        dgrad[i] = dst;
+    }
+    float* vals = c->at<float>(c->pl.o_vals);
+    const arc_status st = run_step(c, t, dgrad, h, g, gbar, nullptr, values_host ? vals : nullptr, s);
+    if (st != ARC_OK) return st;
+    if (sel_host != nullptr)
+        ARC_CUDA(cudaMemcpyAsync(sel_host, c->at<int32_t>(c->pl.o_sel), sizeof(int32_t) * c->pl.sumK,
+                                 cudaMemcpyDeviceToHost, s));
+    if (values_host != nullptr)
+        ARC_CUDA(cudaMemcpyAsync(values_host, vals, sizeof(float) * c->pl.sumKn, cudaMemcpyDeviceToHost, s));
+    return ARC_OK;
+}
+
+arc_status arc_topk_query(arc_topk_ctx* c, int32_t what, void* dst, size_t bytes, void* stream) {
+    if (c == nullptr || dst == nullptr) return ARC_ERR_INVALID_ARG;
+    const Plan& pl = c->pl;
+    size_t off = 0, need = 0;
+    switch (what) {
+        case ARC_Q_V: off = pl.o_V; need = sizeof(float) * pl.sum_nr; break;
+        case ARC_Q_SIGMA: off = pl.o_sigma; need = sizeof(float) * pl.M; break;
+        case ARC_Q_SEL: off = pl.o_sel; need = sizeof(int32_t) * pl.sumK; break;
+        case ARC_Q_P_NODES:
+            if (!pl.keep_pnodes) return ARC_ERR_INVALID_ARG;
+            off = pl.o_pnodes;
+            need = sizeof(float) * static_cast<size_t>(pl.M) * pl.L * c->p.r;
+            break;
+        default: return ARC_ERR_INVALID_ARG;
+    }
+    if (bytes < need) return ARC_ERR_INVALID_ARG;
+    if (need == 0) return ARC_OK;
+    ARC_CUDA(cudaMemcpyAsync(dst, c->ws + off, need, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+    return ARC_OK;
+}
+
+arc_status arc_topk_sizes(const arc_topk_ctx* c, int64_t* sum_K, int64_t* sum_Kn, int64_t* sum_m_arc,
+                          int64_t* sum_nr_arc) {
+    if (c == nullptr) return ARC_ERR_INVALID_ARG;
+    if (sum_K) *sum_K = c->pl.sumK;
+    if (sum_Kn) *sum_Kn = c->pl.sumKn;
+    if (sum_m_arc) *sum_m_arc = c->pl.M;
+    if (sum_nr_arc) *sum_nr_arc = c->pl.sum_nr;
+    return ARC_OK;
+}
+
+int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
+    if (c == nullptr) return -1;
+    const int arc = c->pl.M > 0 ? 2 : 0;   // vgen + ef_sketch
+    return arc + (c->pl.exchange && c->pl.M > 0 ? 1 : 0) + 1 /*select*/ + (c->pl.exchange ? 2 : 1);
+}
+
+arc_status arc_topk_set_timing(arc_topk_ctx* c, int32_t enable) {
+    if (c == nullptr) return ARC_ERR_INVALID_ARG;
+    c->timing = enable != 0;
+    return ARC_OK;
+}
+
+arc_status arc_topk_read_timing(arc_topk_ctx* c, float* ms, int32_t n_phases, int32_t* steps) {
+    if (c == nullptr || ms == nullptr || n_phases < 1 || n_phases > ARC_TIMING_PHASES) return ARC_ERR_INVALID_ARG;
+    for (int k = 0; k < n_phases; ++k) ms[k] = 0.0f;
+    if (c->timed_steps > 0) ARC_CUDA(cudaEventSynchronize(c->ev_pool[static_cast<size_t>(c->timed_steps) * (ARC_TIMING_PHASES + 1) - 1]));
+    for (int st = 0; st < c->timed_steps; ++st) {
+        const size_t b = static_cast<size_t>(st) * (ARC_TIMING_PHASES + 1);
+        for (int k = 0; k < n_phases; ++k) {
+            float x = 0.0f;
+            ARC_CUDA(cudaEventElapsedTime(&x, c->ev_pool[b + k], c->ev_pool[b + k + 1]));
+            ms[k] += x;
+        }
+    }
+    if (steps) *steps = c->timed_steps;
+    c->timed_steps = 0;
+    return ARC_OK;
+}
+
+arc_status arc_topk_get_status(arc_topk_ctx* c, uint32_t* flags) {
+    if (c == nullptr) return ARC_ERR_INVALID_ARG;
+    ARC_CUDA(cudaStreamSynchronize(c->last));
+    uint32_t st = 0;
+    ARC_CUDA(cudaMemcpy(&st, c->ws + c->pl.o_status, 4, cudaMemcpyDeviceToHost));
+    ARC_CUDA(cudaMemset(c->ws + c->pl.o_status, 0, 4));
+    if (flags) *flags = st;
+    if (c->comm != nullptr && c->nccl.ok) {
+        ncclResult_t r = ncclSuccess;
+        if (c->nccl.commGetAsyncError(c->comm, &r) != ncclSuccess || r != ncclSuccess) return ARC_ERR_NCCL;
+    }
+    return (st & kStatusNonfinite) ? ARC_ERR_NONFINITE : ARC_OK;
+}
+
+arc_status arc_topk_destroy(arc_topk_ctx* c) {
+    if (c == nullptr) return ARC_ERR_INVALID_ARG;
+    cudaStreamSynchronize(c->last);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    delete c;
+    return ARC_OK;
+}
+
+}  // extern "C"

@@ -153,12 +153,13 @@ class GradientSource:
         return torch.randn(self.d, generator=_gen(_mix(self.seed, 2, t), self.device),
                            device=self.device, dtype=torch.float32)
 
-    def grads(self, t: int) -> list[torch.Tensor]:
+    def grads(self, t: int, nodes=None) -> list[torch.Tensor]:
+        """Gradients of step t for the given global node ids (default: all N)."""
         zc = self.common(t)
         a = float(self.rho)
         b = float(math.sqrt(1.0 - self.rho ** 2))
         out = []
-        for i in range(self.N):
+        for i in (range(self.N) if nodes is None else nodes):
             zi = torch.randn(self.d, generator=_gen(_mix(self.seed, 3, t, i), self.device),
                              device=self.device, dtype=torch.float32)
             out.append(self.scale * (a * zc + b * zi))

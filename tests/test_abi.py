@@ -1,0 +1,103 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol the
+header declares, and validates arguments before touching the GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2510_26709_b200 import _build, _lib
+    _build.build()
+    return _lib
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "arc_topk.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(arc_topk_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(L):
+    lib = L.lib()
+    declared = _declared_functions()
+    assert len(declared) >= 8
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(L.EXPORTED) == declared
+
+
+def test_binding_fails_loudly_without_library(monkeypatch, L):
+    monkeypatch.setattr(L, "_lib", None)
+    monkeypatch.setattr(L, "LIB_PATH", "/nonexistent/libarctopk.so")
+    with pytest.raises(RuntimeError):
+        L.lib()
+
+
+def _params(L, blocks, **kw):
+    arr = (L.ArcBlock * len(blocks))(*[L.ArcBlock(*b, 0) for b in blocks])
+    d = sum(b[1] for b in blocks)
+    p = L.ArcParams(L.ABI_VERSION, kw.get("N", 2), kw.get("nodes_local", 2), kw.get("rank", 0), kw.get("d", d),
+                    kw.get("r", 4), len(blocks), arr, kw.get("eta", 0.1), kw.get("reduce", 0), 7,
+                    kw.get("flags", 0), 0)
+    p._keep = arr
+    return p
+
+
+def _ws(L, p):
+    n = ctypes.c_size_t()
+    st = L.lib().arc_topk_workspace_bytes(ctypes.byref(p), ctypes.byref(n))
+    return st, n.value
+
+
+def test_workspace_bytes_valid(L):
+    st, n = _ws(L, _params(L, [(0, 1000, 10, 100, 3, 0)]))
+    assert st == L.OK and n > 0
+    # staging adds nodes_local * d floats
+    st2, n2 = _ws(L, _params(L, [(0, 1000, 10, 100, 3, 0)], flags=L.FLAG_HOST_STAGING))
+    assert st2 == L.OK and n2 >= n + 2 * 1000 * 4
+
+
+@pytest.mark.parametrize("blocks,kw", [
+    ([(0, 1000, 10, 100, 0, 0)], {}),                 # K = 0
+    ([(0, 1000, 10, 100, 11, 0)], {}),                # K > m
+    ([(0, 1000, 9, 100, 3, 0)], {}),                  # len > m n
+    ([(0, 1000, 11, 100, 3, 0)], {}),                 # len <= (m-1) n
+    ([(0, 1000, 10, 100, 3, 1)], {}),                 # DENSE with K != m
+    ([(0, 500, 5, 100, 3, 0), (600, 500, 5, 100, 3, 0)], {"d": 1100}),   # gap between blocks
+    ([(0, 1000, 10, 100, 3, 0)], {"d": 1001}),        # blocks do not cover d
+    ([(0, 1000, 10, 100, 3, 0)], {"N": 3}),           # N % nodes_local != 0
+    ([(0, 1000, 10, 100, 3, 0)], {"r": 0}),
+    ([(0, 1000, 10, 100, 3, 0)], {"r": 33}),
+    ([(0, 1000, 10, 100, 3, 0)], {"eta": 0.0}),
+    ([(0, 1000, 10, 100, 3, 0)], {"eta": 1.5}),
+    ([(0, 1000, 10, 100, 3, 0)], {"reduce": 5}),
+    ([(0, 1000, 10, 100, 3, 0)], {"flags": 0x100}),
+    ([(0, 1000, 10, 100, 3, 0)], {"N": 4, "nodes_local": 2, "rank": 2}),
+    ([(0, 1000, 10, 100, 3, 0)], {"nodes_local": 17, "N": 17}),
+    ([(0, 1000, 10, 100, 3, 2)], {}),                 # unknown kind
+])
+def test_workspace_bytes_rejects_invalid(L, blocks, kw):
+    st, _ = _ws(L, _params(L, blocks, **kw))
+    assert st == L.ERR_INVALID_ARG
+
+
+def test_null_arguments_rejected(L):
+    lib = L.lib()
+    assert lib.arc_topk_workspace_bytes(None, None) == L.ERR_INVALID_ARG
+    assert lib.arc_topk_step(None, 0, None, None, None, None, None, None, None) == L.ERR_INVALID_ARG
+    assert lib.arc_topk_destroy(None) == L.ERR_INVALID_ARG
+    assert lib.arc_topk_kernels_per_step(None) == -1
+    for s in range(7):
+        assert isinstance(L.status_string(s), str) and L.status_string(s) != "unknown status"
+
+
+def test_sass_is_sm100a(L):
+    """The library carries sm_100a SASS for every kernel."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", L.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out

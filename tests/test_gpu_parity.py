@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.
+
+With every node on one GPU (G = 1) the whole step follows the fixed order of
+DESIGN.md R9 on both sides, so EVERYTHING is compared bit for bit: the
+selection I, the compact values C, and the state h, g, gbar — over several
+steps, so state feedback is covered too.
+"""
+import numpy as np
+import pytest
+import torch
+
+from synth import ADVERSARIAL, Block, GradientSource, adversarial, config_blocks, flat_blocks
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__ as ge
+    ge.build()
+    torch.cuda.set_device(0)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def assert_same_floats(gpu: np.ndarray, ref: np.ndarray, what: str):
+    """Bit-identical, except that any two NaNs match (payloads are not specified)."""
+    g, r = _bits(gpu.astype(np.float32)), _bits(ref.astype(np.float32))
+    gn, rn = np.isnan(gpu), np.isnan(ref)
+    assert np.array_equal(gn, rn), f"{what}: NaN positions differ"
+    diff = (g != r) & ~gn
+    if diff.any():
+        i = int(np.flatnonzero(diff)[0])
+        raise AssertionError(f"{what}: {int(diff.sum())} of {diff.size} differ; first at {i}: "
+                             f"gpu={gpu.ravel()[i]!r} oracle={ref.ravel()[i]!r}")
+
+
+def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, reduce="nccl",
+               force_exchange=False, check_debug=True, host=False, nodes_local=None):
+    from paper_2510_26709_b200 import ArcTopK
+    nl = N if nodes_local is None else nodes_local
+    assert nl == N, "single-GPU parity: all nodes local"
+    src = GradientSource(d, blocks, N, seed=seed) if grads_fn is None else None
+    ctx = ArcTopK(d, blocks, N=N, eta=eta, r=r, seed=seed, nodes_local=nl, reduce=reduce,
+                  debug_sketch=check_debug, force_exchange=force_exchange, host_staging=host)
+    o = orc.OracleEF21M(d, blocks, N=N, eta=eta, r=r, seed=seed)
+    h = [torch.zeros(d, device=DEV) for _ in range(N)]
+    g = [torch.zeros(d, device=DEV) for _ in range(N)]
+    gbar = torch.zeros(d, device=DEV)
+    for t in range(steps):
+        gr = [x.numpy() for x in src.grads(t)] if grads_fn is None else grads_fn(t)
+        gr = [np.ascontiguousarray(x, dtype=np.float32) for x in gr]
+        if host:
+            gh = [torch.from_numpy(x).pin_memory() for x in gr]
+            sel = torch.empty(ctx.sum_K, dtype=torch.int32).pin_memory()
+            vals = torch.empty(ctx.sum_Kn, dtype=torch.float32).pin_memory()
+            ctx.step_host(t, gh, h, g, gbar, sel, vals)
+        else:
+            sel = torch.empty(ctx.sum_K, dtype=torch.int32, device=DEV)
+            vals = torch.empty(ctx.sum_Kn, dtype=torch.float32, device=DEV)
+            ctx.step(t, [torch.from_numpy(x).to(DEV) for x in gr], h, g, gbar, sel, vals)
+        ref = o.step(t, gr, debug=check_debug)
+        torch.cuda.synchronize()
+        if check_debug:
+            assert_same_floats(ctx.query(0).cpu().numpy(), ref["V"], f"V (t={t})")
+            assert_same_floats(ctx.query(1).cpu().numpy(), ref["sigma"], f"Sigma (t={t})")
+        assert np.array_equal(sel.cpu().numpy(), ref["sel"]), f"selection differs at t={t}"
+        assert_same_floats(vals.cpu().numpy(), ref["values"], f"values (t={t})")
+    for i in range(N):
+        assert_same_floats(h[i].cpu().numpy(), o.h[i], f"h[{i}]")
+        assert_same_floats(g[i].cpu().numpy(), o.g[i], f"g[{i}]")
+    assert_same_floats(gbar.cpu().numpy(), o.gbar, "gbar")
+    st = ctx.status()
+    ctx.close()
+    return st
+
+
+# ------------------------------------------------------------------ configs[0] (C1)
+
+def test_c1_config0_bit_exact(orc):
+    """BASELINE configs[0]: N = 4 simulated nodes, d = 65,536, K = 1 % (656) -> n = 1 (R6),
+    20 steps (state feedback), everything bit-exact."""
+    d, blocks = config_blocks("C1")
+    assert blocks[0].K == 656
+    run_parity(orc, d, blocks, N=4, steps=20, seed=20251030)
+
+
+@pytest.mark.parametrize("n,K", [(128, 6), (256, 3)])
+def test_c1_row_variants(orc, n, K):
+    run_parity(orc, 65_536, flat_blocks(65_536, n, K=K), N=4, steps=5)
+
+
+# ------------------------------------------------------------------ shapes, tails, r
+
+@pytest.mark.parametrize("d,n,K", [
+    (100_003, 768, 13),      # ragged last row (R14), several tiles
+    (4_097, 3, 100),         # n % 4 != 0: scalar path, odd rows
+    (5_461 * 70 + 11, 5_461, 7),   # LLaMA down-proj row length, unaligned rows
+    (33, 33, 1),             # single row
+    (1_000, 1, 1000),        # K = m (identity)
+    (50_000, 40, 1),         # K = 1
+    (64 * 129, 64, 64),      # exactly two tile heights
+])
+def test_shapes(orc, d, n, K):
+    run_parity(orc, d, flat_blocks(d, n, K=K), N=2, steps=3)
+
+
+@pytest.mark.parametrize("r", [1, 3, 4, 5, 8, 16, 32])
+def test_sketch_widths(orc, r):
+    run_parity(orc, 20_000, flat_blocks(20_000, 100, K=9), N=3, steps=2, r=r)
+
+
+@pytest.mark.parametrize("eta", [1.0, 0.5, 1e-3])
+def test_eta(orc, eta):
+    run_parity(orc, 30_000, flat_blocks(30_000, 64, K=20), N=2, steps=3, eta=eta)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 8, 16])
+def test_node_counts(orc, N):
+    run_parity(orc, 12_345, flat_blocks(12_345, 50, K=11), N=N, steps=2)
+
+
+# ------------------------------------------------------------------ adversarial sets
+
+@pytest.mark.parametrize("kind", ADVERSARIAL)
+@pytest.mark.parametrize("n", [1, 7, 64])
+def test_adversarial(orc, kind, n):
+    d, N = 9_000, 4
+    blocks = flat_blocks(d, n, K=max(1, (d // n) // 10))
+    fixed = adversarial(kind, d, N, n=n)
+    st = run_parity(orc, d, blocks, N=N, steps=2, grads_fn=lambda t: fixed)
+    if kind in ("nonfinite",):
+        assert st & 1, "non-finite Sigma must raise the status flag"
+
+
+def test_multi_block_with_dense(orc):
+    """Per-tensor blocks with different n, aligned and unaligned, plus
+    a DENSE block (R20)."""
+    shapes = [(300, 128, 5, 0), (77, 5461 // 43, 3, 0), (64, 64, 64, 0), (1, 1000, 1, 0),
+              (1000, 3, 17, 0), (13, 100, 13, 1), (129, 2048, 2, 0)]
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n, m, n, K, kind))
+        off += m * n
+    run_parity(orc, off, blocks, N=3, steps=3)
+
+
+def test_llama_layout_small_mu(orc):
+    """The C4 layout scaled down: one of each LLaMA tensor shape."""
+    shapes = [(2048, 64), (5461, 64), (2048, 5461 // 64)]
+    blocks, off = [], 0
+    for m, n in shapes:
+        blocks.append(Block(off, m * n, m, n, max(1, m // 100), 0))
+        off += m * n
+    blocks.append(Block(off, 4096, 4, 1024, 4, 1))
+    off += 4096
+    run_parity(orc, off, blocks, N=2, steps=2)
+
+
+# ------------------------------------------------------------------ exchange path on 1 GPU
+
+@pytest.mark.parametrize("reduce", ["nccl", "ordered"])
+def test_exchange_kernels_single_gpu(orc, reduce):
+    """The G > 1 kernel sequence (per-node sketch export, ordered node-sum reduce,
+    wire gather, scatter) run with G = 1 (copies instead of NCCL): bit-exact."""
+    run_parity(orc, 50_000, flat_blocks(50_000, 96, K=40), N=4, steps=3, reduce=reduce, force_exchange=True)
+
+
+def test_host_staging_entry(orc):
+    """arc_topk_step_host: gradients from pinned host memory, results copied back."""
+    run_parity(orc, 40_000, flat_blocks(40_000, 80, K=25), N=2, steps=3, host=True, check_debug=False)
+
+
+def test_determinism_and_graph_capture(orc):
+    """Two runs give byte-identical state; the step can be captured in a CUDA graph
+    and replayed with the same result."""
+    from paper_2510_26709_b200 import ArcTopK
+    d, N = 200_000, 2
+    blocks = flat_blocks(d, 500, K=4)
+    src = GradientSource(d, blocks, N, seed=3)
+    grads = [x.to(DEV) for x in src.grads(0)]
+    outs = []
+    for mode in ("eager", "eager", "graph"):
+        ctx = ArcTopK(d, blocks, N=N, eta=0.1, seed=3)
+        h = [torch.zeros(d, device=DEV) for _ in range(N)]
+        g = [torch.zeros(d, device=DEV) for _ in range(N)]
+        gbar = torch.zeros(d, device=DEV)
+        if mode == "graph":
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(graph, stream=s):
+                    ctx.step(0, grads, h, g, gbar, stream=s)
+            # capture does not execute: replay once
+            graph.replay()
+            torch.cuda.synchronize()
+        else:
+            ctx.step(0, grads, h, g, gbar)
+        torch.cuda.synchronize()
+        outs.append(gbar.cpu().numpy().tobytes() + b"".join(x.cpu().numpy().tobytes() for x in g))
+        ctx.close()
+    assert outs[0] == outs[1] == outs[2]
+
+
+# ------------------------------------------------------------------ full-size configs
+
+@pytest.mark.parametrize("name,N,steps", [("C2", 8, 2), ("C3", 1, 2)])
+def test_full_size_configs(orc, name, N, steps):
+    """BASELINE configs[1] (ResNet-18 d = 11.7M, N = 8 simulated) and configs[2] (GPT-2
+    small d = 124M, one node per GPU, the bench workload): the whole step bit-exact
+    against the oracle at full size."""
+    d, blocks = config_blocks(name)
+    run_parity(orc, d, blocks, N=N, steps=steps, seed=20251030, check_debug=True)
