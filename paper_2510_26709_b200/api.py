@@ -122,6 +122,8 @@ class ArcTopK:
         if self.G > 1:
             if pg is None:
                 raise ValueError("N / nodes_local > 1 needs an NCCL process group")
+            from .dist import check_consistent, params_digest
+            check_consistent(pg, params_digest(d, self.blocks, self.N, self.nodes_local, r, eta, seed, reduce))
             comm = nccl_comm_ptr(pg, self.device)
         ctx = ctypes.c_void_p()
         L.check(self.lib.arc_topk_create(ctypes.byref(self.params), comm, int(self.workspace.data_ptr()),
