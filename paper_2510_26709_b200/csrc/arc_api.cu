@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <new>
@@ -166,7 +167,8 @@ void make_plan(const arc_topk_params* p, Plan& pl) {
 // are sequential, R9).  For a few candidate tile heights the tiles are placed
 // on CTAs longest-first onto the least-loaded CTA (LPT); the plan with the
 // smallest makespan wins.
-void plan_tiles(const Plan& pl, int resident, std::vector<Tile>& tiles, std::vector<int>& cta_begin, int& grid) {
+void plan_tiles(const Plan& pl, int resident, int tile_rows_max, std::vector<Tile>& tiles, std::vector<int>& cta_begin,
+                int& grid) {
     struct Cand { int64_t makespan; std::vector<Tile> tiles; std::vector<int> begin; int grid; };
     Cand best;
     best.makespan = INT64_MAX;
@@ -182,7 +184,7 @@ void plan_tiles(const Plan& pl, int resident, std::vector<Tile>& tiles, std::vec
             const BlockDev& B = pl.bdev[b];
             if (B.kind != ARC_BLOCK_ARC) continue;
             int R = static_cast<int>(target / (B.n + 8));
-            R = std::max(kMinTileRows, std::min(kTileRows, R));
+            R = std::max(std::min(kMinTileRows, tile_rows_max), std::min(tile_rows_max, R));
             R = std::min(R, B.m);
             const int nt = (B.m + R - 1) / R;
             // spread the rows evenly over the block's tiles
@@ -261,7 +263,7 @@ struct arc_topk_ctx {
     Nccl nccl;
     ncclComm_t comm = nullptr;
     unsigned char* ws = nullptr;
-    int grid = 0, num_tiles = 0;
+    int grid = 0, num_tiles = 0, sel_slice = 1, shape = 0;
     float ome = 0.f, c_r = 0.f, Nf = 0.f;
     cudaStream_t last = nullptr;
     // per-phase timing
@@ -346,8 +348,27 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     // static tables
     std::vector<Tile> tiles;
     std::vector<int> cta_begin;
-    plan_tiles(c->pl, ef_sketch_resident_ctas(c->p.r), tiles, cta_begin, c->grid);
+    {   // tile shape of the streaming pass: wide chunks for long aligned rows
+        bool all_vec = true;
+        int min_n = INT32_MAX;
+        for (const BlockDev& B : c->pl.bdev)
+            if (B.kind == ARC_BLOCK_ARC) { all_vec = all_vec && B.vec; min_n = std::min(min_n, B.n); }
+        c->shape = (all_vec && min_n >= 128) ? 2 : (min_n >= 64 ? 1 : 0);
+        if (const char* e = getenv("ARC_SKETCH_SHAPE")) {
+            const int v = atoi(e);
+            if (v >= 0 && v <= 2) c->shape = v;
+        }
+        if (!sketch_shape_ok(c->shape, c->p.r)) c->shape = 1;
+    }
+    plan_tiles(c->pl, ef_sketch_resident_ctas(c->p.r, c->shape), sketch_tile_rows(c->shape), tiles, cta_begin,
+               c->grid);
     c->num_tiles = static_cast<int>(tiles.size());
+    {
+        int max_m = 1;
+        for (const BlockDev& B : c->pl.bdev)
+            if (B.kind == ARC_BLOCK_ARC && B.K < B.m) max_m = std::max(max_m, B.m);
+        c->sel_slice = select_max_slice(max_m);
+    }
     std::vector<SelRow> rows;
     rows.reserve(static_cast<size_t>(c->pl.sumK));
     for (int b = 0; b < c->p.num_blocks; ++b)
@@ -455,6 +476,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.sigma = sigma;
         a.pnodes = pl.keep_pnodes ? c->at<float>(pl.o_pnodes) : nullptr;
         a.mode = pl.exchange ? 1 : 0;
+        a.shape = c->shape;
         a.status = status;
         ARC_MARK(1);
         launch_ef_sketch(a, s);
@@ -479,7 +501,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     }
     ARC_MARK(3);
     // S3
-    launch_select(blocks, c->p.num_blocks, sigma, sel, s);
+    launch_select(blocks, c->p.num_blocks, sigma, sel, c->sel_slice, s);
     ARC_LAUNCHED();
     ARC_MARK(4);
     // S4..S6

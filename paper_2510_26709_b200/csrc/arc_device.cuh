@@ -1,0 +1,42 @@
+// arc_device.cuh — device helpers shared by the kernel files of libarctopk.so:
+// explicitly rounded binary32 operations (no contraction, R9) and streaming loads.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace arc {
+namespace dev {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+static __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+static __device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+static __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+static __device__ __forceinline__ float ffma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+// ---- streaming loads (read-once data: no L1 allocation) ----------------------
+static __device__ __forceinline__ float ld_nc(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+static __device__ __forceinline__ float4 ld_nc4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+// h is read and then rewritten by the same thread: coherent load, no L1 allocation
+static __device__ __forceinline__ float ld_na(const float* p) {
+    float v;
+    asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+static __device__ __forceinline__ float4 ld_na4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
+}  // namespace dev
+}  // namespace arc

@@ -34,10 +34,7 @@ struct SelRow {
     int k;
 };
 
-constexpr int kTileRows = 64;      // rows per sketch tile
-constexpr int kChunk = 32;         // columns per chunk
 constexpr int kSketchThreads = 256;
-constexpr int kLanesPerRow = 4;    // chain lanes per row (j = lane%4 + 4 s)
 
 constexpr uint32_t kStatusNonfinite = 1u;
 
@@ -64,16 +61,20 @@ struct SketchLaunch {
     float* sigma;      // mode 0: written
     float* pnodes;     // [M][nodes_local][r] P_i, or nullptr (mode 0 without debug)
     int mode;          // 0 = reduce locally -> sigma ; 1 = exchange (write pnodes only)
+    int shape;         // tile shape R x W: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128
     unsigned* status;
 };
 void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s);
-int ef_sketch_resident_ctas(int r);   // SMs x occupancy
+int ef_sketch_resident_ctas(int r, int shape);   // SMs x occupancy
+int sketch_tile_rows(int shape);
+int sketch_shape_ok(int shape, int r);
 
 void launch_sketch_reduce(const float* xrecv, int M, int G, int nodes_local, int r, float Nf,
                           float* sigma, unsigned* status, cudaStream_t s);
 
-void launch_select(const BlockDev* blocks, int num_blocks, const float* sigma, int32_t* sel,
+void launch_select(const BlockDev* blocks, int num_blocks, const float* sigma, int32_t* sel, int max_slice,
                    cudaStream_t s);
+int select_max_slice(int max_m);   // keys per CTA of the largest selected block
 
 struct GatherLaunch {
     const BlockDev* blocks;

@@ -18,44 +18,14 @@
 
 #include <cstdint>
 
+#include "arc_device.cuh"
 #include "arc_internal.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace arc {
 namespace {
-
-constexpr unsigned kFull = 0xFFFFFFFFu;
-
-__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ float ffma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-
-// ---- streaming loads (read-once data: no L1 allocation) ----------------------
-__device__ __forceinline__ float ld_nc(const float* p) {
-    float v;
-    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ float4 ld_nc4(const float* p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-}
-// h is read and then rewritten by the same thread: coherent load, no L1 allocation
-__device__ __forceinline__ float ld_na(const float* p) {
-    float v;
-    asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ float4 ld_na4(const float* p) {
-    float4 v;
-    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-}
+using namespace dev;
 
 // =============================================================================
 // S0: ARC-RNG v1 (R8) — Philox4x32-10 + Box–Muller with portable
@@ -179,234 +149,9 @@ __global__ void __launch_bounds__(256) k_vgen(const BlockDev* __restrict__ block
     }
 }
 
-// =============================================================================
-// S1 (+S2 when every node is local): the fused streaming pass.
-//
-// A CTA walks its list of tiles (host-balanced, see api.cu).  A tile is <= 64
-// rows of one block; its rows are consumed in chunks of 32 columns:
-//   load  : all 256 threads stream grad, h, g of the 64 x 32 chunk (coalesced,
-//           128-bit when rows are 16-byte aligned), compute
-//           h' = ((1-eta) h) + (eta grad), store h', Delta = h' - g -> smem.
-//   chain : 4 lanes per row, lane jl owns the sums j = jl + 4s, and walks the
-//           chunk's 32 columns in order: acc_j = acc_j + Delta_q * V_qj —
-//           the plain left-to-right sum of R9, one rounding per op.
-// The next chunk's loads are issued before the current chunk's chain work, and
-// the Delta tile is double buffered, so loads overlap the chains.
-// =============================================================================
-
-template <int RPT>
-struct ChainState {
-    float acc[RPT];
-    float S[RPT];
-};
-
-struct Cursor {
-    int li;      // index into this CTA's tile list
-    int node;    // local node
-    int chunk;   // column chunk
-};
-
 __device__ __forceinline__ int row_valid_cols(const BlockDev& B, int p) {
     const long long rest = B.len - static_cast<long long>(p) * B.n;
     return rest < B.n ? static_cast<int>(rest) : B.n;
-}
-
-template <int RPT>
-__global__ void __launch_bounds__(kSketchThreads) k_ef_sketch(const SketchLaunch a) {
-    __shared__ float Ds[2][kTileRows][kChunk + 1];
-    __shared__ float Vs[2][kChunk * 4 * RPT];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int crow = tid >> 2, jl = tid & 3;    // chain role: row of tile, lane in row
-    const int list_begin = a.cta_begin[blockIdx.x], list_end = a.cta_begin[blockIdx.x + 1];
-    if (list_begin >= list_end) return;
-    const int r = a.r;
-    const int rV = r;                           // V row stride
-
-    float xg[8], xh[8], xd[8];                  // raw loads of one chunk (grad, h, g)
-
-    // ---------------------------------------------------------------- loads
-    auto load_chunk = [&](const Cursor& cu) {
-        const Tile T = a.tiles[cu.li];
-        const BlockDev& B = a.blocks[T.b];
-        const float* __restrict__ pg = a.nodes.grad[cu.node];
-        const float* __restrict__ ph = a.nodes.h[cu.node];
-        const float* __restrict__ pgg = a.nodes.g[cu.node];
-        const int c0 = cu.chunk * kChunk;
-        if (B.vec) {
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                const int row = rr * 32 + warp * 4 + (lane >> 3);
-                const int col = c0 + 4 * (lane & 7);
-                const int p = T.row0 + row;
-                const long long e = B.off + static_cast<long long>(p) * B.n + col;
-                const bool rowok = row < T.rows && col < B.n;
-                const long long lim = B.off + B.len;
-                if (rowok && e + 3 < lim) {
-                    const float4 vg = ld_nc4(pg + e), vh = ld_na4(ph + e), vgg = ld_nc4(pgg + e);
-                    xg[rr * 4 + 0] = vg.x; xg[rr * 4 + 1] = vg.y; xg[rr * 4 + 2] = vg.z; xg[rr * 4 + 3] = vg.w;
-                    xh[rr * 4 + 0] = vh.x; xh[rr * 4 + 1] = vh.y; xh[rr * 4 + 2] = vh.z; xh[rr * 4 + 3] = vh.w;
-                    xd[rr * 4 + 0] = vgg.x; xd[rr * 4 + 1] = vgg.y; xd[rr * 4 + 2] = vgg.z; xd[rr * 4 + 3] = vgg.w;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (rowok && e + k < lim) {
-                            xg[rr * 4 + k] = ld_nc(pg + e + k);
-                            xh[rr * 4 + k] = ld_na(ph + e + k);
-                            xd[rr * 4 + k] = ld_nc(pgg + e + k);
-                        }
-                    }
-                }
-            }
-        } else {
-#pragma unroll
-            for (int rr = 0; rr < 8; ++rr) {
-                const int row = warp + 8 * rr;
-                const int col = c0 + lane;
-                const int p = T.row0 + row;
-                const long long e = B.off + static_cast<long long>(p) * B.n + col;
-                if (row < T.rows && col < B.n && e < B.off + B.len) {
-                    xg[rr] = ld_nc(pg + e);
-                    xh[rr] = ld_na(ph + e);
-                    xd[rr] = ld_nc(pgg + e);
-                }
-            }
-        }
-    };
-
-    // -------------------------------------------- momentum, h store, Delta -> smem
-    auto stage_chunk = [&](const Cursor& cu, int buf) {
-        const Tile T = a.tiles[cu.li];
-        const BlockDev& B = a.blocks[T.b];
-        float* __restrict__ ph = a.nodes.h[cu.node];
-        const int c0 = cu.chunk * kChunk;
-        const long long lim = B.off + B.len;
-        if (B.vec) {
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                const int row = rr * 32 + warp * 4 + (lane >> 3);
-                const int cl = 4 * (lane & 7);
-                const int col = c0 + cl;
-                const int p = T.row0 + row;
-                const long long e = B.off + static_cast<long long>(p) * B.n + col;
-                const bool rowok = row < T.rows && col < B.n;
-                float hn[4], dl[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    hn[k] = fadd(fmul(a.ome, xh[rr * 4 + k]), fmul(a.eta, xg[rr * 4 + k]));   // R11
-                    dl[k] = fsub(hn[k], xd[rr * 4 + k]);                                       // R4
-                }
-                if (rowok && e + 3 < lim) {
-                    *reinterpret_cast<float4*>(ph + e) = make_float4(hn[0], hn[1], hn[2], hn[3]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (rowok && e + k < lim) ph[e + k] = hn[k];
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) Ds[buf][row][cl + k] = dl[k];
-            }
-        } else {
-#pragma unroll
-            for (int rr = 0; rr < 8; ++rr) {
-                const int row = warp + 8 * rr;
-                const int col = c0 + lane;
-                const int p = T.row0 + row;
-                const long long e = B.off + static_cast<long long>(p) * B.n + col;
-                const float hn = fadd(fmul(a.ome, xh[rr]), fmul(a.eta, xg[rr]));
-                if (row < T.rows && col < B.n && e < lim) ph[e] = hn;
-                Ds[buf][row][lane] = fsub(hn, xd[rr]);
-            }
-        }
-        // V rows of this chunk
-        const int nq = min(kChunk, B.n - c0);
-        const float* __restrict__ Vb = a.V + B.v_off + static_cast<long long>(c0) * rV;
-        for (int i = tid; i < nq * r; i += kSketchThreads) Vs[buf][i] = Vb[i];
-    };
-
-    auto advance = [&](Cursor cu) -> Cursor {
-        const Tile T = a.tiles[cu.li];
-        const int nchunks = (a.blocks[T.b].n + kChunk - 1) / kChunk;
-        if (++cu.chunk == nchunks) {
-            cu.chunk = 0;
-            if (++cu.node == a.nodes_local) {
-                cu.node = 0;
-                ++cu.li;
-            }
-        }
-        return cu;
-    };
-
-    ChainState<RPT> st;
-#pragma unroll
-    for (int s = 0; s < RPT; ++s) { st.acc[s] = 0.0f; st.S[s] = 0.0f; }
-
-    Cursor cur{list_begin, 0, 0};
-    load_chunk(cur);
-    int buf = 0;
-    while (true) {
-        stage_chunk(cur, buf);
-        __syncthreads();
-        const Cursor nxt = advance(cur);
-        const bool more = nxt.li < list_end;
-        if (more) load_chunk(nxt);
-
-        // ---------------------------------------------------------- chain sums
-        const Tile T = a.tiles[cur.li];
-        const BlockDev& B = a.blocks[T.b];
-        const int p = T.row0 + crow;
-        const bool row_live = crow < T.rows;
-        const int c0 = cur.chunk * kChunk;
-        int qmax = 0;
-        if (row_live) qmax = min(kChunk, row_valid_cols(B, p) - c0);
-        {
-            const float* __restrict__ drow = &Ds[buf][crow][0];
-            const float* __restrict__ vb = &Vs[buf][0];
-#pragma unroll 4
-            for (int q = 0; q < qmax; ++q) {
-                const float dq = drow[q];
-#pragma unroll
-                for (int s = 0; s < RPT; ++s) {
-                    const int j = jl + 4 * s;
-                    if (j < r) st.acc[s] = fadd(st.acc[s], fmul(dq, vb[q * rV + j]));   // R9
-                }
-            }
-        }
-
-        // ------------------------------------------------ per-(tile, node) epilogue
-        const int nchunks = (B.n + kChunk - 1) / kChunk;
-        if (cur.chunk == nchunks - 1) {
-            const int node = cur.node;
-#pragma unroll
-            for (int s = 0; s < RPT; ++s) {
-                const int j = jl + 4 * s;
-                const float Pi = fmul(a.c_r, st.acc[s]);                                   // R2
-                if (a.pnodes != nullptr && row_live && j < r)
-                    a.pnodes[(static_cast<long long>(B.row_base + p) * a.nodes_local + node) * r + j] = Pi;
-                st.S[s] = (node == 0) ? Pi : fadd(st.S[s], Pi);                            // R9 node order
-                st.acc[s] = 0.0f;
-            }
-            if (a.mode == 0 && node == a.nodes_local - 1) {
-                float sig = 0.0f;
-#pragma unroll
-                for (int s = 0; s < RPT; ++s) {
-                    const float pv = __fdiv_rn(st.S[s], a.Nf);                            // R3
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const float v = __shfl_sync(kFull, pv, (lane & ~3) | jj);
-                        if (4 * s + jj < r) sig = fadd(sig, fmul(v, v));                  // zn28373
-                    }
-                }
-                if (jl == 0 && row_live) {
-                    a.sigma[B.row_base + p] = sig;
-                    if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
-                }
-            }
-        }
-        if (!more) break;
-        cur = nxt;
-        buf ^= 1;
-    }
 }
 
 // =============================================================================
@@ -479,7 +224,8 @@ __device__ __forceinline__ int cta_exclusive_scan(int v, int* warp_sums, int* to
 }
 
 __global__ void __cluster_dims__(kSelCluster, 1, 1) __launch_bounds__(kSelThreads)
-k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, int32_t* __restrict__ sel) {
+k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, int32_t* __restrict__ sel,
+         int cache_cap) {
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = static_cast<int>(cluster.block_rank());
     const int b = blockIdx.x / kSelCluster;
@@ -488,19 +234,29 @@ k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, i
     const int tid = threadIdx.x, lane = tid & 31;
     const int lo = static_cast<int>((static_cast<long long>(m) * crank) / kSelCluster);
     const int hi = static_cast<int>((static_cast<long long>(m) * (crank + 1)) / kSelCluster);
+    const int len = hi - lo;
     int32_t* __restrict__ out = sel + B.sel_base;
 
     if (B.kind != ARC_BLOCK_ARC || K >= m) {        // identity selection (DENSE, or K = m)
         for (int p = lo + tid; p < hi; p += kSelThreads) out[p] = p;
         return;                                     // uniform across the cluster: no DSMEM use
     }
-    const float* __restrict__ sg = sigma + B.row_base;
+    const float* __restrict__ sg = sigma + B.row_base + lo;
 
+    extern __shared__ unsigned s_keys[];            // this CTA's slice of order keys, if it fits
     __shared__ unsigned hist[2][256];
     __shared__ int warp_sums[32];
     __shared__ unsigned s_digit, s_above;
     __shared__ int s_cnt[2];                        // this CTA: #gt, #eq
 
+    const bool cached = len <= cache_cap;
+    if (cached) {
+        for (int i = tid; i < len; i += kSelThreads) s_keys[i] = order_key(sg[i]);
+        __syncthreads();
+    }
+    auto key_at = [&](int i) -> unsigned { return cached ? s_keys[i] : order_key(sg[i]); };
+
+    constexpr int U = 4;                            // keys per thread per sweep (load ILP)
     unsigned prefix = 0, pmask = 0;
     int krem = K;
     for (int pass = 0; pass < 4; ++pass) {
@@ -508,19 +264,23 @@ k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, i
         unsigned* h = hist[pass & 1];
         for (int i = tid; i < 256; i += kSelThreads) h[i] = 0;
         __syncthreads();
-        for (int base = lo; base < hi; base += kSelThreads) {
-            const int p = base + tid;
-            bool match = false;
-            unsigned bin = 0;
-            if (p < hi) {
-                const unsigned key = order_key(sg[p]);
-                match = (key & pmask) == prefix;
-                bin = (key >> shift) & 255u;
+        for (int base = 0; base < len; base += kSelThreads * U) {
+            unsigned kk[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = base + u * kSelThreads + tid;
+                kk[u] = i < len ? key_at(i) : 0u;
             }
-            const unsigned want = __ballot_sync(kFull, match);
-            if (match) {
-                const unsigned grp = __match_any_sync(want, bin);
-                if (lane == __ffs(grp) - 1) atomicAdd(&h[bin], static_cast<unsigned>(__popc(grp)));
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = base + u * kSelThreads + tid;
+                const bool match = i < len && (kk[u] & pmask) == prefix;
+                const unsigned bin = (kk[u] >> shift) & 255u;
+                const unsigned want = __ballot_sync(kFull, match);
+                if (match) {
+                    const unsigned grp = __match_any_sync(want, bin);
+                    if (lane == __ffs(grp) - 1) atomicAdd(&h[bin], static_cast<unsigned>(__popc(grp)));
+                }
             }
         }
         cluster.sync();
@@ -532,6 +292,7 @@ k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, i
             for (int k = 0; k < 8; ++k) {
                 const int bin = 255 - 8 * lane - k;
                 unsigned c = 0;
+#pragma unroll
                 for (int cr = 0; cr < kSelCluster; ++cr) c += cluster.map_shared_rank(h, cr)[bin];
                 cnt[k] = c;
                 mine += c;
@@ -563,8 +324,8 @@ k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, i
 
     // ---- counts of this slice, shared with the cluster
     int ngt = 0, neq = 0;
-    for (int p = lo + tid; p < hi; p += kSelThreads) {
-        const unsigned key = order_key(sg[p]);
+    for (int i = tid; i < len; i += kSelThreads) {
+        const unsigned key = key_at(i);
         ngt += key > T;
         neq += key == T;
     }
@@ -584,15 +345,15 @@ k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, i
     }
 
     // ---- stable compaction of the slice, kSelItems consecutive keys per thread
-    for (int base = lo; base < hi; base += kSelThreads * kSelItems) {
-        const int p0 = base + tid * kSelItems;
+    for (int base = 0; base < len; base += kSelThreads * kSelItems) {
+        const int i0 = base + tid * kSelItems;
         unsigned keys[kSelItems];
         int my_eq = 0;
 #pragma unroll
         for (int e = 0; e < kSelItems; ++e) {
-            const int p = p0 + e;
-            keys[e] = p < hi ? order_key(sg[p]) : 0u;
-            my_eq += (p < hi && keys[e] == T);
+            const int i = i0 + e;
+            keys[e] = i < len ? key_at(i) : 0u;
+            my_eq += (i < len && keys[e] == T);
         }
         int eq_total;
         int eq_rank = eq_before + cta_exclusive_scan(my_eq, warp_sums, &eq_total);
@@ -600,9 +361,8 @@ k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, i
         int my_sel = 0;
 #pragma unroll
         for (int e = 0; e < kSelItems; ++e) {
-            const int p = p0 + e;
             bool t = false;
-            if (p < hi) {
+            if (i0 + e < len) {
                 if (keys[e] > T) t = true;
                 else if (keys[e] == T) { t = eq_rank < need_eq; ++eq_rank; }
             }
@@ -613,7 +373,7 @@ k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, i
         int pos = sel_before + cta_exclusive_scan(my_sel, warp_sums, &sel_total);
 #pragma unroll
         for (int e = 0; e < kSelItems; ++e)
-            if (take[e]) out[pos++] = p0 + e;
+            if (take[e]) out[pos++] = lo + i0 + e;
         sel_before += sel_total;
         eq_before += eq_total;
     }
@@ -629,7 +389,34 @@ k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, i
 //   mode 1: wire[k] = local node sum      (NCCL All-Reduce follows)
 //   mode 2: wire[i][k] = C_i              (ordered exchange follows)
 // =============================================================================
+// 4 consecutive floats of a row: one 128-bit access when the quad is whole and
+// 16-byte aligned, else element by element (masked by `valid` columns).
+struct Quad {
+    float v[4];
+};
+__device__ __forceinline__ Quad load_quad(const float* p, bool vec4, int nvalid) {
+    Quad x;
+    if (vec4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        x.v[0] = t.x; x.v[1] = t.y; x.v[2] = t.z; x.v[3] = t.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x.v[k] = k < nvalid ? p[k] : 0.0f;
+    }
+    return x;
+}
+__device__ __forceinline__ void store_quad(float* p, const Quad& x, bool vec4, int nvalid) {
+    if (vec4) {
+        *reinterpret_cast<float4*>(p) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < nvalid) p[k] = x.v[k];
+    }
+}
+
 __global__ void __launch_bounds__(256) k_gather_ef(const GatherLaunch a) {
+    constexpr int U = 4;                  // quads per lane in flight
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -642,39 +429,77 @@ __global__ void __launch_bounds__(256) k_gather_ef(const GatherLaunch a) {
         const long long e0 = B.off + static_cast<long long>(p) * n;
         const long long o0 = B.val_base + static_cast<long long>(R.k) * n;
         const bool dense = B.kind == ARC_BLOCK_DENSE;
-        for (int q = lane; q < n; q += 32) {
-            if (q < nv) {
-                const long long e = e0 + q;
-                float A = 0.0f;
-                for (int i = 0; i < a.nodes_local; ++i) {
-                    float hv;
-                    if (dense) {   // DENSE block: eq:ef21m-1 applied here (R11, R20)
-                        hv = fadd(fmul(a.ome, a.nodes.h[i][e]), fmul(a.eta, a.nodes.grad[i][e]));
-                        a.nodes.h[i][e] = hv;
-                    } else {
-                        hv = a.nodes.h[i][e];
+        // wire / values rows are 16-byte aligned when n % 4 == 0 (val_base is a sum of K n)
+        const bool vrow = B.vec && (o0 % 4 == 0);
+        const int nq = (n + 3) >> 2;
+        for (int f0 = 0; f0 < nq; f0 += 32 * U) {
+            int cnt[U];           // valid state columns of each quad
+            int ocnt[U];          // columns of each quad inside the row (padding -> +0)
+            bool v4[U], ov4[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = 4 * (f0 + 32 * u + lane);
+                cnt[u] = max(0, min(4, nv - q));
+                ocnt[u] = max(0, min(4, n - q));
+                v4[u] = B.vec && cnt[u] == 4;
+                ov4[u] = vrow && ocnt[u] == 4;
+            }
+            Quad A[U];
+            for (int i = 0; i < a.nodes_local; ++i) {
+                float* __restrict__ ph = a.nodes.h[i];
+                float* __restrict__ pg = a.nodes.g[i];
+                Quad hq[U], gq[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const long long e = e0 + 4 * (f0 + 32 * u + lane);
+                    if (cnt[u] > 0) {
+                        gq[u] = load_quad(pg + e, v4[u], cnt[u]);
+                        if (dense) {   // DENSE block: eq:ef21m-1 applied here (R11, R20)
+                            const Quad hv = load_quad(ph + e, v4[u], cnt[u]);
+                            const Quad gr = load_quad(a.nodes.grad[i] + e, v4[u], cnt[u]);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) hq[u].v[k] = fadd(fmul(a.ome, hv.v[k]), fmul(a.eta, gr.v[k]));
+                            store_quad(ph + e, hq[u], v4[u], cnt[u]);
+                        } else {
+                            hq[u] = load_quad(ph + e, v4[u], cnt[u]);
+                        }
                     }
-                    float* gp = a.nodes.g[i] + e;
-                    const float gv = *gp;
-                    const float c = fsub(hv, gv);
-                    *gp = fadd(gv, c);
-                    A = (i == 0) ? c : fadd(A, c);
-                    if (a.mode == 2) a.values[static_cast<long long>(i) * a.sum_Kn + o0 + q] = c;
                 }
-                if (a.mode == 0) {
-                    const float val = __fdiv_rn(A, a.Nf);
-                    a.gbar[e] = fadd(a.gbar[e], val);
-                    if (a.values != nullptr) a.values[o0 + q] = val;
-                } else if (a.mode == 1) {
-                    a.values[o0 + q] = A;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (ocnt[u] == 0) continue;
+                    const long long e = e0 + 4 * (f0 + 32 * u + lane);
+                    Quad c, gn;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        c.v[k] = k < cnt[u] ? fsub(hq[u].v[k], gq[u].v[k]) : 0.0f;   // C_i (+0 padding)
+                        gn.v[k] = fadd(gq[u].v[k], c.v[k]);                            // R12
+                        A[u].v[k] = (i == 0) ? c.v[k] : fadd(A[u].v[k], c.v[k]);
+                    }
+                    if (cnt[u] > 0) store_quad(pg + e, gn, v4[u], cnt[u]);
+                    if (a.mode == 2)
+                        store_quad(a.values + static_cast<long long>(i) * a.sum_Kn + o0 + 4 * (f0 + 32 * u + lane),
+                                   c, ov4[u] && (a.sum_Kn % 4 == 0), ocnt[u]);
                 }
-            } else {
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (ocnt[u] == 0) continue;
+                const int q = 4 * (f0 + 32 * u + lane);
                 if (a.mode == 0) {
-                    if (a.values != nullptr) a.values[o0 + q] = 0.0f;
+                    const long long e = e0 + q;
+                    Quad val, gb;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) val.v[k] = k < cnt[u] ? __fdiv_rn(A[u].v[k], a.Nf) : 0.0f;   // R3
+                    if (cnt[u] > 0) {
+                        gb = load_quad(a.gbar + e, v4[u], cnt[u]);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) gb.v[k] = fadd(gb.v[k], val.v[k]);                    // R13
+                        store_quad(a.gbar + e, gb, v4[u], cnt[u]);
+                    }
+                    if (a.values != nullptr) store_quad(a.values + o0 + q, val, ov4[u], ocnt[u]);
                 } else if (a.mode == 1) {
-                    a.values[o0 + q] = 0.0f;
-                } else {
-                    for (int i = 0; i < a.nodes_local; ++i) a.values[static_cast<long long>(i) * a.sum_Kn + o0 + q] = 0.0f;
+                    store_quad(a.values + o0 + q, A[u], ov4[u], ocnt[u]);
                 }
             }
         }
@@ -733,30 +558,6 @@ void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r,
                                     static_cast<unsigned>(static_cast<uint64_t>(t) >> 32), V);
 }
 
-template <int RPT>
-static void launch_ef_sketch_t(const SketchLaunch& a, cudaStream_t s) {
-    k_ef_sketch<RPT><<<a.grid, kSketchThreads, 0, s>>>(a);
-}
-
-void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s) {
-    if (a.r <= 4) launch_ef_sketch_t<1>(a, s);
-    else if (a.r <= 8) launch_ef_sketch_t<2>(a, s);
-    else if (a.r <= 16) launch_ef_sketch_t<4>(a, s);
-    else launch_ef_sketch_t<8>(a, s);
-}
-
-int ef_sketch_resident_ctas(int r) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (r <= 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<1>, kSketchThreads, 0);
-    else if (r <= 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<2>, kSketchThreads, 0);
-    else if (r <= 16) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<4>, kSketchThreads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<8>, kSketchThreads, 0);
-    if (per_sm < 1) per_sm = 1;
-    return sms * per_sm;
-}
-
 void launch_sketch_reduce(const float* xrecv, int M, int G, int nodes_local, int r, float Nf, float* sigma,
                           unsigned* status, cudaStream_t s) {
     int grid = (M + 255) / 256;
@@ -765,9 +566,23 @@ void launch_sketch_reduce(const float* xrecv, int M, int G, int nodes_local, int
     k_sketch_reduce<<<grid, 256, 0, s>>>(xrecv, M, G, nodes_local, r, Nf, sigma, status);
 }
 
-void launch_select(const BlockDev* blocks, int num_blocks, const float* sigma, int32_t* sel, cudaStream_t s) {
-    k_select<<<num_blocks * kSelCluster, kSelThreads, 0, s>>>(blocks, sigma, sel);
+constexpr int kSelCacheMaxBytes = 200 * 1024;
+
+void launch_select(const BlockDev* blocks, int num_blocks, const float* sigma, int32_t* sel, int max_slice,
+                   cudaStream_t s) {
+    static int configured = -1;
+    int cap = max_slice;
+    if (cap * 4 > kSelCacheMaxBytes) cap = kSelCacheMaxBytes / 4;
+    if (cap < 1) cap = 1;
+    const int bytes = cap * 4;
+    if (bytes > 48 * 1024 && configured < bytes) {
+        cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelCacheMaxBytes);
+        configured = kSelCacheMaxBytes;
+    }
+    k_select<<<num_blocks * kSelCluster, kSelThreads, bytes, s>>>(blocks, sigma, sel, cap);
 }
+
+int select_max_slice(int max_m) { return (max_m + kSelCluster - 1) / kSelCluster; }
 
 static int rows_grid(int num_rows) {
     int grid = (num_rows + 7) / 8;   // 8 warps per CTA, one warp per row

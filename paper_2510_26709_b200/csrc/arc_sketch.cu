@@ -1,0 +1,311 @@
+// arc_sketch.cu — S1 (+S2 when every node is local): the fused streaming pass
+// of the EF21M + ARC-Top-K step, the one kernel that moves ~98 % of the step's
+// HBM bytes.
+//
+// Per element (eq:ef21m-1 P:325, R11, R4):   h' = ((1-eta) h) + (eta grad)
+//                                             Delta = h' - g          (h' stored)
+// Per row p and sketch column j (Alg.1 l.4, R2, R9):
+//   P'_i[p][j] = (((0 + Delta_p0 V_0j) + Delta_p1 V_1j) + ...)   left to right
+//   P_i = (1/sqrt r) P'_i ; (G == 1) S = P_0 + P_1 + ... ; P = S / N ;
+//   Sigma_p = ((0 + P_p0^2) + P_p1^2) + ...                        (zn28373 P:236)
+//
+// Layout: a CTA walks a host-balanced list of tiles; a tile is <= R rows of
+// one ARC block, consumed in chunks of W columns:
+//   load  : all 256 threads stream grad, h, g of the R x W chunk (128-bit when
+//           the block's rows are 16-byte aligned, else 32-bit), compute h' and
+//           Delta, store h' and put Delta in shared memory;
+//   chain : 4 lanes per row (lane jl owns j = jl + 4s) walk the chunk's W
+//           columns in order — the plain sequential sum, one rounding per op.
+// The next chunk's loads are issued before the current chunk's chains, and the
+// Delta tile is double buffered, so each CTA keeps a chunk in flight while it
+// computes.  Tile/block descriptors are read once per tile through the
+// read-only path, never re-read per chunk.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "arc_device.cuh"
+#include "arc_internal.cuh"
+
+namespace arc {
+namespace {
+using namespace dev;
+
+constexpr int kThreads = kSketchThreads;   // 256
+
+// Per-tile scalars kept in registers.
+struct TileRegs {
+    long long off, len;      // block
+    int n, m_rows, row0;     // block row length; rows in this tile; first row
+    int vec;                 // 16-byte aligned rows
+    int nchunks;
+    long long v_off;
+    int row_base;
+};
+
+template <int W>
+__device__ __forceinline__ TileRegs tile_regs(const SketchLaunch& a, int li) {
+    const Tile T = a.tiles[li];
+    const BlockDev* B = a.blocks + __ldg(&T.b);
+    TileRegs t;
+    t.off = __ldg(&B->off);
+    t.len = __ldg(&B->len);
+    t.n = __ldg(&B->n);
+    t.vec = __ldg(&B->vec);
+    t.v_off = __ldg(&B->v_off);
+    t.row_base = __ldg(&B->row_base);
+    t.row0 = T.row0;
+    t.m_rows = T.rows;
+    t.nchunks = (t.n + W - 1) / W;
+    return t;
+}
+
+// valid columns of tile row `row` (0 for rows beyond the tile): the last row of
+// a padded flat block is short (R14)
+__device__ __forceinline__ int row_cols(const TileRegs& t, int row) {
+    if (row >= t.m_rows) return 0;
+    const long long rest = t.len - static_cast<long long>(t.row0 + row) * t.n;
+    return rest < t.n ? static_cast<int>(rest) : t.n;
+}
+
+template <int R, int W, int RPT>
+__global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a) {
+    static_assert(R * W == 2048, "one chunk = 2048 elements = 8 per thread");
+    static_assert(W % 32 == 0 && W <= 128, "W in {32, 64, 128}");
+    constexpr int NE = R * W / kThreads;        // elements per thread per stream = 8
+    constexpr int LPR = W / 4;                  // vec: lanes per row segment
+    constexpr int RPI = 32 / LPR;               // vec: rows per warp instruction
+    constexpr int DS = W + 4;                   // Delta row stride (floats): 16-byte rows,
+                                                // rows t..t+7 on distinct banks
+    constexpr int VS = 4 * RPT;                 // V row stride in smem (padded r)
+    __shared__ __align__(16) float Ds[2][R][DS];
+    __shared__ __align__(16) float Vs[2][W * VS];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int crow = tid >> 2, jl = tid & 3;    // chain role (threads < 4R)
+    const int list_begin = a.cta_begin[blockIdx.x], list_end = a.cta_begin[blockIdx.x + 1];
+    if (list_begin >= list_end) return;
+    const int r = a.r;
+
+    // element e of this thread in a chunk -> (row, column within chunk)
+    auto vrow = [&](int e) { return (e >> 2) * (8 * RPI) + warp * RPI + lane / LPR; };
+    auto vcol = [&](int e) { return 4 * (lane % LPR) + (e & 3); };
+    auto srow = [&](int e) { return warp + 8 * (e / (W / 32)); };
+    auto scol = [&](int e) { return lane + 32 * (e % (W / 32)); };
+
+    float xg[NE], xh[NE], xd[NE];
+
+    auto load_chunk = [&](const TileRegs& t, int node, int chunk) {
+        const float* __restrict__ pg = a.nodes.grad[node];
+        const float* __restrict__ ph = a.nodes.h[node];
+        const float* __restrict__ pgg = a.nodes.g[node];
+        const int c0 = chunk * W;
+        if (t.vec) {
+#pragma unroll
+            for (int e4 = 0; e4 < NE; e4 += 4) {
+                const int row = vrow(e4), col = c0 + vcol(e4);
+                const int nv = row_cols(t, row);
+                const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
+                if (col + 3 < nv) {
+                    const float4 vg = __ldcs(reinterpret_cast<const float4*>(pg + e));
+                    const float4 vh = __ldcs(reinterpret_cast<const float4*>(ph + e));
+                    const float4 vd = __ldcs(reinterpret_cast<const float4*>(pgg + e));
+                    xg[e4] = vg.x; xg[e4 + 1] = vg.y; xg[e4 + 2] = vg.z; xg[e4 + 3] = vg.w;
+                    xh[e4] = vh.x; xh[e4 + 1] = vh.y; xh[e4 + 2] = vh.z; xh[e4 + 3] = vh.w;
+                    xd[e4] = vd.x; xd[e4 + 1] = vd.y; xd[e4 + 2] = vd.z; xd[e4 + 3] = vd.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (col + k < nv) {
+                            xg[e4 + k] = __ldcs(pg + e + k);
+                            xh[e4 + k] = __ldcs(ph + e + k);
+                            xd[e4 + k] = __ldcs(pgg + e + k);
+                        }
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int e1 = 0; e1 < NE; ++e1) {
+                const int row = srow(e1), col = c0 + scol(e1);
+                const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
+                if (col < row_cols(t, row)) {
+                    xg[e1] = __ldcs(pg + e);
+                    xh[e1] = __ldcs(ph + e);
+                    xd[e1] = __ldcs(pgg + e);
+                }
+            }
+        }
+    };
+
+    auto stage_chunk = [&](const TileRegs& t, int node, int chunk, int buf) {
+        float* __restrict__ ph = a.nodes.h[node];
+        const int c0 = chunk * W;
+        if (t.vec) {
+#pragma unroll
+            for (int e4 = 0; e4 < NE; e4 += 4) {
+                const int row = vrow(e4), cl = vcol(e4), col = c0 + cl;
+                const int nv = row_cols(t, row);
+                const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
+                float hn[4], dl[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    hn[k] = fadd(fmul(a.ome, xh[e4 + k]), fmul(a.eta, xg[e4 + k]));   // R11
+                    dl[k] = fsub(hn[k], xd[e4 + k]);                                   // R4
+                }
+                if (col + 3 < nv) {
+                    __stcs(reinterpret_cast<float4*>(ph + e), make_float4(hn[0], hn[1], hn[2], hn[3]));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (col + k < nv) ph[e + k] = hn[k];
+                }
+                *reinterpret_cast<float4*>(&Ds[buf][row][cl]) = make_float4(dl[0], dl[1], dl[2], dl[3]);
+            }
+        } else {
+#pragma unroll
+            for (int e1 = 0; e1 < NE; ++e1) {
+                const int row = srow(e1), cl = scol(e1), col = c0 + cl;
+                const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
+                const float hn = fadd(fmul(a.ome, xh[e1]), fmul(a.eta, xg[e1]));
+                if (col < row_cols(t, row)) ph[e] = hn;
+                Ds[buf][row][cl] = fsub(hn, xd[e1]);
+            }
+        }
+        // V rows [c0, c0 + W) of this block, r values each -> stride VS (zero padded)
+        const float* __restrict__ Vb = a.V + t.v_off;
+        for (int i = tid; i < W * VS; i += kThreads) {
+            const int q = i / VS, j = i % VS;
+            Vs[buf][i] = (c0 + q < t.n && j < r) ? __ldg(Vb + static_cast<long long>(c0 + q) * r + j) : 0.0f;
+        }
+    };
+
+    float acc[RPT], S[RPT];
+#pragma unroll
+    for (int s = 0; s < RPT; ++s) { acc[s] = 0.0f; S[s] = 0.0f; }
+
+    int li = list_begin, node = 0, chunk = 0;
+    TileRegs tc = tile_regs<W>(a, li);     // tile of the chunk being staged / chained
+    TileRegs tl = tc;                      // tile of the chunk being loaded
+    load_chunk(tc, node, chunk);
+    int buf = 0;
+    while (true) {
+        stage_chunk(tc, node, chunk, buf);
+        __syncthreads();
+        // advance the load cursor and issue the next chunk's loads
+        int nli = li, nnode = node, nchunk = chunk + 1;
+        if (nchunk == tc.nchunks) {
+            nchunk = 0;
+            if (++nnode == a.nodes_local) {
+                nnode = 0;
+                ++nli;
+            }
+        }
+        const bool more = nli < list_end;
+        if (more) {
+            if (nli != li) tl = tile_regs<W>(a, nli);
+            load_chunk(tl, nnode, nchunk);
+        }
+
+        // ------------------------------------------------------------ chains
+        const bool live = crow < tc.m_rows;
+        const int c0 = chunk * W;
+        if (crow < R) {
+            const int qmax = live ? min(W, row_cols(tc, crow) - c0) : 0;
+            const float* __restrict__ drow = &Ds[buf][crow][0];
+            const float* __restrict__ vb = &Vs[buf][jl];
+            if (qmax == W) {
+#pragma unroll 16
+                for (int q = 0; q < W; ++q) {
+                    const float dq = drow[q];
+#pragma unroll
+                    for (int s = 0; s < RPT; ++s) acc[s] = fadd(acc[s], fmul(dq, vb[q * VS + 4 * s]));   // R9
+                }
+            } else {
+                for (int q = 0; q < qmax; ++q) {
+                    const float dq = drow[q];
+#pragma unroll
+                    for (int s = 0; s < RPT; ++s) acc[s] = fadd(acc[s], fmul(dq, vb[q * VS + 4 * s]));
+                }
+            }
+        }
+
+        // ------------------------------------------------ per-(tile, node) epilogue
+        if (chunk == tc.nchunks - 1) {
+            const int p = tc.row0 + crow;
+#pragma unroll
+            for (int s = 0; s < RPT; ++s) {
+                const int j = jl + 4 * s;
+                const float Pi = fmul(a.c_r, acc[s]);                                    // R2
+                if (a.pnodes != nullptr && live && j < r)
+                    a.pnodes[(static_cast<long long>(tc.row_base + p) * a.nodes_local + node) * r + j] = Pi;
+                S[s] = (node == 0) ? Pi : fadd(S[s], Pi);                                 // R9, node order
+                acc[s] = 0.0f;
+            }
+            if (a.mode == 0 && node == a.nodes_local - 1) {
+                float sig = 0.0f;
+#pragma unroll
+                for (int s = 0; s < RPT; ++s) {
+                    const float pv = __fdiv_rn(S[s], a.Nf);                               // R3
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const float v = __shfl_sync(kFull, pv, (lane & ~3) | jj);
+                        if (4 * s + jj < r) sig = fadd(sig, fmul(v, v));                 // zn28373
+                    }
+                }
+                if (jl == 0 && live) {
+                    a.sigma[tc.row_base + p] = sig;
+                    if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
+                }
+            }
+        }
+        if (!more) break;
+        if (nli != li) tc = tl;
+        li = nli;
+        node = nnode;
+        chunk = nchunk;
+        buf ^= 1;
+    }
+}
+
+// RPT (sums per lane) = ceil(r / 4); the widest shape stops at r <= 16 (shared memory)
+template <int R, int W>
+void launch_rw(const SketchLaunch& a, cudaStream_t s) {
+    if (a.r <= 4) k_ef_sketch<R, W, 1><<<a.grid, kThreads, 0, s>>>(a);
+    else if (a.r <= 8) k_ef_sketch<R, W, 2><<<a.grid, kThreads, 0, s>>>(a);
+    else if (a.r <= 16) k_ef_sketch<R, W, 4><<<a.grid, kThreads, 0, s>>>(a);
+    else if constexpr (W < 128) k_ef_sketch<R, W, 8><<<a.grid, kThreads, 0, s>>>(a);
+}
+
+template <int R, int W>
+int occupancy_rw(int r) {
+    int per_sm = 0;
+    if (r <= 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 1>, kThreads, 0);
+    else if (r <= 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 2>, kThreads, 0);
+    else if (r <= 16) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 4>, kThreads, 0);
+    else if constexpr (W < 128) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 8>, kThreads, 0);
+    return per_sm;
+}
+
+}  // namespace
+
+// tile shapes: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128 (r <= 16)
+int sketch_tile_rows(int shape) { return shape == 0 ? 64 : shape == 1 ? 32 : 16; }
+int sketch_shape_ok(int shape, int r) { return shape != 2 || r <= 16; }
+
+void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s) {
+    if (a.shape == 0) launch_rw<64, 32>(a, s);
+    else if (a.shape == 1) launch_rw<32, 64>(a, s);
+    else launch_rw<16, 128>(a, s);
+}
+
+int ef_sketch_resident_ctas(int r, int shape) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = shape == 0 ? occupancy_rw<64, 32>(r) : shape == 1 ? occupancy_rw<32, 64>(r) : occupancy_rw<16, 128>(r);
+    if (per_sm < 1) per_sm = 1;
+    return sms * per_sm;
+}
+
+}  // namespace arc
