@@ -353,7 +353,8 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         int min_n = INT32_MAX;
         for (const BlockDev& B : c->pl.bdev)
             if (B.kind == ARC_BLOCK_ARC) { all_vec = all_vec && B.vec; min_n = std::min(min_n, B.n); }
-        c->shape = (all_vec && min_n >= 128) ? 2 : (min_n >= 64 ? 1 : 0);
+        (void)all_vec;
+        c->shape = min_n >= 64 ? 1 : 0;   // 32 x 64 measured best on C3
         if (const char* e = getenv("ARC_SKETCH_SHAPE")) {
             const int v = atoi(e);
             if (v >= 0 && v <= 2) c->shape = v;

@@ -45,8 +45,8 @@ struct TileRegs {
 
 template <int W>
 __device__ __forceinline__ TileRegs tile_regs(const SketchLaunch& a, int li) {
-    const Tile T = a.tiles[li];
-    const BlockDev* B = a.blocks + __ldg(&T.b);
+    const Tile* T = a.tiles + li;
+    const BlockDev* B = a.blocks + __ldg(&T->b);
     TileRegs t;
     t.off = __ldg(&B->off);
     t.len = __ldg(&B->len);
@@ -54,8 +54,8 @@ __device__ __forceinline__ TileRegs tile_regs(const SketchLaunch& a, int li) {
     t.vec = __ldg(&B->vec);
     t.v_off = __ldg(&B->v_off);
     t.row_base = __ldg(&B->row_base);
-    t.row0 = T.row0;
-    t.m_rows = T.rows;
+    t.row0 = __ldg(&T->row0);
+    t.m_rows = __ldg(&T->rows);
     t.nchunks = (t.n + W - 1) / W;
     return t;
 }
