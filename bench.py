@@ -29,7 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "ARC-Top-K step ms and grad GB/s at 1/2/4/8 B200; % of HBM/NVLink roofline"
-PHASES = ["vgen", "ef_sketch", "exchange1_reduce", "select", "gather_ef", "exchange2_scatter", "copy_out"]
+PHASES = ["vgen", "ef_sketch", "exchange1_reduce", "select_gather", "exchange2_scatter", "copy_out"]
 
 
 def _peaks():
@@ -202,6 +202,7 @@ def main():
     ap.add_argument("--reduce", default="nccl", choices=["nccl", "ordered"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--pool", type=int, default=8, help="distinct gradient sets cycled in the timed loop")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     if args.impl == "reference":
@@ -229,7 +230,12 @@ def main():
     d, blocks, N = workload(args.config, L, world)
     src = GradientSource(d, blocks, N, seed=20251030, device=dev)
     nodes = list(range(rank * L, (rank + 1) * L))
-    grads = src.grads(0, nodes)
+    # A pool of distinct gradient sets cycled step by step, like a training
+    # stream (re-using one set would drive h and g to a fixed point where every
+    # residual row is exactly 0: an all-ties degenerate workload).
+    pool_n = max(1, min(args.pool, int((torch.cuda.mem_get_info(dev)[0] * 0.5) // (4 * d * L))))
+    pool = [src.grads(t, nodes) for t in range(pool_n)]
+    grads = pool[0]
     h = [torch.zeros(d, device=dev) for _ in range(L)]
     g = [torch.zeros(d, device=dev) for _ in range(L)]
     gbar = torch.zeros(d, device=dev)
@@ -243,22 +249,29 @@ def main():
 
     # ---------------------------------------------------------------- device-timed steps
     for t in range(args.warmup):
-        ctx.step(t, grads, h, g, gbar)
+        ctx.step(t, pool[t % pool_n], h, g, gbar)
     torch.cuda.synchronize()
-    ctx.read_timing()
-    ctx.set_timing(True)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for k in range(args.steps):
-            ctx.step(args.warmup + k, grads, h, g, gbar)
+            t = args.warmup + k
+            ctx.step(t, pool[t % pool_n], h, g, gbar)
         e1.record(stream)
         e1.synchronize()
     torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    # second timed pass of K steps with CUDA events between the step's phases
+    # (on the step's stream): per-kernel durations for the roofline.  Kept out of
+    # the pass above because each event pair adds ~2-3 us to the step.
+    ctx.read_timing()
+    ctx.set_timing(True)
+    for k in range(args.steps):
+        t = args.warmup + args.steps + k
+        ctx.step(t, pool[t % pool_n], h, g, gbar)
     phases_sum, nsteps = ctx.read_timing()
     ctx.set_timing(False)
     phase_ms = {k: v / max(nsteps, 1) for k, v in phases_sum.items()}
@@ -328,7 +341,8 @@ def main():
                                    if args.config == "C3" else args.config,
                        "d": d, "N_nodes": N, "nodes_per_gpu": L, "reduce": args.reduce,
                        "parallelism": f"dp{world}",
-                       "l2": "no flush: per-step inputs (16 B x d = %.1f GB) exceed the 126 MB L2" % (16 * d / 1e9)},
+                       "l2": "no flush: per-step inputs (16 B x d = %.1f GB) exceed the 126 MB L2" % (16 * d / 1e9),
+                       "gradient_pool": pool_n},
             "roofline": {"bound": "hbm", "kernel": "k_ef_sketch", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": ab["ef_sketch"], "peak_source": peak_src,

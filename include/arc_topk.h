@@ -154,11 +154,12 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* ctx);
 
 /* Per-phase device timing (CUDA events recorded on the step's stream between
  * the step's phases; off by default, and must stay off during graph capture).
- * Phases: 0 S0 vgen, 1 S1 ef_sketch, 2 exchange #1 + S2 reduce, 3 S3 select,
- * 4 S4 gather/EF, 5 exchange #2 + S6 scatter, 6 output copies.
- * read_timing synchronises and returns the summed milliseconds of each phase
- * over the timed steps since the last read (n_phases <= 7), then resets. */
-#define ARC_TIMING_PHASES 7
+ * Phases: 0 S0 vgen, 1 S1 ef_sketch, 2 exchange #1 + S2 reduce,
+ * 3 S3 select + S4 gather/EF (+S5/S6 at G == 1), 4 exchange #2 + S6 scatter,
+ * 5 output copies.  read_timing synchronises and returns the summed
+ * milliseconds of each phase over the timed steps since the last read
+ * (n_phases <= 6), then resets. */
+#define ARC_TIMING_PHASES 6
 arc_status arc_topk_set_timing(arc_topk_ctx* ctx, int32_t enable);
 arc_status arc_topk_read_timing(arc_topk_ctx* ctx, float* ms, int32_t n_phases, int32_t* steps);
 

@@ -31,8 +31,8 @@ EXPORTED = [
     "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_kernels_per_step",
     "arc_topk_destroy", "arc_topk_status_string", "arc_topk_set_timing", "arc_topk_read_timing",
 ]
-TIMING_PHASES = 7
-PHASE_NAMES = ["vgen", "ef_sketch", "exchange1_reduce", "select", "gather_ef", "exchange2_scatter", "copy_out"]
+TIMING_PHASES = 6
+PHASE_NAMES = ["vgen", "ef_sketch", "exchange1_reduce", "select_gather", "exchange2_scatter", "copy_out"]
 
 
 class ArcBlock(ctypes.Structure):

@@ -56,13 +56,18 @@ struct Plan {
     bool keep_pnodes = false;
     int M = 0;                   // sum of ARC m_b (global ARC rows)
     int64_t sumK = 0, sumKn = 0, sum_nr = 0;
+    int64_t num_segs = 0;        // gather / scatter row segments
+    int num_slices = 0;          // selection slices (all blocks)
+    int slice_rows = kSliceMin;
+    std::vector<SliceItem> items;
     int max_nR4 = 0;
     int max_tiles = 0;
     std::vector<BlockDev> bdev;
     // workspace offsets (bytes)
     size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
            o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
-           o_vals = 0, o_hash = 0, total = 0;
+           o_vals = 0, o_hash = 0, o_hist1 = 0, o_hist2 = 0, o_hist3 = 0, o_slice_gt = 0, o_slice_eq = 0,
+           o_items = 0, total = 0;
 };
 
 arc_status validate(const arc_topk_params* p) {
@@ -93,11 +98,12 @@ arc_status validate(const arc_topk_params* p) {
         sumK += B.K;
     }
     if (pos != p->d) return ARC_ERR_INVALID_ARG;
-    if (M > INT32_MAX || sumK > INT32_MAX) return ARC_ERR_INVALID_ARG;
+    if (M > INT32_MAX || sumK > INT32_MAX / 64) return ARC_ERR_INVALID_ARG;
     return ARC_OK;
 }
 
-void make_plan(const arc_topk_params* p, Plan& pl) {
+void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
+    pl.slice_rows = slice_rows;
     pl.L = p->nodes_local;
     pl.G = p->N / p->nodes_local;
     pl.exchange = pl.G > 1 || (p->flags & ARC_FLAG_FORCE_EXCHANGE);
@@ -120,7 +126,12 @@ void make_plan(const arc_topk_params* p, Plan& pl) {
         D.sel_base = static_cast<int>(sumK);
         D.val_base = sumKn;
         D.vec = (B.offset % 4 == 0) && (B.n % 4 == 0);
-        D.pad_ = 0;
+        D.slice_base = pl.num_slices;
+        {
+            const int nsl = static_cast<int>((B.m + pl.slice_rows - 1) / pl.slice_rows);
+            for (int c = 0; c < nsl; ++c) pl.items.push_back(SliceItem{b, c});
+            pl.num_slices += nsl;
+        }
         if (B.kind == ARC_BLOCK_ARC) {
             M += B.m;
             sum_nr += B.n * p->r;
@@ -129,6 +140,7 @@ void make_plan(const arc_topk_params* p, Plan& pl) {
         }
         sumK += B.K;
         sumKn += B.K * B.n;
+        pl.num_segs += B.K * (((B.n + 3) / 4 + kSegQuads - 1) / kSegQuads);
     }
     pl.M = static_cast<int>(M);
     pl.sumK = sumK;
@@ -141,11 +153,17 @@ void make_plan(const arc_topk_params* p, Plan& pl) {
     pl.o_blocks = take(sizeof(BlockDev) * p->num_blocks);
     pl.o_tiles = take(sizeof(Tile) * pl.max_tiles);
     pl.o_cta = take(sizeof(int) * (kMaxGrid + 1));
-    pl.o_selrows = take(sizeof(SelRow) * sumK);
+    pl.o_selrows = take(sizeof(SelRow) * pl.num_segs);
     pl.o_V = take(sizeof(float) * sum_nr);
     pl.o_sigma = take(sizeof(float) * std::max<int64_t>(M, 1));
     pl.o_sel = take(sizeof(int32_t) * sumK);
     pl.o_status = take(16);
+    pl.o_hist1 = take(sizeof(unsigned) * kHist1Bins * p->num_blocks);
+    pl.o_hist2 = take(sizeof(unsigned) * 2048 * p->num_blocks);
+    pl.o_hist3 = take(sizeof(unsigned) * 1024 * p->num_blocks);
+    pl.o_slice_gt = take(sizeof(int) * pl.num_slices);
+    pl.o_slice_eq = take(sizeof(int) * pl.num_slices);
+    pl.o_items = take(sizeof(SliceItem) * pl.items.size());
     pl.o_hash = take(sizeof(uint64_t) * (pl.G + 1));
     const size_t pn = sizeof(float) * static_cast<size_t>(M) * pl.L * p->r;
     pl.o_pnodes = pl.keep_pnodes ? take(pn) : 0;
@@ -263,7 +281,7 @@ struct arc_topk_ctx {
     Nccl nccl;
     ncclComm_t comm = nullptr;
     unsigned char* ws = nullptr;
-    int grid = 0, num_tiles = 0, sel_slice = 1, shape = 0;
+    int grid = 0, num_tiles = 0, shape = 0, max_m = 1;
     float ome = 0.f, c_r = 0.f, Nf = 0.f;
     cudaStream_t last = nullptr;
     // per-phase timing
@@ -325,6 +343,25 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     c->p.blocks = c->blocks.data();
     make_plan(&c->p, c->pl);
     if (workspace_bytes < c->pl.total) { delete c; return ARC_ERR_INVALID_ARG; }
+    {   // the select/gather kernel is cooperative: one CTA per slice, all co-resident
+        const int resident = select_gather_resident_ctas();
+        int rows = kSliceMin;
+        while (rows < select_max_slice_rows()) {
+            int64_t n = 0;
+            for (const arc_block& B : c->blocks) n += (B.m + rows - 1) / rows;
+            if (n <= resident) break;
+            rows *= 2;
+        }
+        int64_t n = 0;
+        for (const arc_block& B : c->blocks) n += (B.m + rows - 1) / rows;
+        if (n > resident) { delete c; return ARC_ERR_UNSUPPORTED; }
+        const size_t total = c->pl.total;
+        if (rows != kSliceMin) {
+            c->pl = Plan();
+            make_plan(&c->p, c->pl, rows);
+            c->pl.total = total;   // fewer slices: the workspace laid out for 1024-row slices is larger
+        }
+    }
     c->ws = static_cast<unsigned char*>(workspace);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     c->last = s;
@@ -365,15 +402,16 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
                c->grid);
     c->num_tiles = static_cast<int>(tiles.size());
     {
-        int max_m = 1;
         for (const BlockDev& B : c->pl.bdev)
-            if (B.kind == ARC_BLOCK_ARC && B.K < B.m) max_m = std::max(max_m, B.m);
-        c->sel_slice = select_max_slice(max_m);
+            if (B.kind == ARC_BLOCK_ARC) c->max_m = std::max(c->max_m, B.m);
     }
     std::vector<SelRow> rows;
-    rows.reserve(static_cast<size_t>(c->pl.sumK));
-    for (int b = 0; b < c->p.num_blocks; ++b)
-        for (int64_t k = 0; k < c->blocks[b].K; ++k) rows.push_back(SelRow{b, static_cast<int>(k)});
+    rows.reserve(static_cast<size_t>(c->pl.num_segs));
+    for (int b = 0; b < c->p.num_blocks; ++b) {
+        const int nq = static_cast<int>((c->blocks[b].n + 3) / 4);
+        for (int64_t k = 0; k < c->blocks[b].K; ++k)
+            for (int q0 = 0; q0 < nq; q0 += kSegQuads) rows.push_back(SelRow{b, static_cast<int>(k), q0});
+    }
 
 #define UPLOAD(off, vec) \
     if (!(vec).empty()) ARC_CUDA(cudaMemcpyAsync(c->ws + (off), (vec).data(), sizeof((vec)[0]) * (vec).size(), cudaMemcpyHostToDevice, s))
@@ -384,7 +422,11 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
             UPLOAD(c->pl.o_tiles, tiles);
             UPLOAD(c->pl.o_cta, cta_begin);
             UPLOAD(c->pl.o_selrows, rows);
+            UPLOAD(c->pl.o_items, c->pl.items);
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist2, 0, sizeof(unsigned) * 2048 * c->p.num_blocks, s));
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist3, 0, sizeof(unsigned) * 1024 * c->p.num_blocks, s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_status, 0, 16, s));
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist1, 0, sizeof(unsigned) * kHist1Bins * c->p.num_blocks, s));
             ARC_CUDA(cudaStreamSynchronize(s));
             return ARC_OK;
         };
@@ -449,6 +491,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     float* sigma = c->at<float>(pl.o_sigma);
     int32_t* sel = c->at<int32_t>(pl.o_sel);
     unsigned* status = c->at<unsigned>(pl.o_status);
+    unsigned* hist1 = c->at<unsigned>(pl.o_hist1);
     const SelRow* rows = c->at<SelRow>(pl.o_selrows);
 
     ARC_MARK(0);
@@ -475,6 +518,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.Nf = c->Nf;
         a.V = V;
         a.sigma = sigma;
+        a.hist1 = hist1;
         a.pnodes = pl.keep_pnodes ? c->at<float>(pl.o_pnodes) : nullptr;
         a.mode = pl.exchange ? 1 : 0;
         a.shape = c->shape;
@@ -486,7 +530,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         ARC_MARK(1);
     }
     ARC_MARK(2);
-    // (DENSE blocks skip the sketch pass: k_gather_ef applies their momentum.)
+    // (DENSE blocks skip the sketch pass: the select/gather kernel applies their momentum.)
     // Exchange #1 + S2 for G > 1
     if (pl.exchange && pl.M > 0) {
         const size_t cnt = static_cast<size_t>(pl.M) * L * c->p.r;
@@ -497,19 +541,15 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         } else {
             ARC_CUDA(cudaMemcpyAsync(xr, xs, cnt * sizeof(float), cudaMemcpyDeviceToDevice, s));
         }
-        launch_sketch_reduce(xr, pl.M, pl.G, L, c->p.r, c->Nf, sigma, status, s);
+        launch_sketch_reduce(blocks, c->p.num_blocks, c->max_m, xr, pl.M, pl.G, L, c->p.r, c->Nf, sigma, hist1, status, s);
         ARC_LAUNCHED();
     }
     ARC_MARK(3);
-    // S3
-    launch_select(blocks, c->p.num_blocks, sigma, sel, c->sel_slice, s);
-    ARC_LAUNCHED();
-    ARC_MARK(4);
-    // S4..S6
+    // S3 + S4 (+ S5, S6 when every node is local): one cooperative kernel
     GatherLaunch ga{};
     ga.blocks = blocks;
     ga.rows = rows;
-    ga.num_rows = static_cast<int>(pl.sumK);
+    ga.num_rows = static_cast<int>(pl.num_segs);
     ga.sel = sel;
     ga.nodes = np;
     ga.nodes_local = L;
@@ -517,21 +557,36 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ga.ome = c->ome;
     ga.Nf = c->Nf;
     ga.sum_Kn = pl.sumKn;
+    const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
+    float* wire = pl.exchange ? c->at<float>(pl.o_wire) : nullptr;
     if (!pl.exchange) {
         ga.mode = 0;
         ga.gbar = gbar;
         ga.values = values_out;
-        launch_gather_ef(ga, s);
-        ARC_LAUNCHED();
-        ARC_MARK(5);
     } else {
-        const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
-        float* wire = c->at<float>(pl.o_wire);
         ga.mode = ordered ? 2 : 1;
         ga.values = wire;
-        launch_gather_ef(ga, s);
-        ARC_LAUNCHED();
-        ARC_MARK(5);
+    }
+    {
+        SelectGatherLaunch sg{};
+        sg.blocks = blocks;
+        sg.items = c->at<SliceItem>(pl.o_items);
+        sg.num_items = static_cast<int>(pl.items.size());
+        sg.slice_rows = pl.slice_rows;
+        sg.sigma = sigma;
+        sg.hist1 = hist1;
+        sg.hist2 = c->at<unsigned>(pl.o_hist2);
+        sg.hist3 = c->at<unsigned>(pl.o_hist3);
+        sg.slice_gt = c->at<int>(pl.o_slice_gt);
+        sg.slice_eq = c->at<int>(pl.o_slice_eq);
+        sg.sel = sel;
+        if (launch_select_gather(sg, ga, s) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return ARC_ERR_CUDA;
+        }
+    }
+    ARC_MARK(4);
+    if (pl.exchange) {   // exchange #2 + S6
         const float* reduced = wire;
         if (!ordered) {
             if (c->comm != nullptr && pl.G > 1) {
@@ -551,7 +606,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         ScatterLaunch sa{};
         sa.blocks = blocks;
         sa.rows = rows;
-        sa.num_rows = static_cast<int>(pl.sumK);
+        sa.num_rows = static_cast<int>(pl.num_segs);
         sa.sel = sel;
         sa.wire = reduced;
         sa.mode = ordered ? 1 : 0;
@@ -563,10 +618,10 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         launch_scatter(sa, s);
         ARC_LAUNCHED();
     }
-    ARC_MARK(6);
+    ARC_MARK(5);
     if (sel_out != nullptr)
         ARC_CUDA(cudaMemcpyAsync(sel_out, sel, sizeof(int32_t) * pl.sumK, cudaMemcpyDeviceToDevice, s));
-    ARC_MARK(7);
+    ARC_MARK(6);
     if (c->timing) ++c->timed_steps;
     return ARC_OK;
 }
@@ -636,7 +691,8 @@ arc_status arc_topk_sizes(const arc_topk_ctx* c, int64_t* sum_K, int64_t* sum_Kn
 int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     if (c == nullptr) return -1;
     const int arc = c->pl.M > 0 ? 2 : 0;   // vgen + ef_sketch
-    return arc + (c->pl.exchange && c->pl.M > 0 ? 1 : 0) + 1 /*select*/ + (c->pl.exchange ? 2 : 1);
+    // vgen + ef_sketch, [sketch_reduce], select_gather, [scatter]
+    return arc + (c->pl.exchange && c->pl.M > 0 ? 1 : 0) + 1 + (c->pl.exchange ? 1 : 0);
 }
 
 arc_status arc_topk_set_timing(arc_topk_ctx* c, int32_t enable) {

@@ -38,5 +38,11 @@ static __device__ __forceinline__ float4 ld_na4(const float* p) {
     return v;
 }
 
+// Order key of a Sigma value (R15): its binary32 bit pattern (Sigma >= +0, so
+// unsigned order is numeric order); every NaN maps to the largest key.
+static __device__ __forceinline__ unsigned order_key_dev(float s) {
+    return isnan(s) ? 0xFFFFFFFFu : __float_as_uint(s);
+}
+
 }  // namespace dev
 }  // namespace arc

@@ -18,7 +18,7 @@ struct BlockDev {
     int sel_base;       // offset of I_b in the selection array
     long long val_base; // offset of the compact rows in values / wire
     int vec;            // rows 16-byte aligned: off % 4 == 0 && n % 4 == 0
-    int pad_;
+    int slice_base;     // first selection slice of the block
 };
 
 // A sketch tile: rows [row0, row0 + rows) of one ARC block, rows <= kTileRows.
@@ -28,15 +28,45 @@ struct Tile {
     int rows;
 };
 
-// Selected-row work item for gather / scatter: (block, k).
+// Gather / scatter work item: columns [4*q0, 4*q0 + kSegQuads*4) of the k-th
+// selected row of block b.
+constexpr int kSegQuads = 64;      // 32 lanes x 2 quads = 256 columns
 struct SelRow {
     int b;
     int k;
+    int q0;
 };
 
 constexpr int kSketchThreads = 256;
 
 constexpr uint32_t kStatusNonfinite = 1u;
+
+// Selection: digit 1 of the order key (bits [31:21]) is histogrammed per block
+// by the pass that produces Sigma; k_select resolves the rest on candidates.
+constexpr int kHist1Bins = 2048;
+constexpr int kHist1Shift = 21;
+constexpr unsigned kHist1Mask = 0xFFE00000u;
+constexpr int kSliceMin = 1024;    // rows per selection slice (one CTA), at least
+
+struct SliceItem {
+    int b;   // block
+    int c;   // slice in the block
+};
+
+
+struct SelectGatherLaunch {
+    const BlockDev* blocks;
+    const SliceItem* items;        // every slice of every block (one CTA each)
+    int num_items;
+    int slice_rows;                // rows per slice (<= 4096)
+    const float* sigma;
+    unsigned* hist1;               // [num_blocks][2048] digit key[31:21] (filled by the Sigma pass)
+    unsigned* hist2;               // [num_blocks][2048] digit key[20:10]
+    unsigned* hist3;               // [num_blocks][1024] digit key[9:0]
+    int* slice_gt;                 // [num_slices] keys > T
+    int* slice_eq;                 // [num_slices] keys == T
+    int32_t* sel;
+};
 
 struct NodePtrs {
     const float* grad[ARC_MAX_NODES_LOCAL];
@@ -59,6 +89,7 @@ struct SketchLaunch {
     float eta, ome, c_r, Nf;
     const float* V;
     float* sigma;      // mode 0: written
+    unsigned* hist1;   // [num_blocks][kHist1Bins] digit-1 histogram of Sigma (mode 0)
     float* pnodes;     // [M][nodes_local][r] P_i, or nullptr (mode 0 without debug)
     int mode;          // 0 = reduce locally -> sigma ; 1 = exchange (write pnodes only)
     int shape;         // tile shape R x W: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128
@@ -69,17 +100,19 @@ int ef_sketch_resident_ctas(int r, int shape);   // SMs x occupancy
 int sketch_tile_rows(int shape);
 int sketch_shape_ok(int shape, int r);
 
-void launch_sketch_reduce(const float* xrecv, int M, int G, int nodes_local, int r, float Nf,
-                          float* sigma, unsigned* status, cudaStream_t s);
+void launch_sketch_reduce(const BlockDev* blocks, int num_blocks, int max_m, const float* xrecv, int M, int G,
+                          int nodes_local, int r, float Nf, float* sigma, unsigned* hist1, unsigned* status,
+                          cudaStream_t s);
 
-void launch_select(const BlockDev* blocks, int num_blocks, const float* sigma, int32_t* sel, int max_slice,
-                   cudaStream_t s);
-int select_max_slice(int max_m);   // keys per CTA of the largest selected block
+struct GatherLaunch;
+cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch& ga, cudaStream_t st);
+int select_gather_resident_ctas();
+int select_max_slice_rows();
 
 struct GatherLaunch {
     const BlockDev* blocks;
     const SelRow* rows;
-    int num_rows;       // sum_b K_b
+    int num_rows;       // number of row segments
     const int32_t* sel;
     NodePtrs nodes;
     int nodes_local;
@@ -90,7 +123,6 @@ struct GatherLaunch {
     int mode;           // 0 = fused local (G==1); 1 = wire pre-sum; 2 = wire per node [nodes_local][sumKn]
     long long sum_Kn;
 };
-void launch_gather_ef(const GatherLaunch& a, cudaStream_t s);
 
 struct ScatterLaunch {
     const BlockDev* blocks;

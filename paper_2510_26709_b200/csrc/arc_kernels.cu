@@ -154,13 +154,20 @@ __device__ __forceinline__ int row_valid_cols(const BlockDev& B, int p) {
     return rest < B.n ? static_cast<int>(rest) : B.n;
 }
 
+__device__ __forceinline__ unsigned order_key(float s) { return order_key_dev(s); }
+
 // =============================================================================
 // S2 for G > 1: ordered node sum of the all-gathered P_i (R9, R21) and Sigma.
 // xrecv layout [G][M][L][r]; global node id = g*L + l.
 // =============================================================================
-__global__ void __launch_bounds__(256) k_sketch_reduce(const float* __restrict__ xrecv, int M, int G, int L, int r,
-                                                       float Nf, float* __restrict__ sigma, unsigned* status) {
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < M; p += gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(256) k_sketch_reduce(const BlockDev* __restrict__ blocks, const float* __restrict__ xrecv,
+                                                       int M, int G, int L, int r, float Nf, float* __restrict__ sigma,
+                                                       unsigned* __restrict__ hist1, unsigned* status) {
+    const int b = blockIdx.y;
+    if (blocks[b].kind != ARC_BLOCK_ARC) return;
+    const int m = blocks[b].m, base = blocks[b].row_base;
+    for (int pr = blockIdx.x * blockDim.x + threadIdx.x; pr < m; pr += gridDim.x * blockDim.x) {
+        const int p = base + pr;
         float sig = 0.0f;
         for (int j = 0; j < r; ++j) {
             float S = 0.0f;
@@ -173,336 +180,8 @@ __global__ void __launch_bounds__(256) k_sketch_reduce(const float* __restrict__
             sig = fadd(sig, fmul(pv, pv));
         }
         sigma[p] = sig;
+        atomicAdd(&hist1[static_cast<long long>(b) * kHist1Bins + (order_key(sig) >> kHist1Shift)], 1u);
         if (!isfinite(sig)) atomicOr(status, kStatusNonfinite);
-    }
-}
-
-// =============================================================================
-// S3: I_b = argtop_{K_b}(Sigma_b) — one 8-CTA cluster per block.
-// MSB-first radix select over the order keys (R15) with 8-bit digits: each CTA
-// histograms its slice in shared memory, the cluster merges the histograms
-// through distributed shared memory, and every CTA derives the same digit.
-// After 4 passes the K-th key T and the number of keys == T still to take are
-// known; a stable compaction then writes the selected rows in ascending order,
-// taking the keys equal to T with the smallest indices (R5).
-// =============================================================================
-constexpr int kSelCluster = 8;
-constexpr int kSelThreads = 1024;
-constexpr int kSelItems = 8;
-
-__device__ __forceinline__ unsigned order_key(float s) {
-    return isnan(s) ? 0xFFFFFFFFu : __float_as_uint(s);
-}
-
-// exclusive scan of one int per thread over the CTA; returns the exclusive
-// prefix and writes the CTA total to *total.
-__device__ __forceinline__ int cta_exclusive_scan(int v, int* warp_sums, int* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(kFull, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        const int nw = blockDim.x >> 5;
-        int w = lane < nw ? warp_sums[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, w, o);
-            if (lane >= o) w += y;
-        }
-        if (lane < nw) warp_sums[lane] = w;       // inclusive
-    }
-    __syncthreads();
-    const int excl = x - v + (warp > 0 ? warp_sums[warp - 1] : 0);
-    *total = warp_sums[(blockDim.x >> 5) - 1];
-    __syncthreads();
-    return excl;
-}
-
-__global__ void __cluster_dims__(kSelCluster, 1, 1) __launch_bounds__(kSelThreads)
-k_select(const BlockDev* __restrict__ blocks, const float* __restrict__ sigma, int32_t* __restrict__ sel,
-         int cache_cap) {
-    cg::cluster_group cluster = cg::this_cluster();
-    const int crank = static_cast<int>(cluster.block_rank());
-    const int b = blockIdx.x / kSelCluster;
-    const BlockDev B = blocks[b];
-    const int m = B.m, K = B.K;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int lo = static_cast<int>((static_cast<long long>(m) * crank) / kSelCluster);
-    const int hi = static_cast<int>((static_cast<long long>(m) * (crank + 1)) / kSelCluster);
-    const int len = hi - lo;
-    int32_t* __restrict__ out = sel + B.sel_base;
-
-    if (B.kind != ARC_BLOCK_ARC || K >= m) {        // identity selection (DENSE, or K = m)
-        for (int p = lo + tid; p < hi; p += kSelThreads) out[p] = p;
-        return;                                     // uniform across the cluster: no DSMEM use
-    }
-    const float* __restrict__ sg = sigma + B.row_base + lo;
-
-    extern __shared__ unsigned s_keys[];            // this CTA's slice of order keys, if it fits
-    __shared__ unsigned hist[2][256];
-    __shared__ int warp_sums[32];
-    __shared__ unsigned s_digit, s_above;
-    __shared__ int s_cnt[2];                        // this CTA: #gt, #eq
-
-    const bool cached = len <= cache_cap;
-    if (cached) {
-        for (int i = tid; i < len; i += kSelThreads) s_keys[i] = order_key(sg[i]);
-        __syncthreads();
-    }
-    auto key_at = [&](int i) -> unsigned { return cached ? s_keys[i] : order_key(sg[i]); };
-
-    constexpr int U = 4;                            // keys per thread per sweep (load ILP)
-    unsigned prefix = 0, pmask = 0;
-    int krem = K;
-    for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
-        unsigned* h = hist[pass & 1];
-        for (int i = tid; i < 256; i += kSelThreads) h[i] = 0;
-        __syncthreads();
-        for (int base = 0; base < len; base += kSelThreads * U) {
-            unsigned kk[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = base + u * kSelThreads + tid;
-                kk[u] = i < len ? key_at(i) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = base + u * kSelThreads + tid;
-                const bool match = i < len && (kk[u] & pmask) == prefix;
-                const unsigned bin = (kk[u] >> shift) & 255u;
-                const unsigned want = __ballot_sync(kFull, match);
-                if (match) {
-                    const unsigned grp = __match_any_sync(want, bin);
-                    if (lane == __ffs(grp) - 1) atomicAdd(&h[bin], static_cast<unsigned>(__popc(grp)));
-                }
-            }
-        }
-        cluster.sync();
-        if (tid < 32) {
-            // lane l owns bins 255-8l .. 248-8l (descending); sum over the cluster
-            unsigned cnt[8];
-            unsigned mine = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int bin = 255 - 8 * lane - k;
-                unsigned c = 0;
-#pragma unroll
-                for (int cr = 0; cr < kSelCluster; ++cr) c += cluster.map_shared_rank(h, cr)[bin];
-                cnt[k] = c;
-                mine += c;
-            }
-            unsigned incl = mine;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const unsigned excl = incl - mine;   // keys in bins above my 8
-            const bool here = excl < static_cast<unsigned>(krem) && incl >= static_cast<unsigned>(krem);
-            if (here) {
-                unsigned above = excl;
-                int k = 0;
-                while (above + cnt[k] < static_cast<unsigned>(krem)) { above += cnt[k]; ++k; }
-                s_digit = 255u - 8u * lane - k;
-                s_above = above;
-            }
-        }
-        __syncthreads();
-        prefix |= s_digit << shift;
-        pmask |= 255u << shift;
-        krem -= static_cast<int>(s_above);
-        __syncthreads();
-    }
-    const unsigned T = prefix;       // the K-th largest key
-    const int need_eq = krem;        // keys == T to take (>= 1), smallest indices first
-
-    // ---- counts of this slice, shared with the cluster
-    int ngt = 0, neq = 0;
-    for (int i = tid; i < len; i += kSelThreads) {
-        const unsigned key = key_at(i);
-        ngt += key > T;
-        neq += key == T;
-    }
-    int tot;
-    cta_exclusive_scan(ngt, warp_sums, &tot);
-    if (tid == 0) s_cnt[0] = tot;
-    cta_exclusive_scan(neq, warp_sums, &tot);
-    if (tid == 0) s_cnt[1] = tot;
-    cluster.sync();
-    int sel_before = 0, eq_before = 0;
-    for (int cr = 0; cr < crank; ++cr) {
-        const int* rc = cluster.map_shared_rank(s_cnt, cr);
-        const int g = rc[0], e = rc[1];
-        const int take = max(0, min(e, need_eq - eq_before));
-        sel_before += g + take;
-        eq_before += e;
-    }
-
-    // ---- stable compaction of the slice, kSelItems consecutive keys per thread
-    for (int base = 0; base < len; base += kSelThreads * kSelItems) {
-        const int i0 = base + tid * kSelItems;
-        unsigned keys[kSelItems];
-        int my_eq = 0;
-#pragma unroll
-        for (int e = 0; e < kSelItems; ++e) {
-            const int i = i0 + e;
-            keys[e] = i < len ? key_at(i) : 0u;
-            my_eq += (i < len && keys[e] == T);
-        }
-        int eq_total;
-        int eq_rank = eq_before + cta_exclusive_scan(my_eq, warp_sums, &eq_total);
-        bool take[kSelItems];
-        int my_sel = 0;
-#pragma unroll
-        for (int e = 0; e < kSelItems; ++e) {
-            bool t = false;
-            if (i0 + e < len) {
-                if (keys[e] > T) t = true;
-                else if (keys[e] == T) { t = eq_rank < need_eq; ++eq_rank; }
-            }
-            take[e] = t;
-            my_sel += t;
-        }
-        int sel_total;
-        int pos = sel_before + cta_exclusive_scan(my_sel, warp_sums, &sel_total);
-#pragma unroll
-        for (int e = 0; e < kSelItems; ++e)
-            if (take[e]) out[pos++] = lo + i0 + e;
-        sel_before += sel_total;
-        eq_before += eq_total;
-    }
-    cluster.sync();   // keep shared memory alive until every CTA has read it
-}
-
-// =============================================================================
-// S4 (+S5, S6 when G == 1): one warp per selected row.
-//   (DENSE blocks first apply eq:ef21m-1, since the sketch pass skips them)
-//   C_i = h_i - g_i on row I_k; g_i <- g_i + C_i                    eq:ef21m-2 (R12)
-//   mode 0: A = C_0 + C_1 + ... (ascending node); val = A / N;
-//           gbar <- gbar + val; values[k] = val                     P:242, R13
-//   mode 1: wire[k] = local node sum      (NCCL All-Reduce follows)
-//   mode 2: wire[i][k] = C_i              (ordered exchange follows)
-// =============================================================================
-// 4 consecutive floats of a row: one 128-bit access when the quad is whole and
-// 16-byte aligned, else element by element (masked by `valid` columns).
-struct Quad {
-    float v[4];
-};
-__device__ __forceinline__ Quad load_quad(const float* p, bool vec4, int nvalid) {
-    Quad x;
-    if (vec4) {
-        const float4 t = *reinterpret_cast<const float4*>(p);
-        x.v[0] = t.x; x.v[1] = t.y; x.v[2] = t.z; x.v[3] = t.w;
-    } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) x.v[k] = k < nvalid ? p[k] : 0.0f;
-    }
-    return x;
-}
-__device__ __forceinline__ void store_quad(float* p, const Quad& x, bool vec4, int nvalid) {
-    if (vec4) {
-        *reinterpret_cast<float4*>(p) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
-    } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (k < nvalid) p[k] = x.v[k];
-    }
-}
-
-__global__ void __launch_bounds__(256) k_gather_ef(const GatherLaunch a) {
-    constexpr int U = 4;                  // quads per lane in flight
-    const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int w = gw; w < a.num_rows; w += nw) {
-        const SelRow R = a.rows[w];
-        const BlockDev& B = a.blocks[R.b];
-        const int p = a.sel[B.sel_base + R.k];
-        const int n = B.n;
-        const int nv = row_valid_cols(B, p);
-        const long long e0 = B.off + static_cast<long long>(p) * n;
-        const long long o0 = B.val_base + static_cast<long long>(R.k) * n;
-        const bool dense = B.kind == ARC_BLOCK_DENSE;
-        // wire / values rows are 16-byte aligned when n % 4 == 0 (val_base is a sum of K n)
-        const bool vrow = B.vec && (o0 % 4 == 0);
-        const int nq = (n + 3) >> 2;
-        for (int f0 = 0; f0 < nq; f0 += 32 * U) {
-            int cnt[U];           // valid state columns of each quad
-            int ocnt[U];          // columns of each quad inside the row (padding -> +0)
-            bool v4[U], ov4[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int q = 4 * (f0 + 32 * u + lane);
-                cnt[u] = max(0, min(4, nv - q));
-                ocnt[u] = max(0, min(4, n - q));
-                v4[u] = B.vec && cnt[u] == 4;
-                ov4[u] = vrow && ocnt[u] == 4;
-            }
-            Quad A[U];
-            for (int i = 0; i < a.nodes_local; ++i) {
-                float* __restrict__ ph = a.nodes.h[i];
-                float* __restrict__ pg = a.nodes.g[i];
-                Quad hq[U], gq[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const long long e = e0 + 4 * (f0 + 32 * u + lane);
-                    if (cnt[u] > 0) {
-                        gq[u] = load_quad(pg + e, v4[u], cnt[u]);
-                        if (dense) {   // DENSE block: eq:ef21m-1 applied here (R11, R20)
-                            const Quad hv = load_quad(ph + e, v4[u], cnt[u]);
-                            const Quad gr = load_quad(a.nodes.grad[i] + e, v4[u], cnt[u]);
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) hq[u].v[k] = fadd(fmul(a.ome, hv.v[k]), fmul(a.eta, gr.v[k]));
-                            store_quad(ph + e, hq[u], v4[u], cnt[u]);
-                        } else {
-                            hq[u] = load_quad(ph + e, v4[u], cnt[u]);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (ocnt[u] == 0) continue;
-                    const long long e = e0 + 4 * (f0 + 32 * u + lane);
-                    Quad c, gn;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        c.v[k] = k < cnt[u] ? fsub(hq[u].v[k], gq[u].v[k]) : 0.0f;   // C_i (+0 padding)
-                        gn.v[k] = fadd(gq[u].v[k], c.v[k]);                            // R12
-                        A[u].v[k] = (i == 0) ? c.v[k] : fadd(A[u].v[k], c.v[k]);
-                    }
-                    if (cnt[u] > 0) store_quad(pg + e, gn, v4[u], cnt[u]);
-                    if (a.mode == 2)
-                        store_quad(a.values + static_cast<long long>(i) * a.sum_Kn + o0 + 4 * (f0 + 32 * u + lane),
-                                   c, ov4[u] && (a.sum_Kn % 4 == 0), ocnt[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (ocnt[u] == 0) continue;
-                const int q = 4 * (f0 + 32 * u + lane);
-                if (a.mode == 0) {
-                    const long long e = e0 + q;
-                    Quad val, gb;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) val.v[k] = k < cnt[u] ? __fdiv_rn(A[u].v[k], a.Nf) : 0.0f;   // R3
-                    if (cnt[u] > 0) {
-                        gb = load_quad(a.gbar + e, v4[u], cnt[u]);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) gb.v[k] = fadd(gb.v[k], val.v[k]);                    // R13
-                        store_quad(a.gbar + e, gb, v4[u], cnt[u]);
-                    }
-                    if (a.values != nullptr) store_quad(a.values + o0 + q, val, ov4[u], ocnt[u]);
-                } else if (a.mode == 1) {
-                    store_quad(a.values + o0 + q, A[u], ov4[u], ocnt[u]);
-                }
-            }
-        }
     }
 }
 
@@ -523,7 +202,8 @@ __global__ void __launch_bounds__(256) k_scatter(const ScatterLaunch a) {
         const int nv = row_valid_cols(B, p);
         const long long e0 = B.off + static_cast<long long>(p) * n;
         const long long o0 = B.val_base + static_cast<long long>(R.k) * n;
-        for (int q = lane; q < n; q += 32) {
+        const int qend = min(n, 4 * (R.q0 + kSegQuads));
+        for (int q = 4 * R.q0 + lane; q < qend; q += 32) {
             if (q < nv) {
                 float A;
                 if (a.mode == 0) {
@@ -558,41 +238,20 @@ void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r,
                                     static_cast<unsigned>(static_cast<uint64_t>(t) >> 32), V);
 }
 
-void launch_sketch_reduce(const float* xrecv, int M, int G, int nodes_local, int r, float Nf, float* sigma,
-                          unsigned* status, cudaStream_t s) {
-    int grid = (M + 255) / 256;
-    if (grid < 1) grid = 1;
-    if (grid > 4096) grid = 4096;
-    k_sketch_reduce<<<grid, 256, 0, s>>>(xrecv, M, G, nodes_local, r, Nf, sigma, status);
+void launch_sketch_reduce(const BlockDev* blocks, int num_blocks, int max_m, const float* xrecv, int M, int G,
+                          int nodes_local, int r, float Nf, float* sigma, unsigned* hist1, unsigned* status,
+                          cudaStream_t s) {
+    int gx = (max_m + 255) / 256;
+    if (gx < 1) gx = 1;
+    if (gx > 1024) gx = 1024;
+    k_sketch_reduce<<<dim3(gx, num_blocks), 256, 0, s>>>(blocks, xrecv, M, G, nodes_local, r, Nf, sigma, hist1, status);
 }
-
-constexpr int kSelCacheMaxBytes = 200 * 1024;
-
-void launch_select(const BlockDev* blocks, int num_blocks, const float* sigma, int32_t* sel, int max_slice,
-                   cudaStream_t s) {
-    static int configured = -1;
-    int cap = max_slice;
-    if (cap * 4 > kSelCacheMaxBytes) cap = kSelCacheMaxBytes / 4;
-    if (cap < 1) cap = 1;
-    const int bytes = cap * 4;
-    if (bytes > 48 * 1024 && configured < bytes) {
-        cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelCacheMaxBytes);
-        configured = kSelCacheMaxBytes;
-    }
-    k_select<<<num_blocks * kSelCluster, kSelThreads, bytes, s>>>(blocks, sigma, sel, cap);
-}
-
-int select_max_slice(int max_m) { return (max_m + kSelCluster - 1) / kSelCluster; }
 
 static int rows_grid(int num_rows) {
-    int grid = (num_rows + 7) / 8;   // 8 warps per CTA, one warp per row
+    int grid = (num_rows + 7) / 8;   // 8 warps per CTA, one warp per row segment
     if (grid < 1) grid = 1;
     if (grid > 148 * 16) grid = 148 * 16;
     return grid;
-}
-
-void launch_gather_ef(const GatherLaunch& a, cudaStream_t s) {
-    k_gather_ef<<<rows_grid(a.num_rows), 256, 0, s>>>(a);
 }
 
 void launch_scatter(const ScatterLaunch& a, cudaStream_t s) {

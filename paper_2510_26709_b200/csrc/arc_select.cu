@@ -1,0 +1,370 @@
+// arc_select.cu — S3 (+S4, and S5/S6 when every node is local) in ONE
+// cooperative kernel: the shared Top-K selection and the compaction / EF update
+// of the selected rows.
+//
+// S3  I_b = argtop_{K_b}(Sigma_b)  (zn28373 P:236-237; ties -> smaller row,
+//     R5; NaN above +Inf, R15): an MSB-first radix select on the 32-bit order
+//     keys with digits key[31:21] | key[20:10] | key[9:0].  Every CTA owns a
+//     slice of `slice_rows` consecutive rows of one block and keeps its keys in
+//     shared memory; the per-digit histograms of a block are summed in global
+//     memory with one atomic per nonzero bin per slice, and a grid-wide barrier
+//     separates the digits.  Digit 1 was histogrammed by the pass that produced
+//     Sigma, so the kernel needs three barriers.  Every slice derives the same
+//     threshold key T and tie quota need_eq; the selected rows of a slice are
+//     key > T, or key == T among the first need_eq rows with key == T in row
+//     order (per-slice counts give the running offsets).  No step is serial in
+//     the number of tied keys.
+// S4  each slice then writes its selected rows in ascending order at its
+//     prefix offset and applies, for every selected row k (row p) and node i,
+//       C_i = h_i - g_i ; g_i <- g_i + C_i                      eq:ef21m-2 (R12)
+//     and, when every node is on this GPU (mode 0),
+//       A = C_0 + C_1 + ... ; val = A / N ; gbar <- gbar + val  P:242, R3, R13
+//     or writes the exchange payload (modes 1, 2).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "arc_device.cuh"
+#include "arc_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace arc {
+namespace {
+using namespace dev;
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ unsigned order_key(float s) { return order_key_dev(s); }
+
+// exclusive scan of one int per thread over the CTA; *total = CTA sum.
+__device__ __forceinline__ int cta_exclusive_scan(int v, int* warp_sums, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        int w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < nw) warp_sums[lane] = w;   // inclusive
+    }
+    __syncthreads();
+    const int excl = x - v + (warp > 0 ? warp_sums[warp - 1] : 0);
+    *total = warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return excl;
+}
+
+// The bin of a histogram (largest bin first) where the running count reaches
+// `krem`; *above = count in higher bins.  All threads call; h in shared memory.
+__device__ __forceinline__ unsigned top_digit(const unsigned* h, int nbins, int krem, int* warp_sums,
+                                              unsigned* s_dig, int* s_abv, int* above) {
+    const int per = nbins / kThreads;   // 8 or 4
+    const int hi_bin = nbins - 1 - per * static_cast<int>(threadIdx.x);
+    int mine = 0;
+    for (int k = 0; k < per; ++k) mine += static_cast<int>(h[hi_bin - k]);
+    int tot;
+    const int ex = cta_exclusive_scan(mine, warp_sums, &tot);
+    if (ex < krem && ex + mine >= krem) {
+        int acc = ex, k = 0;
+        while (acc + static_cast<int>(h[hi_bin - k]) < krem) { acc += static_cast<int>(h[hi_bin - k]); ++k; }
+        *s_dig = static_cast<unsigned>(hi_bin - k);
+        *s_abv = acc;
+    }
+    __syncthreads();
+    *above = *s_abv;
+    const unsigned d = *s_dig;
+    __syncthreads();
+    return d;
+}
+
+// load a block's global histogram into shared memory
+__device__ __forceinline__ void load_hist(unsigned* h, const unsigned* g, int nbins) {
+    for (int i = threadIdx.x; i < nbins; i += kThreads) h[i] = __ldcg(g + i);
+    __syncthreads();
+}
+// add this CTA's nonzero bins to the block's global histogram, then clear
+__device__ __forceinline__ void flush_hist(unsigned* h, unsigned* g, int nbins) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbins; i += kThreads) {
+        const unsigned v = h[i];
+        if (v) atomicAdd(g + i, v);
+    }
+}
+
+// ---- compaction / EF update of one selected row --------------------------------
+struct Quad {
+    float v[4];
+};
+__device__ __forceinline__ Quad load_quad(const float* p, bool vec4, int nvalid) {
+    Quad x;
+    if (vec4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        x.v[0] = t.x; x.v[1] = t.y; x.v[2] = t.z; x.v[3] = t.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x.v[k] = k < nvalid ? p[k] : 0.0f;
+    }
+    return x;
+}
+__device__ __forceinline__ void store_quad(float* p, const Quad& x, bool vec4, int nvalid) {
+    if (vec4) {
+        *reinterpret_cast<float4*>(p) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < nvalid) p[k] = x.v[k];
+    }
+}
+
+__device__ __forceinline__ int row_valid_cols(const BlockDev& B, int p) {
+    const long long rest = B.len - static_cast<long long>(p) * B.n;
+    return rest < B.n ? static_cast<int>(rest) : B.n;
+}
+
+// One warp: row p of block B, the k-th selected row.  (DENSE blocks apply
+// eq:ef21m-1 here, since the sketch pass skips them — R11, R20.)
+__device__ void gather_row(const GatherLaunch& a, const BlockDev& B, int k, int p, int lane) {
+    constexpr int U = 2;   // quads per lane in flight
+    const int n = B.n;
+    const int nv = row_valid_cols(B, p);
+    const long long e0 = B.off + static_cast<long long>(p) * n;
+    const long long o0 = B.val_base + static_cast<long long>(k) * n;
+    const bool dense = B.kind == ARC_BLOCK_DENSE;
+    const bool vrow = B.vec && (o0 % 4 == 0);
+    const int nq = (n + 3) >> 2;
+    for (int f0 = 0; f0 < nq; f0 += 32 * U) {
+        int cnt[U], ocnt[U];
+        bool v4[U], ov4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int f = f0 + 32 * u + lane;
+            const int q = 4 * f;
+            cnt[u] = f < nq ? max(0, min(4, nv - q)) : 0;
+            ocnt[u] = f < nq ? max(0, min(4, n - q)) : 0;
+            v4[u] = B.vec && cnt[u] == 4;
+            ov4[u] = vrow && ocnt[u] == 4;
+        }
+        Quad A[U];
+        for (int i = 0; i < a.nodes_local; ++i) {
+            float* __restrict__ ph = a.nodes.h[i];
+            float* __restrict__ pg = a.nodes.g[i];
+            Quad hq[U], gq[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long e = e0 + 4 * (f0 + 32 * u + lane);
+                if (cnt[u] > 0) {
+                    gq[u] = load_quad(pg + e, v4[u], cnt[u]);
+                    if (dense) {
+                        const Quad hv = load_quad(ph + e, v4[u], cnt[u]);
+                        const Quad gr = load_quad(a.nodes.grad[i] + e, v4[u], cnt[u]);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) hq[u].v[kk] = fadd(fmul(a.ome, hv.v[kk]), fmul(a.eta, gr.v[kk]));
+                        store_quad(ph + e, hq[u], v4[u], cnt[u]);
+                    } else {
+                        hq[u] = load_quad(ph + e, v4[u], cnt[u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (ocnt[u] == 0) continue;
+                const long long e = e0 + 4 * (f0 + 32 * u + lane);
+                Quad c, gn;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    c.v[kk] = kk < cnt[u] ? fsub(hq[u].v[kk], gq[u].v[kk]) : 0.0f;   // C_i (+0 padding)
+                    gn.v[kk] = fadd(gq[u].v[kk], c.v[kk]);                             // R12
+                    A[u].v[kk] = (i == 0) ? c.v[kk] : fadd(A[u].v[kk], c.v[kk]);       // R9 node order
+                }
+                if (cnt[u] > 0) store_quad(pg + e, gn, v4[u], cnt[u]);
+                if (a.mode == 2)
+                    store_quad(a.values + static_cast<long long>(i) * a.sum_Kn + o0 + 4 * (f0 + 32 * u + lane), c,
+                               ov4[u] && (a.sum_Kn % 4 == 0), ocnt[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (ocnt[u] == 0) continue;
+            const int q = 4 * (f0 + 32 * u + lane);
+            if (a.mode == 0) {
+                const long long e = e0 + q;
+                Quad val, gb;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) val.v[kk] = kk < cnt[u] ? __fdiv_rn(A[u].v[kk], a.Nf) : 0.0f;   // R3
+                if (cnt[u] > 0) {
+                    gb = load_quad(a.gbar + e, v4[u], cnt[u]);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) gb.v[kk] = fadd(gb.v[kk], val.v[kk]);                    // R13
+                    store_quad(a.gbar + e, gb, v4[u], cnt[u]);
+                }
+                if (a.values != nullptr) store_quad(a.values + o0 + q, val, ov4[u], ocnt[u]);
+            } else if (a.mode == 1) {
+                store_quad(a.values + o0 + q, A[u], ov4[u], ocnt[u]);
+            }
+        }
+    }
+}
+
+constexpr int kMaxSliceRows = 4096;
+
+__global__ void __launch_bounds__(kThreads) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned sh[2048];                   // histogram
+    __shared__ unsigned s_keys[kMaxSliceRows];      // this slice's order keys
+    __shared__ int s_rows[kMaxSliceRows];           // this slice's selected rows (ascending)
+    __shared__ int warp_sums[32];
+    __shared__ unsigned s_dig;
+    __shared__ int s_abv;
+
+    const SliceItem it = s.items[blockIdx.x];
+    const BlockDev B = s.blocks[it.b];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lo = it.c * s.slice_rows, hi = min(B.m, lo + s.slice_rows), nk = hi - lo;
+    const bool arc = B.kind == ARC_BLOCK_ARC && B.K < B.m;
+    const long long bb = it.b;
+    const int sidx = B.slice_base + it.c;
+
+    // ------------------------------------------------ digit 1 (histogram given)
+    unsigned b1 = 0, b2 = 0, T = 0;
+    int krem = B.K;
+    if (arc) {
+        const float* __restrict__ sg = s.sigma + B.row_base + lo;
+        for (int i = tid; i < nk; i += kThreads) s_keys[i] = order_key(sg[i]);
+        load_hist(sh, s.hist1 + bb * kHist1Bins, kHist1Bins);
+        int above;
+        b1 = top_digit(sh, kHist1Bins, krem, warp_sums, &s_dig, &s_abv, &above);
+        krem -= above;
+        for (int i = tid; i < 2048; i += kThreads) sh[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < nk; i += kThreads) {
+            const unsigned key = s_keys[i];
+            if ((key >> 21) == b1) atomicAdd(&sh[(key >> 10) & 2047u], 1u);
+        }
+        flush_hist(sh, s.hist2 + bb * 2048, 2048);
+    }
+    grid.sync();
+    // ------------------------------------------------ digit 2
+    if (arc) {
+        if (it.c == 0)   // every slice has read the digit-1 histogram: reset it for the next step
+            for (int i = tid; i < kHist1Bins; i += kThreads) s.hist1[bb * kHist1Bins + i] = 0;
+        load_hist(sh, s.hist2 + bb * 2048, 2048);
+        int above;
+        b2 = top_digit(sh, 2048, krem, warp_sums, &s_dig, &s_abv, &above);
+        krem -= above;
+        const unsigned pre = (b1 << 11) | b2;        // key[31:10]
+        for (int i = tid; i < 1024; i += kThreads) sh[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < nk; i += kThreads) {
+            const unsigned key = s_keys[i];
+            if ((key >> 10) == pre) atomicAdd(&sh[key & 1023u], 1u);
+        }
+        flush_hist(sh, s.hist3 + bb * 1024, 1024);
+    }
+    grid.sync();
+    // ------------------------------------------------ digit 3, slice counts
+    int need_eq = 0;
+    if (arc) {
+        if (it.c == 0)
+            for (int i = tid; i < 2048; i += kThreads) s.hist2[bb * 2048 + i] = 0;
+        load_hist(sh, s.hist3 + bb * 1024, 1024);
+        int above;
+        const unsigned b3 = top_digit(sh, 1024, krem, warp_sums, &s_dig, &s_abv, &above);
+        T = (b1 << 21) | (b2 << 10) | b3;            // the K-th largest key
+        need_eq = krem - above;                      // keys == T to take, in row order
+        int gt = 0, eq = 0;
+        for (int i = tid; i < nk; i += kThreads) {
+            gt += s_keys[i] > T;
+            eq += s_keys[i] == T;
+        }
+        int tg, te;
+        cta_exclusive_scan(gt, warp_sums, &tg);
+        cta_exclusive_scan(eq, warp_sums, &te);
+        if (tid == 0) { s.slice_gt[sidx] = tg; s.slice_eq[sidx] = te; }
+    }
+    grid.sync();
+    // ------------------------------------------------ compaction, S4..S6
+    int nsel = 0;
+    int32_t* __restrict__ out = s.sel + B.sel_base;
+    if (arc) {
+        if (it.c == 0)
+            for (int i = tid; i < 1024; i += kThreads) s.hist3[bb * 1024 + i] = 0;
+        int gb = 0, eb = 0;                          // counts of the preceding slices of this block
+        for (int c = tid; c < it.c; c += kThreads) {
+            gb += __ldcg(s.slice_gt + B.slice_base + c);
+            eb += __ldcg(s.slice_eq + B.slice_base + c);
+        }
+        int gtot, etot;
+        cta_exclusive_scan(gb, warp_sums, &gtot);
+        cta_exclusive_scan(eb, warp_sums, &etot);
+        const int sel_before = gtot + min(etot, need_eq);
+        // kPer consecutive rows per thread, ascending
+        const int per = (s.slice_rows + kThreads - 1) / kThreads;
+        int my_eq = 0;
+        for (int k = 0; k < per; ++k) {
+            const int i = tid * per + k;
+            my_eq += (i < nk && s_keys[i] == T);
+        }
+        int eq_tot;
+        int eq_rank = etot + cta_exclusive_scan(my_eq, warp_sums, &eq_tot);
+        int my_sel = 0;
+        unsigned take_mask = 0;                      // per <= 16
+        for (int k = 0; k < per; ++k) {
+            const int i = tid * per + k;
+            bool t = false;
+            if (i < nk) {
+                const unsigned key = s_keys[i];
+                if (key > T) t = true;
+                else if (key == T) { t = eq_rank < need_eq; ++eq_rank; }
+            }
+            if (t) { take_mask |= 1u << k; ++my_sel; }
+        }
+        int pos = cta_exclusive_scan(my_sel, warp_sums, &nsel);
+        for (int k = 0; k < per; ++k) {
+            if (take_mask & (1u << k)) {
+                const int p = lo + tid * per + k;
+                out[sel_before + pos] = p;
+                s_rows[pos] = p;
+                ++pos;
+            }
+        }
+        __syncthreads();
+        // gather / EF update of this slice's rows: warp w takes rows w, w+8, ...
+        for (int j = warp; j < nsel; j += kThreads / 32) gather_row(ga, B, sel_before + j, s_rows[j], lane);
+    } else {
+        // identity selection: DENSE blocks and K = m
+        for (int p = lo + tid; p < hi; p += kThreads) out[p] = p;
+        for (int p = lo + warp; p < hi; p += kThreads / 32) gather_row(ga, B, p, p, lane);
+    }
+}
+
+}  // namespace
+
+int select_gather_resident_ctas() {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_gather, kThreads, 0);
+    return sms * (per_sm < 1 ? 1 : per_sm);
+}
+
+int select_max_slice_rows() { return kMaxSliceRows; }
+
+cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch& ga, cudaStream_t st) {
+    void* args[] = {const_cast<SelectGatherLaunch*>(&s), const_cast<GatherLaunch*>(&ga)};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_select_gather), dim3(s.num_items),
+                                       dim3(kThreads), args, 0, st);
+}
+
+}  // namespace arc

@@ -41,13 +41,16 @@ struct TileRegs {
     int nchunks;
     long long v_off;
     int row_base;
+    int b;
 };
 
 template <int W>
 __device__ __forceinline__ TileRegs tile_regs(const SketchLaunch& a, int li) {
     const Tile* T = a.tiles + li;
-    const BlockDev* B = a.blocks + __ldg(&T->b);
+    const int b = __ldg(&T->b);
+    const BlockDev* B = a.blocks + b;
     TileRegs t;
+    t.b = b;
     t.off = __ldg(&B->off);
     t.len = __ldg(&B->len);
     t.n = __ldg(&B->n);
@@ -80,12 +83,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
     constexpr int VS = 4 * RPT;                 // V row stride in smem (padded r)
     __shared__ __align__(16) float Ds[2][R][DS];
     __shared__ __align__(16) float Vs[2][W * VS];
+    __shared__ unsigned hist[kHist1Bins];       // digit-1 histogram of this CTA's Sigma (mode 0)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int crow = tid >> 2, jl = tid & 3;    // chain role (threads < 4R)
     const int list_begin = a.cta_begin[blockIdx.x], list_end = a.cta_begin[blockIdx.x + 1];
     if (list_begin >= list_end) return;
     const int r = a.r;
+    for (int i = tid; i < kHist1Bins; i += kThreads) hist[i] = 0;
+    // (the first __syncthreads of the main loop orders this before any use)
+    auto flush_hist = [&](int b) {               // all threads; after a __syncthreads
+        unsigned* gh = a.hist1 + static_cast<long long>(b) * kHist1Bins;
+        for (int i = tid; i < kHist1Bins; i += kThreads) {
+            const unsigned v = hist[i];
+            if (v) { atomicAdd(gh + i, v); hist[i] = 0; }
+        }
+    };
 
     // element e of this thread in a chunk -> (row, column within chunk)
     auto vrow = [&](int e) { return (e >> 2) * (8 * RPI) + warp * RPI + lane / LPR; };
@@ -255,9 +268,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
                 }
                 if (jl == 0 && live) {
                     a.sigma[tc.row_base + p] = sig;
+                    atomicAdd(&hist[order_key_dev(sig) >> kHist1Shift], 1u);   // digit-1 histogram
                     if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
                 }
             }
+        }
+        if (!more || tl.b != tc.b) {             // block boundary: publish the histogram
+            __syncthreads();
+            if (a.mode == 0) flush_hist(tc.b);
+            __syncthreads();
         }
         if (!more) break;
         if (nli != li) tc = tl;
