@@ -46,7 +46,7 @@ constexpr uint32_t kStatusNonfinite = 1u;
 constexpr int kHist1Bins = 2048;
 constexpr int kHist1Shift = 21;
 constexpr unsigned kHist1Mask = 0xFFE00000u;
-constexpr int kSliceMin = 1024;    // rows per selection slice (one CTA), at least
+constexpr int kSliceMin = 512;     // rows per selection slice (one CTA), at least
 
 struct SliceItem {
     int b;   // block

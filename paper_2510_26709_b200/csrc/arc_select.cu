@@ -91,7 +91,17 @@ __device__ __forceinline__ unsigned top_digit(const unsigned* h, int nbins, int 
 
 // load a block's global histogram into shared memory
 __device__ __forceinline__ void load_hist(unsigned* h, const unsigned* g, int nbins) {
-    for (int i = threadIdx.x; i < nbins; i += kThreads) h[i] = __ldcg(g + i);
+    unsigned v[8];   // nbins / kThreads <= 8 loads in flight per thread
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x + k * kThreads;
+        v[k] = i < nbins ? __ldcg(g + i) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x + k * kThreads;
+        if (i < nbins) h[i] = v[k];
+    }
     __syncthreads();
 }
 // add this CTA's nonzero bins to the block's global histogram, then clear
@@ -133,54 +143,61 @@ __device__ __forceinline__ int row_valid_cols(const BlockDev& B, int p) {
     return rest < B.n ? static_cast<int>(rest) : B.n;
 }
 
-// One warp: row p of block B, the k-th selected row.  (DENSE blocks apply
-// eq:ef21m-1 here, since the sketch pass skips them — R11, R20.)
-__device__ void gather_row(const GatherLaunch& a, const BlockDev& B, int k, int p, int lane) {
-    constexpr int U = 2;   // quads per lane in flight
+// The CTA's selected rows (rows[j] is the (k0 + j)-th selected row of block B):
+// every (row, quad) pair is one item, spread over all threads with UN items
+// in flight per thread.  DENSE blocks apply eq:ef21m-1 here, since the sketch
+// pass skips them (R11, R20).
+__device__ void gather_rows(const GatherLaunch& a, const BlockDev& B, const int* rows, int k0, int nrows) {
+    constexpr int UN = 4;
     const int n = B.n;
-    const int nv = row_valid_cols(B, p);
-    const long long e0 = B.off + static_cast<long long>(p) * n;
-    const long long o0 = B.val_base + static_cast<long long>(k) * n;
-    const bool dense = B.kind == ARC_BLOCK_DENSE;
-    const bool vrow = B.vec && (o0 % 4 == 0);
     const int nq = (n + 3) >> 2;
-    for (int f0 = 0; f0 < nq; f0 += 32 * U) {
-        int cnt[U], ocnt[U];
-        bool v4[U], ov4[U];
+    const int items = nrows * nq;
+    const bool dense = B.kind == ARC_BLOCK_DENSE;
+    for (int base = 0; base < items; base += kThreads * UN) {
+        int cnt[UN], ocnt[UN];
+        long long e[UN], o[UN];
+        bool v4[UN], ov4[UN];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int f = f0 + 32 * u + lane;
-            const int q = 4 * f;
-            cnt[u] = f < nq ? max(0, min(4, nv - q)) : 0;
-            ocnt[u] = f < nq ? max(0, min(4, n - q)) : 0;
+        for (int u = 0; u < UN; ++u) {
+            const int item = base + u * kThreads + static_cast<int>(threadIdx.x);
+            cnt[u] = ocnt[u] = 0;
+            e[u] = o[u] = 0;
+            if (item < items) {
+                const int j = item / nq, f = item - j * nq;
+                const int p = rows[j], k = k0 + j;
+                const int q = 4 * f;
+                const int nv = row_valid_cols(B, p);
+                cnt[u] = max(0, min(4, nv - q));
+                ocnt[u] = min(4, n - q);
+                e[u] = B.off + static_cast<long long>(p) * n + q;
+                o[u] = B.val_base + static_cast<long long>(k) * n + q;
+            }
             v4[u] = B.vec && cnt[u] == 4;
-            ov4[u] = vrow && ocnt[u] == 4;
+            ov4[u] = B.vec && (o[u] % 4 == 0) && ocnt[u] == 4;
         }
-        Quad A[U];
+        Quad A[UN];
         for (int i = 0; i < a.nodes_local; ++i) {
             float* __restrict__ ph = a.nodes.h[i];
             float* __restrict__ pg = a.nodes.g[i];
-            Quad hq[U], gq[U];
+            Quad hq[UN], gq[UN];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const long long e = e0 + 4 * (f0 + 32 * u + lane);
+            for (int u = 0; u < UN; ++u) {
                 if (cnt[u] > 0) {
-                    gq[u] = load_quad(pg + e, v4[u], cnt[u]);
+                    gq[u] = load_quad(pg + e[u], v4[u], cnt[u]);
                     if (dense) {
-                        const Quad hv = load_quad(ph + e, v4[u], cnt[u]);
-                        const Quad gr = load_quad(a.nodes.grad[i] + e, v4[u], cnt[u]);
+                        const Quad hv = load_quad(ph + e[u], v4[u], cnt[u]);
+                        const Quad gr = load_quad(a.nodes.grad[i] + e[u], v4[u], cnt[u]);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) hq[u].v[kk] = fadd(fmul(a.ome, hv.v[kk]), fmul(a.eta, gr.v[kk]));
-                        store_quad(ph + e, hq[u], v4[u], cnt[u]);
+                        store_quad(ph + e[u], hq[u], v4[u], cnt[u]);
                     } else {
-                        hq[u] = load_quad(ph + e, v4[u], cnt[u]);
+                        hq[u] = load_quad(ph + e[u], v4[u], cnt[u]);
                     }
                 }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (ocnt[u] == 0) continue;
-                const long long e = e0 + 4 * (f0 + 32 * u + lane);
+            for (int u = 0; u < UN; ++u) {
+                if (ocnt[u] <= 0) continue;
                 Quad c, gn;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
@@ -188,30 +205,28 @@ __device__ void gather_row(const GatherLaunch& a, const BlockDev& B, int k, int 
                     gn.v[kk] = fadd(gq[u].v[kk], c.v[kk]);                             // R12
                     A[u].v[kk] = (i == 0) ? c.v[kk] : fadd(A[u].v[kk], c.v[kk]);       // R9 node order
                 }
-                if (cnt[u] > 0) store_quad(pg + e, gn, v4[u], cnt[u]);
+                if (cnt[u] > 0) store_quad(pg + e[u], gn, v4[u], cnt[u]);
                 if (a.mode == 2)
-                    store_quad(a.values + static_cast<long long>(i) * a.sum_Kn + o0 + 4 * (f0 + 32 * u + lane), c,
+                    store_quad(a.values + static_cast<long long>(i) * a.sum_Kn + o[u], c,
                                ov4[u] && (a.sum_Kn % 4 == 0), ocnt[u]);
             }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (ocnt[u] == 0) continue;
-            const int q = 4 * (f0 + 32 * u + lane);
+        for (int u = 0; u < UN; ++u) {
+            if (ocnt[u] <= 0) continue;
             if (a.mode == 0) {
-                const long long e = e0 + q;
                 Quad val, gb;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) val.v[kk] = kk < cnt[u] ? __fdiv_rn(A[u].v[kk], a.Nf) : 0.0f;   // R3
                 if (cnt[u] > 0) {
-                    gb = load_quad(a.gbar + e, v4[u], cnt[u]);
+                    gb = load_quad(a.gbar + e[u], v4[u], cnt[u]);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) gb.v[kk] = fadd(gb.v[kk], val.v[kk]);                    // R13
-                    store_quad(a.gbar + e, gb, v4[u], cnt[u]);
+                    store_quad(a.gbar + e[u], gb, v4[u], cnt[u]);
                 }
-                if (a.values != nullptr) store_quad(a.values + o0 + q, val, ov4[u], ocnt[u]);
+                if (a.values != nullptr) store_quad(a.values + o[u], val, ov4[u], ocnt[u]);
             } else if (a.mode == 1) {
-                store_quad(a.values + o0 + q, A[u], ov4[u], ocnt[u]);
+                store_quad(a.values + o[u], A[u], ov4[u], ocnt[u]);
             }
         }
     }
@@ -219,7 +234,7 @@ __device__ void gather_row(const GatherLaunch& a, const BlockDev& B, int k, int 
 
 constexpr int kMaxSliceRows = 4096;
 
-__global__ void __launch_bounds__(kThreads) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
+__global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned sh[2048];                   // histogram
     __shared__ unsigned s_keys[kMaxSliceRows];      // this slice's order keys
@@ -230,7 +245,7 @@ __global__ void __launch_bounds__(kThreads) k_select_gather(const SelectGatherLa
 
     const SliceItem it = s.items[blockIdx.x];
     const BlockDev B = s.blocks[it.b];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int lo = it.c * s.slice_rows, hi = min(B.m, lo + s.slice_rows), nk = hi - lo;
     const bool arc = B.kind == ARC_BLOCK_ARC && B.K < B.m;
     const long long bb = it.b;
@@ -241,7 +256,19 @@ __global__ void __launch_bounds__(kThreads) k_select_gather(const SelectGatherLa
     int krem = B.K;
     if (arc) {
         const float* __restrict__ sg = s.sigma + B.row_base + lo;
-        for (int i = tid; i < nk; i += kThreads) s_keys[i] = order_key(sg[i]);
+        for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {   // 4 loads in flight per thread
+            float v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k * kThreads + tid;
+                v[k] = i < nk ? sg[i] : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k * kThreads + tid;
+                if (i < nk) s_keys[i] = order_key(v[k]);
+            }
+        }
         load_hist(sh, s.hist1 + bb * kHist1Bins, kHist1Bins);
         int above;
         b1 = top_digit(sh, kHist1Bins, krem, warp_sums, &s_dig, &s_abv, &above);
@@ -340,12 +367,12 @@ __global__ void __launch_bounds__(kThreads) k_select_gather(const SelectGatherLa
             }
         }
         __syncthreads();
-        // gather / EF update of this slice's rows: warp w takes rows w, w+8, ...
-        for (int j = warp; j < nsel; j += kThreads / 32) gather_row(ga, B, sel_before + j, s_rows[j], lane);
+        gather_rows(ga, B, s_rows, sel_before, nsel);      // S4 (+S5, S6) of this slice's rows
     } else {
         // identity selection: DENSE blocks and K = m
-        for (int p = lo + tid; p < hi; p += kThreads) out[p] = p;
-        for (int p = lo + warp; p < hi; p += kThreads / 32) gather_row(ga, B, p, p, lane);
+        for (int p = lo + tid; p < hi; p += kThreads) { out[p] = p; s_rows[p - lo] = p; }
+        __syncthreads();
+        gather_rows(ga, B, s_rows, lo, nk);
     }
 }
 
