@@ -125,6 +125,8 @@ class ArcTopK:
             from .dist import check_consistent, params_digest
             check_consistent(pg, params_digest(d, self.blocks, self.N, self.nodes_local, r, eta, seed, reduce))
             comm = nccl_comm_ptr(pg, self.device)
+        elif pg is not None and force_exchange:
+            comm = nccl_comm_ptr(pg, self.device)   # G = 1: the exchange path through a 1-rank communicator
         ctx = ctypes.c_void_p()
         L.check(self.lib.arc_topk_create(ctypes.byref(self.params), comm, int(self.workspace.data_ptr()),
                                           int(nbytes.value), _stream_handle(stream), ctypes.byref(ctx)),

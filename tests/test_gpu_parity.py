@@ -41,13 +41,13 @@ def assert_same_floats(gpu: np.ndarray, ref: np.ndarray, what: str):
 
 
 def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, reduce="nccl",
-               force_exchange=False, check_debug=True, host=False, nodes_local=None):
+               force_exchange=False, check_debug=True, host=False, nodes_local=None, pg=None):
     from paper_2510_26709_b200 import ArcTopK
     nl = N if nodes_local is None else nodes_local
     assert nl == N, "single-GPU parity: all nodes local"
     src = GradientSource(d, blocks, N, seed=seed) if grads_fn is None else None
     ctx = ArcTopK(d, blocks, N=N, eta=eta, r=r, seed=seed, nodes_local=nl, reduce=reduce,
-                  debug_sketch=check_debug, force_exchange=force_exchange, host_staging=host)
+                  debug_sketch=check_debug, force_exchange=force_exchange, host_staging=host, pg=pg)
     o = orc.OracleEF21M(d, blocks, N=N, eta=eta, r=r, seed=seed)
     h = [torch.zeros(d, device=DEV) for _ in range(N)]
     g = [torch.zeros(d, device=DEV) for _ in range(N)]
@@ -169,6 +169,24 @@ def test_exchange_kernels_single_gpu(orc, reduce):
     """The G > 1 kernel sequence (per-node sketch export, ordered node-sum reduce,
     wire gather, scatter) run with G = 1 (copies instead of NCCL): bit-exact."""
     run_parity(orc, 50_000, flat_blocks(50_000, 96, K=40), N=4, steps=3, reduce=reduce, force_exchange=True)
+
+
+@pytest.mark.parametrize("reduce", ["nccl", "ordered"])
+def test_exchange_through_nccl_one_rank(orc, reduce):
+    """The exchange path with a real NCCL communicator borrowed from a 1-rank torch
+    ProcessGroupNCCL (dlopen'd libnccl, ncclAllGather of the per-node sketches and
+    of the ordered wire): bit-exact against the oracle."""
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        run_parity(orc, 30_000, flat_blocks(30_000, 128, K=21), N=2, steps=3, reduce=reduce, force_exchange=True,
+                   pg=dist.group.WORLD)
+    finally:
+        pass
 
 
 def test_host_staging_entry(orc):
