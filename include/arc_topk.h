@@ -136,7 +136,8 @@ typedef enum {
     ARC_Q_V = 0,        /* float [sum_ARC n_b * r]       V_b row-major, blocks in order        */
     ARC_Q_SIGMA = 1,    /* float [sum_ARC m_b]           Sigma per ARC block row               */
     ARC_Q_SEL = 2,      /* int32 [sum_b K_b]             I_b                                   */
-    ARC_Q_P_NODES = 3   /* float [sum_ARC m_b][nodes_local][r]  P_i (needs DEBUG_SKETCH, or G>1) */
+    ARC_Q_P_NODES = 3,  /* float [sum_ARC m_b][nodes_local][r]  P_i (needs DEBUG_SKETCH, or G>1) */
+    ARC_Q_CANDIDATES = 4 /* uint32 [num_blocks] rows sharing the boundary bin of the last selection */
 } arc_query;
 arc_status arc_topk_query(arc_topk_ctx* ctx, int32_t what, void* dst, size_t bytes, void* stream);
 
@@ -162,6 +163,12 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* ctx);
 #define ARC_TIMING_PHASES 6
 arc_status arc_topk_set_timing(arc_topk_ctx* ctx, int32_t enable);
 arc_status arc_topk_read_timing(arc_topk_ctx* ctx, float* ms, int32_t n_phases, int32_t* steps);
+
+/* Debug: per-CTA %globaltimer stamps (ns) at the phase boundaries of the last
+ * step's select/gather kernel, when the context was created with the
+ * environment variable ARC_DEBUG_STAMPS=1 (else ARC_ERR_INVALID_ARG).  Copies
+ * min(n, grid * 8) uint64 values into host memory (synchronises). */
+arc_status arc_topk_debug_stamps(arc_topk_ctx* ctx, uint64_t* stamps_host, int64_t n, int32_t* grid);
 
 /* Frees the host context (synchronises first).  Never frees caller memory. */
 arc_status arc_topk_destroy(arc_topk_ctx* ctx);

@@ -24,12 +24,13 @@ REDUCE_NCCL, REDUCE_ORDERED = 0, 1
 # flags
 FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE = 0x1, 0x2, 0x4
 # arc_query
-Q_V, Q_SIGMA, Q_SEL, Q_P_NODES = 0, 1, 2, 3
+Q_V, Q_SIGMA, Q_SEL, Q_P_NODES, Q_CANDIDATES = 0, 1, 2, 3, 4
 
 EXPORTED = [
     "arc_topk_workspace_bytes", "arc_topk_create", "arc_topk_step", "arc_topk_step_host",
     "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_kernels_per_step",
     "arc_topk_destroy", "arc_topk_status_string", "arc_topk_set_timing", "arc_topk_read_timing",
+    "arc_topk_debug_stamps",
 ]
 TIMING_PHASES = 6
 PHASE_NAMES = ["vgen", "ef_sketch", "exchange1_reduce", "select_gather", "exchange2_scatter", "copy_out"]
@@ -79,6 +80,8 @@ def lib():
         L.arc_topk_kernels_per_step.restype = i32
         L.arc_topk_set_timing.argtypes = [vp, i32]
         L.arc_topk_read_timing.argtypes = [vp, P(ctypes.c_float), i32, P(i32)]
+        L.arc_topk_debug_stamps.argtypes = [vp, vp, i64, P(i32)]
+        L.arc_topk_debug_stamps.restype = ctypes.c_int
         L.arc_topk_destroy.argtypes = [vp]
         L.arc_topk_status_string.argtypes = [ctypes.c_int]
         L.arc_topk_status_string.restype = ctypes.c_char_p

@@ -181,7 +181,8 @@ class ArcTopK:
     def query(self, what: int, stream=None) -> torch.Tensor:
         shapes = {L.Q_V: (self.sum_nr_arc, torch.float32), L.Q_SIGMA: (self.sum_m_arc, torch.float32),
                   L.Q_SEL: (self.sum_K, torch.int32),
-                  L.Q_P_NODES: (self.sum_m_arc * self.nodes_local * self.r, torch.float32)}
+                  L.Q_P_NODES: (self.sum_m_arc * self.nodes_local * self.r, torch.float32),
+                  L.Q_CANDIDATES: (len(self.blocks), torch.int32)}
         n, dt = shapes[what]
         out = torch.empty(max(n, 1), dtype=dt, device=self.device)
         L.check(self.lib.arc_topk_query(self.ctx, int(what), int(out.data_ptr()), out.numel() * out.element_size(),

@@ -67,7 +67,7 @@ struct Plan {
     size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
            o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
            o_vals = 0, o_hash = 0, o_hist1 = 0, o_hist2 = 0, o_hist3 = 0, o_slice_gt = 0, o_slice_eq = 0,
-           o_items = 0, total = 0;
+           o_items = 0, o_cand = 0, o_cand_count = 0, total = 0;
 };
 
 arc_status validate(const arc_topk_params* p) {
@@ -164,6 +164,8 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_slice_gt = take(sizeof(int) * pl.num_slices);
     pl.o_slice_eq = take(sizeof(int) * pl.num_slices);
     pl.o_items = take(sizeof(SliceItem) * pl.items.size());
+    pl.o_cand = take(sizeof(unsigned) * 2 * 2 * kCandCap * p->num_blocks);
+    pl.o_cand_count = take(sizeof(unsigned) * 2 * p->num_blocks);
     pl.o_hash = take(sizeof(uint64_t) * (pl.G + 1));
     const size_t pn = sizeof(float) * static_cast<size_t>(M) * pl.L * p->r;
     pl.o_pnodes = pl.keep_pnodes ? take(pn) : 0;
@@ -288,6 +290,8 @@ struct arc_topk_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;   // (ARC_TIMING_PHASES + 1) per timed step
     int timed_steps = 0;
+    uint64_t step_count = 0;     // parity of the selection's double-buffered candidate counters
+    unsigned long long* stamps = nullptr;   // debug (ARC_DEBUG_STAMPS=1): library-owned device buffer
 
     template <class T> T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
 };
@@ -423,6 +427,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
             UPLOAD(c->pl.o_cta, cta_begin);
             UPLOAD(c->pl.o_selrows, rows);
             UPLOAD(c->pl.o_items, c->pl.items);
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_cand_count, 0, sizeof(unsigned) * 2 * c->p.num_blocks, s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist2, 0, sizeof(unsigned) * 2048 * c->p.num_blocks, s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist3, 0, sizeof(unsigned) * 1024 * c->p.num_blocks, s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_status, 0, 16, s));
@@ -452,6 +457,10 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         }
         for (uint64_t x : all)
             if (x != mine) { delete c; return ARC_ERR_PARAM_MISMATCH; }
+    }
+    if (const char* e = getenv("ARC_DEBUG_STAMPS")) {
+        if (e[0] == '1' && cudaMalloc(&c->stamps, sizeof(unsigned long long) * 8 * c->pl.items.size()) != cudaSuccess)
+            c->stamps = nullptr;
     }
     *out = c;
     return ARC_OK;
@@ -556,6 +565,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ga.eta = c->p.eta;
     ga.ome = c->ome;
     ga.Nf = c->Nf;
+    ga.N_int = c->p.N;
     ga.sum_Kn = pl.sumKn;
     const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
     float* wire = pl.exchange ? c->at<float>(pl.o_wire) : nullptr;
@@ -579,7 +589,12 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.hist3 = c->at<unsigned>(pl.o_hist3);
         sg.slice_gt = c->at<int>(pl.o_slice_gt);
         sg.slice_eq = c->at<int>(pl.o_slice_eq);
+        sg.cand = c->at<unsigned>(pl.o_cand);
+        sg.cand_count = c->at<unsigned>(pl.o_cand_count);
+        sg.num_blocks = c->p.num_blocks;
+        sg.parity = static_cast<int>(c->step_count & 1);
         sg.sel = sel;
+        sg.stamps = c->stamps;
         if (launch_select_gather(sg, ga, s) != cudaSuccess) {
             (void)cudaGetLastError();
             return ARC_ERR_CUDA;
@@ -623,6 +638,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         ARC_CUDA(cudaMemcpyAsync(sel_out, sel, sizeof(int32_t) * pl.sumK, cudaMemcpyDeviceToDevice, s));
     ARC_MARK(6);
     if (c->timing) ++c->timed_steps;
+    ++c->step_count;
     return ARC_OK;
 }
 
@@ -669,6 +685,10 @@ arc_status arc_topk_query(arc_topk_ctx* c, int32_t what, void* dst, size_t bytes
             if (!pl.keep_pnodes) return ARC_ERR_INVALID_ARG;
             off = pl.o_pnodes;
             need = sizeof(float) * static_cast<size_t>(pl.M) * pl.L * c->p.r;
+            break;
+        case ARC_Q_CANDIDATES:   // counters of the last step's parity
+            off = pl.o_cand_count + sizeof(unsigned) * c->p.num_blocks * ((c->step_count + 1) & 1);
+            need = sizeof(unsigned) * c->p.num_blocks;
             break;
         default: return ARC_ERR_INVALID_ARG;
     }
@@ -732,9 +752,19 @@ arc_status arc_topk_get_status(arc_topk_ctx* c, uint32_t* flags) {
     return (st & kStatusNonfinite) ? ARC_ERR_NONFINITE : ARC_OK;
 }
 
+arc_status arc_topk_debug_stamps(arc_topk_ctx* c, uint64_t* stamps_host, int64_t n, int32_t* grid) {
+    if (c == nullptr || c->stamps == nullptr || stamps_host == nullptr) return ARC_ERR_INVALID_ARG;
+    const int64_t all = static_cast<int64_t>(c->pl.items.size()) * 8;
+    ARC_CUDA(cudaStreamSynchronize(c->last));
+    ARC_CUDA(cudaMemcpy(stamps_host, c->stamps, sizeof(uint64_t) * (n < all ? n : all), cudaMemcpyDeviceToHost));
+    if (grid) *grid = static_cast<int32_t>(c->pl.items.size());
+    return ARC_OK;
+}
+
 arc_status arc_topk_destroy(arc_topk_ctx* c) {
     if (c == nullptr) return ARC_ERR_INVALID_ARG;
     cudaStreamSynchronize(c->last);
+    if (c->stamps) cudaFree(c->stamps);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
     return ARC_OK;

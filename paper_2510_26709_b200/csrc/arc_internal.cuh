@@ -47,6 +47,7 @@ constexpr int kHist1Bins = 2048;
 constexpr int kHist1Shift = 21;
 constexpr unsigned kHist1Mask = 0xFFE00000u;
 constexpr int kSliceMin = 512;     // rows per selection slice (one CTA), at least
+constexpr int kCandCap = 2048;     // boundary-bin candidates per block resolved in every CTA
 
 struct SliceItem {
     int b;   // block
@@ -63,9 +64,14 @@ struct SelectGatherLaunch {
     unsigned* hist1;               // [num_blocks][2048] digit key[31:21] (filled by the Sigma pass)
     unsigned* hist2;               // [num_blocks][2048] digit key[20:10]
     unsigned* hist3;               // [num_blocks][1024] digit key[9:0]
-    int* slice_gt;                 // [num_slices] keys > T
+    int* slice_gt;                 // [num_slices] keys > T (or above digit-1 bin)
     int* slice_eq;                 // [num_slices] keys == T
+    unsigned* cand;                // [2][num_blocks][2 * kCandCap] boundary-bin candidates (key | row)
+    unsigned* cand_count;          // [2][num_blocks]
+    int num_blocks;
+    int parity;                    // step parity: selects this step's candidate buffers
     int32_t* sel;
+    unsigned long long* stamps;    // debug: [grid][8] %globaltimer at phase boundaries, or nullptr
 };
 
 struct NodePtrs {
@@ -118,6 +124,7 @@ struct GatherLaunch {
     int nodes_local;
     float eta, ome;     // DENSE blocks: the momentum update happens here (no sketch pass)
     float Nf;
+    int N_int;          // N as an integer (power-of-two test for A / N)
     float* gbar;        // mode 0: updated ; mode 1: nullptr
     float* values;      // mode 0: optional A/N ; mode 1: the wire (local pre-sum or per-node)
     int mode;           // 0 = fused local (G==1); 1 = wire pre-sum; 2 = wire per node [nodes_local][sumKn]

@@ -143,48 +143,59 @@ __device__ __forceinline__ int row_valid_cols(const BlockDev& B, int p) {
     return rest < B.n ? static_cast<int>(rest) : B.n;
 }
 
-// The CTA's selected rows (rows[j] is the (k0 + j)-th selected row of block B):
-// every (row, quad) pair is one item, spread over all threads with UN items
-// in flight per thread.  DENSE blocks apply eq:ef21m-1 here, since the sketch
-// pass skips them (R11, R20).
-__device__ void gather_rows(const GatherLaunch& a, const BlockDev& B, const int* rows, int k0, int nrows) {
-    constexpr int UN = 4;
-    const int n = B.n;
-    const int nq = (n + 3) >> 2;
-    const int items = nrows * nq;
-    const bool dense = B.kind == ARC_BLOCK_DENSE;
+// Balanced S4 (+S5, S6): the selected rows of every block cut into segments of
+// kSegQuads quads (host table), CTA b processes segments [seg0, seg1); every
+// (segment, quad) pair is one item, kThreads * UN items in flight per pass.
+// A / N: for N a power of two the product with the exact reciprocal is the
+// same correctly rounded value as the quotient (R3), and much cheaper.
+__device__ __forceinline__ float div_N(float A, float Nf, float invN, bool pow2) {
+    return pow2 ? fmul(A, invN) : __fdiv_rn(A, Nf);
+}
+
+template <int UN>
+__device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const SelRow* pre) {
+    const int items = (seg1 - seg0) * kSegQuads;
+    const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
+    const float invN = 1.0f / a.Nf;
     for (int base = 0; base < items; base += kThreads * UN) {
         int cnt[UN], ocnt[UN];
         long long e[UN], o[UN];
-        bool v4[UN], ov4[UN];
+        bool v4[UN], ov4[UN], dense[UN];
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
             const int item = base + u * kThreads + static_cast<int>(threadIdx.x);
             cnt[u] = ocnt[u] = 0;
             e[u] = o[u] = 0;
+            v4[u] = ov4[u] = dense[u] = false;
             if (item < items) {
-                const int j = item / nq, f = item - j * nq;
-                const int p = rows[j], k = k0 + j;
+                const SelRow R = (base == 0 && pre != nullptr) ? pre[u] : a.rows[seg0 + item / kSegQuads];
+                const BlockDev& B = a.blocks[R.b];
+                const int f = R.q0 + item % kSegQuads;
                 const int q = 4 * f;
-                const int nv = row_valid_cols(B, p);
-                cnt[u] = max(0, min(4, nv - q));
-                ocnt[u] = min(4, n - q);
-                e[u] = B.off + static_cast<long long>(p) * n + q;
-                o[u] = B.val_base + static_cast<long long>(k) * n + q;
+                if (q < B.n) {
+                    const int p = __ldcg(a.sel + B.sel_base + R.k);
+                    const int nv = row_valid_cols(B, p);
+                    cnt[u] = max(0, min(4, nv - q));
+                    ocnt[u] = min(4, B.n - q);
+                    e[u] = B.off + static_cast<long long>(p) * B.n + q;
+                    o[u] = B.val_base + static_cast<long long>(R.k) * B.n + q;
+                    v4[u] = B.vec && cnt[u] == 4;
+                    ov4[u] = B.vec && (o[u] % 4 == 0) && ocnt[u] == 4;
+                    dense[u] = B.kind == ARC_BLOCK_DENSE;
+                }
             }
-            v4[u] = B.vec && cnt[u] == 4;
-            ov4[u] = B.vec && (o[u] % 4 == 0) && ocnt[u] == 4;
         }
-        Quad A[UN];
+        Quad A[UN], gb[UN];
         for (int i = 0; i < a.nodes_local; ++i) {
             float* __restrict__ ph = a.nodes.h[i];
             float* __restrict__ pg = a.nodes.g[i];
             Quad hq[UN], gq[UN];
 #pragma unroll
             for (int u = 0; u < UN; ++u) {
+                if (i == 0 && a.mode == 0 && cnt[u] > 0) gb[u] = load_quad(a.gbar + e[u], v4[u], cnt[u]);
                 if (cnt[u] > 0) {
                     gq[u] = load_quad(pg + e[u], v4[u], cnt[u]);
-                    if (dense) {
+                    if (dense[u]) {   // DENSE block: eq:ef21m-1 here (R11, R20)
                         const Quad hv = load_quad(ph + e[u], v4[u], cnt[u]);
                         const Quad gr = load_quad(a.nodes.grad[i] + e[u], v4[u], cnt[u]);
 #pragma unroll
@@ -215,14 +226,13 @@ __device__ void gather_rows(const GatherLaunch& a, const BlockDev& B, const int*
         for (int u = 0; u < UN; ++u) {
             if (ocnt[u] <= 0) continue;
             if (a.mode == 0) {
-                Quad val, gb;
+                Quad val;
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) val.v[kk] = kk < cnt[u] ? __fdiv_rn(A[u].v[kk], a.Nf) : 0.0f;   // R3
+                for (int kk = 0; kk < 4; ++kk) val.v[kk] = kk < cnt[u] ? div_N(A[u].v[kk], a.Nf, invN, pow2) : 0.0f;   // R3
                 if (cnt[u] > 0) {
-                    gb = load_quad(a.gbar + e[u], v4[u], cnt[u]);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) gb.v[kk] = fadd(gb.v[kk], val.v[kk]);                    // R13
-                    store_quad(a.gbar + e[u], gb, v4[u], cnt[u]);
+                    for (int kk = 0; kk < 4; ++kk) gb[u].v[kk] = fadd(gb[u].v[kk], val.v[kk]);              // R13
+                    store_quad(a.gbar + e[u], gb[u], v4[u], cnt[u]);
                 }
                 if (a.values != nullptr) store_quad(a.values + o[u], val, ov4[u], ocnt[u]);
             } else if (a.mode == 1) {
@@ -234,11 +244,64 @@ __device__ void gather_rows(const GatherLaunch& a, const BlockDev& B, const int*
 
 constexpr int kMaxSliceRows = 4096;
 
+// Candidate resolution on a small list in shared memory (every CTA of the block
+// computes the same result): T = the krem-th largest key among the candidates
+// (digits key[20:10], key[9:0] below the common digit 1), and the row cutoff
+// P_eq among the candidates equal to T (the need_eq smallest rows are taken).
+__device__ void resolve_candidates(const unsigned* ck, const int* ci, int C, unsigned b1, int krem, unsigned* sh,
+                                   int* warp_sums, unsigned* s_dig, int* s_abv, unsigned* T_out, int* Peq_out) {
+    const int tid = threadIdx.x;
+    unsigned prefix = b1 << 21, pmask = 0xFFE00000u;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int shift = pass == 0 ? 10 : 0, nbins = pass == 0 ? 2048 : 1024;
+        for (int i = tid; i < nbins; i += kThreads) sh[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < C; i += kThreads)
+            if ((ck[i] & pmask) == prefix) atomicAdd(&sh[(ck[i] >> shift) & (nbins - 1)], 1u);
+        __syncthreads();
+        int above;
+        const unsigned d = top_digit(sh, nbins, krem, warp_sums, s_dig, s_abv, &above);
+        prefix |= d << shift;
+        pmask |= static_cast<unsigned>(nbins - 1) << shift;
+        krem -= above;
+    }
+    const unsigned T = prefix;
+    const int need_eq = krem;
+    int eq_local = 0;
+    for (int i = tid; i < C; i += kThreads) eq_local += ck[i] == T;
+    int E;
+    cta_exclusive_scan(eq_local, warp_sums, &E);
+    int P_eq = 0x7FFFFFFF;                           // every key == T is taken
+    if (need_eq < E) {
+        // the equal key whose row has exactly need_eq - 1 equal keys at smaller rows
+        for (int i = tid; i < C; i += kThreads) {
+            if (ck[i] != T) continue;
+            int rank = 0;
+            for (int j = 0; j < C; ++j) rank += (ck[j] == T && ci[j] < ci[i]);
+            if (rank == need_eq - 1) *s_abv = ci[i];
+        }
+        __syncthreads();
+        P_eq = *s_abv;
+        __syncthreads();
+    }
+    *T_out = T;
+    *Peq_out = P_eq;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
     cg::grid_group grid = cg::this_grid();
+#define STAMP(k) \
+    if (s.stamps != nullptr && threadIdx.x == 0) s.stamps[blockIdx.x * 8 + (k)] = globaltimer()
+    STAMP(0);
     __shared__ unsigned sh[2048];                   // histogram
     __shared__ unsigned s_keys[kMaxSliceRows];      // this slice's order keys
-    __shared__ int s_rows[kMaxSliceRows];           // this slice's selected rows (ascending)
+    __shared__ int s_rows[kMaxSliceRows];           // boundary-bin candidates (keys | rows)
     __shared__ int warp_sums[32];
     __shared__ unsigned s_dig;
     __shared__ int s_abv;
@@ -250,13 +313,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGathe
     const bool arc = B.kind == ARC_BLOCK_ARC && B.K < B.m;
     const long long bb = it.b;
     const int sidx = B.slice_base + it.c;
+    const int par = s.parity;
+    unsigned* ccount = s.cand_count + par * s.num_blocks;                 // this step's counters
+    unsigned* cand = s.cand + (static_cast<long long>(par) * s.num_blocks + bb) * (2 * kCandCap);
 
-    // ------------------------------------------------ digit 1 (histogram given)
-    unsigned b1 = 0, b2 = 0, T = 0;
+    // ------------------------------------------------ phase A
+    unsigned b1 = 0;
     int krem = B.K;
     if (arc) {
         const float* __restrict__ sg = s.sigma + B.row_base + lo;
-        for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {   // 4 loads in flight per thread
+        unsigned hv[8];                              // digit-1 histogram, loaded alongside the keys
+#pragma unroll
+        for (int k = 0; k < 8; ++k) hv[k] = __ldcg(s.hist1 + bb * kHist1Bins + tid + k * kThreads);
+        for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {
             float v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -269,82 +338,148 @@ __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGathe
                 if (i < nk) s_keys[i] = order_key(v[k]);
             }
         }
-        load_hist(sh, s.hist1 + bb * kHist1Bins, kHist1Bins);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sh[tid + k * kThreads] = hv[k];
+        __syncthreads();
         int above;
         b1 = top_digit(sh, kHist1Bins, krem, warp_sums, &s_dig, &s_abv, &above);
         krem -= above;
+        // keys above bin b1, the digit-2 histogram of bin b1 (fallback), candidates of bin b1
         for (int i = tid; i < 2048; i += kThreads) sh[i] = 0;
         __syncthreads();
+        int gt1 = 0, nc = 0;
         for (int i = tid; i < nk; i += kThreads) {
             const unsigned key = s_keys[i];
-            if ((key >> 21) == b1) atomicAdd(&sh[(key >> 10) & 2047u], 1u);
+            const unsigned d1 = key >> 21;
+            gt1 += d1 > b1;
+            if (d1 == b1) { ++nc; atomicAdd(&sh[(key >> 10) & 2047u], 1u); }
         }
+        // candidates of this slice: one global atomic for the CTA's whole run
+        int ctot;
+        int cpos = cta_exclusive_scan(nc, warp_sums, &ctot);
+        if (tid == 0) s_abv = ctot > 0 ? static_cast<int>(atomicAdd(ccount + bb, static_cast<unsigned>(ctot))) : 0;
+        __syncthreads();
+        cpos += s_abv;
+        for (int i = tid; i < nk && nc > 0; i += kThreads) {
+            const unsigned key = s_keys[i];
+            if ((key >> 21) == b1) {
+                if (cpos < kCandCap) { cand[cpos] = key; cand[kCandCap + cpos] = static_cast<unsigned>(lo + i); }
+                ++cpos;
+            }
+        }
+        int tg;
+        cta_exclusive_scan(gt1, warp_sums, &tg);
+        if (tid == 0) s.slice_gt[sidx] = tg;
         flush_hist(sh, s.hist2 + bb * 2048, 2048);
     }
-    grid.sync();
-    // ------------------------------------------------ digit 2
-    if (arc) {
-        if (it.c == 0)   // every slice has read the digit-1 histogram: reset it for the next step
-            for (int i = tid; i < kHist1Bins; i += kThreads) s.hist1[bb * kHist1Bins + i] = 0;
-        load_hist(sh, s.hist2 + bb * 2048, 2048);
-        int above;
-        b2 = top_digit(sh, 2048, krem, warp_sums, &s_dig, &s_abv, &above);
-        krem -= above;
-        const unsigned pre = (b1 << 11) | b2;        // key[31:10]
-        for (int i = tid; i < 1024; i += kThreads) sh[i] = 0;
-        __syncthreads();
-        for (int i = tid; i < nk; i += kThreads) {
-            const unsigned key = s_keys[i];
-            if ((key >> 10) == pre) atomicAdd(&sh[key & 1023u], 1u);
+    STAMP(1);
+    if (it.c == 0)   // next step's candidate counter of this block
+        for (int i = tid; i < 1; i += kThreads) s.cand_count[(par ^ 1) * s.num_blocks + bb] = 0;
+    grid.sync();                                     // ---------------- barrier 1
+    STAMP(2);
+    // any block with more candidates than fit takes the digit-by-digit path
+    // (uniform across the grid, so every CTA meets the same barriers)
+    bool overflow = false;
+    for (int b = tid; b < s.num_blocks; b += kThreads) overflow |= __ldcg(ccount + b) > static_cast<unsigned>(kCandCap);
+    // this block's candidates and the preceding slices' counts, loaded together
+    const int C = arc ? static_cast<int>(min(__ldcg(ccount + bb), static_cast<unsigned>(kCandCap))) : 0;
+    int before = 0;
+    if (arc)
+        for (int c = tid; c < it.c; c += kThreads) before += __ldcg(s.slice_gt + B.slice_base + c);
+    {
+        unsigned* ck = reinterpret_cast<unsigned*>(s_rows);
+        int* ci = s_rows + kCandCap;
+        for (int i = tid; i < C; i += kThreads) {
+            ck[i] = __ldcg(cand + i);
+            ci[i] = static_cast<int>(__ldcg(cand + kCandCap + i));
         }
-        flush_hist(sh, s.hist3 + bb * 1024, 1024);
     }
-    grid.sync();
-    // ------------------------------------------------ digit 3, slice counts
-    int need_eq = 0;
-    if (arc) {
-        if (it.c == 0)
-            for (int i = tid; i < 2048; i += kThreads) s.hist2[bb * 2048 + i] = 0;
-        load_hist(sh, s.hist3 + bb * 1024, 1024);
-        int above;
-        const unsigned b3 = top_digit(sh, 1024, krem, warp_sums, &s_dig, &s_abv, &above);
-        T = (b1 << 21) | (b2 << 10) | b3;            // the K-th largest key
-        need_eq = krem - above;                      // keys == T to take, in row order
-        int gt = 0, eq = 0;
-        for (int i = tid; i < nk; i += kThreads) {
-            gt += s_keys[i] > T;
-            eq += s_keys[i] == T;
+    overflow = __syncthreads_or(overflow);
+    STAMP(3);
+    unsigned T = 0;
+    int P_eq = 0x7FFFFFFF, need_eq = 0, sel_before = 0;
+    bool use_peq = true;
+    if (arc && it.c == 0)
+        for (int i = tid; i < kHist1Bins; i += kThreads) s.hist1[bb * kHist1Bins + i] = 0;
+    if (!overflow) {
+        if (arc) {
+            if (it.c == 0)
+                for (int i = tid; i < 2048; i += kThreads) s.hist2[bb * 2048 + i] = 0;
+            unsigned* ck = reinterpret_cast<unsigned*>(s_rows);
+            int* ci = s_rows + kCandCap;
+            resolve_candidates(ck, ci, C, b1, krem, sh, warp_sums, &s_dig, &s_abv, &T, &P_eq);
+            // rows selected before this slice: keys above bin b1 in earlier slices,
+            // plus the selected candidates at earlier rows
+            for (int i = tid; i < C; i += kThreads)
+                before += (ci[i] < lo && (ck[i] > T || (ck[i] == T && ci[i] <= P_eq)));
+            int tot;
+            cta_exclusive_scan(before, warp_sums, &tot);
+            sel_before = tot;
         }
-        int tg, te;
-        cta_exclusive_scan(gt, warp_sums, &tg);
-        cta_exclusive_scan(eq, warp_sums, &te);
-        if (tid == 0) { s.slice_gt[sidx] = tg; s.slice_eq[sidx] = te; }
+    } else {
+        // ---- digit by digit: digit 2 from the global histogram, digit 3 below
+        unsigned b2 = 0;
+        if (arc) {
+            load_hist(sh, s.hist2 + bb * 2048, 2048);
+            int above;
+            b2 = top_digit(sh, 2048, krem, warp_sums, &s_dig, &s_abv, &above);
+            krem -= above;
+            const unsigned pre = (b1 << 11) | b2;
+            for (int i = tid; i < 1024; i += kThreads) sh[i] = 0;
+            __syncthreads();
+            for (int i = tid; i < nk; i += kThreads)
+                if ((s_keys[i] >> 10) == pre) atomicAdd(&sh[s_keys[i] & 1023u], 1u);
+            flush_hist(sh, s.hist3 + bb * 1024, 1024);
+        }
+        grid.sync();                                 // ---------------- barrier 2
+        if (arc) {
+            if (it.c == 0)
+                for (int i = tid; i < 2048; i += kThreads) s.hist2[bb * 2048 + i] = 0;
+            load_hist(sh, s.hist3 + bb * 1024, 1024);
+            int above;
+            const unsigned b3 = top_digit(sh, 1024, krem, warp_sums, &s_dig, &s_abv, &above);
+            T = (b1 << 21) | (b2 << 10) | b3;
+            need_eq = krem - above;
+            int gt = 0, eq = 0;
+            for (int i = tid; i < nk; i += kThreads) {
+                gt += s_keys[i] > T;
+                eq += s_keys[i] == T;
+            }
+            int tg, te;
+            cta_exclusive_scan(gt, warp_sums, &tg);
+            cta_exclusive_scan(eq, warp_sums, &te);
+            if (tid == 0) { s.slice_gt[sidx] = tg; s.slice_eq[sidx] = te; }
+        }
+        grid.sync();                                 // ---------------- barrier 3
+        if (arc) {
+            if (it.c == 0)
+                for (int i = tid; i < 1024; i += kThreads) s.hist3[bb * 1024 + i] = 0;
+            int gb = 0, eb = 0;
+            for (int c = tid; c < it.c; c += kThreads) {
+                gb += __ldcg(s.slice_gt + B.slice_base + c);
+                eb += __ldcg(s.slice_eq + B.slice_base + c);
+            }
+            int gtot, etot;
+            cta_exclusive_scan(gb, warp_sums, &gtot);
+            cta_exclusive_scan(eb, warp_sums, &etot);
+            sel_before = gtot + min(etot, need_eq);
+            need_eq = max(0, need_eq - etot);        // quota left for this slice's equal keys
+            use_peq = false;
+        }
     }
-    grid.sync();
+    STAMP(4);
     // ------------------------------------------------ compaction, S4..S6
-    int nsel = 0;
     int32_t* __restrict__ out = s.sel + B.sel_base;
     if (arc) {
-        if (it.c == 0)
-            for (int i = tid; i < 1024; i += kThreads) s.hist3[bb * 1024 + i] = 0;
-        int gb = 0, eb = 0;                          // counts of the preceding slices of this block
-        for (int c = tid; c < it.c; c += kThreads) {
-            gb += __ldcg(s.slice_gt + B.slice_base + c);
-            eb += __ldcg(s.slice_eq + B.slice_base + c);
-        }
-        int gtot, etot;
-        cta_exclusive_scan(gb, warp_sums, &gtot);
-        cta_exclusive_scan(eb, warp_sums, &etot);
-        const int sel_before = gtot + min(etot, need_eq);
-        // kPer consecutive rows per thread, ascending
-        const int per = (s.slice_rows + kThreads - 1) / kThreads;
+        const int per = (s.slice_rows + kThreads - 1) / kThreads;   // consecutive rows per thread
         int my_eq = 0;
-        for (int k = 0; k < per; ++k) {
-            const int i = tid * per + k;
-            my_eq += (i < nk && s_keys[i] == T);
-        }
+        if (!use_peq)
+            for (int k = 0; k < per; ++k) {
+                const int i = tid * per + k;
+                my_eq += (i < nk && s_keys[i] == T);
+            }
         int eq_tot;
-        int eq_rank = etot + cta_exclusive_scan(my_eq, warp_sums, &eq_tot);
+        int eq_rank = use_peq ? 0 : cta_exclusive_scan(my_eq, warp_sums, &eq_tot);
         int my_sel = 0;
         unsigned take_mask = 0;                      // per <= 16
         for (int k = 0; k < per; ++k) {
@@ -353,27 +488,47 @@ __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGathe
             if (i < nk) {
                 const unsigned key = s_keys[i];
                 if (key > T) t = true;
-                else if (key == T) { t = eq_rank < need_eq; ++eq_rank; }
+                else if (key == T) {
+                    if (use_peq) t = lo + i <= P_eq;
+                    else { t = eq_rank < need_eq; ++eq_rank; }
+                }
             }
             if (t) { take_mask |= 1u << k; ++my_sel; }
         }
+        int nsel;
         int pos = cta_exclusive_scan(my_sel, warp_sums, &nsel);
         for (int k = 0; k < per; ++k) {
             if (take_mask & (1u << k)) {
                 const int p = lo + tid * per + k;
                 out[sel_before + pos] = p;
-                s_rows[pos] = p;
                 ++pos;
             }
         }
-        __syncthreads();
-        gather_rows(ga, B, s_rows, sel_before, nsel);      // S4 (+S5, S6) of this slice's rows
     } else {
         // identity selection: DENSE blocks and K = m
-        for (int p = lo + tid; p < hi; p += kThreads) { out[p] = p; s_rows[p - lo] = p; }
-        __syncthreads();
-        gather_rows(ga, B, s_rows, lo, nk);
+        for (int p = lo + tid; p < hi; p += kThreads) out[p] = p;
     }
+    STAMP(5);
+    // S4 (+S5, S6): all selected-row segments spread evenly over the grid; the
+    // (static) segment descriptors of this thread's first items are fetched
+    // before the barrier
+    constexpr int UN = 4;
+    const long long S = ga.num_rows;
+    const int seg0 = static_cast<int>(S * blockIdx.x / gridDim.x);
+    const int seg1 = static_cast<int>(S * (blockIdx.x + 1) / gridDim.x);
+    SelRow pre[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+        const int item = u * kThreads + tid;
+        pre[u] = item < (seg1 - seg0) * kSegQuads ? ga.rows[seg0 + item / kSegQuads] : SelRow{0, 0, 0};
+    }
+    __threadfence();
+    grid.sync();                                     // ---------------- the selection is complete
+    STAMP(6);
+    gather_segments<UN>(ga, seg0, seg1, pre);
+    __syncthreads();
+    STAMP(7);
+#undef STAMP
 }
 
 }  // namespace
