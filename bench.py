@@ -191,6 +191,68 @@ def cpu_baseline_leg(d, blocks, L, budget_s=20.0):
                       f"{dt:.2f} s/step"}
 
 
+def run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, stream, barrier):
+    """Baselines measured in the same run, same gradients:
+    * dense_ef21m: EF21M with the identity compressor (one DENSE block: every row
+      kept, the value exchange is an All-Reduce of all d entries; P:89 "Dense 2mn");
+    * nccl_allreduce_d (G > 1): a bare ncclAllReduce of d fp32 per GPU;
+    * allgather_topk: vanilla EF21M with per-node row Top-K, whose
+      exchange is an All-Gather of K values rows plus K indices per node."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_26709_b200 import ArcTopK, Block
+    steps = max(3, min(args.steps, 50))
+    out = {}
+
+    def timed(fn):
+        for t in range(3):
+            fn(t)
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in range(steps):
+            fn(3 + k)
+        b.record(stream)
+        b.synchronize()
+        barrier()
+        ms = a.elapsed_time(b) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return {"ms_per_step": ms, "value": 4.0 * d * N / (ms * 1e-3) / 1e9, "unit": "GB/s", "steps": steps}
+
+    nd = 1024
+    md = -(-d // nd)
+    dense = [Block(0, d, md, nd, md, 1)]
+    hs = [torch.zeros(d, device=dev) for _ in range(L)]
+    gs = [torch.zeros(d, device=dev) for _ in range(L)]
+    gb = torch.zeros(d, device=dev)
+    ctx = ArcTopK(d, dense, N=N, eta=0.1, r=4, seed=20251030, nodes_local=L, pg=pg, rank=rank, reduce=args.reduce)
+    out["dense_ef21m"] = timed(lambda t: ctx.step(t, pool[t % pool_n], hs, gs, gb))
+    out["dense_ef21m"]["note"] = "identity compressor through the same library (DENSE block), fp32 All-Reduce of d"
+    ctx.close()
+    del hs, gs, gb
+    if world > 1:
+        buf = torch.zeros(d, device=dev)
+        out["nccl_allreduce_d"] = timed(lambda t: dist.all_reduce(buf))
+        out["nccl_allreduce_d"]["bus_GBps"] = 2 * (world - 1) / world * 4 * d / (out["nccl_allreduce_d"]["ms_per_step"] * 1e-3) / 1e9
+    try:
+        hs = [torch.zeros(d, device=dev) for _ in range(L)]
+        gs = [torch.zeros(d, device=dev) for _ in range(L)]
+        gb = torch.zeros(d, device=dev)
+        ctx = ArcTopK(d, blocks, N=N, eta=0.1, r=4, seed=20251030, nodes_local=L, pg=pg, rank=rank,
+                      method="topk_allgather")
+        out["allgather_topk"] = timed(lambda t: ctx.step(t, pool[t % pool_n], hs, gs, gb))
+        out["allgather_topk"]["note"] = "per-node exact row-norm Top-K, All-Gather of K n values + K indices per node"
+        ctx.close()
+    except Exception as e:  # not built yet / unsupported layout
+        out["allgather_topk"] = {"unavailable": str(e)[:200]}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,6 +265,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--pool", type=int, default=8, help="distinct gradient sets cycled in the timed loop")
+    ap.add_argument("--no-baselines", action="store_true")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     if args.impl == "reference":
@@ -327,6 +390,11 @@ def main():
     t_roof = ab["total"] / (peak * 1e9) + bus["total"] / (nvl_peak * 1e9)
     launches = ctx.kernels_per_step * args.steps
 
+    # ---------------------------------------------------------------- baselines (same run)
+    baselines = {}
+    if not args.no_baselines:
+        baselines = run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, stream, barrier)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_leg(d, blocks, L)
@@ -350,6 +418,7 @@ def main():
             "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
                               "hbm_bytes": ab["total"], "nvlink_bus_bytes": bus["total"]},
             "phases_ms": phase_ms,
+            "baselines": baselines,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 4 * d * L, "d2h_bytes_per_step": 4 * ctx.sum_K + 4 * ctx.sum_Kn},

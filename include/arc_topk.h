@@ -66,6 +66,14 @@ typedef enum {
     ARC_REDUCE_ORDERED = 1   /* exchange #2 = all-gather + ascending node-id sum: bit-exact gbar */
 } arc_reduce_mode;
 
+/* Compressor.  ARC_METHOD_TOPK_ALLGATHER is the baseline of Table I row "Top-K"
+ * (P:91): vanilla EF21M where every node keeps the K_b
+ * rows of ITS OWN residual with the largest exact ||row||^2 (ties -> smaller
+ * row), g_i <- g_i + C_i on those rows, the nodes all-gather K_b n_b values +
+ * K_b indices each, and gbar <- gbar + C_j / N for j = 0 .. N-1 in node order.
+ * For it sel_out / values_out must be NULL (the payload is per node). */
+typedef enum { ARC_METHOD_ARC = 0, ARC_METHOD_TOPK_ALLGATHER = 1 } arc_method;
+
 /* flags */
 #define ARC_FLAG_HOST_STAGING   0x1u  /* reserve device staging for arc_topk_step_host          */
 #define ARC_FLAG_DEBUG_SKETCH   0x2u  /* keep P_i for arc_topk_query(ARC_Q_P_NODES)              */
@@ -95,7 +103,7 @@ typedef struct {
     int32_t  value_reduce;  /* arc_reduce_mode                                        */
     uint64_t seed;          /* shared base seed (R7), identical on every rank         */
     uint32_t flags;         /* ARC_FLAG_*                                             */
-    uint32_t reserved;      /* 0                                                      */
+    uint32_t method;        /* arc_method: ARC_METHOD_ARC (0) or the baseline below   */
 } arc_topk_params;
 
 /* Bytes of device workspace `create` needs for these params (host-only call). */

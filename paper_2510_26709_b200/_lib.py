@@ -23,6 +23,8 @@ BLOCK_ARC, BLOCK_DENSE = 0, 1
 REDUCE_NCCL, REDUCE_ORDERED = 0, 1
 # flags
 FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE = 0x1, 0x2, 0x4
+# arc_method
+METHOD_ARC, METHOD_TOPK_ALLGATHER = 0, 1
 # arc_query
 Q_V, Q_SIGMA, Q_SEL, Q_P_NODES, Q_CANDIDATES = 0, 1, 2, 3, 4
 
@@ -47,7 +49,7 @@ class ArcParams(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("d", ctypes.c_int64), ("r", ctypes.c_int32),
                 ("num_blocks", ctypes.c_int32), ("blocks", ctypes.POINTER(ArcBlock)),
                 ("eta", ctypes.c_float), ("value_reduce", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("method", ctypes.c_uint32)]
 
 
 class ArcError(RuntimeError):

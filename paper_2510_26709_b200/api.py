@@ -99,7 +99,7 @@ class ArcTopK:
     def __init__(self, d: int, blocks: Sequence, N: int, eta: float, r: int = 4, seed: int = 20251030,
                  nodes_local: int | None = None, pg=None, rank: int = 0, reduce: str = "nccl",
                  host_staging: bool = False, debug_sketch: bool = False, force_exchange: bool = False,
-                 device=None, stream=None):
+                 method: str = "arc", device=None, stream=None):
         self.lib = L.lib()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.d, self.N = int(d), int(N)
@@ -113,7 +113,9 @@ class ArcTopK:
         self.params = L.ArcParams(L.ABI_VERSION, self.N, self.nodes_local, int(rank), self.d, int(r),
                                   len(self.blocks), self._cblocks, float(eta),
                                   {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED}[reduce],
-                                  int(seed) & (2**64 - 1), flags, 0)
+                                  int(seed) & (2**64 - 1), flags,
+                                  {"arc": L.METHOD_ARC, "topk_allgather": L.METHOD_TOPK_ALLGATHER}[method])
+        self.method = method
         nbytes = ctypes.c_size_t()
         L.check(self.lib.arc_topk_workspace_bytes(ctypes.byref(self.params), ctypes.byref(nbytes)),
                 "arc_topk_workspace_bytes")

@@ -62,12 +62,19 @@ struct Plan {
     std::vector<SliceItem> items;
     int max_nR4 = 0;
     int max_tiles = 0;
-    std::vector<BlockDev> bdev;
+    std::vector<BlockDev> bdev;      // the caller's blocks
+    bool topk = false;               // ARC_METHOD_TOPK_ALLGATHER baseline
+    int64_t W = 0;                   // Top-K: payload words per node (sum K n values + sum K indices)
+    std::vector<BlockDev> sbdev;     // selection blocks: bdev, or (Top-K) one copy per local node
+    std::vector<SelRow> segs;        // gather segments over sbdev
+    std::vector<SelRow> segs_real;   // segments over bdev (scatter, Top-K merge)
+    bool dense_fast = false;         // DENSE blocks handled by k_dense (G == 1, ARC)
+    std::vector<int> dense_ids;
     // workspace offsets (bytes)
     size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
            o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
            o_vals = 0, o_hash = 0, o_hist1 = 0, o_hist2 = 0, o_hist3 = 0, o_slice_gt = 0, o_slice_eq = 0,
-           o_items = 0, o_cand = 0, o_cand_count = 0, total = 0;
+           o_items = 0, o_cand = 0, o_cand_count = 0, o_sblocks = 0, o_segs_real = 0, o_dense_ids = 0, total = 0;
 };
 
 arc_status validate(const arc_topk_params* p) {
@@ -82,6 +89,7 @@ arc_status validate(const arc_topk_params* p) {
     if (p->value_reduce != ARC_REDUCE_NCCL && p->value_reduce != ARC_REDUCE_ORDERED) return ARC_ERR_INVALID_ARG;
     if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
     if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE)) return ARC_ERR_INVALID_ARG;
+    if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER) return ARC_ERR_INVALID_ARG;
     int64_t pos = 0, M = 0, sumK = 0;
     for (int b = 0; b < p->num_blocks; ++b) {
         const arc_block& B = p->blocks[b];
@@ -126,12 +134,9 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         D.sel_base = static_cast<int>(sumK);
         D.val_base = sumKn;
         D.vec = (B.offset % 4 == 0) && (B.n % 4 == 0);
-        D.slice_base = pl.num_slices;
-        {
-            const int nsl = static_cast<int>((B.m + pl.slice_rows - 1) / pl.slice_rows);
-            for (int c = 0; c < nsl; ++c) pl.items.push_back(SliceItem{b, c});
-            pl.num_slices += nsl;
-        }
+        D.slice_base = 0;
+        D.node = 0;
+        D.pad_ = 0;
         if (B.kind == ARC_BLOCK_ARC) {
             M += B.m;
             sum_nr += B.n * p->r;
@@ -140,36 +145,81 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         }
         sumK += B.K;
         sumKn += B.K * B.n;
-        pl.num_segs += B.K * (((B.n + 3) / 4 + kSegQuads - 1) / kSegQuads);
+        const int nq = static_cast<int>((B.n + 3) / 4);
+        for (int64_t k = 0; k < B.K; ++k)
+            for (int q0 = 0; q0 < nq; q0 += kSegQuads) pl.segs_real.push_back(SelRow{b, static_cast<int>(k), q0});
     }
     pl.M = static_cast<int>(M);
     pl.sumK = sumK;
     pl.sumKn = sumKn;
     pl.sum_nr = sum_nr;
     pl.max_tiles = std::max(max_tiles, 1);
+    // selection blocks: one per (local node, block) for the Top-K baseline, whose
+    // nodes rank their own rows; the node's payload is [values | indices]
+    pl.topk = p->method == ARC_METHOD_TOPK_ALLGATHER;
+    pl.W = sumKn + sumK;
+    // every node local and ARC: DENSE blocks take the streaming kernel, not the selection
+    pl.dense_fast = !pl.topk && !pl.exchange;
+    for (int b = 0; b < p->num_blocks; ++b)
+        if (pl.dense_fast && pl.bdev[b].kind == ARC_BLOCK_DENSE) pl.dense_ids.push_back(b);
+    const int nl = pl.topk ? pl.L : 1;
+    for (int l = 0; l < nl; ++l) {
+        for (int b = 0; b < p->num_blocks; ++b) {
+            BlockDev S = pl.bdev[b];
+            if (pl.dense_fast && S.kind == ARC_BLOCK_DENSE) {   // keep indices aligned with bdev
+                S.slice_base = pl.num_slices;
+                pl.sbdev.push_back(S);
+                continue;
+            }
+            S.node = l;
+            if (pl.topk) {
+                S.row_base = l * pl.M + S.row_base;
+                S.sel_base = static_cast<int>(l * pl.W + sumKn + S.sel_base);
+                S.val_base = l * pl.W + S.val_base;
+            }
+            S.slice_base = pl.num_slices;
+            const int nsl = (S.m + pl.slice_rows - 1) / pl.slice_rows;
+            const int vb = static_cast<int>(pl.sbdev.size());
+            for (int c = 0; c < nsl; ++c) pl.items.push_back(SliceItem{vb, c});
+            pl.num_slices += nsl;
+            const int nq = (S.n + 3) / 4;
+            for (int k = 0; k < S.K; ++k)
+                for (int q0 = 0; q0 < nq; q0 += kSegQuads) pl.segs.push_back(SelRow{vb, k, q0});
+            pl.sbdev.push_back(S);
+        }
+    }
+    pl.num_segs = static_cast<int64_t>(pl.segs.size());
+    const int nsb = static_cast<int>(pl.sbdev.size());
 
     size_t off = 0;
     auto take = [&](size_t bytes) { const size_t o = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o; };
     pl.o_blocks = take(sizeof(BlockDev) * p->num_blocks);
+    pl.o_sblocks = take(sizeof(BlockDev) * nsb);
+    pl.o_segs_real = take(sizeof(SelRow) * pl.segs_real.size());
+    pl.o_dense_ids = take(sizeof(int) * pl.dense_ids.size());
     pl.o_tiles = take(sizeof(Tile) * pl.max_tiles);
     pl.o_cta = take(sizeof(int) * (kMaxGrid + 1));
     pl.o_selrows = take(sizeof(SelRow) * pl.num_segs);
     pl.o_V = take(sizeof(float) * sum_nr);
-    pl.o_sigma = take(sizeof(float) * std::max<int64_t>(M, 1));
+    pl.o_sigma = take(sizeof(float) * std::max<int64_t>(M * nl, 1));
     pl.o_sel = take(sizeof(int32_t) * sumK);
     pl.o_status = take(16);
-    pl.o_hist1 = take(sizeof(unsigned) * kHist1Bins * p->num_blocks);
-    pl.o_hist2 = take(sizeof(unsigned) * 2048 * p->num_blocks);
-    pl.o_hist3 = take(sizeof(unsigned) * 1024 * p->num_blocks);
+    pl.o_hist1 = take(sizeof(unsigned) * kHist1Bins * nsb);
+    pl.o_hist2 = take(sizeof(unsigned) * 2048 * nsb);
+    pl.o_hist3 = take(sizeof(unsigned) * 1024 * nsb);
     pl.o_slice_gt = take(sizeof(int) * pl.num_slices);
     pl.o_slice_eq = take(sizeof(int) * pl.num_slices);
     pl.o_items = take(sizeof(SliceItem) * pl.items.size());
-    pl.o_cand = take(sizeof(unsigned) * 2 * 2 * kCandCap * p->num_blocks);
-    pl.o_cand_count = take(sizeof(unsigned) * 2 * p->num_blocks);
+    pl.o_cand = take(sizeof(unsigned) * 2 * 2 * kCandCap * nsb);
+    pl.o_cand_count = take(sizeof(unsigned) * 2 * nsb);
     pl.o_hash = take(sizeof(uint64_t) * (pl.G + 1));
     const size_t pn = sizeof(float) * static_cast<size_t>(M) * pl.L * p->r;
     pl.o_pnodes = pl.keep_pnodes ? take(pn) : 0;
-    if (pl.exchange) {
+    if (pl.topk) {
+        pl.exchange = false;   // the baseline has its own exchange (all-gather of the payloads)
+        pl.o_wire = take(sizeof(float) * pl.W * pl.L);
+        pl.o_wire_all = pl.G > 1 ? take(sizeof(float) * pl.W * pl.L * pl.G) : 0;
+    } else if (pl.exchange) {
         pl.o_xrecv = take(pn * pl.G);
         const bool ordered = p->value_reduce == ARC_REDUCE_ORDERED;
         pl.o_wire = take(sizeof(float) * sumKn * (ordered ? pl.L : 1));
@@ -352,12 +402,12 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         int rows = kSliceMin;
         while (rows < select_max_slice_rows()) {
             int64_t n = 0;
-            for (const arc_block& B : c->blocks) n += (B.m + rows - 1) / rows;
+            for (const BlockDev& B : c->pl.sbdev) n += (B.m + rows - 1) / rows;
             if (n <= resident) break;
             rows *= 2;
         }
         int64_t n = 0;
-        for (const arc_block& B : c->blocks) n += (B.m + rows - 1) / rows;
+        for (const BlockDev& B : c->pl.sbdev) n += (B.m + rows - 1) / rows;
         if (n > resident) { delete c; return ARC_ERR_UNSUPPORTED; }
         const size_t total = c->pl.total;
         if (rows != kSliceMin) {
@@ -409,13 +459,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         for (const BlockDev& B : c->pl.bdev)
             if (B.kind == ARC_BLOCK_ARC) c->max_m = std::max(c->max_m, B.m);
     }
-    std::vector<SelRow> rows;
-    rows.reserve(static_cast<size_t>(c->pl.num_segs));
-    for (int b = 0; b < c->p.num_blocks; ++b) {
-        const int nq = static_cast<int>((c->blocks[b].n + 3) / 4);
-        for (int64_t k = 0; k < c->blocks[b].K; ++k)
-            for (int q0 = 0; q0 < nq; q0 += kSegQuads) rows.push_back(SelRow{b, static_cast<int>(k), q0});
-    }
+    const std::vector<SelRow>& rows = c->pl.segs;
 
 #define UPLOAD(off, vec) \
     if (!(vec).empty()) ARC_CUDA(cudaMemcpyAsync(c->ws + (off), (vec).data(), sizeof((vec)[0]) * (vec).size(), cudaMemcpyHostToDevice, s))
@@ -423,15 +467,18 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         arc_status st = ARC_OK;
         auto up = [&]() -> arc_status {
             UPLOAD(c->pl.o_blocks, c->pl.bdev);
+            UPLOAD(c->pl.o_sblocks, c->pl.sbdev);
+            UPLOAD(c->pl.o_segs_real, c->pl.segs_real);
+            UPLOAD(c->pl.o_dense_ids, c->pl.dense_ids);
             UPLOAD(c->pl.o_tiles, tiles);
             UPLOAD(c->pl.o_cta, cta_begin);
             UPLOAD(c->pl.o_selrows, rows);
             UPLOAD(c->pl.o_items, c->pl.items);
-            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_cand_count, 0, sizeof(unsigned) * 2 * c->p.num_blocks, s));
-            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist2, 0, sizeof(unsigned) * 2048 * c->p.num_blocks, s));
-            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist3, 0, sizeof(unsigned) * 1024 * c->p.num_blocks, s));
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_cand_count, 0, sizeof(unsigned) * 2 * c->pl.sbdev.size(), s));
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist2, 0, sizeof(unsigned) * 2048 * c->pl.sbdev.size(), s));
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist3, 0, sizeof(unsigned) * 1024 * c->pl.sbdev.size(), s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_status, 0, 16, s));
-            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist1, 0, sizeof(unsigned) * kHist1Bins * c->p.num_blocks, s));
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist1, 0, sizeof(unsigned) * kHist1Bins * c->pl.sbdev.size(), s));
             ARC_CUDA(cudaStreamSynchronize(s));
             return ARC_OK;
         };
@@ -502,10 +549,12 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     unsigned* status = c->at<unsigned>(pl.o_status);
     unsigned* hist1 = c->at<unsigned>(pl.o_hist1);
     const SelRow* rows = c->at<SelRow>(pl.o_selrows);
+    const BlockDev* sblocks = c->at<BlockDev>(pl.o_sblocks);
+    if (pl.topk && (sel_out != nullptr || values_out != nullptr)) return ARC_ERR_INVALID_ARG;
 
     ARC_MARK(0);
     // S0
-    if (pl.M > 0) {
+    if (pl.M > 0 && !pl.topk) {
         launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V, s);
         ARC_LAUNCHED();
     }
@@ -529,7 +578,9 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.sigma = sigma;
         a.hist1 = hist1;
         a.pnodes = pl.keep_pnodes ? c->at<float>(pl.o_pnodes) : nullptr;
-        a.mode = pl.exchange ? 1 : 0;
+        a.mode = pl.topk ? 2 : (pl.exchange ? 1 : 0);
+        a.M = pl.M;
+        a.num_blocks = c->p.num_blocks;
         a.shape = c->shape;
         a.status = status;
         ARC_MARK(1);
@@ -568,8 +619,13 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ga.N_int = c->p.N;
     ga.sum_Kn = pl.sumKn;
     const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
-    float* wire = pl.exchange ? c->at<float>(pl.o_wire) : nullptr;
-    if (!pl.exchange) {
+    float* wire = (pl.exchange || pl.topk) ? c->at<float>(pl.o_wire) : nullptr;
+    ga.blocks = sblocks;
+    if (pl.topk) {   // baseline: each node's payload [values | indices] in the wire
+        ga.mode = 3;
+        ga.values = wire;
+        ga.sel = reinterpret_cast<const int32_t*>(wire);
+    } else if (!pl.exchange) {
         ga.mode = 0;
         ga.gbar = gbar;
         ga.values = values_out;
@@ -579,7 +635,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     }
     {
         SelectGatherLaunch sg{};
-        sg.blocks = blocks;
+        sg.blocks = sblocks;
         sg.items = c->at<SliceItem>(pl.o_items);
         sg.num_items = static_cast<int>(pl.items.size());
         sg.slice_rows = pl.slice_rows;
@@ -591,17 +647,55 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.slice_eq = c->at<int>(pl.o_slice_eq);
         sg.cand = c->at<unsigned>(pl.o_cand);
         sg.cand_count = c->at<unsigned>(pl.o_cand_count);
-        sg.num_blocks = c->p.num_blocks;
+        sg.num_blocks = static_cast<int>(pl.sbdev.size());
         sg.parity = static_cast<int>(c->step_count & 1);
-        sg.sel = sel;
+        sg.sel = pl.topk ? reinterpret_cast<int32_t*>(wire) : sel;
         sg.stamps = c->stamps;
-        if (launch_select_gather(sg, ga, s) != cudaSuccess) {
+        if (sg.num_items > 0 && launch_select_gather(sg, ga, s) != cudaSuccess) {
             (void)cudaGetLastError();
             return ARC_ERR_CUDA;
         }
     }
+    if (!pl.dense_ids.empty()) {   // DENSE blocks, every node local: identity compressor, streaming
+        DenseLaunch dl{};
+        dl.blocks = blocks;
+        dl.dense_ids = c->at<int>(pl.o_dense_ids);
+        dl.num_dense = static_cast<int>(pl.dense_ids.size());
+        dl.nodes = np;
+        dl.nodes_local = L;
+        dl.eta = c->p.eta;
+        dl.ome = c->ome;
+        dl.Nf = c->Nf;
+        dl.N_int = c->p.N;
+        dl.gbar = gbar;
+        dl.values = values_out;
+        dl.sel = sel;
+        launch_dense(dl, s);
+        ARC_LAUNCHED();
+    }
     ARC_MARK(4);
-    if (pl.exchange) {   // exchange #2 + S6
+    if (pl.topk) {   // baseline: all-gather the payloads, merge them in node order
+        const float* all = wire;
+        if (pl.G > 1) {
+            float* dst = c->at<float>(pl.o_wire_all);
+            if (c->nccl.allGather(wire, dst, static_cast<size_t>(pl.W) * L, ncclFloat32, c->comm, s) != ncclSuccess)
+                return ARC_ERR_NCCL;
+            all = dst;
+        }
+        for (int j = 0; j < c->p.N; ++j) {
+            MergeLaunch ml{};
+            ml.blocks = blocks;
+            ml.rows = c->at<SelRow>(pl.o_segs_real);
+            ml.num_rows = static_cast<int>(pl.segs_real.size());
+            ml.values = all + static_cast<size_t>(j) * pl.W;
+            ml.idx = reinterpret_cast<const int32_t*>(all + static_cast<size_t>(j) * pl.W + pl.sumKn);
+            ml.Nf = c->Nf;
+            ml.N_int = c->p.N;
+            ml.gbar = gbar;
+            launch_topk_merge(ml, s);
+            ARC_LAUNCHED();
+        }
+    } else if (pl.exchange) {   // exchange #2 + S6
         const float* reduced = wire;
         if (!ordered) {
             if (c->comm != nullptr && pl.G > 1) {
@@ -620,8 +714,8 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         }
         ScatterLaunch sa{};
         sa.blocks = blocks;
-        sa.rows = rows;
-        sa.num_rows = static_cast<int>(pl.num_segs);
+        sa.rows = c->at<SelRow>(pl.o_segs_real);
+        sa.num_rows = static_cast<int>(pl.segs_real.size());
         sa.sel = sel;
         sa.wire = reduced;
         sa.mode = ordered ? 1 : 0;
@@ -663,6 +757,7 @@ arc_status arc_topk_step_host(arc_topk_ctx* c, int64_t t, const float* const* gr
         dgrad[i] = dst;
     }
     float* vals = c->at<float>(c->pl.o_vals);
+    if (c->pl.topk && (sel_host != nullptr || values_host != nullptr)) return ARC_ERR_INVALID_ARG;
     const arc_status st = run_step(c, t, dgrad, h, g, gbar, nullptr, values_host ? vals : nullptr, s);
     if (st != ARC_OK) return st;
     if (sel_host != nullptr)
@@ -711,8 +806,10 @@ arc_status arc_topk_sizes(const arc_topk_ctx* c, int64_t* sum_K, int64_t* sum_Kn
 int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     if (c == nullptr) return -1;
     const int arc = c->pl.M > 0 ? 2 : 0;   // vgen + ef_sketch
-    // vgen + ef_sketch, [sketch_reduce], select_gather, [scatter]
-    return arc + (c->pl.exchange && c->pl.M > 0 ? 1 : 0) + 1 + (c->pl.exchange ? 1 : 0);
+    // vgen + ef_sketch, [sketch_reduce], select_gather, [scatter]; Top-K: no vgen, N merges
+    if (c->pl.topk) return (c->pl.M > 0 ? 1 : 0) + 1 + c->p.N;
+    return arc + (c->pl.exchange && c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) +
+           (c->pl.dense_ids.empty() ? 0 : 1) + (c->pl.exchange ? 1 : 0);
 }
 
 arc_status arc_topk_set_timing(arc_topk_ctx* c, int32_t enable) {

@@ -19,6 +19,8 @@ struct BlockDev {
     long long val_base; // offset of the compact rows in values / wire
     int vec;            // rows 16-byte aligned: off % 4 == 0 && n % 4 == 0
     int slice_base;     // first selection slice of the block
+    int node;           // Top-K baseline: the local node whose own rows this selection block ranks
+    int pad_;
 };
 
 // A sketch tile: rows [row0, row0 + rows) of one ARC block, rows <= kTileRows.
@@ -97,7 +99,10 @@ struct SketchLaunch {
     float* sigma;      // mode 0: written
     unsigned* hist1;   // [num_blocks][kHist1Bins] digit-1 histogram of Sigma (mode 0)
     float* pnodes;     // [M][nodes_local][r] P_i, or nullptr (mode 0 without debug)
-    int mode;          // 0 = reduce locally -> sigma ; 1 = exchange (write pnodes only)
+    int mode;          // 0 = reduce locally -> sigma ; 1 = exchange (write pnodes only) ;
+                       // 2 = Top-K baseline: per-node exact ||row||^2 -> sigma[node][M]
+    int M;             // ARC rows (stride of the per-node sigma in mode 2)
+    int num_blocks;
     int shape;         // tile shape R x W: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128
     unsigned* status;
 };
@@ -127,7 +132,8 @@ struct GatherLaunch {
     int N_int;          // N as an integer (power-of-two test for A / N)
     float* gbar;        // mode 0: updated ; mode 1: nullptr
     float* values;      // mode 0: optional A/N ; mode 1: the wire (local pre-sum or per-node)
-    int mode;           // 0 = fused local (G==1); 1 = wire pre-sum; 2 = wire per node [nodes_local][sumKn]
+    int mode;           // 0 = fused local (G==1); 1 = wire pre-sum; 2 = wire per node [nodes_local][sumKn];
+                        // 3 = Top-K baseline: node B.node only, wire values at B.val_base
     long long sum_Kn;
 };
 
@@ -145,5 +151,33 @@ struct ScatterLaunch {
     float* values;          // optional A/N
 };
 void launch_scatter(const ScatterLaunch& a, cudaStream_t s);
+
+// DENSE blocks with every node on this GPU: one streaming pass (identity compressor).
+struct DenseLaunch {
+    const BlockDev* blocks;
+    const int* dense_ids;       // indices of the DENSE blocks
+    int num_dense;
+    NodePtrs nodes;
+    int nodes_local;
+    float eta, ome, Nf;
+    int N_int;
+    float* gbar;
+    float* values;              // optional
+    int32_t* sel;               // identity selection written here
+};
+void launch_dense(const DenseLaunch& a, cudaStream_t s);
+
+// Top-K baseline merge of one node's gathered payload: gbar[I_j] += C_j / N.
+struct MergeLaunch {
+    const BlockDev* blocks;     // real blocks
+    const SelRow* rows;         // segments over the real blocks
+    int num_rows;
+    const float* values;        // this node's values (block val_base offsets)
+    const int32_t* idx;         // this node's indices (block sel_base offsets)
+    float Nf;
+    int N_int;
+    float* gbar;
+};
+void launch_topk_merge(const MergeLaunch& a, cudaStream_t s);
 
 }  // namespace arc

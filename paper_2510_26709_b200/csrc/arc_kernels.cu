@@ -222,6 +222,110 @@ __global__ void __launch_bounds__(256) k_scatter(const ScatterLaunch a) {
     }
 }
 
+// =============================================================================
+// Top-K baseline (ARC_METHOD_TOPK_ALLGATHER), S6: node j's gathered rows
+// merged into the replicated tracker, gbar[I_j[k]] += C_j[k] / N (one launch per
+// node, in node order: the nodes' supports overlap).
+// =============================================================================
+__global__ void __launch_bounds__(256) k_topk_merge(const MergeLaunch a) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
+    const float invN = 1.0f / a.Nf;
+    for (int w = gw; w < a.num_rows; w += nw) {
+        const SelRow R = a.rows[w];
+        const BlockDev& B = a.blocks[R.b];
+        const int p = a.idx[B.sel_base + R.k];
+        const int n = B.n;
+        const int nv = row_valid_cols(B, p);
+        const long long e0 = B.off + static_cast<long long>(p) * n;
+        const long long o0 = B.val_base + static_cast<long long>(R.k) * n;
+        const int qend = min(nv, 4 * (R.q0 + kSegQuads));
+        for (int q = 4 * R.q0 + lane; q < qend; q += 32) {
+            const float v = a.values[o0 + q];
+            const float c = pow2 ? fmul(v, invN) : __fdiv_rn(v, a.Nf);   // R3: c / N
+            a.gbar[e0 + q] = fadd(a.gbar[e0 + q], c);
+        }
+    }
+}
+
+// =============================================================================
+// DENSE blocks (R20) when every node is on this GPU: the identity compressor
+// as one coalesced streaming pass per element e of the block:
+//   h_i <- (1-eta) h_i + eta grad_i ; C_i = h_i - g_i ; g_i <- g_i + C_i
+//   A = C_0 + C_1 + ... ; gbar <- gbar + A / N ; values[e] = A / N
+// (the same operations, in the same order, as the selected-row path).
+// =============================================================================
+__global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
+    const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
+    const float invN = 1.0f / a.Nf;
+    for (int db = 0; db < a.num_dense; ++db) {
+        const BlockDev& B = a.blocks[a.dense_ids[db]];
+        const long long len = B.len;
+        // identity selection
+        for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < B.m; p += (long long)gridDim.x * blockDim.x)
+            a.sel[B.sel_base + p] = static_cast<int32_t>(p);
+        // element loop: quads when the block is 16-byte aligned, else scalars
+        const bool vec = (B.off % 4) == 0;
+        const long long nq = vec ? len / 4 : 0;
+        for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < nq; f += (long long)gridDim.x * blockDim.x) {
+            const long long e = B.off + 4 * f;
+            float A[4];
+            for (int i = 0; i < a.nodes_local; ++i) {
+                const float4 hv = *reinterpret_cast<const float4*>(a.nodes.h[i] + e);
+                const float4 gr = __ldcs(reinterpret_cast<const float4*>(a.nodes.grad[i] + e));
+                const float4 gv = *reinterpret_cast<const float4*>(a.nodes.g[i] + e);
+                const float h4[4] = {hv.x, hv.y, hv.z, hv.w}, r4[4] = {gr.x, gr.y, gr.z, gr.w}, g4[4] = {gv.x, gv.y, gv.z, gv.w};
+                float hn[4], gn[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    hn[k] = fadd(fmul(a.ome, h4[k]), fmul(a.eta, r4[k]));   // R11
+                    const float c = fsub(hn[k], g4[k]);                      // R4
+                    gn[k] = fadd(g4[k], c);                                  // R12
+                    A[k] = (i == 0) ? c : fadd(A[k], c);                     // R9 node order
+                }
+                *reinterpret_cast<float4*>(a.nodes.h[i] + e) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+                *reinterpret_cast<float4*>(a.nodes.g[i] + e) = make_float4(gn[0], gn[1], gn[2], gn[3]);
+            }
+            const float4 bv = *reinterpret_cast<const float4*>(a.gbar + e);
+            const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
+            float v[4], bn[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[k] = pow2 ? fmul(A[k], invN) : __fdiv_rn(A[k], a.Nf);    // R3
+                bn[k] = fadd(b4[k], v[k]);                                   // R13
+            }
+            *reinterpret_cast<float4*>(a.gbar + e) = make_float4(bn[0], bn[1], bn[2], bn[3]);
+            if (a.values != nullptr)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) a.values[B.val_base + 4 * f + k] = v[k];
+        }
+        // scalar remainder (unaligned blocks, tails) and the padded tail of the values
+        const long long total = static_cast<long long>(B.m) * B.n;
+        for (long long q = 4 * nq + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+             q += (long long)gridDim.x * blockDim.x) {
+            if (q >= len) {
+                if (a.values != nullptr) a.values[B.val_base + q] = 0.0f;
+                continue;
+            }
+            const long long e = B.off + q;
+            float A = 0.0f;
+            for (int i = 0; i < a.nodes_local; ++i) {
+                const float hn = fadd(fmul(a.ome, a.nodes.h[i][e]), fmul(a.eta, a.nodes.grad[i][e]));
+                a.nodes.h[i][e] = hn;
+                const float gv = a.nodes.g[i][e];
+                const float c = fsub(hn, gv);
+                a.nodes.g[i][e] = fadd(gv, c);
+                A = (i == 0) ? c : fadd(A, c);
+            }
+            const float v = pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf);
+            a.gbar[e] = fadd(a.gbar[e], v);
+            if (a.values != nullptr) a.values[B.val_base + q] = v;
+        }
+    }
+}
+
 }  // namespace
 
 // ---- launchers ---------------------------------------------------------------
@@ -252,6 +356,14 @@ static int rows_grid(int num_rows) {
     if (grid < 1) grid = 1;
     if (grid > 148 * 16) grid = 148 * 16;
     return grid;
+}
+
+void launch_dense(const DenseLaunch& a, cudaStream_t s) {
+    k_dense<<<148 * 8, 256, 0, s>>>(a);
+}
+
+void launch_topk_merge(const MergeLaunch& a, cudaStream_t s) {
+    k_topk_merge<<<rows_grid(a.num_rows), 256, 0, s>>>(a);
 }
 
 void launch_scatter(const ScatterLaunch& a, cudaStream_t s) {

@@ -158,13 +158,14 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
     const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
     const float invN = 1.0f / a.Nf;
     for (int base = 0; base < items; base += kThreads * UN) {
-        int cnt[UN], ocnt[UN];
+        int cnt[UN], ocnt[UN], nd[UN];
         long long e[UN], o[UN];
         bool v4[UN], ov4[UN], dense[UN];
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
             const int item = base + u * kThreads + static_cast<int>(threadIdx.x);
             cnt[u] = ocnt[u] = 0;
+            nd[u] = -1;
             e[u] = o[u] = 0;
             v4[u] = ov4[u] = dense[u] = false;
             if (item < items) {
@@ -182,10 +183,13 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                     v4[u] = B.vec && cnt[u] == 4;
                     ov4[u] = B.vec && (o[u] % 4 == 0) && ocnt[u] == 4;
                     dense[u] = B.kind == ARC_BLOCK_DENSE;
+                    nd[u] = B.node;
                 }
             }
         }
         Quad A[UN], gb[UN];
+        // Top-K baseline (mode 3): a selection block belongs to one node (nd)
+        const bool per_node = a.mode == 3;
         for (int i = 0; i < a.nodes_local; ++i) {
             float* __restrict__ ph = a.nodes.h[i];
             float* __restrict__ pg = a.nodes.g[i];
@@ -193,7 +197,7 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
 #pragma unroll
             for (int u = 0; u < UN; ++u) {
                 if (i == 0 && a.mode == 0 && cnt[u] > 0) gb[u] = load_quad(a.gbar + e[u], v4[u], cnt[u]);
-                if (cnt[u] > 0) {
+                if (cnt[u] > 0 && (!per_node || nd[u] == i)) {
                     gq[u] = load_quad(pg + e[u], v4[u], cnt[u]);
                     if (dense[u]) {   // DENSE block: eq:ef21m-1 here (R11, R20)
                         const Quad hv = load_quad(ph + e[u], v4[u], cnt[u]);
@@ -208,13 +212,13 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
             }
 #pragma unroll
             for (int u = 0; u < UN; ++u) {
-                if (ocnt[u] <= 0) continue;
+                if (ocnt[u] <= 0 || (per_node && nd[u] != i)) continue;
                 Quad c, gn;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                     c.v[kk] = kk < cnt[u] ? fsub(hq[u].v[kk], gq[u].v[kk]) : 0.0f;   // C_i (+0 padding)
                     gn.v[kk] = fadd(gq[u].v[kk], c.v[kk]);                             // R12
-                    A[u].v[kk] = (i == 0) ? c.v[kk] : fadd(A[u].v[kk], c.v[kk]);       // R9 node order
+                    A[u].v[kk] = (i == 0 || per_node) ? c.v[kk] : fadd(A[u].v[kk], c.v[kk]);   // R9 node order
                 }
                 if (cnt[u] > 0) store_quad(pg + e[u], gn, v4[u], cnt[u]);
                 if (a.mode == 2)
@@ -235,8 +239,8 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                     store_quad(a.gbar + e[u], gb[u], v4[u], cnt[u]);
                 }
                 if (a.values != nullptr) store_quad(a.values + o[u], val, ov4[u], ocnt[u]);
-            } else if (a.mode == 1) {
-                store_quad(a.values + o[u], A[u], ov4[u], ocnt[u]);
+            } else if (a.mode == 1 || a.mode == 3) {
+                store_quad(a.values + o[u], A[u], ov4[u] && a.mode == 1, ocnt[u]);
             }
         }
     }

@@ -223,7 +223,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         // ------------------------------------------------------------ chains
         const bool live = crow < tc.m_rows;
         const int c0 = chunk * W;
-        if (crow < R) {
+        if (a.mode == 2) {
+            // Top-K baseline: lane 0 of the row sums Delta_q^2 in column order
+            if (crow < R && jl == 0) {
+                const int qmax = live ? min(W, row_cols(tc, crow) - c0) : 0;
+                const float* __restrict__ drow = &Ds[buf][crow][0];
+                for (int q = 0; q < qmax; ++q) acc[0] = fadd(acc[0], fmul(drow[q], drow[q]));
+            }
+        } else if (crow < R) {
             const int qmax = live ? min(W, row_cols(tc, crow) - c0) : 0;
             const float* __restrict__ drow = &Ds[buf][crow][0];
             const float* __restrict__ vb = &Vs[buf][jl];
@@ -244,7 +251,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         }
 
         // ------------------------------------------------ per-(tile, node) epilogue
-        if (chunk == tc.nchunks - 1) {
+        if (chunk == tc.nchunks - 1 && a.mode == 2) {
+            // Top-K baseline: this node's own ||row||^2 and its selection histogram
+            const int p = tc.row0 + crow;
+            if (jl == 0 && live) {
+                const float sig = acc[0];
+                a.sigma[static_cast<long long>(node) * a.M + tc.row_base + p] = sig;
+                atomicAdd(&a.hist1[(static_cast<long long>(node) * a.num_blocks + tc.b) * kHist1Bins +
+                                   (order_key_dev(sig) >> kHist1Shift)], 1u);
+                if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < RPT; ++s2) acc[s2] = 0.0f;
+        } else if (chunk == tc.nchunks - 1) {
             const int p = tc.row0 + crow;
 #pragma unroll
             for (int s = 0; s < RPT; ++s) {

@@ -235,3 +235,55 @@ def test_full_size_configs(orc, name, N, steps):
     against the oracle at full size."""
     d, blocks = config_blocks(name)
     run_parity(orc, d, blocks, N=N, steps=steps, seed=20251030, check_debug=True)
+
+
+# ------------------------------------------------------------------ All-Gather Top-K baseline
+
+@pytest.mark.parametrize("N,d,n,K", [(1, 50_000, 100, 7), (4, 60_000, 96, 12), (3, 4_097, 3, 40)])
+def test_topk_allgather_baseline(orc, N, d, n, K):
+    """The baseline of Table I row "Top-K": per-node exact row-norm Top-K,
+    g_i += C_i, gbar += C_j / N in node order — bit-exact against the oracle's
+    orc_step_topk, with overlapping supports across nodes."""
+    from paper_2510_26709_b200 import ArcTopK
+    blocks = flat_blocks(d, n, K=K)
+    src = GradientSource(d, blocks, N, seed=17)
+    ctx = ArcTopK(d, blocks, N=N, eta=0.3, seed=17, nodes_local=N, method="topk_allgather")
+    o = orc.OracleEF21M(d, blocks, N=N, eta=0.3, r=4, seed=17)
+    h = [torch.zeros(d, device=DEV) for _ in range(N)]
+    g = [torch.zeros(d, device=DEV) for _ in range(N)]
+    gbar = torch.zeros(d, device=DEV)
+    for t in range(4):
+        gr = [x.numpy() for x in src.grads(t)]
+        ctx.step(t, [torch.from_numpy(x).to(DEV) for x in gr], h, g, gbar)
+        o.step_topk(t, gr)
+    torch.cuda.synchronize()
+    for i in range(N):
+        assert_same_floats(h[i].cpu().numpy(), o.h[i], f"h[{i}]")
+        assert_same_floats(g[i].cpu().numpy(), o.g[i], f"g[{i}]")
+    assert_same_floats(gbar.cpu().numpy(), o.gbar, "gbar")
+    ctx.close()
+
+
+def test_topk_allgather_multiblock_dense(orc):
+    from paper_2510_26709_b200 import ArcTopK
+    shapes = [(300, 64, 5, 0), (13, 100, 13, 1), (77, 33, 4, 0)]
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n, m, n, K, kind))
+        off += m * n
+    N = 2
+    src = GradientSource(off, blocks, N, seed=3)
+    ctx = ArcTopK(off, blocks, N=N, eta=0.5, seed=3, nodes_local=N, method="topk_allgather")
+    o = orc.OracleEF21M(off, blocks, N=N, eta=0.5, r=4, seed=3)
+    h = [torch.zeros(off, device=DEV) for _ in range(N)]
+    g = [torch.zeros(off, device=DEV) for _ in range(N)]
+    gbar = torch.zeros(off, device=DEV)
+    for t in range(3):
+        gr = [x.numpy() for x in src.grads(t)]
+        ctx.step(t, [torch.from_numpy(x).to(DEV) for x in gr], h, g, gbar)
+        o.step_topk(t, gr)
+    torch.cuda.synchronize()
+    for i in range(N):
+        assert_same_floats(g[i].cpu().numpy(), o.g[i], f"g[{i}]")
+    assert_same_floats(gbar.cpu().numpy(), o.gbar, "gbar")
+    ctx.close()
