@@ -255,41 +255,51 @@ constexpr int kMaxSliceRows = 4096;
 __device__ void resolve_candidates(const unsigned* ck, const int* ci, int C, unsigned b1, int krem, unsigned* sh,
                                    int* warp_sums, unsigned* s_dig, int* s_abv, unsigned* T_out, int* Peq_out) {
     const int tid = threadIdx.x;
-    unsigned prefix = b1 << 21, pmask = 0xFFE00000u;
-    for (int pass = 0; pass < 2; ++pass) {
-        const int shift = pass == 0 ? 10 : 0, nbins = pass == 0 ? 2048 : 1024;
-        for (int i = tid; i < nbins; i += kThreads) sh[i] = 0;
-        __syncthreads();
-        for (int i = tid; i < C; i += kThreads)
-            if ((ck[i] & pmask) == prefix) atomicAdd(&sh[(ck[i] >> shift) & (nbins - 1)], 1u);
-        __syncthreads();
-        int above;
-        const unsigned d = top_digit(sh, nbins, krem, warp_sums, s_dig, s_abv, &above);
-        prefix |= d << shift;
-        pmask |= static_cast<unsigned>(nbins - 1) << shift;
-        krem -= above;
-    }
-    const unsigned T = prefix;
-    const int need_eq = krem;
-    int eq_local = 0;
-    for (int i = tid; i < C; i += kThreads) eq_local += ck[i] == T;
+    // digit 2 (key[20:10]) of the candidates
+    for (int i = tid; i < 2048; i += kThreads) sh[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < C; i += kThreads) atomicAdd(&sh[(ck[i] >> 10) & 2047u], 1u);
+    __syncthreads();
+    int above;
+    const unsigned b2 = top_digit(sh, 2048, krem, warp_sums, s_dig, s_abv, &above);
+    krem -= above;
+    const unsigned pre = (b1 << 11) | b2;            // key[31:10] of the K-th key
+    // the candidates of bin (b1, b2) — usually a handful — compacted into a
+    // short list (sh is free again), then ranked in the order (key desc, row asc):
+    // the krem-th one is (T, P_eq)
+    constexpr int kList = 1024;
+    unsigned* lk = sh;
+    int* li = reinterpret_cast<int*>(sh + kList);
+    int mine = 0;
+    for (int i = tid; i < C; i += kThreads) mine += (ck[i] >> 10) == pre;
     int E;
-    cta_exclusive_scan(eq_local, warp_sums, &E);
-    int P_eq = 0x7FFFFFFF;                           // every key == T is taken
-    if (need_eq < E) {
-        // the equal key whose row has exactly need_eq - 1 equal keys at smaller rows
-        for (int i = tid; i < C; i += kThreads) {
-            if (ck[i] != T) continue;
+    int pos = cta_exclusive_scan(mine, warp_sums, &E);
+    if (E <= kList) {
+        for (int i = tid; i < C; i += kThreads)
+            if ((ck[i] >> 10) == pre) { lk[pos] = ck[i]; li[pos] = ci[i]; ++pos; }
+        __syncthreads();
+        for (int i = tid; i < E; i += kThreads) {
+            const unsigned key = lk[i];
+            const int row = li[i];
             int rank = 0;
-            for (int j = 0; j < C; ++j) rank += (ck[j] == T && ci[j] < ci[i]);
-            if (rank == need_eq - 1) *s_abv = ci[i];
+#pragma unroll 8
+            for (int j = 0; j < E; ++j) rank += lk[j] > key || (lk[j] == key && li[j] < row);
+            if (rank == krem - 1) { *s_dig = key; *s_abv = row; }
         }
-        __syncthreads();
-        P_eq = *s_abv;
-        __syncthreads();
+    } else {   // massive ties inside one sub-bin: rank against the whole list
+        for (int i = tid; i < C; i += kThreads) {
+            if ((ck[i] >> 10) != pre) continue;
+            int rank = 0;
+#pragma unroll 8
+            for (int j = 0; j < C; ++j)
+                rank += ((ck[j] >> 10) == pre) && (ck[j] > ck[i] || (ck[j] == ck[i] && ci[j] < ci[i]));
+            if (rank == krem - 1) { *s_dig = ck[i]; *s_abv = ci[i]; }
+        }
     }
-    *T_out = T;
-    *Peq_out = P_eq;
+    __syncthreads();
+    *T_out = *s_dig;
+    *Peq_out = *s_abv;
+    __syncthreads();
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -298,7 +308,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
+__global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
     cg::grid_group grid = cg::this_grid();
 #define STAMP(k) \
     if (s.stamps != nullptr && threadIdx.x == 0) s.stamps[blockIdx.x * 8 + (k)] = globaltimer()
@@ -348,22 +358,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGathe
         int above;
         b1 = top_digit(sh, kHist1Bins, krem, warp_sums, &s_dig, &s_abv, &above);
         krem -= above;
-        // keys above bin b1, the digit-2 histogram of bin b1 (fallback), candidates of bin b1
-        for (int i = tid; i < 2048; i += kThreads) sh[i] = 0;
-        __syncthreads();
+        // keys above bin b1 and the candidates (keys in bin b1) of this slice;
+        // both counts in one packed scan (each <= 4096)
         int gt1 = 0, nc = 0;
         for (int i = tid; i < nk; i += kThreads) {
-            const unsigned key = s_keys[i];
-            const unsigned d1 = key >> 21;
+            const unsigned d1 = s_keys[i] >> 21;
             gt1 += d1 > b1;
-            if (d1 == b1) { ++nc; atomicAdd(&sh[(key >> 10) & 2047u], 1u); }
+            nc += d1 == b1;
         }
-        // candidates of this slice: one global atomic for the CTA's whole run
-        int ctot;
-        int cpos = cta_exclusive_scan(nc, warp_sums, &ctot);
-        if (tid == 0) s_abv = ctot > 0 ? static_cast<int>(atomicAdd(ccount + bb, static_cast<unsigned>(ctot))) : 0;
+        int packed_tot;
+        const int packed = cta_exclusive_scan((gt1 << 16) | nc, warp_sums, &packed_tot);
+        const int ctot = packed_tot & 0xFFFF;
+        if (tid == 0) {
+            s.slice_gt[sidx] = packed_tot >> 16;
+            s_abv = ctot > 0 ? static_cast<int>(atomicAdd(ccount + bb, static_cast<unsigned>(ctot))) : 0;
+        }
         __syncthreads();
-        cpos += s_abv;
+        int cpos = s_abv + (packed & 0xFFFF);
         for (int i = tid; i < nk && nc > 0; i += kThreads) {
             const unsigned key = s_keys[i];
             if ((key >> 21) == b1) {
@@ -371,10 +382,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGathe
                 ++cpos;
             }
         }
-        int tg;
-        cta_exclusive_scan(gt1, warp_sums, &tg);
-        if (tid == 0) s.slice_gt[sidx] = tg;
-        flush_hist(sh, s.hist2 + bb * 2048, 2048);
     }
     STAMP(1);
     if (it.c == 0)   // next step's candidate counter of this block
@@ -386,14 +393,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGathe
     bool overflow = false;
     for (int b = tid; b < s.num_blocks; b += kThreads) overflow |= __ldcg(ccount + b) > static_cast<unsigned>(kCandCap);
     // this block's candidates and the preceding slices' counts, loaded together
+    // this block's candidate slots (all of them: one round, no wait for the count)
+    // and the preceding slices' counts, loaded together
     const int C = arc ? static_cast<int>(min(__ldcg(ccount + bb), static_cast<unsigned>(kCandCap))) : 0;
     int before = 0;
-    if (arc)
+    if (arc) {
         for (int c = tid; c < it.c; c += kThreads) before += __ldcg(s.slice_gt + B.slice_base + c);
-    {
         unsigned* ck = reinterpret_cast<unsigned*>(s_rows);
         int* ci = s_rows + kCandCap;
-        for (int i = tid; i < C; i += kThreads) {
+#pragma unroll
+        for (int k = 0; k < kCandCap / kThreads; ++k) {
+            const int i = tid + k * kThreads;
             ck[i] = __ldcg(cand + i);
             ci[i] = static_cast<int>(__ldcg(cand + kCandCap + i));
         }
@@ -407,8 +417,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGathe
         for (int i = tid; i < kHist1Bins; i += kThreads) s.hist1[bb * kHist1Bins + i] = 0;
     if (!overflow) {
         if (arc) {
-            if (it.c == 0)
-                for (int i = tid; i < 2048; i += kThreads) s.hist2[bb * 2048 + i] = 0;
             unsigned* ck = reinterpret_cast<unsigned*>(s_rows);
             int* ci = s_rows + kCandCap;
             resolve_candidates(ck, ci, C, b1, krem, sh, warp_sums, &s_dig, &s_abv, &T, &P_eq);
@@ -421,8 +429,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_select_gather(const SelectGathe
             sel_before = tot;
         }
     } else {
-        // ---- digit by digit: digit 2 from the global histogram, digit 3 below
+        // ---- digit by digit (some block's boundary bin overflowed the candidate
+        // list): digit-2 histogram of bin b1, then digit 3, one barrier each
         unsigned b2 = 0;
+        if (arc) {
+            for (int i = tid; i < 2048; i += kThreads) sh[i] = 0;
+            __syncthreads();
+            for (int i = tid; i < nk; i += kThreads)
+                if ((s_keys[i] >> 21) == b1) atomicAdd(&sh[(s_keys[i] >> 10) & 2047u], 1u);
+            flush_hist(sh, s.hist2 + bb * 2048, 2048);
+        }
+        grid.sync();                                 // ---------------- barrier 1b
         if (arc) {
             load_hist(sh, s.hist2 + bb * 2048, 2048);
             int above;

@@ -14,8 +14,8 @@ src = GradientSource(d, blocks, 1, seed=20251030, device=dev)
 pool = [src.grads(t) for t in range(4)]
 h, g, gbar = [torch.zeros(d, device=dev)], [torch.zeros(d, device=dev)], torch.zeros(d, device=dev)
 ctx = ArcTopK(d, blocks, N=1, eta=0.1, seed=20251030)
-names = ["A:keys+hist1+digit1+classify", "cand-reset", "barrier1", "post-barrier loads", "resolve+before",
-         "compaction", "barrier2", "gather"]
+names = ["A: keys, hist1, digit 1, candidates", "barrier 1", "post-barrier loads", "resolve + before",
+         "compaction", "segment prefetch + barrier 2", "gather"]
 for t in range(60):
     ctx.step(t, pool[t % 4], h, g, gbar)
     if t in (10, 30, 59):
