@@ -200,7 +200,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_tiles = take(sizeof(Tile) * pl.max_tiles);
     pl.o_cta = take(sizeof(int) * (kMaxGrid + 1));
     pl.o_selrows = take(sizeof(SelRow) * pl.num_segs);
-    pl.o_V = take(sizeof(float) * sum_nr);
+    pl.o_V = take(sizeof(float) * sum_nr * 2);   // double-buffered by t parity
     pl.o_sigma = take(sizeof(float) * std::max<int64_t>(M * nl, 1));
     pl.o_sel = take(sizeof(int32_t) * sumK);
     pl.o_status = take(16);
@@ -342,6 +342,9 @@ struct arc_topk_ctx {
     int timed_steps = 0;
     uint64_t step_count = 0;     // parity of the selection's double-buffered candidate counters
     unsigned long long* stamps = nullptr;   // debug (ARC_DEBUG_STAMPS=1): library-owned device buffer
+    int64_t v_ready = -1;        // t whose V the previous step generated speculatively
+    int64_t last_t = 0;
+    int64_t v_items = 0;
 
     template <class T> T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
 };
@@ -487,6 +490,8 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     } while (0);
 #undef UPLOAD
 
+    for (const BlockDev& B : c->pl.bdev)
+        if (B.kind == ARC_BLOCK_ARC) c->v_items += static_cast<int64_t>(B.n) * ((c->p.r + 3) / 4);
     c->ome = 1.0f - c->p.eta;                       // R11, fp32
     c->c_r = 1.0f / sqrtf(static_cast<float>(c->p.r));   // R2: fl(1 / sqrt_rn(r))
     c->Nf = static_cast<float>(c->p.N);             // R3
@@ -553,11 +558,13 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     if (pl.topk && (sel_out != nullptr || values_out != nullptr)) return ARC_ERR_INVALID_ARG;
 
     ARC_MARK(0);
-    // S0
-    if (pl.M > 0 && !pl.topk) {
-        launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V, s);
+    // S0 (skipped when the previous step already generated V for this t)
+    float* V_t = V + static_cast<size_t>(t & 1) * pl.sum_nr;
+    if (pl.M > 0 && !pl.topk && c->v_ready != t) {
+        launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V_t, s);
         ARC_LAUNCHED();
     }
+    c->last_t = t;
     // S1 (+S2)
     if (pl.M > 0) {
         SketchLaunch a{};
@@ -574,7 +581,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.ome = c->ome;
         a.c_r = c->c_r;
         a.Nf = c->Nf;
-        a.V = V;
+        a.V = V_t;
         a.sigma = sigma;
         a.hist1 = hist1;
         a.pnodes = pl.keep_pnodes ? c->at<float>(pl.o_pnodes) : nullptr;
@@ -651,6 +658,19 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.parity = static_cast<int>(c->step_count & 1);
         sg.sel = pl.topk ? reinterpret_cast<int32_t*>(wire) : sel;
         sg.stamps = c->stamps;
+        const bool spec = pl.M > 0 && !pl.topk && t < INT64_MAX;
+        if (spec) {
+            const uint64_t tn = static_cast<uint64_t>(t + 1);
+            sg.vblocks = blocks;
+            sg.num_vblocks = c->p.num_blocks;
+            sg.V_next = V + static_cast<size_t>((t + 1) & 1) * pl.sum_nr;
+            sg.v_items = c->v_items;
+            sg.r = c->p.r;
+            sg.key = make_uint2(static_cast<unsigned>(c->p.seed), static_cast<unsigned>(c->p.seed >> 32));
+            sg.t_lo = static_cast<unsigned>(tn);
+            sg.t_hi = static_cast<unsigned>(tn >> 32);
+        }
+        c->v_ready = (spec && sg.num_items > 0) ? t + 1 : -1;
         if (sg.num_items > 0 && launch_select_gather(sg, ga, s) != cudaSuccess) {
             (void)cudaGetLastError();
             return ARC_ERR_CUDA;
@@ -773,7 +793,7 @@ arc_status arc_topk_query(arc_topk_ctx* c, int32_t what, void* dst, size_t bytes
     const Plan& pl = c->pl;
     size_t off = 0, need = 0;
     switch (what) {
-        case ARC_Q_V: off = pl.o_V; need = sizeof(float) * pl.sum_nr; break;
+        case ARC_Q_V: off = pl.o_V + sizeof(float) * pl.sum_nr * (c->last_t & 1); need = sizeof(float) * pl.sum_nr; break;
         case ARC_Q_SIGMA: off = pl.o_sigma; need = sizeof(float) * pl.M; break;
         case ARC_Q_SEL: off = pl.o_sel; need = sizeof(int32_t) * pl.sumK; break;
         case ARC_Q_P_NODES:
@@ -805,7 +825,8 @@ arc_status arc_topk_sizes(const arc_topk_ctx* c, int64_t* sum_K, int64_t* sum_Kn
 
 int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     if (c == nullptr) return -1;
-    const int arc = c->pl.M > 0 ? 2 : 0;   // vgen + ef_sketch
+    // steady state with consecutive t: V comes from the previous step (no k_vgen)
+    const int arc = c->pl.M > 0 ? (c->pl.items.empty() ? 2 : 1) : 0;
     // vgen + ef_sketch, [sketch_reduce], select_gather, [scatter]; Top-K: no vgen, N merges
     if (c->pl.topk) return (c->pl.M > 0 ? 1 : 0) + 1 + c->p.N;
     return arc + (c->pl.exchange && c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) +

@@ -74,6 +74,14 @@ struct SelectGatherLaunch {
     int parity;                    // step parity: selects this step's candidate buffers
     int32_t* sel;
     unsigned long long* stamps;    // debug: [grid][8] %globaltimer at phase boundaries, or nullptr
+    // speculative S0 of the next step: V for t_next (nullptr: none)
+    const BlockDev* vblocks;       // the caller's blocks (V offsets)
+    int num_vblocks;
+    float* V_next;
+    long long v_items;             // sum over ARC blocks of n_b * ceil(r / 4)
+    int r;
+    uint2 key;
+    unsigned t_lo, t_hi;
 };
 
 struct NodePtrs {

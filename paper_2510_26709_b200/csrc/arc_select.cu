@@ -27,6 +27,7 @@
 
 #include "arc_device.cuh"
 #include "arc_internal.cuh"
+#include "arc_rng.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -383,6 +384,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
             }
         }
     }
+    // S0 of the next step, generated here speculatively (V depends only on
+    // (seed, t, b)); the host uses it only if the next step's t matches
+    if (s.V_next != nullptr)
+        for (long long i = blockIdx.x * static_cast<long long>(kThreads) + tid; i < s.v_items;
+             i += static_cast<long long>(gridDim.x) * kThreads)
+            rng::gen_V_item(s.vblocks, s.num_vblocks, s.r, s.key, s.t_lo, s.t_hi, i, s.V_next);
     STAMP(1);
     if (it.c == 0)   // next step's candidate counter of this block
         for (int i = tid; i < 1; i += kThreads) s.cand_count[(par ^ 1) * s.num_blocks + bb] = 0;

@@ -41,7 +41,7 @@ def assert_same_floats(gpu: np.ndarray, ref: np.ndarray, what: str):
 
 
 def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, reduce="nccl",
-               force_exchange=False, check_debug=True, host=False, nodes_local=None, pg=None):
+               force_exchange=False, check_debug=True, host=False, nodes_local=None, pg=None, ts=None):
     from paper_2510_26709_b200 import ArcTopK
     nl = N if nodes_local is None else nodes_local
     assert nl == N, "single-GPU parity: all nodes local"
@@ -52,7 +52,7 @@ def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, 
     h = [torch.zeros(d, device=DEV) for _ in range(N)]
     g = [torch.zeros(d, device=DEV) for _ in range(N)]
     gbar = torch.zeros(d, device=DEV)
-    for t in range(steps):
+    for t in (range(steps) if ts is None else ts):
         gr = [x.numpy() for x in src.grads(t)] if grads_fn is None else grads_fn(t)
         gr = [np.ascontiguousarray(x, dtype=np.float32) for x in gr]
         if host:
@@ -187,6 +187,12 @@ def test_exchange_through_nccl_one_rank(orc, reduce):
                    pg=dist.group.WORLD)
     finally:
         pass
+
+
+def test_nonconsecutive_steps(orc):
+    """V for step t+1 is generated speculatively during step t; a caller that skips
+    or repeats iteration numbers must still get V(seed, t) (R7)."""
+    run_parity(orc, 30_000, flat_blocks(30_000, 96, K=15), N=2, ts=[0, 1, 5, 6, 6, 2, 3, 1 << 33, (1 << 33) + 1])
 
 
 def test_host_staging_entry(orc):
