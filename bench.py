@@ -95,9 +95,9 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def workload(name: str, nodes_per_gpu: int, world: int):
+def workload(name: str, nodes_per_gpu: int, world: int, mu_bp=None):
     from synth import config_blocks
-    d, blocks = config_blocks(name)
+    d, blocks = config_blocks(name, mu_bp)
     return d, blocks, nodes_per_gpu * world
 
 
@@ -266,6 +266,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--pool", type=int, default=8, help="distinct gradient sets cycled in the timed loop")
     ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--mu-bp", type=int, default=None, help="override K/m in basis points (e.g. 10, 100, 1000)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     if args.impl == "reference":
@@ -290,7 +291,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
     L = args.nodes_per_gpu
-    d, blocks, N = workload(args.config, L, world)
+    d, blocks, N = workload(args.config, L, world, args.mu_bp)
     src = GradientSource(d, blocks, N, seed=20251030, device=dev)
     nodes = list(range(rank * L, (rank + 1) * L))
     # A pool of distinct gradient sets cycled step by step, like a training
@@ -406,7 +407,9 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config}: GPT-2-small-sized gradient d={d}, n={blocks[0].n}, "
                                    f"K=1% ({blocks[0].K} rows), r=4, eta=0.1, one paper node per GPU"
-                                   if args.config == "C3" else args.config,
+                                   if args.config == "C3" and args.mu_bp is None else
+                                   f"{args.config}: d={d}, {len(blocks)} block(s), sum K={sum(b.K for b in blocks)}, "
+                                   f"mu_bp={args.mu_bp}, r=4, eta=0.1, {L} node(s) per GPU",
                        "d": d, "N_nodes": N, "nodes_per_gpu": L, "reduce": args.reduce,
                        "parallelism": f"dp{world}",
                        "l2": "no flush: per-step inputs (16 B x d = %.1f GB) exceed the 126 MB L2" % (16 * d / 1e9),

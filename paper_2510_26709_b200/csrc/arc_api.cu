@@ -115,7 +115,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.L = p->nodes_local;
     pl.G = p->N / p->nodes_local;
     pl.exchange = pl.G > 1 || (p->flags & ARC_FLAG_FORCE_EXCHANGE);
-    pl.keep_pnodes = pl.exchange || (p->flags & ARC_FLAG_DEBUG_SKETCH);
+    pl.keep_pnodes = pl.exchange || pl.L > 1 || (p->flags & ARC_FLAG_DEBUG_SKETCH);
     pl.bdev.resize(p->num_blocks);
     int64_t M = 0, sumK = 0, sumKn = 0, sum_nr = 0;
     int max_tiles = 0;
@@ -141,7 +141,8 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
             M += B.m;
             sum_nr += B.n * p->r;
             pl.max_nR4 = std::max<int64_t>(pl.max_nR4, B.n * R4);
-            max_tiles += static_cast<int>((B.m + kMinTileRows - 1) / kMinTileRows);
+            max_tiles += static_cast<int>((B.m + kMinTileRows - 1) / kMinTileRows) *
+                         (p->method == ARC_METHOD_TOPK_ALLGATHER || p->nodes_local > 1 ? p->nodes_local : 1);
         }
         sumK += B.K;
         sumKn += B.K * B.n;
@@ -233,37 +234,46 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
 }
 
 // ---- the tile scheduler: balance the streaming pass over the resident CTAs ----
-// Tiles are <= 64 rows of one ARC block (a row never spans two CTAs: its sums
-// are sequential, R9).  For a few candidate tile heights the tiles are placed
-// on CTAs longest-first onto the least-loaded CTA (LPT); the plan with the
-// smallest makespan wins.
+// A tile is <= R_shape rows of one ARC block for one local node (a row's sums
+// are sequential, R9, so a row never spans two CTAs; different nodes are
+// independent).  A chunk costs about the same whether or not all R_shape rows
+// are live (masked rows still run the load and staging code), so a tile of r
+// rows is charged nchunks * max(r, 0.6 R_shape); tiles go longest-first to the
+// least-loaded CTA (LPT).
 void plan_tiles(const Plan& pl, int resident, int tile_rows_max, std::vector<Tile>& tiles, std::vector<int>& cta_begin,
                 int& grid) {
-    struct Cand { int64_t makespan; std::vector<Tile> tiles; std::vector<int> begin; int grid; };
+    struct Cand { int64_t makespan = INT64_MAX; std::vector<Tile> tiles; std::vector<int> begin; int grid = 0; };
     Cand best;
-    best.makespan = INT64_MAX;
-    int64_t work = 0;
-    for (const BlockDev& B : pl.bdev)
-        if (B.kind == ARC_BLOCK_ARC) work += static_cast<int64_t>(B.m) * (B.n + 8);
     resident = std::max(1, std::min(resident, kMaxGrid));
-    for (int waves = 1; waves <= 12; ++waves) {
-        const double target = static_cast<double>(work) / (static_cast<double>(resident) * waves);
+    const int nodes = pl.topk || pl.L > 1 ? pl.L : 1;
+    const int W = tile_rows_max == 64 ? 32 : (tile_rows_max == 32 ? 64 : 128);   // chunk columns of the shape
+    const int64_t floor_rows = (tile_rows_max * 6 + 9) / 10;
+    // Full-height tiles are the cheapest per element (measured on C3: 32-row
+    // tiles 94 %, 30 rows 93 %, 24 rows 90 % of HBM peak; on C2 8-row tiles ran
+    // instruction-bound at 36 %), and a bandwidth-bound grid absorbs a ragged
+    // last round well, so the tile height is always the shape's.
+    const int R_pick = tile_rows_max;
+    int R_lo = R_pick, R_hi = R_pick;
+    if (const char* e = getenv("ARC_TILE_ROWS")) {   // debug knob: one tile height
+        const int v = atoi(e);
+        if (v >= 1 && v <= tile_rows_max) R_lo = R_hi = v;
+    }
+    for (int R = R_hi; R >= R_lo; --R) {
         std::vector<Tile> ts;
         std::vector<int64_t> cost;
         for (size_t b = 0; b < pl.bdev.size(); ++b) {
             const BlockDev& B = pl.bdev[b];
             if (B.kind != ARC_BLOCK_ARC) continue;
-            int R = static_cast<int>(target / (B.n + 8));
-            R = std::max(std::min(kMinTileRows, tile_rows_max), std::min(tile_rows_max, R));
-            R = std::min(R, B.m);
-            const int nt = (B.m + R - 1) / R;
-            // spread the rows evenly over the block's tiles
-            for (int i = 0; i < nt; ++i) {
-                const int r0 = static_cast<int>(static_cast<int64_t>(B.m) * i / nt);
-                const int r1 = static_cast<int>(static_cast<int64_t>(B.m) * (i + 1) / nt);
-                ts.push_back(Tile{static_cast<int>(b), r0, r1 - r0});
-                cost.push_back(static_cast<int64_t>(r1 - r0 + 2) * (B.n + 8));
-            }
+            const int Rb = std::min(R, B.m);
+            const int nt = (B.m + Rb - 1) / Rb;
+            const int64_t nch = (B.n + W - 1) / W;
+            for (int l = 0; l < nodes; ++l)
+                for (int i = 0; i < nt; ++i) {   // rows spread evenly over the block's tiles
+                    const int r0 = static_cast<int>(static_cast<int64_t>(B.m) * i / nt);
+                    const int r1 = static_cast<int>(static_cast<int64_t>(B.m) * (i + 1) / nt);
+                    ts.push_back(Tile{static_cast<int>(b), r0, r1 - r0, l});
+                    cost.push_back(nch * std::max<int64_t>(r1 - r0, floor_rows) + 4);
+                }
         }
         if (static_cast<int>(ts.size()) > pl.max_tiles) continue;
         const int g = std::min<int>(resident, static_cast<int>(ts.size()));
@@ -276,12 +286,12 @@ void plan_tiles(const Plan& pl, int resident, int tile_rows_max, std::vector<Til
         std::vector<std::vector<int>> lists(g);
         int64_t makespan = 0;
         for (int idx : order) {
-            Slot s = heap.top();
+            Slot sl = heap.top();
             heap.pop();
-            s.first += cost[idx];
-            makespan = std::max(makespan, s.first);
-            lists[s.second].push_back(idx);
-            heap.push(s);
+            sl.first += cost[idx];
+            makespan = std::max(makespan, sl.first);
+            lists[sl.second].push_back(idx);
+            heap.push(sl);
         }
         if (makespan < best.makespan) {
             Cand c;
@@ -585,7 +595,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.sigma = sigma;
         a.hist1 = hist1;
         a.pnodes = pl.keep_pnodes ? c->at<float>(pl.o_pnodes) : nullptr;
-        a.mode = pl.topk ? 2 : (pl.exchange ? 1 : 0);
+        a.mode = pl.topk ? 2 : ((pl.exchange || L > 1) ? 1 : 0);
         a.M = pl.M;
         a.num_blocks = c->p.num_blocks;
         a.shape = c->shape;
@@ -598,6 +608,12 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     }
     ARC_MARK(2);
     // (DENSE blocks skip the sketch pass: the select/gather kernel applies their momentum.)
+    // S2 with several local nodes and no exchange: ordered node sum of the P_i
+    if (!pl.exchange && !pl.topk && L > 1 && pl.M > 0) {
+        launch_sketch_reduce(blocks, c->p.num_blocks, c->max_m, c->at<float>(pl.o_pnodes), pl.M, 1, L, c->p.r, c->Nf,
+                             sigma, hist1, status, s);
+        ARC_LAUNCHED();
+    }
     // Exchange #1 + S2 for G > 1
     if (pl.exchange && pl.M > 0) {
         const size_t cnt = static_cast<size_t>(pl.M) * L * c->p.r;
@@ -829,7 +845,7 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     const int arc = c->pl.M > 0 ? (c->pl.items.empty() ? 2 : 1) : 0;
     // vgen + ef_sketch, [sketch_reduce], select_gather, [scatter]; Top-K: no vgen, N merges
     if (c->pl.topk) return (c->pl.M > 0 ? 1 : 0) + 1 + c->p.N;
-    return arc + (c->pl.exchange && c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) +
+    return arc + ((c->pl.exchange || c->pl.L > 1) && c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) +
            (c->pl.dense_ids.empty() ? 0 : 1) + (c->pl.exchange ? 1 : 0);
 }
 

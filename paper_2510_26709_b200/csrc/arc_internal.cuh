@@ -23,11 +23,13 @@ struct BlockDev {
     int pad_;
 };
 
-// A sketch tile: rows [row0, row0 + rows) of one ARC block, rows <= kTileRows.
+// A sketch tile: rows [row0, row0 + rows) of one ARC block for one local node
+// (the nodes' sketches are independent; their ordered sum is a separate pass).
 struct Tile {
     int b;
     int row0;
     int rows;
+    int node;
 };
 
 // Gather / scatter work item: columns [4*q0, 4*q0 + kSegQuads*4) of the k-th

@@ -59,7 +59,6 @@ __device__ __forceinline__ int row_valid_cols(const BlockDev& B, int p) {
     return rest < B.n ? static_cast<int>(rest) : B.n;
 }
 
-__device__ __forceinline__ unsigned order_key(float s) { return order_key_dev(s); }
 
 // =============================================================================
 // S2 for G > 1: ordered node sum of the all-gathered P_i (R9, R21) and Sigma.
@@ -68,8 +67,11 @@ __device__ __forceinline__ unsigned order_key(float s) { return order_key_dev(s)
 __global__ void __launch_bounds__(256) k_sketch_reduce(const BlockDev* __restrict__ blocks, const float* __restrict__ xrecv,
                                                        int M, int G, int L, int r, float Nf, float* __restrict__ sigma,
                                                        unsigned* __restrict__ hist1, unsigned* status) {
+    __shared__ unsigned hist[kHist1Bins];
     const int b = blockIdx.y;
     if (blocks[b].kind != ARC_BLOCK_ARC) return;
+    for (int i = threadIdx.x; i < kHist1Bins; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
     const int m = blocks[b].m, base = blocks[b].row_base;
     for (int pr = blockIdx.x * blockDim.x + threadIdx.x; pr < m; pr += gridDim.x * blockDim.x) {
         const int p = base + pr;
@@ -85,9 +87,13 @@ __global__ void __launch_bounds__(256) k_sketch_reduce(const BlockDev* __restric
             sig = fadd(sig, fmul(pv, pv));
         }
         sigma[p] = sig;
-        atomicAdd(&hist1[static_cast<long long>(b) * kHist1Bins + (order_key(sig) >> kHist1Shift)], 1u);
+        atomicAdd(&hist[order_key_dev(sig) >> kHist1Shift], 1u);   // digit-1 histogram (shared, then one flush)
         if (!isfinite(sig)) atomicOr(status, kStatusNonfinite);
     }
+    __syncthreads();
+    unsigned* gh = hist1 + static_cast<long long>(b) * kHist1Bins;
+    for (int i = threadIdx.x; i < kHist1Bins; i += blockDim.x)
+        if (hist[i]) atomicAdd(gh + i, hist[i]);
 }
 
 // =============================================================================

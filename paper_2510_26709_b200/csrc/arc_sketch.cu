@@ -42,6 +42,7 @@ struct TileRegs {
     long long v_off;
     int row_base;
     int b;
+    int node;
 };
 
 template <int W>
@@ -59,6 +60,7 @@ __device__ __forceinline__ TileRegs tile_regs(const SketchLaunch& a, int li) {
     t.row_base = __ldg(&B->row_base);
     t.row0 = __ldg(&T->row0);
     t.m_rows = __ldg(&T->rows);
+    t.node = __ldg(&T->node);
     t.nchunks = (t.n + W - 1) / W;
     return t;
 }
@@ -197,28 +199,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
 #pragma unroll
     for (int s = 0; s < RPT; ++s) { acc[s] = 0.0f; S[s] = 0.0f; }
 
-    int li = list_begin, node = 0, chunk = 0;
+    int li = list_begin, chunk = 0;
     TileRegs tc = tile_regs<W>(a, li);     // tile of the chunk being staged / chained
     TileRegs tl = tc;                      // tile of the chunk being loaded
-    load_chunk(tc, node, chunk);
+    load_chunk(tc, tc.node, chunk);
     int buf = 0;
     while (true) {
-        stage_chunk(tc, node, chunk, buf);
+        stage_chunk(tc, tc.node, chunk, buf);
         __syncthreads();
         // advance the load cursor and issue the next chunk's loads
-        int nli = li, nnode = node, nchunk = chunk + 1;
+        int nli = li, nchunk = chunk + 1;
         if (nchunk == tc.nchunks) {
             nchunk = 0;
-            if (++nnode == a.nodes_local) {
-                nnode = 0;
-                ++nli;
-            }
+            ++nli;
         }
         const bool more = nli < list_end;
         if (more) {
             if (nli != li) tl = tile_regs<W>(a, nli);
-            load_chunk(tl, nnode, nchunk);
+            load_chunk(tl, tl.node, nchunk);
         }
+        const int node = tc.node;
 
         // ------------------------------------------------------------ chains
         const bool live = crow < tc.m_rows;
@@ -271,10 +271,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
                 const float Pi = fmul(a.c_r, acc[s]);                                    // R2
                 if (a.pnodes != nullptr && live && j < r)
                     a.pnodes[(static_cast<long long>(tc.row_base + p) * a.nodes_local + node) * r + j] = Pi;
-                S[s] = (node == 0) ? Pi : fadd(S[s], Pi);                                 // R9, node order
+                S[s] = Pi;        // mode 0 has one local node: S = P_0 (more nodes: ordered sum pass)
                 acc[s] = 0.0f;
             }
-            if (a.mode == 0 && node == a.nodes_local - 1) {
+            if (a.mode == 0) {
                 float sig = 0.0f;
 #pragma unroll
                 for (int s = 0; s < RPT; ++s) {
@@ -300,7 +300,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         if (!more) break;
         if (nli != li) tc = tl;
         li = nli;
-        node = nnode;
         chunk = nchunk;
         buf ^= 1;
     }
