@@ -293,3 +293,13 @@ def test_topk_allgather_multiblock_dense(orc):
         assert_same_floats(g[i].cpu().numpy(), o.g[i], f"g[{i}]")
     assert_same_floats(gbar.cpu().numpy(), o.gbar, "gbar")
     ctx.close()
+
+
+def test_full_size_c4_llama_per_tensor(orc):
+    """BASELINE configs[3]: the 1.3B-parameter LLaMA-1B-shaped gradient with per-tensor
+    compression (170 ARC blocks incl. unaligned n = 5461 rows, plus the DENSE block of
+    1-D parameters), K = 0.1 % per tensor, one node per GPU (the bench launch
+    configuration): selection, values and state bit-exact at full size, 2 steps."""
+    d, blocks = config_blocks("C4")
+    assert len(blocks) == 171 and d == 1_339_082_752
+    run_parity(orc, d, blocks, N=1, steps=2, seed=20251030, check_debug=True)
