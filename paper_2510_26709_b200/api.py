@@ -121,14 +121,18 @@ class ArcTopK:
                 "arc_topk_workspace_bytes")
         self.workspace = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=self.device)
         comm = None
-        if self.G > 1:
+        self._pg = None
+        if self.G > 1 or (pg is not None and force_exchange):
             if pg is None:
                 raise ValueError("N / nodes_local > 1 needs an NCCL process group")
-            from .dist import check_consistent, params_digest
+            from .dist import check_consistent, params_digest, private_nccl_group
             check_consistent(pg, params_digest(d, self.blocks, self.N, self.nodes_local, r, eta, seed, reduce))
-            comm = nccl_comm_ptr(pg, self.device)
-        elif pg is not None and force_exchange:
-            comm = nccl_comm_ptr(pg, self.device)   # G = 1: the exchange path through a 1-rank communicator
+            # the library's collectives get a communicator of their own, so they can
+            # never interleave with torch's collectives on the caller's group
+            self._pg = private_nccl_group(pg, self.device)
+            import torch.distributed as dist
+            self.params.rank = dist.get_rank(self._pg)     # this GPU's rank in the library's communicator
+            comm = nccl_comm_ptr(self._pg, self.device)
         ctx = ctypes.c_void_p()
         L.check(self.lib.arc_topk_create(ctypes.byref(self.params), comm, int(self.workspace.data_ptr()),
                                           int(nbytes.value), _stream_handle(stream), ctypes.byref(ctx)),
@@ -219,6 +223,7 @@ class ArcTopK:
         if getattr(self, "ctx", None):
             self.lib.arc_topk_destroy(self.ctx)
             self.ctx = None
+        self._pg = None
 
     def __del__(self):
         try:

@@ -38,3 +38,19 @@ def check_consistent(pg, digest: str) -> None:
     bad = [i for i, x in enumerate(got) if x != got[0]]
     if bad:
         raise ValueError(f"ARC-Top-K parameters differ across ranks (ranks {bad} vs rank 0)")
+
+
+def private_nccl_group(pg, device):
+    """A new NCCL process group over the ranks of `pg`, used only by the library
+    (its communicator is split from / created next to torch's).  Collective:
+    every rank of `pg` calls it in the same order."""
+    import torch
+    import torch.distributed as dist
+    ranks = dist.get_process_group_ranks(pg)
+    new = dist.new_group(ranks=ranks, backend="nccl", device_id=device, use_local_synchronization=True)
+    backend = new._get_backend(device)
+    if int(backend._comm_ptr()) == 0:        # lazily created: one tiny collective creates it
+        t = torch.zeros(1, device=device)
+        dist.all_reduce(t, group=new)
+        torch.cuda.synchronize(device)
+    return new
