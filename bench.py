@@ -197,7 +197,8 @@ def run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, str
       kept, the value exchange is an All-Reduce of all d entries; P:89 "Dense 2mn");
     * nccl_allreduce_d (G > 1): a bare ncclAllReduce of d fp32 per GPU;
     * allgather_topk: vanilla EF21M with per-node row Top-K, whose
-      exchange is an All-Gather of K values rows plus K indices per node."""
+      exchange is an All-Gather of K values rows plus K indices per node;
+    * randk_shared_seed: Rand-K — the same path with data-independent rows."""
     import torch
     import torch.distributed as dist
 
@@ -250,6 +251,10 @@ def run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, str
         ctx.close()
     except Exception as e:  # not built yet / unsupported layout
         out["allgather_topk"] = {"unavailable": str(e)[:200]}
+    ctx = ArcTopK(d, blocks, N=N, eta=0.1, r=4, seed=20251030, nodes_local=L, pg=pg, rank=rank, method="randk")
+    out["randk_shared_seed"] = timed(lambda t: ctx.step(t, pool[t % pool_n], hs, gs, gb))
+    out["randk_shared_seed"]["note"] = "Rand-K rows from a shared seed (Table I row Rand-K), same EF21M path, no sketch"
+    ctx.close()
     return out
 
 

@@ -72,7 +72,11 @@ typedef enum {
  * row), g_i <- g_i + C_i on those rows, the nodes all-gather K_b n_b values +
  * K_b indices each, and gbar <- gbar + C_j / N for j = 0 .. N-1 in node order.
  * For it sel_out / values_out must be NULL (the payload is per node). */
-typedef enum { ARC_METHOD_ARC = 0, ARC_METHOD_TOPK_ALLGATHER = 1 } arc_method;
+/* ARC_METHOD_RANDK is Table I row "Rand-K" with a shared seed
+ * (R16): each block keeps K_b uniformly random rows, the same on every node
+ * (row p's key is Philox(seed; p, b | 2^31, t) >> 2, the K_b largest keys win),
+ * with the same EF21M update and index-free value All-Reduce as ARC-Top-K. */
+typedef enum { ARC_METHOD_ARC = 0, ARC_METHOD_TOPK_ALLGATHER = 1, ARC_METHOD_RANDK = 2 } arc_method;
 
 /* flags */
 #define ARC_FLAG_HOST_STAGING   0x1u  /* reserve device staging for arc_topk_step_host          */

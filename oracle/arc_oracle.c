@@ -333,12 +333,32 @@ void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int3
 /* eq:ef21m-3 consumes [R13].                                          */
 /* ------------------------------------------------------------------------- */
 
+/* ------------------------------------------------------------------------- */
+/* Rand-K with a shared seed (Table I row "Rand-K"): K rows   */
+/* of each block drawn uniformly without replacement, the same on every node   */
+/* [R16].  Row p of block b draws a 30-bit key from Philox (counter            */
+/* (p, b | 2^31, lo32 t, hi32 t), first word >> 2) and the K largest keys are  */
+/* kept (ties -> smaller row): a uniformly random K-subset.                    */
+/* ------------------------------------------------------------------------- */
+void orc_randk_keys(uint64_t seed, int64_t t, int32_t b, int64_t m, float* keys)
+{
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    for (int64_t p = 0; p < m; p++) {
+        uint32_t ctr[4] = { (uint32_t)p, (uint32_t)b | 0x80000000u,
+                            (uint32_t)(uint64_t)t, (uint32_t)((uint64_t)t >> 32) };
+        uint32_t x[4];
+        orc_philox4x32_10(ctr, key, x);
+        keys[p] = bits_to_float(x[0] >> 2);     /* a finite float whose bits are the key */
+    }
+}
+
 typedef struct {
     int32_t N;             /* nodes                                        */
     int32_t r;             /* sketch width                                 */
     int64_t d;             /* per-node vector length                       */
     float eta;             /* EF21M momentum                               */
-    int32_t exact;         /* sketch mode (0 Gaussian, 1 exact, test only)  */
+    int32_t exact;         /* sketch mode (0 Gaussian, 1 exact, test only,  */
+                           /* 2 = Rand-K with a shared seed)               */
     uint64_t seed;         /* shared base seed [R7]                         */
     int32_t num_blocks;
     int32_t pad_;
@@ -375,7 +395,29 @@ int orc_step(const orc_cfg* cfg, int64_t t,
         float* Cl = (float*)malloc((size_t)N * K * n * sizeof(float));
         float* Cg = (float*)malloc((size_t)K * n * sizeof(float));
 
-        if (B->kind == 0) {
+        if (B->kind == 0 && cfg->exact == 2) {
+            /* Rand-K: the selection ignores the data */
+            float* keys = (float*)malloc((size_t)m * sizeof(float));
+            orc_randk_keys(cfg->seed, t, b, m, keys);
+            orc_argtop_k(keys, m, K, sel);
+            for (int64_t k = 0; k < K; k++) {
+                int64_t p = sel[k];
+                int64_t nv = row_len(len, n, p);
+                for (int64_t q = 0; q < n; q++) {
+                    float a = 0.0f;
+                    for (int32_t i = 0; i < N; i++) {
+                        float c = (q < nv) ? D[i][p * n + q] : 0.0f;
+                        Cl[((size_t)i * K + k) * n + q] = c;
+                        a = (i == 0) ? c : a + c;
+                    }
+                    Cg[(size_t)k * n + q] = a / (float)N;
+                }
+            }
+            if (sigma_out) memcpy(sigma_out + sig_pos, keys, (size_t)m * sizeof(float));
+            sig_pos += m;
+            V_pos += n * cfg->r;
+            free(keys);
+        } else if (B->kind == 0) {
             float* V = (float*)malloc((size_t)n * cfg->r * sizeof(float));
             orc_gaussian_V(cfg->seed, t, b, n, cfg->r, V);
             float* sg = (float*)malloc((size_t)m * sizeof(float));

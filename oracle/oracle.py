@@ -55,6 +55,7 @@ def lib():
         L.orc_arc_round.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_int32] + [ctypes.c_void_p] * 6
+        L.orc_randk_keys.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p]
         L.orc_ln_array.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         L.orc_sincos2pi_array.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_step.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 8
@@ -142,6 +143,12 @@ def gaussian_V(seed: int, t: int, b: int, n: int, r: int) -> np.ndarray:
     return V
 
 
+def randk_keys(seed: int, t: int, b: int, m: int) -> np.ndarray:
+    k = np.empty(m, dtype=np.float32)
+    lib().orc_randk_keys(int(seed) & (2**64 - 1), int(t), int(b), int(m), _ptr(k))
+    return k
+
+
 def sigma_key(s: float) -> int:
     return int(lib().orc_sigma_key(float(s)))
 
@@ -189,12 +196,14 @@ class OracleEF21M:
     ``h[i]``, ``g[i]`` (per node) and ``gbar`` (the replicated tracker)."""
 
     def __init__(self, d: int, blocks, N: int, eta: float, r: int, seed: int, exact: bool = False,
-                 h0=None, g0=None, gbar0=None):
+                 h0=None, g0=None, gbar0=None, method: str = "arc"):
         self.d, self.N, self.eta, self.r, self.seed, self.exact = int(d), int(N), float(eta), int(r), int(seed), bool(exact)
+        self.method = method
         self.blocks = list(blocks)
         self._cblocks = (_Block * len(self.blocks))(*[
             _Block(b.offset, b.len, b.m, b.n, b.K, b.kind, 0) for b in self.blocks])
-        self._cfg = _Cfg(self.N, self.r, self.d, self.eta, int(self.exact), self.seed & (2**64 - 1),
+        mode = 2 if method == "randk" else int(self.exact)
+        self._cfg = _Cfg(self.N, self.r, self.d, self.eta, mode, self.seed & (2**64 - 1),
                          len(self.blocks), 0, self._cblocks)
         self.h = [np.zeros(d, np.float32) if h0 is None else _f32(h0[i]).copy() for i in range(N)]
         self.g = [np.zeros(d, np.float32) if g0 is None else _f32(g0[i]).copy() for i in range(N)]
@@ -238,4 +247,4 @@ class OracleEF21M:
 
 
 __all__ = ["Block", "OracleEF21M", "arc_round", "argtop_k", "build", "gaussian_V", "ln", "ln_array", "lib",
-           "philox4x32_10", "sigma_key", "sincos2pi", "sincos2pi_array", "uniform"]
+           "philox4x32_10", "randk_keys", "sigma_key", "sincos2pi", "sincos2pi_array", "uniform"]

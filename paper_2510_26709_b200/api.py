@@ -114,7 +114,8 @@ class ArcTopK:
                                   len(self.blocks), self._cblocks, float(eta),
                                   {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED}[reduce],
                                   int(seed) & (2**64 - 1), flags,
-                                  {"arc": L.METHOD_ARC, "topk_allgather": L.METHOD_TOPK_ALLGATHER}[method])
+                                  {"arc": L.METHOD_ARC, "topk_allgather": L.METHOD_TOPK_ALLGATHER,
+                                   "randk": L.METHOD_RANDK}[method])
         self.method = method
         nbytes = ctypes.c_size_t()
         L.check(self.lib.arc_topk_workspace_bytes(ctypes.byref(self.params), ctypes.byref(nbytes)),

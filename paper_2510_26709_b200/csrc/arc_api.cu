@@ -64,6 +64,7 @@ struct Plan {
     int max_tiles = 0;
     std::vector<BlockDev> bdev;      // the caller's blocks
     bool topk = false;               // ARC_METHOD_TOPK_ALLGATHER baseline
+    bool randk = false;              // ARC_METHOD_RANDK: data-independent shared selection
     int64_t W = 0;                   // Top-K: payload words per node (sum K n values + sum K indices)
     std::vector<BlockDev> sbdev;     // selection blocks: bdev, or (Top-K) one copy per local node
     std::vector<SelRow> segs;        // gather segments over sbdev
@@ -89,7 +90,8 @@ arc_status validate(const arc_topk_params* p) {
     if (p->value_reduce != ARC_REDUCE_NCCL && p->value_reduce != ARC_REDUCE_ORDERED) return ARC_ERR_INVALID_ARG;
     if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
     if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE)) return ARC_ERR_INVALID_ARG;
-    if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER) return ARC_ERR_INVALID_ARG;
+    if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER && p->method != ARC_METHOD_RANDK)
+        return ARC_ERR_INVALID_ARG;
     int64_t pos = 0, M = 0, sumK = 0;
     for (int b = 0; b < p->num_blocks; ++b) {
         const arc_block& B = p->blocks[b];
@@ -115,7 +117,8 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.L = p->nodes_local;
     pl.G = p->N / p->nodes_local;
     pl.exchange = pl.G > 1 || (p->flags & ARC_FLAG_FORCE_EXCHANGE);
-    pl.keep_pnodes = pl.exchange || pl.L > 1 || (p->flags & ARC_FLAG_DEBUG_SKETCH);
+    pl.randk = p->method == ARC_METHOD_RANDK;
+    pl.keep_pnodes = !pl.randk && (pl.exchange || pl.L > 1 || (p->flags & ARC_FLAG_DEBUG_SKETCH));
     pl.bdev.resize(p->num_blocks);
     int64_t M = 0, sumK = 0, sumKn = 0, sum_nr = 0;
     int max_tiles = 0;
@@ -221,7 +224,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         pl.o_wire = take(sizeof(float) * pl.W * pl.L);
         pl.o_wire_all = pl.G > 1 ? take(sizeof(float) * pl.W * pl.L * pl.G) : 0;
     } else if (pl.exchange) {
-        pl.o_xrecv = take(pn * pl.G);
+        pl.o_xrecv = pl.randk ? 0 : take(pn * pl.G);
         const bool ordered = p->value_reduce == ARC_REDUCE_ORDERED;
         pl.o_wire = take(sizeof(float) * sumKn * (ordered ? pl.L : 1));
         pl.o_wire_all = ordered ? take(sizeof(float) * sumKn * pl.L * pl.G) : 0;
@@ -570,7 +573,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ARC_MARK(0);
     // S0 (skipped when the previous step already generated V for this t)
     float* V_t = V + static_cast<size_t>(t & 1) * pl.sum_nr;
-    if (pl.M > 0 && !pl.topk && c->v_ready != t) {
+    if (pl.M > 0 && !pl.topk && !pl.randk && c->v_ready != t) {
         launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V_t, s);
         ARC_LAUNCHED();
     }
@@ -595,7 +598,10 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.sigma = sigma;
         a.hist1 = hist1;
         a.pnodes = pl.keep_pnodes ? c->at<float>(pl.o_pnodes) : nullptr;
-        a.mode = pl.topk ? 2 : ((pl.exchange || L > 1) ? 1 : 0);
+        a.mode = pl.topk ? 2 : pl.randk ? 3 : ((pl.exchange || L > 1) ? 1 : 0);
+        a.key = make_uint2(static_cast<unsigned>(c->p.seed), static_cast<unsigned>(c->p.seed >> 32));
+        a.t_lo = static_cast<unsigned>(static_cast<uint64_t>(t));
+        a.t_hi = static_cast<unsigned>(static_cast<uint64_t>(t) >> 32);
         a.M = pl.M;
         a.num_blocks = c->p.num_blocks;
         a.shape = c->shape;
@@ -609,13 +615,13 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ARC_MARK(2);
     // (DENSE blocks skip the sketch pass: the select/gather kernel applies their momentum.)
     // S2 with several local nodes and no exchange: ordered node sum of the P_i
-    if (!pl.exchange && !pl.topk && L > 1 && pl.M > 0) {
+    if (!pl.exchange && !pl.topk && !pl.randk && L > 1 && pl.M > 0) {
         launch_sketch_reduce(blocks, c->p.num_blocks, c->max_m, c->at<float>(pl.o_pnodes), pl.M, 1, L, c->p.r, c->Nf,
                              sigma, hist1, status, s);
         ARC_LAUNCHED();
     }
-    // Exchange #1 + S2 for G > 1
-    if (pl.exchange && pl.M > 0) {
+    // Exchange #1 + S2 for G > 1 (Rand-K needs none: every rank draws the same keys)
+    if (pl.exchange && !pl.randk && pl.M > 0) {
         const size_t cnt = static_cast<size_t>(pl.M) * L * c->p.r;
         float* xs = c->at<float>(pl.o_pnodes);
         float* xr = c->at<float>(pl.o_xrecv);
@@ -674,7 +680,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.parity = static_cast<int>(c->step_count & 1);
         sg.sel = pl.topk ? reinterpret_cast<int32_t*>(wire) : sel;
         sg.stamps = c->stamps;
-        const bool spec = pl.M > 0 && !pl.topk && t < INT64_MAX;
+        const bool spec = pl.M > 0 && !pl.topk && !pl.randk && t < INT64_MAX;
         if (spec) {
             const uint64_t tn = static_cast<uint64_t>(t + 1);
             sg.vblocks = blocks;
@@ -845,6 +851,9 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     const int arc = c->pl.M > 0 ? (c->pl.items.empty() ? 2 : 1) : 0;
     // vgen + ef_sketch, [sketch_reduce], select_gather, [scatter]; Top-K: no vgen, N merges
     if (c->pl.topk) return (c->pl.M > 0 ? 1 : 0) + 1 + c->p.N;
+    if (c->pl.randk)
+        return (c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) + (c->pl.dense_ids.empty() ? 0 : 1) +
+               (c->pl.exchange ? 1 : 0);
     return arc + ((c->pl.exchange || c->pl.L > 1) && c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) +
            (c->pl.dense_ids.empty() ? 0 : 1) + (c->pl.exchange ? 1 : 0);
 }

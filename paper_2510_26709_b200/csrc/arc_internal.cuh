@@ -111,7 +111,10 @@ struct SketchLaunch {
     float* pnodes;     // [M][nodes_local][r] P_i, or nullptr (mode 0 without debug)
     int mode;          // 0 = reduce locally -> sigma ; 1 = exchange (write pnodes only) ;
                        // 2 = Top-K baseline: per-node exact ||row||^2 -> sigma[node][M]
-    int M;             // ARC rows (stride of the per-node sigma in mode 2)
+                       // 3 = Rand-K: the row's shared random key -> sigma (node-0 tiles)
+    int M;
+    uint2 key;         // Rand-K: Philox key (seed)
+    unsigned t_lo, t_hi;             // ARC rows (stride of the per-node sigma in mode 2)
     int num_blocks;
     int shape;         // tile shape R x W: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128
     unsigned* status;

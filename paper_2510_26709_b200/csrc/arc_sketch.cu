@@ -26,6 +26,7 @@
 
 #include "arc_device.cuh"
 #include "arc_internal.cuh"
+#include "arc_rng.cuh"
 
 namespace arc {
 namespace {
@@ -223,7 +224,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         // ------------------------------------------------------------ chains
         const bool live = crow < tc.m_rows;
         const int c0 = chunk * W;
-        if (a.mode == 2) {
+        if (a.mode == 3) {
+            // Rand-K: no sketch, the selection does not look at the data
+        } else if (a.mode == 2) {
             // Top-K baseline: lane 0 of the row sums Delta_q^2 in column order
             if (crow < R && jl == 0) {
                 const int qmax = live ? min(W, row_cols(tc, crow) - c0) : 0;
@@ -251,7 +254,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         }
 
         // ------------------------------------------------ per-(tile, node) epilogue
-        if (chunk == tc.nchunks - 1 && a.mode == 2) {
+        if (chunk == tc.nchunks - 1 && a.mode == 3) {
+            // Rand-K: row p's shared key (R16), written once (node-0 tiles)
+            const int p = tc.row0 + crow;
+            if (jl == 0 && live && node == 0) {
+                const uint4 x = rng::philox4x32_10(
+                    make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(tc.b) | 0x80000000u, a.t_lo, a.t_hi), a.key);
+                const float sig = __uint_as_float(x.x >> 2);
+                a.sigma[tc.row_base + p] = sig;
+                atomicAdd(&hist[order_key_dev(sig) >> kHist1Shift], 1u);
+            }
+        } else if (chunk == tc.nchunks - 1 && a.mode == 2) {
             // Top-K baseline: this node's own ||row||^2 and its selection histogram
             const int p = tc.row0 + crow;
             if (jl == 0 && live) {
@@ -294,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         }
         if (!more || tl.b != tc.b) {             // block boundary: publish the histogram
             __syncthreads();
-            if (a.mode == 0) flush_hist(tc.b);
+            if (a.mode == 0 || a.mode == 3) flush_hist(tc.b);
             __syncthreads();
         }
         if (!more) break;

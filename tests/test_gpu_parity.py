@@ -41,14 +41,16 @@ def assert_same_floats(gpu: np.ndarray, ref: np.ndarray, what: str):
 
 
 def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, reduce="nccl",
-               force_exchange=False, check_debug=True, host=False, nodes_local=None, pg=None, ts=None):
+               force_exchange=False, check_debug=True, host=False, nodes_local=None, pg=None, ts=None,
+               method="arc"):
     from paper_2510_26709_b200 import ArcTopK
     nl = N if nodes_local is None else nodes_local
     assert nl == N, "single-GPU parity: all nodes local"
     src = GradientSource(d, blocks, N, seed=seed) if grads_fn is None else None
     ctx = ArcTopK(d, blocks, N=N, eta=eta, r=r, seed=seed, nodes_local=nl, reduce=reduce,
-                  debug_sketch=check_debug, force_exchange=force_exchange, host_staging=host, pg=pg)
-    o = orc.OracleEF21M(d, blocks, N=N, eta=eta, r=r, seed=seed)
+                  debug_sketch=check_debug, force_exchange=force_exchange, host_staging=host, pg=pg,
+                  method=method)
+    o = orc.OracleEF21M(d, blocks, N=N, eta=eta, r=r, seed=seed, method=method)
     h = [torch.zeros(d, device=DEV) for _ in range(N)]
     g = [torch.zeros(d, device=DEV) for _ in range(N)]
     gbar = torch.zeros(d, device=DEV)
@@ -66,8 +68,9 @@ def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, 
             ctx.step(t, [torch.from_numpy(x).to(DEV) for x in gr], h, g, gbar, sel, vals)
         ref = o.step(t, gr, debug=check_debug)
         torch.cuda.synchronize()
-        if check_debug:
+        if check_debug and method == "arc":
             assert_same_floats(ctx.query(0).cpu().numpy(), ref["V"], f"V (t={t})")
+        if check_debug:
             assert_same_floats(ctx.query(1).cpu().numpy(), ref["sigma"], f"Sigma (t={t})")
         assert np.array_equal(sel.cpu().numpy(), ref["sel"]), f"selection differs at t={t}"
         assert_same_floats(vals.cpu().numpy(), ref["values"], f"values (t={t})")
@@ -303,3 +306,22 @@ def test_full_size_c4_llama_per_tensor(orc):
     d, blocks = config_blocks("C4")
     assert len(blocks) == 171 and d == 1_339_082_752
     run_parity(orc, d, blocks, N=1, steps=2, seed=20251030, check_debug=True)
+
+
+# ------------------------------------------------------------------ Rand-K (Table I row "Rand-K")
+
+@pytest.mark.parametrize("N,d,n,K", [(1, 50_000, 100, 7), (4, 60_000, 96, 12), (3, 4_097, 3, 40)])
+def test_randk(orc, N, d, n, K):
+    """Shared-seed Rand-K through the same path: the keys, the selection, values and
+    state bit-exact against the oracle."""
+    run_parity(orc, d, flat_blocks(d, n, K=K), N=N, steps=4, method="randk")
+
+
+def test_randk_multiblock_and_exchange(orc):
+    shapes = [(300, 64, 5, 0), (13, 100, 13, 1), (77, 33, 4, 0)]
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n, m, n, K, kind))
+        off += m * n
+    run_parity(orc, off, blocks, N=2, steps=3, method="randk")
+    run_parity(orc, off, blocks, N=2, steps=3, method="randk", force_exchange=True, reduce="ordered")

@@ -506,3 +506,52 @@ def test_determinism(orc):
     for x, y in zip(a, b):
         assert np.array_equal(x["sel"], y["sel"]) and x["values"].tobytes() == y["values"].tobytes()
     assert oa.gbar.tobytes() == ob.gbar.tobytes()
+
+
+# ---------------------------------------------------------------- Rand-K (Table I)
+
+def test_randk_uniform_rows(orc):
+    """m = 10, K = 3 over 10^5 draws: every row kept with frequency 0.3 +- 0.01,
+    and the 120 possible 3-subsets are equally likely (chi-square)."""
+    from scipy import stats
+    m, K, T = 10, 3, 100_000
+    counts = np.zeros(m)
+    subsets = {}
+    for t in range(T):
+        sel = tuple(orc.argtop_k(orc.randk_keys(77, t, 0, m), K).tolist())
+        counts[list(sel)] += 1
+        subsets[sel] = subsets.get(sel, 0) + 1
+    assert np.all(np.abs(counts / T - 0.3) <= 0.01)
+    assert len(subsets) == 120
+    assert stats.chisquare(list(subsets.values())).pvalue > 1e-3
+
+
+def test_randk_shared_and_data_independent(orc):
+    """Shared seed: identical on every node, independent of the data, K = m keeps every
+    row; another seed or iteration gives another subset."""
+    d, n, K = 4000, 40, 9
+    blocks = flat_blocks(d, n, K=K)
+    rng = np.random.default_rng(1)
+    sels = []
+    for data in (np.zeros(d, np.float32), rng.standard_normal(d).astype(np.float32)):
+        o = orc.OracleEF21M(d, blocks, N=3, eta=0.5, r=4, seed=123, method="randk")
+        sels.append(o.step(4, [data] * 3)["sel"])
+    assert np.array_equal(sels[0], sels[1])
+    keys = orc.randk_keys(123, 4, 0, d // n)
+    assert np.array_equal(sels[0], orc.argtop_k(keys, K))
+    assert not np.array_equal(orc.argtop_k(orc.randk_keys(124, 4, 0, 100), K), orc.argtop_k(keys, K))
+    assert not np.array_equal(orc.argtop_k(orc.randk_keys(123, 5, 0, 100), K), orc.argtop_k(keys, K))
+    o = orc.OracleEF21M(d, flat_blocks(d, n, K=d // n), N=2, eta=1.0, r=4, seed=1, method="randk")
+    assert o.step(0, [rng.standard_normal(d)] * 2)["sel"].tolist() == list(range(d // n))
+
+
+def test_randk_values_are_node_average_of_rows(orc):
+    """C(g) = (1/N) sum_i [G_i]_{I,:} on the shared random rows (P:242 with Rand-K rows)."""
+    rng = np.random.default_rng(2)
+    d, n, K, N = 3000, 30, 7, 4
+    o = orc.OracleEF21M(d, flat_blocks(d, n, K=K), N=N, eta=1.0, r=4, seed=5, method="randk")
+    gr = [rng.standard_normal(d).astype(np.float32) for _ in range(N)]
+    res = o.step(0, gr)
+    rows = np.stack([x.reshape(-1, n) for x in gr])[:, res["sel"]].astype(np.float64)
+    mean, mag = rows.mean(0), np.abs(rows).mean(0)
+    assert np.all(np.abs(res["values"].reshape(K, n) - mean) <= N * 2 ** -24 * mag + 1e-30)
