@@ -1,0 +1,124 @@
+"""EF21M + ARC-Top-K as a PyTorch DDP communication hook.
+
+Every DDP gradient bucket gets its own compression context (per-tensor blocks
+in the bucket's order: each 2-D (or conv) tensor is an ARC block of rows =
+output units, every other tensor a DENSE block — P:510 "we compress only
+two-dimensional tensors"; per-tensor K).  The hook returns the
+bucket's replicated tracker gbar = (1/N) sum_i g_i, so the optimizer that
+follows applies x <- x - gamma gbar (eq:ef21m-3) — or Adam on gbar, as
+in the paper's experiments.
+
+For the first `warmup_steps` iterations the hook averages the gradients
+densely (the paper starts compression after 1000 iterations); at the
+switch it initialises the EF21M state with h = g = the local gradient and gbar
+= their average (V_0 = 0, the Theorem 1 setting).
+
+Each bucket's step runs on a side stream that first waits for the backward
+stream, so a bucket's compression overlaps the backward pass of the layers
+still to come; the returned future carries the side stream's completion.
+
+    from paper_2510_26709_b200.ddp import ArcTopKHookState, arc_topk_hook
+    state = ArcTopKHookState(mu_bp=100, eta=0.1, r=4, seed=1234, warmup_steps=1000)
+    ddp_model.register_comm_hook(state, arc_topk_hook)
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .api import ArcTopK, Block
+from . import _lib as L
+
+
+def bucket_layout(shapes, mu_bp: int, dense_n: int = 1024) -> tuple[int, list[Block]]:
+    """Blocks for tensors laid out back to back in this order."""
+    blocks, off = [], 0
+    for s in shapes:
+        numel = 1
+        for x in s:
+            numel *= int(x)
+        if len(s) >= 2 and numel > 0:
+            m, n = int(s[0]), numel // int(s[0])
+            K = max(1, min(m, -(-m * int(mu_bp) // 10000)))
+            blocks.append(Block(off, numel, m, n, K, L.BLOCK_ARC))
+        elif numel > 0:
+            n = min(numel, dense_n)
+            m = -(-numel // n)
+            blocks.append(Block(off, numel, m, n, m, L.BLOCK_DENSE))
+        off += numel
+    return off, blocks
+
+
+class ArcTopKHookState:
+    """Hook state: compression settings plus one context and EF21M state per bucket."""
+
+    def __init__(self, mu_bp: int = 100, eta: float = 0.1, r: int = 4, seed: int = 20251030,
+                 warmup_steps: int = 0, process_group=None, reduce: str = "nccl"):
+        self.mu_bp, self.eta, self.r, self.seed = int(mu_bp), float(eta), int(r), int(seed)
+        self.warmup_steps = int(warmup_steps)
+        self.pg = process_group
+        self.reduce = reduce
+        self.iteration = 0
+        self.buckets: dict[int, dict] = {}
+        self._stream = None
+
+    def world(self) -> int:
+        return dist.get_world_size(self.pg) if dist.is_initialized() else 1
+
+    def stream(self, device) -> torch.cuda.Stream:
+        if self._stream is None:
+            self._stream = torch.cuda.Stream(device=device)
+        return self._stream
+
+    def context(self, index: int, bucket) -> dict:
+        b = self.buckets.get(index)
+        buf = bucket.buffer()
+        shapes = [tuple(p.shape) for p in bucket.parameters()]
+        if b is None or b["shapes"] != shapes:   # new bucket (DDP rebuilds its buckets once, early)
+            d, blocks = bucket_layout(shapes, self.mu_bp)
+            assert d == buf.numel(), "bucket buffer does not match its parameters"
+            N = self.world()
+            pg = self.pg if self.pg is not None else (dist.group.WORLD if N > 1 else None)
+            ctx = ArcTopK(d, blocks, N=N, eta=self.eta, r=self.r, seed=self.seed + 7919 * index, nodes_local=1,
+                          pg=pg, rank=dist.get_rank(pg) if pg is not None else 0, reduce=self.reduce,
+                          device=buf.device)
+            b = {"d": d, "ctx": ctx, "h": torch.zeros_like(buf), "g": torch.zeros_like(buf),
+                 "gbar": torch.zeros_like(buf), "shapes": shapes, "blocks": blocks}
+            self.buckets[index] = b
+        return b
+
+
+def arc_topk_hook(state: ArcTopKHookState, bucket) -> torch.futures.Future:
+    """DDP comm hook: dense average during warm-up, then one EF21M + ARC-Top-K step
+    per bucket; the bucket's gradient becomes gbar."""
+    buf = bucket.buffer()
+    device = buf.device
+    idx = bucket.index()
+    t = state.iteration
+    if bucket.is_last():
+        state.iteration += 1
+    N = state.world()
+    main = torch.cuda.current_stream(device)
+    side = state.stream(device)
+    side.wait_stream(main)
+    fut = torch.futures.Future(devices=[device])
+    with torch.cuda.stream(side):
+        buf.record_stream(side)
+        if t < state.warmup_steps:
+            if N > 1:
+                dist.all_reduce(buf, group=state.pg)
+                buf.div_(N)
+        else:
+            b = state.context(idx, bucket)
+            if t == state.warmup_steps:          # switch: h = g = local gradient, gbar = average
+                b["h"].copy_(buf)
+                b["g"].copy_(buf)
+                b["gbar"].copy_(buf)
+                if N > 1:
+                    dist.all_reduce(b["gbar"], group=state.pg)
+                    b["gbar"].div_(N)
+            else:
+                b["ctx"].step(t, [buf], [b["h"]], [b["g"]], b["gbar"], stream=side)
+            buf.copy_(b["gbar"])
+        fut.set_result(buf)
+    return fut
