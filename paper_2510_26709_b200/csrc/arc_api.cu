@@ -356,6 +356,7 @@ struct arc_topk_ctx {
     uint64_t step_count = 0;     // parity of the selection's double-buffered candidate counters
     unsigned long long* stamps = nullptr;   // debug (ARC_DEBUG_STAMPS=1): library-owned device buffer
     int64_t v_ready = -1;        // t whose V the previous step generated speculatively
+    bool pdl = true;             // programmatic dependent launch between the step's kernels (ARC_PDL=0: off)
     int64_t last_t = 0;
     int64_t v_items = 0;
 
@@ -505,6 +506,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
 
     for (const BlockDev& B : c->pl.bdev)
         if (B.kind == ARC_BLOCK_ARC) c->v_items += static_cast<int64_t>(B.n) * ((c->p.r + 3) / 4);
+    if (const char* e = getenv("ARC_PDL")) c->pdl = e[0] != '0';
     c->ome = 1.0f - c->p.eta;                       // R11, fp32
     c->c_r = 1.0f / sqrtf(static_cast<float>(c->p.r));   // R2: fl(1 / sqrt_rn(r))
     c->Nf = static_cast<float>(c->p.N);             // R3
@@ -605,6 +607,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.M = pl.M;
         a.num_blocks = c->p.num_blocks;
         a.shape = c->shape;
+        a.pdl = c->pdl && !c->timing ? 1 : 0;
         a.status = status;
         ARC_MARK(1);
         launch_ef_sketch(a, s);
@@ -680,6 +683,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.parity = static_cast<int>(c->step_count & 1);
         sg.sel = pl.topk ? reinterpret_cast<int32_t*>(wire) : sel;
         sg.stamps = c->stamps;
+        sg.pdl = c->pdl && !c->timing && !(pl.exchange && pl.M > 0) ? 1 : 0;
         const bool spec = pl.M > 0 && !pl.topk && !pl.randk && t < INT64_MAX;
         if (spec) {
             const uint64_t tn = static_cast<uint64_t>(t + 1);

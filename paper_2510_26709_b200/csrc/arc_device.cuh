@@ -44,5 +44,9 @@ static __device__ __forceinline__ unsigned order_key_dev(float s) {
     return isnan(s) ? 0xFFFFFFFFu : __float_as_uint(s);
 }
 
+// Programmatic dependent launch: wait until the preceding kernel's writes are
+// visible (a no-op when the kernel was launched without the PDL attribute).
+static __device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace dev
 }  // namespace arc

@@ -84,6 +84,7 @@ struct SelectGatherLaunch {
     int r;
     uint2 key;
     unsigned t_lo, t_hi;
+    int pdl;                       // launch with programmatic stream serialization
 };
 
 struct NodePtrs {
@@ -117,6 +118,7 @@ struct SketchLaunch {
     unsigned t_lo, t_hi;             // ARC rows (stride of the per-node sigma in mode 2)
     int num_blocks;
     int shape;         // tile shape R x W: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128
+    int pdl;           // launch with programmatic stream serialization (overlap the launch)
     unsigned* status;
 };
 void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s);

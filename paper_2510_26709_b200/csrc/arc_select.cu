@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
 
     const SliceItem it = s.items[blockIdx.x];
     const BlockDev B = s.blocks[it.b];
+    grid_dependency_wait();   // Sigma and the digit-1 histogram are complete
     const int tid = threadIdx.x;
     const int lo = it.c * s.slice_rows, hi = min(B.m, lo + s.slice_rows), nk = hi - lo;
     const bool arc = B.kind == ARC_BLOCK_ARC && B.K < B.m;
@@ -572,9 +573,19 @@ int select_gather_resident_ctas() {
 int select_max_slice_rows() { return kMaxSliceRows; }
 
 cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch& ga, cudaStream_t st) {
-    void* args[] = {const_cast<SelectGatherLaunch*>(&s), const_cast<GatherLaunch*>(&ga)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_select_gather), dim3(s.num_items),
-                                       dim3(kThreads), args, 0, st);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(s.num_items);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = s.pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, k_select_gather, s, ga);
 }
 
 }  // namespace arc

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
     if (list_begin >= list_end) return;
     const int r = a.r;
     for (int i = tid; i < kHist1Bins; i += kThreads) hist[i] = 0;
+    grid_dependency_wait();   // the previous kernel (g, V, histogram reset) is complete
     // (the first __syncthreads of the main loop orders this before any use)
     auto flush_hist = [&](int b) {               // all threads; after a __syncthreads
         unsigned* gh = a.hist1 + static_cast<long long>(b) * kHist1Bins;
@@ -319,12 +320,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
 }
 
 // RPT (sums per lane) = ceil(r / 4); the widest shape stops at r <= 16 (shared memory)
+template <class K>
+void launch_pdl(K kernel, const SketchLaunch& a, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(a.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 template <int R, int W>
 void launch_rw(const SketchLaunch& a, cudaStream_t s) {
-    if (a.r <= 4) k_ef_sketch<R, W, 1><<<a.grid, kThreads, 0, s>>>(a);
-    else if (a.r <= 8) k_ef_sketch<R, W, 2><<<a.grid, kThreads, 0, s>>>(a);
-    else if (a.r <= 16) k_ef_sketch<R, W, 4><<<a.grid, kThreads, 0, s>>>(a);
-    else if constexpr (W < 128) k_ef_sketch<R, W, 8><<<a.grid, kThreads, 0, s>>>(a);
+    if (a.r <= 4) launch_pdl(k_ef_sketch<R, W, 1>, a, s);
+    else if (a.r <= 8) launch_pdl(k_ef_sketch<R, W, 2>, a, s);
+    else if (a.r <= 16) launch_pdl(k_ef_sketch<R, W, 4>, a, s);
+    else if constexpr (W < 128) launch_pdl(k_ef_sketch<R, W, 8>, a, s);
 }
 
 template <int R, int W>
