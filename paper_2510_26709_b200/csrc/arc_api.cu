@@ -69,7 +69,7 @@ struct Plan {
     std::vector<BlockDev> sbdev;     // selection blocks: bdev, or (Top-K) one copy per local node
     std::vector<SelRow> segs;        // gather segments over sbdev
     std::vector<SelRow> segs_real;   // segments over bdev (scatter, Top-K merge)
-    bool dense_fast = false;         // DENSE blocks handled by k_dense (G == 1, ARC)
+    bool dense_fast = false;         // DENSE blocks handled by the streaming k_dense (not Top-K)
     std::vector<int> dense_ids;
     // workspace offsets (bytes)
     size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
@@ -149,9 +149,11 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         }
         sumK += B.K;
         sumKn += B.K * B.n;
-        const int nq = static_cast<int>((B.n + 3) / 4);
-        for (int64_t k = 0; k < B.K; ++k)
-            for (int q0 = 0; q0 < nq; q0 += kSegQuads) pl.segs_real.push_back(SelRow{b, static_cast<int>(k), q0});
+        if (!(B.kind == ARC_BLOCK_DENSE && p->method != ARC_METHOD_TOPK_ALLGATHER)) {   // DENSE: streaming kernels
+            const int nq = static_cast<int>((B.n + 3) / 4);
+            for (int64_t k = 0; k < B.K; ++k)
+                for (int q0 = 0; q0 < nq; q0 += kSegQuads) pl.segs_real.push_back(SelRow{b, static_cast<int>(k), q0});
+        }
     }
     pl.M = static_cast<int>(M);
     pl.sumK = sumK;
@@ -163,7 +165,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.topk = p->method == ARC_METHOD_TOPK_ALLGATHER;
     pl.W = sumKn + sumK;
     // every node local and ARC: DENSE blocks take the streaming kernel, not the selection
-    pl.dense_fast = !pl.topk && !pl.exchange;
+    pl.dense_fast = !pl.topk;
     for (int b = 0; b < p->num_blocks; ++b)
         if (pl.dense_fast && pl.bdev[b].kind == ARC_BLOCK_DENSE) pl.dense_ids.push_back(b);
     const int nl = pl.topk ? pl.L : 1;
@@ -702,7 +704,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             return ARC_ERR_CUDA;
         }
     }
-    if (!pl.dense_ids.empty()) {   // DENSE blocks, every node local: identity compressor, streaming
+    if (!pl.dense_ids.empty()) {   // DENSE blocks: identity compressor, streaming
         DenseLaunch dl{};
         dl.blocks = blocks;
         dl.dense_ids = c->at<int>(pl.o_dense_ids);
@@ -714,8 +716,10 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         dl.Nf = c->Nf;
         dl.N_int = c->p.N;
         dl.gbar = gbar;
-        dl.values = values_out;
         dl.sel = sel;
+        dl.mode = !pl.exchange ? 0 : (ordered ? 2 : 1);
+        dl.values = !pl.exchange ? values_out : wire;
+        dl.sum_Kn = pl.sumKn;
         launch_dense(dl, s);
         ARC_LAUNCHED();
     }
@@ -770,8 +774,26 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sa.Nf = c->Nf;
         sa.gbar = gbar;
         sa.values = values_out;
-        launch_scatter(sa, s);
-        ARC_LAUNCHED();
+        if (sa.num_rows > 0) {
+            launch_scatter(sa, s);
+            ARC_LAUNCHED();
+        }
+        if (!pl.dense_ids.empty()) {
+            DenseScatterLaunch ds{};
+            ds.blocks = blocks;
+            ds.dense_ids = c->at<int>(pl.o_dense_ids);
+            ds.num_dense = static_cast<int>(pl.dense_ids.size());
+            ds.wire = reduced;
+            ds.mode = ordered ? 1 : 0;
+            ds.nodes_total = c->p.N;
+            ds.sum_Kn = pl.sumKn;
+            ds.Nf = c->Nf;
+            ds.N_int = c->p.N;
+            ds.gbar = gbar;
+            ds.values = values_out;
+            launch_dense_scatter(ds, s);
+            ARC_LAUNCHED();
+        }
     }
     ARC_MARK(5);
     if (sel_out != nullptr)

@@ -177,10 +177,29 @@ struct DenseLaunch {
     float eta, ome, Nf;
     int N_int;
     float* gbar;
-    float* values;              // optional
+    float* values;              // mode 0: optional A/N; modes 1, 2: the exchange payload
     int32_t* sel;               // identity selection written here
+    int mode;                   // 0 = fused local; 1 = payload = local node sum; 2 = payload per node
+    long long sum_Kn;           // mode 2: per-node payload stride
 };
 void launch_dense(const DenseLaunch& a, cudaStream_t s);
+
+// DENSE blocks after exchange #2: gbar += A / N (A all-reduced, or the ordered
+// sum over the all-gathered per-node payloads).
+struct DenseScatterLaunch {
+    const BlockDev* blocks;
+    const int* dense_ids;
+    int num_dense;
+    const float* wire;
+    int mode;                   // 0 = summed; 1 = [N][sum_Kn] per node, ordered sum
+    int nodes_total;
+    long long sum_Kn;
+    float Nf;
+    int N_int;
+    float* gbar;
+    float* values;              // optional A/N
+};
+void launch_dense_scatter(const DenseScatterLaunch& a, cudaStream_t s);
 
 // Top-K baseline merge of one node's gathered payload: gbar[I_j] += C_j / N.
 struct MergeLaunch {

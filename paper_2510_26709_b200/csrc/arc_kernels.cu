@@ -177,6 +177,10 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
         // identity selection
         for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < B.m; p += (long long)gridDim.x * blockDim.x)
             a.sel[B.sel_base + p] = static_cast<int32_t>(p);
+        // payload element (block-relative q) of node i (mode 2) or of the local sum
+        auto out_at = [&](long long q, int i) -> float* {
+            return a.values + (a.mode == 2 ? static_cast<long long>(i) * a.sum_Kn : 0LL) + B.val_base + q;
+        };
         // element loop: quads when the block is 16-byte aligned, else scalars
         const bool vec = (B.off % 4) == 0;
         const long long nq = vec ? len / 4 : 0;
@@ -188,17 +192,26 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
                 const float4 gr = __ldcs(reinterpret_cast<const float4*>(a.nodes.grad[i] + e));
                 const float4 gv = *reinterpret_cast<const float4*>(a.nodes.g[i] + e);
                 const float h4[4] = {hv.x, hv.y, hv.z, hv.w}, r4[4] = {gr.x, gr.y, gr.z, gr.w}, g4[4] = {gv.x, gv.y, gv.z, gv.w};
-                float hn[4], gn[4];
+                float hn[4], gn[4], c4[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     hn[k] = fadd(fmul(a.ome, h4[k]), fmul(a.eta, r4[k]));   // R11
-                    const float c = fsub(hn[k], g4[k]);                      // R4
-                    gn[k] = fadd(g4[k], c);                                  // R12
-                    A[k] = (i == 0) ? c : fadd(A[k], c);                     // R9 node order
+                    c4[k] = fsub(hn[k], g4[k]);                              // R4
+                    gn[k] = fadd(g4[k], c4[k]);                              // R12
+                    A[k] = (i == 0) ? c4[k] : fadd(A[k], c4[k]);             // R9 node order
                 }
                 *reinterpret_cast<float4*>(a.nodes.h[i] + e) = make_float4(hn[0], hn[1], hn[2], hn[3]);
                 *reinterpret_cast<float4*>(a.nodes.g[i] + e) = make_float4(gn[0], gn[1], gn[2], gn[3]);
+                if (a.mode == 2)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) *out_at(4 * f + k, i) = c4[k];
             }
+            if (a.mode == 1) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) *out_at(4 * f + k, 0) = A[k];
+                continue;
+            }
+            if (a.mode == 2) continue;
             const float4 bv = *reinterpret_cast<const float4*>(a.gbar + e);
             const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
             float v[4], bn[4];
@@ -217,7 +230,11 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
         for (long long q = 4 * nq + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
              q += (long long)gridDim.x * blockDim.x) {
             if (q >= len) {
-                if (a.values != nullptr) a.values[B.val_base + q] = 0.0f;
+                if (a.mode == 2) {
+                    for (int i = 0; i < a.nodes_local; ++i) *out_at(q, i) = 0.0f;
+                } else if (a.values != nullptr) {
+                    *out_at(q, 0) = 0.0f;
+                }
                 continue;
             }
             const long long e = B.off + q;
@@ -229,10 +246,32 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
                 const float c = fsub(hn, gv);
                 a.nodes.g[i][e] = fadd(gv, c);
                 A = (i == 0) ? c : fadd(A, c);
+                if (a.mode == 2) *out_at(q, i) = c;
             }
+            if (a.mode == 1) { *out_at(q, 0) = A; continue; }
+            if (a.mode == 2) continue;
             const float v = pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf);
             a.gbar[e] = fadd(a.gbar[e], v);
             if (a.values != nullptr) a.values[B.val_base + q] = v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_dense_scatter(const DenseScatterLaunch a) {
+    const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
+    const float invN = 1.0f / a.Nf;
+    for (int db = 0; db < a.num_dense; ++db) {
+        const BlockDev& B = a.blocks[a.dense_ids[db]];
+        const long long total = static_cast<long long>(B.m) * B.n;
+        for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+             q += (long long)gridDim.x * blockDim.x) {
+            const long long o = B.val_base + q;
+            float A = a.wire[o];
+            if (a.mode == 1)
+                for (int i = 1; i < a.nodes_total; ++i) A = fadd(A, a.wire[static_cast<long long>(i) * a.sum_Kn + o]);
+            const float v = q < B.len ? (pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf)) : 0.0f;
+            if (q < B.len) a.gbar[B.off + q] = fadd(a.gbar[B.off + q], v);
+            if (a.values != nullptr) a.values[o] = v;
         }
     }
 }
@@ -271,6 +310,10 @@ static int rows_grid(int num_rows) {
 
 void launch_dense(const DenseLaunch& a, cudaStream_t s) {
     k_dense<<<148 * 8, 256, 0, s>>>(a);
+}
+
+void launch_dense_scatter(const DenseScatterLaunch& a, cudaStream_t s) {
+    k_dense_scatter<<<148 * 8, 256, 0, s>>>(a);
 }
 
 void launch_topk_merge(const MergeLaunch& a, cudaStream_t s) {

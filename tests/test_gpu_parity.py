@@ -151,6 +151,9 @@ def test_multi_block_with_dense(orc):
         blocks.append(Block(off, m * n, m, n, K, kind))
         off += m * n
     run_parity(orc, off, blocks, N=3, steps=3)
+    # the exchange path: DENSE rows through the streaming kernels and the payload
+    run_parity(orc, off, blocks, N=3, steps=3, force_exchange=True, reduce="nccl")
+    run_parity(orc, off, blocks, N=3, steps=3, force_exchange=True, reduce="ordered")
 
 
 def test_llama_layout_small_mu(orc):
