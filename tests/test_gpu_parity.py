@@ -328,3 +328,34 @@ def test_randk_multiblock_and_exchange(orc):
         off += m * n
     run_parity(orc, off, blocks, N=2, steps=3, method="randk")
     run_parity(orc, off, blocks, N=2, steps=3, method="randk", force_exchange=True, reduce="ordered")
+
+
+# ------------------------------------------------------------------ randomized sweep
+
+def _random_case(rng):
+    nb = int(rng.integers(1, 5))
+    blocks, off = [], 0
+    for _ in range(nb):
+        n = int(rng.choice([1, 2, 3, 4, 5, 7, 31, 64, 96, 127, 128, 500, 768, 1024, 2051]))
+        m = int(rng.integers(1, max(2, 60_000 // n)))
+        ln = m * n - int(rng.integers(0, n)) if rng.random() < 0.4 else m * n   # ragged last row
+        kind = 1 if rng.random() < 0.15 else 0
+        K = m if kind == 1 else int(rng.integers(1, m + 1)) if rng.random() < 0.2 else max(1, m // int(rng.integers(2, 200)))
+        blocks.append(Block(off, ln, m, n, K, kind))
+        off += ln
+    return off, blocks
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_randomized_configurations(orc, case):
+    """Seeded random layouts, sketch widths, node counts, momenta, methods and paths."""
+    rng = np.random.default_rng(1000 + case)
+    d, blocks = _random_case(rng)
+    N = int(rng.integers(1, 6))
+    r = int(rng.choice([1, 2, 4, 5, 8, 16]))
+    eta = float(rng.choice([1.0, 0.5, 0.1, 0.01]))
+    method = str(rng.choice(["arc", "arc", "arc", "randk"]))
+    fx = bool(rng.random() < 0.3)
+    reduce = str(rng.choice(["nccl", "ordered"]))
+    run_parity(orc, d, blocks, N=N, steps=2, eta=eta, r=r, seed=case, method=method,
+               force_exchange=fx, reduce=reduce)
