@@ -272,6 +272,8 @@ def main():
     ap.add_argument("--pool", type=int, default=8, help="distinct gradient sets cycled in the timed loop")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--mu-bp", type=int, default=None, help="override K/m in basis points (e.g. 10, 100, 1000)")
+    ap.add_argument("--force-exchange", action="store_true",
+                    help="diagnostic: run the multi-GPU kernel sequence on one GPU (collectives become copies)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     if args.impl == "reference":
@@ -309,7 +311,7 @@ def main():
     g = [torch.zeros(d, device=dev) for _ in range(L)]
     gbar = torch.zeros(d, device=dev)
     ctx = ArcTopK(d, blocks, N=N, eta=0.1, r=4, seed=20251030, nodes_local=L, pg=pg, rank=rank,
-                  reduce=args.reduce, host_staging=True)
+                  reduce=args.reduce, host_staging=True, force_exchange=args.force_exchange)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -399,7 +401,10 @@ def main():
     # ---------------------------------------------------------------- baselines (same run)
     baselines = {}
     if not args.no_baselines:
-        baselines = run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, stream, barrier)
+        try:
+            baselines = run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, stream, barrier)
+        except Exception as e:  # a baseline must never cost the headline line
+            baselines = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

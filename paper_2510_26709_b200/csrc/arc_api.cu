@@ -348,7 +348,7 @@ struct arc_topk_ctx {
     Nccl nccl;
     ncclComm_t comm = nullptr;
     unsigned char* ws = nullptr;
-    int grid = 0, num_tiles = 0, shape = 0, max_m = 1;
+    int grid = 0, num_tiles = 0, shape = 0;
     float ome = 0.f, c_r = 0.f, Nf = 0.f;
     cudaStream_t last = nullptr;
     // per-phase timing
@@ -475,8 +475,6 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
                c->grid);
     c->num_tiles = static_cast<int>(tiles.size());
     {
-        for (const BlockDev& B : c->pl.bdev)
-            if (B.kind == ARC_BLOCK_ARC) c->max_m = std::max(c->max_m, B.m);
     }
     const std::vector<SelRow>& rows = c->pl.segs;
 
@@ -619,12 +617,6 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     }
     ARC_MARK(2);
     // (DENSE blocks skip the sketch pass: the select/gather kernel applies their momentum.)
-    // S2 with several local nodes and no exchange: ordered node sum of the P_i
-    if (!pl.exchange && !pl.topk && !pl.randk && L > 1 && pl.M > 0) {
-        launch_sketch_reduce(blocks, c->p.num_blocks, c->max_m, c->at<float>(pl.o_pnodes), pl.M, 1, L, c->p.r, c->Nf,
-                             sigma, hist1, status, s);
-        ARC_LAUNCHED();
-    }
     // Exchange #1 + S2 for G > 1 (Rand-K needs none: every rank draws the same keys)
     if (pl.exchange && !pl.randk && pl.M > 0) {
         const size_t cnt = static_cast<size_t>(pl.M) * L * c->p.r;
@@ -635,8 +627,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         } else {
             ARC_CUDA(cudaMemcpyAsync(xr, xs, cnt * sizeof(float), cudaMemcpyDeviceToDevice, s));
         }
-        launch_sketch_reduce(blocks, c->p.num_blocks, c->max_m, xr, pl.M, pl.G, L, c->p.r, c->Nf, sigma, hist1, status, s);
-        ARC_LAUNCHED();
+        // (S2 itself — the ordered node sum and Sigma — is phase 0 of the selection kernel)
     }
     ARC_MARK(3);
     // S3 + S4 (+ S5, S6 when every node is local): one cooperative kernel
@@ -686,6 +677,17 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.sel = pl.topk ? reinterpret_cast<int32_t*>(wire) : sel;
         sg.stamps = c->stamps;
         sg.pdl = c->pdl && !c->timing && !(pl.exchange && pl.M > 0) ? 1 : 0;
+        if ((pl.exchange || L > 1) && !pl.randk && !pl.topk && pl.M > 0) {
+            // S2 (ordered node sum, Sigma) as phase 0 of the selection kernel, from the
+            // all-gathered sketches (exchange) or this GPU's per-node sketches
+            sg.xrecv = pl.exchange ? c->at<float>(pl.o_xrecv) : c->at<float>(pl.o_pnodes);
+            sg.sigma_w = sigma;
+            sg.G = pl.exchange ? pl.G : 1;
+            sg.L = L;
+            sg.M = pl.M;
+            sg.Nf = c->Nf;
+            sg.status = status;
+        }
         const bool spec = pl.M > 0 && !pl.topk && !pl.randk && t < INT64_MAX;
         if (spec) {
             const uint64_t tn = static_cast<uint64_t>(t + 1);
@@ -772,6 +774,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sa.nodes_total = c->p.N;
         sa.sum_Kn = pl.sumKn;
         sa.Nf = c->Nf;
+        sa.N_int = c->p.N;
         sa.gbar = gbar;
         sa.values = values_out;
         if (sa.num_rows > 0) {
@@ -880,7 +883,7 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     if (c->pl.randk)
         return (c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) + (c->pl.dense_ids.empty() ? 0 : 1) +
                (c->pl.exchange ? 1 : 0);
-    return arc + ((c->pl.exchange || c->pl.L > 1) && c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) +
+    return arc + (c->pl.items.empty() ? 0 : 1) +
            (c->pl.dense_ids.empty() ? 0 : 1) + (c->pl.exchange ? 1 : 0);
 }
 

@@ -85,6 +85,12 @@ struct SelectGatherLaunch {
     uint2 key;
     unsigned t_lo, t_hi;
     int pdl;                       // launch with programmatic stream serialization
+    // exchange path: Sigma computed here from the all-gathered sketches (else nullptr)
+    const float* xrecv;            // [G][M][L][r]
+    float* sigma_w;                // Sigma written for queries
+    int G, L, M;
+    float Nf;
+    unsigned* status;
 };
 
 struct NodePtrs {
@@ -126,9 +132,7 @@ int ef_sketch_resident_ctas(int r, int shape);   // SMs x occupancy
 int sketch_tile_rows(int shape);
 int sketch_shape_ok(int shape, int r);
 
-void launch_sketch_reduce(const BlockDev* blocks, int num_blocks, int max_m, const float* xrecv, int M, int G,
-                          int nodes_local, int r, float Nf, float* sigma, unsigned* hist1, unsigned* status,
-                          cudaStream_t s);
+
 
 struct GatherLaunch;
 cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch& ga, cudaStream_t st);
@@ -162,6 +166,7 @@ struct ScatterLaunch {
     int nodes_total;        // N (mode 1)
     long long sum_Kn;
     float Nf;
+    int N_int;
     float* gbar;
     float* values;          // optional A/N
 };

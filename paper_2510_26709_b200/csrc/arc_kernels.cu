@@ -9,7 +9,6 @@
 //   k_vgen          S0  V_b = Gaussian(seed, t, b)                  P:229-230, Alg.1 l.3
 //   k_ef_sketch     S1+S2  h' = (1-eta)h + eta grad; Delta = h' - g;  eq:ef21m-1 P:325,
 //                      P_i = (1/sqrt r) Delta V; (G==1) P, Sigma      P:231-237, Alg.1 l.4-6
-//   k_sketch_reduce S2 (G>1) ordered node sum of exchanged P_i, Sigma
 //   k_select        S3  I_b = argtop_K(Sigma), cluster radix select  zn28373 P:236-237
 //   k_gather_ef     S4 (+S5+S6 when G==1)                            2zn20 P:241-243, eq:ef21m-2
 //   k_scatter       S6 (G>1)                                         eq:ef21m-3 P:327
@@ -61,75 +60,49 @@ __device__ __forceinline__ int row_valid_cols(const BlockDev& B, int p) {
 
 
 // =============================================================================
-// S2 for G > 1: ordered node sum of the all-gathered P_i (R9, R21) and Sigma.
-// xrecv layout [G][M][L][r]; global node id = g*L + l.
-// =============================================================================
-__global__ void __launch_bounds__(256) k_sketch_reduce(const BlockDev* __restrict__ blocks, const float* __restrict__ xrecv,
-                                                       int M, int G, int L, int r, float Nf, float* __restrict__ sigma,
-                                                       unsigned* __restrict__ hist1, unsigned* status) {
-    __shared__ unsigned hist[kHist1Bins];
-    const int b = blockIdx.y;
-    if (blocks[b].kind != ARC_BLOCK_ARC) return;
-    for (int i = threadIdx.x; i < kHist1Bins; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    const int m = blocks[b].m, base = blocks[b].row_base;
-    for (int pr = blockIdx.x * blockDim.x + threadIdx.x; pr < m; pr += gridDim.x * blockDim.x) {
-        const int p = base + pr;
-        float sig = 0.0f;
-        for (int j = 0; j < r; ++j) {
-            float S = 0.0f;
-            for (int g = 0; g < G; ++g)
-                for (int l = 0; l < L; ++l) {
-                    const float v = xrecv[((static_cast<long long>(g) * M + p) * L + l) * r + j];
-                    S = (g == 0 && l == 0) ? v : fadd(S, v);
-                }
-            const float pv = __fdiv_rn(S, Nf);
-            sig = fadd(sig, fmul(pv, pv));
-        }
-        sigma[p] = sig;
-        atomicAdd(&hist[order_key_dev(sig) >> kHist1Shift], 1u);   // digit-1 histogram (shared, then one flush)
-        if (!isfinite(sig)) atomicOr(status, kStatusNonfinite);
-    }
-    __syncthreads();
-    unsigned* gh = hist1 + static_cast<long long>(b) * kHist1Bins;
-    for (int i = threadIdx.x; i < kHist1Bins; i += blockDim.x)
-        if (hist[i]) atomicAdd(gh + i, hist[i]);
-}
-
-// =============================================================================
 // S6 for G > 1: gbar[I] += A / N after exchange #2.
 //   mode 0: wire holds the summed rows (NCCL All-Reduce)
 //   mode 1: wire holds [N][sumKn] per-node rows: ordered sum (R9) first
 // =============================================================================
 __global__ void __launch_bounds__(256) k_scatter(const ScatterLaunch a) {
-    const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int w = gw; w < a.num_rows; w += nw) {
-        const SelRow R = a.rows[w];
+    // one thread per 4 consecutive columns of a selected-row segment
+    const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
+    const float invN = 1.0f / a.Nf;
+    const long long items = static_cast<long long>(a.num_rows) * kSegQuads;
+    for (long long it = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; it < items;
+         it += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const SelRow R = a.rows[it / kSegQuads];
         const BlockDev& B = a.blocks[R.b];
+        const int q = 4 * (R.q0 + static_cast<int>(it % kSegQuads));
+        if (q >= B.n) continue;
         const int p = a.sel[B.sel_base + R.k];
-        const int n = B.n;
         const int nv = row_valid_cols(B, p);
-        const long long e0 = B.off + static_cast<long long>(p) * n;
-        const long long o0 = B.val_base + static_cast<long long>(R.k) * n;
-        const int qend = min(n, 4 * (R.q0 + kSegQuads));
-        for (int q = 4 * R.q0 + lane; q < qend; q += 32) {
-            if (q < nv) {
-                float A;
-                if (a.mode == 0) {
-                    A = a.wire[o0 + q];
-                } else {
-                    A = a.wire[o0 + q];
-                    for (int i = 1; i < a.nodes_total; ++i) A = fadd(A, a.wire[static_cast<long long>(i) * a.sum_Kn + o0 + q]);
-                }
-                const float val = __fdiv_rn(A, a.Nf);
-                a.gbar[e0 + q] = fadd(a.gbar[e0 + q], val);
-                if (a.values != nullptr) a.values[o0 + q] = val;
-            } else if (a.values != nullptr) {
-                a.values[o0 + q] = 0.0f;
-            }
+        const long long e0 = B.off + static_cast<long long>(p) * B.n;
+        const long long o0 = B.val_base + static_cast<long long>(R.k) * B.n;
+        const int cnt = max(0, min(4, nv - q)), ocnt = min(4, B.n - q);
+        float val[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= ocnt) continue;
+            float A = a.wire[o0 + q + k];
+            if (a.mode == 1)
+                for (int i = 1; i < a.nodes_total; ++i) A = fadd(A, a.wire[static_cast<long long>(i) * a.sum_Kn + o0 + q + k]);
+            val[k] = k < cnt ? (pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf)) : 0.0f;   // R3; +0 padding
         }
+        if (B.vec && cnt == 4) {
+            float4* gp = reinterpret_cast<float4*>(a.gbar + e0 + q);
+            float4 gb = *gp;
+            gb.x = fadd(gb.x, val[0]); gb.y = fadd(gb.y, val[1]); gb.z = fadd(gb.z, val[2]); gb.w = fadd(gb.w, val[3]);
+            *gp = gb;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < cnt) a.gbar[e0 + q + k] = fadd(a.gbar[e0 + q + k], val[k]);   // R13
+        }
+        if (a.values != nullptr)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < ocnt) a.values[o0 + q + k] = val[k];
     }
 }
 
@@ -292,15 +265,6 @@ void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r,
                                     static_cast<unsigned>(static_cast<uint64_t>(t) >> 32), V);
 }
 
-void launch_sketch_reduce(const BlockDev* blocks, int num_blocks, int max_m, const float* xrecv, int M, int G,
-                          int nodes_local, int r, float Nf, float* sigma, unsigned* hist1, unsigned* status,
-                          cudaStream_t s) {
-    int gx = (max_m + 255) / 256;
-    if (gx < 1) gx = 1;
-    if (gx > 1024) gx = 1024;
-    k_sketch_reduce<<<dim3(gx, num_blocks), 256, 0, s>>>(blocks, xrecv, M, G, nodes_local, r, Nf, sigma, hist1, status);
-}
-
 static int rows_grid(int num_rows) {
     int grid = (num_rows + 7) / 8;   // 8 warps per CTA, one warp per row segment
     if (grid < 1) grid = 1;
@@ -321,7 +285,11 @@ void launch_topk_merge(const MergeLaunch& a, cudaStream_t s) {
 }
 
 void launch_scatter(const ScatterLaunch& a, cudaStream_t s) {
-    k_scatter<<<rows_grid(a.num_rows), 256, 0, s>>>(a);
+    const long long quads = static_cast<long long>(a.num_rows) * kSegQuads;
+    long long grid = (quads + 255) / 256;
+    if (grid > 148 * 8) grid = 148 * 8;
+    if (grid < 1) grid = 1;
+    k_scatter<<<static_cast<int>(grid), 256, 0, s>>>(a);
 }
 
 }  // namespace arc

@@ -309,6 +309,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+template <bool kPhase0>
 __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
     cg::grid_group grid = cg::this_grid();
 #define STAMP(k) \
@@ -333,6 +334,87 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     unsigned* ccount = s.cand_count + par * s.num_blocks;                 // this step's counters
     unsigned* cand = s.cand + (static_cast<long long>(par) * s.num_blocks + bb) * (2 * kCandCap);
 
+    // ------------------------------------------------ phase 0 (exchange path)
+    // S2 after exchange #1: Sigma of this slice's rows from the all-gathered
+    // per-node sketches (sum in global node order, R9, R21), its digit-1
+    // histogram, then a grid barrier so the block's histogram is complete.
+    if constexpr (kPhase0) {
+        if (B.kind == ARC_BLOCK_ARC) {   // every ARC block gets its Sigma (queries); K < m ones select
+            for (int i = tid; i < kHist1Bins; i += kThreads) sh[i] = 0;
+            __syncthreads();
+            const long long M = s.M;
+            const int GL = s.G * s.L;                // global node id = g L + l
+            auto finish = [&](int i, const float* S) {
+                const long long p = B.row_base + lo + i;
+                float sig = 0.0f;
+                for (int j = 0; j < s.r; ++j) {
+                    const float pv = __fdiv_rn(S[j], s.Nf);                // R3
+                    sig = fadd(sig, fmul(pv, pv));                         // zn28373
+                }
+                s.sigma_w[p] = sig;
+                const unsigned key = order_key(sig);
+                s_keys[i] = key;
+                atomicAdd(&sh[key >> kHist1Shift], 1u);
+                if (!isfinite(sig)) atomicOr(s.status, kStatusNonfinite);
+            };
+            if (s.r == 4) {
+                // 4 rows per thread, 4 nodes per round: 16 float4 loads in flight
+                for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {
+                    float S[4][4];
+                    for (int n0 = 0; n0 < GL; n0 += 4) {
+                        float4 v[4][4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = i0 + u * kThreads + tid;
+                            const long long p = B.row_base + lo + i;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int node = n0 + k;
+                                if (i < nk && node < GL) {
+                                    const long long g = node / s.L, l = node % s.L;
+                                    v[u][k] = __ldcg(reinterpret_cast<const float4*>(s.xrecv + ((g * M + p) * s.L + l) * 4));
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                if (n0 + k >= GL) continue;
+                                const float4 w = v[u][k];
+                                if (n0 + k == 0) { S[u][0] = w.x; S[u][1] = w.y; S[u][2] = w.z; S[u][3] = w.w; }
+                                else {                                                   // R9 node order
+                                    S[u][0] = fadd(S[u][0], w.x); S[u][1] = fadd(S[u][1], w.y);
+                                    S[u][2] = fadd(S[u][2], w.z); S[u][3] = fadd(S[u][3], w.w);
+                                }
+                            }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + u * kThreads + tid;
+                        if (i < nk) finish(i, S[u]);
+                    }
+                }
+            } else {
+                for (int i = tid; i < nk; i += kThreads) {
+                    const long long p = B.row_base + lo + i;
+                    float S[32];
+                    for (int j = 0; j < s.r; ++j) {
+                        float a = 0.0f;
+                        for (int node = 0; node < GL; ++node) {
+                            const long long g = node / s.L, l = node % s.L;
+                            const float v = __ldcg(s.xrecv + ((g * M + p) * s.L + l) * s.r + j);
+                            a = node == 0 ? v : fadd(a, v);
+                        }
+                        S[j] = a;
+                    }
+                    finish(i, S);
+                }
+            }
+            if (arc) flush_hist(sh, s.hist1 + bb * kHist1Bins, kHist1Bins);
+        }
+        grid.sync();                                 // ---------------- barrier 0
+    }
     // ------------------------------------------------ phase A
     unsigned b1 = 0;
     int krem = B.K;
@@ -341,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
         unsigned hv[8];                              // digit-1 histogram, loaded alongside the keys
 #pragma unroll
         for (int k = 0; k < 8; ++k) hv[k] = __ldcg(s.hist1 + bb * kHist1Bins + tid + k * kThreads);
-        for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {
+        for (int i0 = 0; i0 < nk && !kPhase0; i0 += 4 * kThreads) {
             float v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -421,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     unsigned T = 0;
     int P_eq = 0x7FFFFFFF, need_eq = 0, sel_before = 0;
     bool use_peq = true;
-    if (arc && it.c == 0)
+    if (B.kind == ARC_BLOCK_ARC && it.c == 0)   // read by every slice before barrier 1: reset
         for (int i = tid; i < kHist1Bins; i += kThreads) s.hist1[bb * kHist1Bins + i] = 0;
     if (!overflow) {
         if (arc) {
@@ -566,7 +648,10 @@ int select_gather_resident_ctas() {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_gather, kThreads, 0);
+    int per_sm2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_gather<false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<true>, kThreads, 0);
+    if (per_sm2 < per_sm) per_sm = per_sm2;
     return sms * (per_sm < 1 ? 1 : per_sm);
 }
 
@@ -585,7 +670,8 @@ cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = s.pdl ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, k_select_gather, s, ga);
+    if (s.xrecv != nullptr) return cudaLaunchKernelEx(&cfg, k_select_gather<true>, s, ga);
+    return cudaLaunchKernelEx(&cfg, k_select_gather<false>, s, ga);
 }
 
 }  // namespace arc

@@ -13,7 +13,7 @@ dev = torch.device("cuda", 0)
 src = GradientSource(d, blocks, 1, seed=20251030, device=dev)
 pool = [src.grads(t) for t in range(4)]
 h, g, gbar = [torch.zeros(d, device=dev)], [torch.zeros(d, device=dev)], torch.zeros(d, device=dev)
-ctx = ArcTopK(d, blocks, N=1, eta=0.1, seed=20251030)
+ctx = ArcTopK(d, blocks, N=1, eta=0.1, seed=20251030, force_exchange=os.environ.get("ARC_PROBE_FX") == "1")
 names = ["A: keys, hist1, digit 1, candidates", "barrier 1", "post-barrier loads", "resolve + before",
          "compaction", "segment prefetch + barrier 2", "gather"]
 for t in range(60):
