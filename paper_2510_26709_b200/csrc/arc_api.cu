@@ -359,6 +359,7 @@ struct arc_topk_ctx {
     unsigned long long* stamps = nullptr;   // debug (ARC_DEBUG_STAMPS=1): library-owned device buffer
     int64_t v_ready = -1;        // t whose V the previous step generated speculatively
     bool pdl = true;             // programmatic dependent launch between the step's kernels (ARC_PDL=0: off)
+    bool early = true;           // early gather of the certain rows in the select kernel (ARC_EARLY=0: off)
     int64_t last_t = 0;
     int64_t v_items = 0;
 
@@ -417,17 +418,22 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     make_plan(&c->p, c->pl);
     if (workspace_bytes < c->pl.total) { delete c; return ARC_ERR_INVALID_ARG; }
     {   // the select/gather kernel is cooperative: one CTA per slice, all co-resident
+        // the smallest slice (multiple of 32 rows) whose slices all fit, so the
+        // grid fills the GPU; ARC_SLICE_ROWS forces a size (experiments)
         const int resident = select_gather_resident_ctas();
-        int rows = kSliceMin;
-        while (rows < select_max_slice_rows()) {
+        auto slices = [&](int rows) {
             int64_t n = 0;
-            for (const BlockDev& B : c->pl.sbdev) n += (B.m + rows - 1) / rows;
-            if (n <= resident) break;
-            rows *= 2;
+            for (const BlockDev& B : c->pl.sbdev)
+                if (!(c->pl.dense_fast && B.kind == ARC_BLOCK_DENSE)) n += (B.m + rows - 1) / rows;
+            return n;
+        };
+        int rows = kSliceMin;
+        while (rows < select_max_slice_rows() && slices(rows) > resident) rows += 32;
+        if (const char* e = std::getenv("ARC_SLICE_ROWS")) {
+            const int f = std::atoi(e);
+            if (f >= kSliceMin && f <= select_max_slice_rows() && slices(f) <= resident) rows = f;
         }
-        int64_t n = 0;
-        for (const BlockDev& B : c->pl.sbdev) n += (B.m + rows - 1) / rows;
-        if (n > resident) { delete c; return ARC_ERR_UNSUPPORTED; }
+        if (slices(rows) > resident) { delete c; return ARC_ERR_UNSUPPORTED; }
         const size_t total = c->pl.total;
         if (rows != kSliceMin) {
             c->pl = Plan();
@@ -507,6 +513,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     for (const BlockDev& B : c->pl.bdev)
         if (B.kind == ARC_BLOCK_ARC) c->v_items += static_cast<int64_t>(B.n) * ((c->p.r + 3) / 4);
     if (const char* e = getenv("ARC_PDL")) c->pdl = e[0] != '0';
+    if (const char* e = getenv("ARC_EARLY")) c->early = e[0] != '0';
     c->ome = 1.0f - c->p.eta;                       // R11, fp32
     c->c_r = 1.0f / sqrtf(static_cast<float>(c->p.r));   // R2: fl(1 / sqrt_rn(r))
     c->Nf = static_cast<float>(c->p.N);             // R3
@@ -677,6 +684,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.sel = pl.topk ? reinterpret_cast<int32_t*>(wire) : sel;
         sg.stamps = c->stamps;
         sg.pdl = c->pdl && !c->timing && !(pl.exchange && pl.M > 0) ? 1 : 0;
+        sg.early = c->early && ga.mode == 0 && ga.values == nullptr ? 1 : 0;
         if ((pl.exchange || L > 1) && !pl.randk && !pl.topk && pl.M > 0) {
             // S2 (ordered node sum, Sigma) as phase 0 of the selection kernel, from the
             // all-gathered sketches (exchange) or this GPU's per-node sketches

@@ -50,7 +50,7 @@ constexpr uint32_t kStatusNonfinite = 1u;
 constexpr int kHist1Bins = 2048;
 constexpr int kHist1Shift = 21;
 constexpr unsigned kHist1Mask = 0xFFE00000u;
-constexpr int kSliceMin = 512;     // rows per selection slice (one CTA), at least
+constexpr int kSliceMin = 256;     // rows per selection slice (one CTA), at least
 constexpr int kCandCap = 2048;     // boundary-bin candidates per block resolved in every CTA
 
 struct SliceItem {
@@ -85,6 +85,8 @@ struct SelectGatherLaunch {
     uint2 key;
     unsigned t_lo, t_hi;
     int pdl;                       // launch with programmatic stream serialization
+    int early;                     // mode 0 without values: gather the certainly selected rows
+                                   // (digit 1 above the boundary bin) before barrier 1 completes
     // exchange path: Sigma computed here from the all-gathered sketches (else nullptr)
     const float* xrecv;            // [G][M][L][r]
     float* sigma_w;                // Sigma written for queries

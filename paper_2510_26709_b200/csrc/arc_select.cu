@@ -247,6 +247,69 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
     }
 }
 
+// S4 + S5 + S6 of a list of selected rows of one block, every node local (mode 0,
+// no values output): the same arithmetic as gather_segments mode 0.  Row j of
+// the list is lo + list[j] (list == nullptr: lo + j).  The row's position in
+// the selection is not needed, so a CTA can run this before the selection of
+// the other slices is known.
+template <int UN>
+__device__ void gather_rows_local(const GatherLaunch& a, const BlockDev& B, int lo, const int* list, int cnt) {
+    const int nq = (B.n + 3) >> 2;
+    const int items = cnt * nq;
+    const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
+    const float invN = 1.0f / a.Nf;
+    for (int base = 0; base < items; base += kThreads * UN) {
+        int nv[UN];
+        long long e[UN];
+        bool v4[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const int item = base + u * kThreads + static_cast<int>(threadIdx.x);
+            nv[u] = 0;
+            e[u] = 0;
+            if (item < items) {
+                const int j = item / nq, q = 4 * (item - j * nq);
+                const int p = lo + (list != nullptr ? list[j] : j);
+                nv[u] = max(0, min(4, row_valid_cols(B, p) - q));
+                e[u] = B.off + static_cast<long long>(p) * B.n + q;
+            }
+            v4[u] = B.vec && nv[u] == 4;
+        }
+        Quad A[UN], gb[UN];
+        for (int i = 0; i < a.nodes_local; ++i) {
+            float* __restrict__ ph = a.nodes.h[i];
+            float* __restrict__ pg = a.nodes.g[i];
+            Quad hq[UN], gq[UN];
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                if (nv[u] == 0) continue;
+                if (i == 0) gb[u] = load_quad(a.gbar + e[u], v4[u], nv[u]);
+                gq[u] = load_quad(pg + e[u], v4[u], nv[u]);
+                hq[u] = load_quad(ph + e[u], v4[u], nv[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                if (nv[u] == 0) continue;
+                Quad gn;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const float c = fsub(hq[u].v[kk], gq[u].v[kk]);               // C_i
+                    gn.v[kk] = fadd(gq[u].v[kk], c);                               // R12
+                    A[u].v[kk] = i == 0 ? c : fadd(A[u].v[kk], c);                 // R9 node order
+                }
+                store_quad(pg + e[u], gn, v4[u], nv[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            if (nv[u] == 0) continue;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) gb[u].v[kk] = fadd(gb[u].v[kk], div_N(A[u].v[kk], a.Nf, invN, pow2));   // R3, R13
+            store_quad(a.gbar + e[u], gb[u], v4[u], nv[u]);
+        }
+    }
+}
+
 constexpr int kMaxSliceRows = 4096;
 
 // Candidate resolution on a small list in shared memory (every CTA of the block
@@ -321,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     __shared__ int warp_sums[32];
     __shared__ unsigned s_dig;
     __shared__ int s_abv;
+    __shared__ int s_nb;                            // early mode: selected boundary-bin rows
 
     const SliceItem it = s.items[blockIdx.x];
     const BlockDev B = s.blocks[it.b];
@@ -418,6 +482,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     // ------------------------------------------------ phase A
     unsigned b1 = 0;
     int krem = B.K;
+    int gt_pos = 0, gt_tot = 0;                      // this thread's / the slice's rows above bin b1
     if (arc) {
         const float* __restrict__ sg = s.sigma + B.row_base + lo;
         unsigned hv[8];                              // digit-1 histogram, loaded alongside the keys
@@ -453,6 +518,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
         int packed_tot;
         const int packed = cta_exclusive_scan((gt1 << 16) | nc, warp_sums, &packed_tot);
         const int ctot = packed_tot & 0xFFFF;
+        gt_pos = packed >> 16;
+        gt_tot = packed_tot >> 16;
         if (tid == 0) {
             s.slice_gt[sidx] = packed_tot >> 16;
             s_abv = ctot > 0 ? static_cast<int>(atomicAdd(ccount + bb, static_cast<unsigned>(ctot))) : 0;
@@ -476,7 +543,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     STAMP(1);
     if (it.c == 0)   // next step's candidate counter of this block
         for (int i = tid; i < 1; i += kThreads) s.cand_count[(par ^ 1) * s.num_blocks + bb] = 0;
-    grid.sync();                                     // ---------------- barrier 1
+    if (s.early) {
+        // split barrier 1: the rows of this slice above the boundary bin b1 are
+        // selected whatever the candidates resolve to (fewer than K keys lie above
+        // b1), so their S4..S6 runs while the other CTAs reach the barrier
+        auto token = grid.barrier_arrive();
+        if (arc) {
+            int pos = gt_pos;
+            for (int i = tid; i < nk; i += kThreads)
+                if ((s_keys[i] >> 21) > b1) s_rows[pos++] = i;
+            __syncthreads();
+            gather_rows_local<4>(ga, B, lo, s_rows, gt_tot);
+        } else {
+            gather_rows_local<4>(ga, B, lo, nullptr, nk);   // K = m: every row
+        }
+        __syncthreads();                             // s_rows is reused below
+        grid.barrier_wait(std::move(token));
+    } else {
+        grid.sync();                                 // ---------------- barrier 1
+    }
     STAMP(2);
     // any block with more candidates than fit takes the digit-by-digit path
     // (uniform across the grid, so every CTA meets the same barriers)
@@ -606,13 +691,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
             }
             if (t) { take_mask |= 1u << k; ++my_sel; }
         }
+        if (tid == 0) s_nb = 0;
         int nsel;
         int pos = cta_exclusive_scan(my_sel, warp_sums, &nsel);
         for (int k = 0; k < per; ++k) {
             if (take_mask & (1u << k)) {
-                const int p = lo + tid * per + k;
-                out[sel_before + pos] = p;
+                const int i = tid * per + k;
+                out[sel_before + pos] = lo + i;
                 ++pos;
+                // early mode: the selected rows of the boundary bin are still to do
+                if (s.early && (s_keys[i] >> 21) == b1) s_rows[atomicAdd(&s_nb, 1)] = i;
             }
         }
     } else {
@@ -620,6 +708,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
         for (int p = lo + tid; p < hi; p += kThreads) out[p] = p;
     }
     STAMP(5);
+    if (s.early) {
+        if (arc) {
+            __syncthreads();
+            gather_rows_local<4>(ga, B, lo, s_rows, s_nb);
+        }
+        STAMP(6);
+        STAMP(7);
+        return;
+    }
     // S4 (+S5, S6): all selected-row segments spread evenly over the grid; the
     // (static) segment descriptors of this thread's first items are fetched
     // before the barrier
