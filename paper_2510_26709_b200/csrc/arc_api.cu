@@ -203,7 +203,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_sblocks = take(sizeof(BlockDev) * nsb);
     pl.o_segs_real = take(sizeof(SelRow) * pl.segs_real.size());
     pl.o_dense_ids = take(sizeof(int) * pl.dense_ids.size());
-    pl.o_tiles = take(sizeof(Tile) * pl.max_tiles);
+    pl.o_tiles = take(sizeof(TileDesc) * pl.max_tiles);
     pl.o_cta = take(sizeof(int) * (kMaxGrid + 1));
     pl.o_selrows = take(sizeof(SelRow) * pl.num_segs);
     pl.o_V = take(sizeof(float) * sum_nr * 2);   // double-buffered by t parity
@@ -245,13 +245,12 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
 // are live (masked rows still run the load and staging code), so a tile of r
 // rows is charged nchunks * max(r, 0.6 R_shape); tiles go longest-first to the
 // least-loaded CTA (LPT).
-void plan_tiles(const Plan& pl, int resident, int tile_rows_max, std::vector<Tile>& tiles, std::vector<int>& cta_begin,
-                int& grid) {
+void plan_tiles(const Plan& pl, int resident, int tile_rows_max, int W, std::vector<Tile>& tiles,
+                std::vector<int>& cta_begin, int& grid) {
     struct Cand { int64_t makespan = INT64_MAX; std::vector<Tile> tiles; std::vector<int> begin; int grid = 0; };
     Cand best;
     resident = std::max(1, std::min(resident, kMaxGrid));
     const int nodes = pl.topk || pl.L > 1 ? pl.L : 1;
-    const int W = tile_rows_max == 64 ? 32 : (tile_rows_max == 32 ? 64 : 128);   // chunk columns of the shape
     const int64_t floor_rows = (tile_rows_max * 6 + 9) / 10;
     // Full-height tiles are the cheapest per element (measured on C3: 32-row
     // tiles 94 %, 30 rows 93 %, 24 rows 90 % of HBM peak; on C2 8-row tiles ran
@@ -470,16 +469,34 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         for (const BlockDev& B : c->pl.bdev)
             if (B.kind == ARC_BLOCK_ARC) { all_vec = all_vec && B.vec; min_n = std::min(min_n, B.n); }
         (void)all_vec;
-        c->shape = min_n >= 64 ? 1 : 0;   // 32 x 64 measured best on C3
+        // 32 x 64 measured best on C3 (n = 768) and C5 (n = 1024); 32 x 256 in
+        // 8-row rounds (1 KB row segments) on the LLaMA layout (n >= 2048)
+        c->shape = min_n >= 2048 && sketch_shape_ok(3, c->p.r) ? 3 : min_n >= 64 ? 1 : 0;
         if (const char* e = getenv("ARC_SKETCH_SHAPE")) {
             const int v = atoi(e);
-            if (v >= 0 && v <= 2) c->shape = v;
+            if (v >= 0 && v <= 4) c->shape = v;
         }
         if (!sketch_shape_ok(c->shape, c->p.r)) c->shape = 1;
     }
-    plan_tiles(c->pl, ef_sketch_resident_ctas(c->p.r, c->shape), sketch_tile_rows(c->shape), tiles, cta_begin,
-               c->grid);
+    plan_tiles(c->pl, ef_sketch_resident_ctas(c->p.r, c->shape), sketch_tile_rows(c->shape),
+               sketch_tile_cols(c->shape), tiles, cta_begin, c->grid);
     c->num_tiles = static_cast<int>(tiles.size());
+    std::vector<TileDesc> tdesc(tiles.size());
+    for (size_t i = 0; i < tiles.size(); ++i) {
+        const BlockDev& B = c->pl.bdev[tiles[i].b];
+        TileDesc& D = tdesc[i];
+        D = TileDesc{};
+        D.off = B.off;
+        D.len = B.len;
+        D.v_off = B.v_off;
+        D.n = B.n;
+        D.row0 = tiles[i].row0;
+        D.rows = tiles[i].rows;
+        D.vec = B.vec;
+        D.row_base = B.row_base;
+        D.b = tiles[i].b;
+        D.node = tiles[i].node;
+    }
     {
     }
     const std::vector<SelRow>& rows = c->pl.segs;
@@ -493,7 +510,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
             UPLOAD(c->pl.o_sblocks, c->pl.sbdev);
             UPLOAD(c->pl.o_segs_real, c->pl.segs_real);
             UPLOAD(c->pl.o_dense_ids, c->pl.dense_ids);
-            UPLOAD(c->pl.o_tiles, tiles);
+            UPLOAD(c->pl.o_tiles, tdesc);
             UPLOAD(c->pl.o_cta, cta_begin);
             UPLOAD(c->pl.o_selrows, rows);
             UPLOAD(c->pl.o_items, c->pl.items);
@@ -591,7 +608,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     if (pl.M > 0) {
         SketchLaunch a{};
         a.blocks = blocks;
-        a.tiles = c->at<Tile>(pl.o_tiles);
+        a.tiles = c->at<TileDesc>(pl.o_tiles);
         a.cta_begin = c->at<int>(pl.o_cta);
         a.num_tiles = c->num_tiles;
         a.grid = c->grid;

@@ -32,6 +32,15 @@ struct Tile {
     int node;
 };
 
+// A tile with its block's fields, as the streaming kernel reads it (64 B; the
+// next tile's descriptor is fetched into shared memory while a tile runs).
+struct alignas(16) TileDesc {
+    long long off, len, v_off;   // block
+    int n, row0, rows, vec, row_base, b, node;
+    int pad_[3];
+};
+static_assert(sizeof(TileDesc) == 64, "TileDesc is four 16-byte words");
+
 // Gather / scatter work item: columns [4*q0, 4*q0 + kSegQuads*4) of the k-th
 // selected row of block b.
 constexpr int kSegQuads = 64;      // 32 lanes x 2 quads = 256 columns
@@ -107,7 +116,7 @@ void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r,
 
 struct SketchLaunch {
     const BlockDev* blocks;
-    const Tile* tiles;      // all tiles, grouped by CTA
+    const TileDesc* tiles;  // all tiles, grouped by CTA
     const int* cta_begin;   // [grid + 1]: CTA c runs tiles [cta_begin[c], cta_begin[c+1])
     int num_tiles;
     int grid;
@@ -125,13 +134,14 @@ struct SketchLaunch {
     uint2 key;         // Rand-K: Philox key (seed)
     unsigned t_lo, t_hi;             // ARC rows (stride of the per-node sigma in mode 2)
     int num_blocks;
-    int shape;         // tile shape R x W: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128
+    int shape;         // tile shape R x W: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128, 3 = 32 x 256, 4 = 32 x 128
     int pdl;           // launch with programmatic stream serialization (overlap the launch)
     unsigned* status;
 };
 void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s);
 int ef_sketch_resident_ctas(int r, int shape);   // SMs x occupancy
 int sketch_tile_rows(int shape);
+int sketch_tile_cols(int shape);
 int sketch_shape_ok(int shape, int r);
 
 

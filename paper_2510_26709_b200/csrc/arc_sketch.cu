@@ -47,23 +47,33 @@ struct TileRegs {
 };
 
 template <int W>
-__device__ __forceinline__ TileRegs tile_regs(const SketchLaunch& a, int li) {
-    const Tile* T = a.tiles + li;
-    const int b = __ldg(&T->b);
-    const BlockDev* B = a.blocks + b;
+__device__ __forceinline__ TileRegs tile_regs(const TileDesc& T) {
     TileRegs t;
-    t.b = b;
-    t.off = __ldg(&B->off);
-    t.len = __ldg(&B->len);
-    t.n = __ldg(&B->n);
-    t.vec = __ldg(&B->vec);
-    t.v_off = __ldg(&B->v_off);
-    t.row_base = __ldg(&B->row_base);
-    t.row0 = __ldg(&T->row0);
-    t.m_rows = __ldg(&T->rows);
-    t.node = __ldg(&T->node);
+    t.b = T.b;
+    t.off = T.off;
+    t.len = T.len;
+    t.n = T.n;
+    t.vec = T.vec;
+    t.v_off = T.v_off;
+    t.row_base = T.row_base;
+    t.row0 = T.row0;
+    t.m_rows = T.rows;
+    t.node = T.node;
     t.nchunks = (t.n + W - 1) / W;
     return t;
+}
+
+// the descriptor of tile li into shared memory, asynchronously (threads 0..3,
+// one 16-byte word each; they wait for it before a later __syncthreads)
+__device__ __forceinline__ void fetch_tile(const TileDesc* tiles, int li, TileDesc* dst) {
+    if (threadIdx.x < 4) {
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(reinterpret_cast<char*>(dst) + 16 * threadIdx.x));
+        const char* src = reinterpret_cast<const char*>(tiles + li) + 16 * threadIdx.x;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(d), "l"(src) : "memory");
+    }
+}
+__device__ __forceinline__ void fetch_wait() {
+    if (threadIdx.x < 4) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // valid columns of tile row `row` (0 for rows beyond the tile): the last row of
@@ -74,19 +84,21 @@ __device__ __forceinline__ int row_cols(const TileRegs& t, int row) {
     return rest < t.n ? static_cast<int>(rest) : t.n;
 }
 
-template <int R, int W, int RPT>
+template <int R, int W, int RPT, int NR>
 __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a) {
-    static_assert(R * W == 2048, "one chunk = 2048 elements = 8 per thread");
-    static_assert(W % 32 == 0 && W <= 128, "W in {32, 64, 128}");
-    constexpr int NE = R * W / kThreads;        // elements per thread per stream = 8
-    constexpr int LPR = W / 4;                  // vec: lanes per row segment
-    constexpr int RPI = 32 / LPR;               // vec: rows per warp instruction
+    static_assert(R * W == 2048 * NR, "one load round = 2048 elements = 8 per thread");
+    static_assert(W % 32 == 0 && W <= 256, "W in {32, 64, 128, 256}");
+    constexpr int RR = R / NR;                  // rows per load round
+    constexpr int NB = NR == 1 ? 2 : 1;         // Delta / V buffers
+    constexpr int NE = RR * W / kThreads;       // elements per thread per stream = 8
+    constexpr int LPR = W / 4;                  // vec: threads per row segment (one float4 each)
     constexpr int DS = W + 4;                   // Delta row stride (floats): 16-byte rows,
                                                 // rows t..t+7 on distinct banks
     constexpr int VS = 4 * RPT;                 // V row stride in smem (padded r)
-    __shared__ __align__(16) float Ds[2][R][DS];
-    __shared__ __align__(16) float Vs[2][W * VS];
+    __shared__ __align__(16) float Ds[NB][R][DS];
+    __shared__ __align__(16) float Vs[NB][W * VS];
     __shared__ unsigned hist[kHist1Bins];       // digit-1 histogram of this CTA's Sigma (mode 0)
+    __shared__ TileDesc s_tile[2];              // tile descriptors: list position parity
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int crow = tid >> 2, jl = tid & 3;    // chain role (threads < 4R)
@@ -94,6 +106,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
     if (list_begin >= list_end) return;
     const int r = a.r;
     for (int i = tid; i < kHist1Bins; i += kThreads) hist[i] = 0;
+    fetch_tile(a.tiles, list_begin, &s_tile[0]);
+    if (list_begin + 1 < list_end) fetch_tile(a.tiles, list_begin + 1, &s_tile[1]);
+    fetch_wait();
+    __syncthreads();
     grid_dependency_wait();   // the previous kernel (g, V, histogram reset) is complete
     // (the first __syncthreads of the main loop orders this before any use)
     auto flush_hist = [&](int b) {               // all threads; after a __syncthreads
@@ -105,22 +121,34 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
     };
 
     // element e of this thread in a chunk -> (row, column within chunk)
-    auto vrow = [&](int e) { return (e >> 2) * (8 * RPI) + warp * RPI + lane / LPR; };
-    auto vcol = [&](int e) { return 4 * (lane % LPR) + (e & 3); };
+    // (vec: float4 number q = tid + 256 (e / 4) of the chunk, row-major)
+    auto vrow = [&](int e) { return (tid + kThreads * (e >> 2)) / LPR; };
+    auto vcol = [&](int e) { return 4 * ((tid + kThreads * (e >> 2)) % LPR) + (e & 3); };
     auto srow = [&](int e) { return warp + 8 * (e / (W / 32)); };
     auto scol = [&](int e) { return lane + 32 * (e % (W / 32)); };
 
     float xg[NE], xh[NE], xd[NE];
+    constexpr int NV = (W * VS + kThreads - 1) / kThreads;
+    float xv[NV];                                // this thread's V entries of the chunk
 
-    auto load_chunk = [&](const TileRegs& t, int node, int chunk) {
+
+    auto load_chunk = [&](const TileRegs& t, int node, int chunk, int rnd) {
         const float* __restrict__ pg = a.nodes.grad[node];
         const float* __restrict__ ph = a.nodes.h[node];
         const float* __restrict__ pgg = a.nodes.g[node];
         const int c0 = chunk * W;
+        if (rnd == 0) {   // V rows [c0, c0 + W) of the block, r values each -> stride VS (zero padded)
+            const float* __restrict__ Vb = a.V + t.v_off;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int i = tid + k * kThreads, q = i / VS, j = i % VS;
+                xv[k] = (i < W * VS && c0 + q < t.n && j < r) ? __ldg(Vb + static_cast<long long>(c0 + q) * r + j) : 0.0f;
+            }
+        }
         if (t.vec) {
 #pragma unroll
             for (int e4 = 0; e4 < NE; e4 += 4) {
-                const int row = vrow(e4), col = c0 + vcol(e4);
+                const int row = rnd * RR + vrow(e4), col = c0 + vcol(e4);
                 const int nv = row_cols(t, row);
                 const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
                 if (col + 3 < nv) {
@@ -144,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         } else {
 #pragma unroll
             for (int e1 = 0; e1 < NE; ++e1) {
-                const int row = srow(e1), col = c0 + scol(e1);
+                const int row = rnd * RR + srow(e1), col = c0 + scol(e1);
                 const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
                 if (col < row_cols(t, row)) {
                     xg[e1] = __ldcs(pg + e);
@@ -155,13 +183,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         }
     };
 
-    auto stage_chunk = [&](const TileRegs& t, int node, int chunk, int buf) {
+    auto stage_chunk = [&](const TileRegs& t, int node, int chunk, int rnd, int buf) {
         float* __restrict__ ph = a.nodes.h[node];
         const int c0 = chunk * W;
         if (t.vec) {
 #pragma unroll
             for (int e4 = 0; e4 < NE; e4 += 4) {
-                const int row = vrow(e4), cl = vcol(e4), col = c0 + cl;
+                const int row = rnd * RR + vrow(e4), cl = vcol(e4), col = c0 + cl;
                 const int nv = row_cols(t, row);
                 const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
                 float hn[4], dl[4];
@@ -182,18 +210,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         } else {
 #pragma unroll
             for (int e1 = 0; e1 < NE; ++e1) {
-                const int row = srow(e1), cl = scol(e1), col = c0 + cl;
+                const int row = rnd * RR + srow(e1), cl = scol(e1), col = c0 + cl;
                 const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
                 const float hn = fadd(fmul(a.ome, xh[e1]), fmul(a.eta, xg[e1]));
                 if (col < row_cols(t, row)) ph[e] = hn;
                 Ds[buf][row][cl] = fsub(hn, xd[e1]);
             }
         }
-        // V rows [c0, c0 + W) of this block, r values each -> stride VS (zero padded)
-        const float* __restrict__ Vb = a.V + t.v_off;
-        for (int i = tid; i < W * VS; i += kThreads) {
-            const int q = i / VS, j = i % VS;
-            Vs[buf][i] = (c0 + q < t.n && j < r) ? __ldg(Vb + static_cast<long long>(c0 + q) * r + j) : 0.0f;
+        if (rnd == 0) {   // V, loaded with the chunk
+#pragma unroll
+            for (int k = 0; k < NV; ++k)
+                if (tid + k * kThreads < W * VS) Vs[buf][tid + k * kThreads] = xv[k];
         }
     };
 
@@ -202,12 +229,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
     for (int s = 0; s < RPT; ++s) { acc[s] = 0.0f; S[s] = 0.0f; }
 
     int li = list_begin, chunk = 0;
-    TileRegs tc = tile_regs<W>(a, li);     // tile of the chunk being staged / chained
+    TileRegs tc = tile_regs<W>(s_tile[0]); // tile of the chunk being staged / chained
     TileRegs tl = tc;                      // tile of the chunk being loaded
-    load_chunk(tc, tc.node, chunk);
+    load_chunk(tc, tc.node, chunk, 0);
     int buf = 0;
     while (true) {
-        stage_chunk(tc, tc.node, chunk, buf);
+        // NR rounds of RR rows; each round's loads fly while the previous one is staged
+        if (NB == 1) __syncthreads();      // the single Delta buffer is free again
+#pragma unroll 1
+        for (int k = 0; k < NR; ++k) {
+            stage_chunk(tc, tc.node, chunk, k, buf);
+            if (k + 1 < NR) {
+                if (NR > 1 && (k + 1) * RR >= tc.m_rows) break;   // rounds past the tile's rows
+                load_chunk(tc, tc.node, chunk, k + 1);
+            }
+        }
+        fetch_wait();                      // (the descriptor fetched one tile ahead)
         __syncthreads();
         // advance the load cursor and issue the next chunk's loads
         int nli = li, nchunk = chunk + 1;
@@ -217,8 +254,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         }
         const bool more = nli < list_end;
         if (more) {
-            if (nli != li) tl = tile_regs<W>(a, nli);
-            load_chunk(tl, tl.node, nchunk);
+            if (nli != li) {
+                tl = tile_regs<W>(s_tile[(nli - list_begin) & 1]);
+                if (nli + 1 < list_end) fetch_tile(a.tiles, nli + 1, &s_tile[(nli + 1 - list_begin) & 1]);
+            }
+            load_chunk(tl, tl.node, nchunk, 0);
         }
         const int node = tc.node;
 
@@ -315,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         if (nli != li) tc = tl;
         li = nli;
         chunk = nchunk;
-        buf ^= 1;
+        buf ^= NB - 1;
     }
 }
 
@@ -335,41 +375,61 @@ void launch_pdl(K kernel, const SketchLaunch& a, cudaStream_t s) {
     cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
-template <int R, int W>
+template <int R, int W, int NR = 1>
 void launch_rw(const SketchLaunch& a, cudaStream_t s) {
-    if (a.r <= 4) launch_pdl(k_ef_sketch<R, W, 1>, a, s);
-    else if (a.r <= 8) launch_pdl(k_ef_sketch<R, W, 2>, a, s);
-    else if (a.r <= 16) launch_pdl(k_ef_sketch<R, W, 4>, a, s);
-    else if constexpr (W < 128) launch_pdl(k_ef_sketch<R, W, 8>, a, s);
+    if (a.r <= 4) launch_pdl(k_ef_sketch<R, W, 1, NR>, a, s);
+    else if constexpr (W <= 128) {
+        if (a.r <= 8) launch_pdl(k_ef_sketch<R, W, 2, NR>, a, s);
+    }
+    if constexpr (W <= 128 && NR == 1) {
+        if (a.r > 8 && a.r <= 16) launch_pdl(k_ef_sketch<R, W, 4, NR>, a, s);
+        else if constexpr (W < 128) { if (a.r > 16) launch_pdl(k_ef_sketch<R, W, 8, NR>, a, s); }
+    }
 }
 
-template <int R, int W>
+template <int R, int W, int NR = 1>
 int occupancy_rw(int r) {
     int per_sm = 0;
-    if (r <= 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 1>, kThreads, 0);
-    else if (r <= 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 2>, kThreads, 0);
-    else if (r <= 16) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 4>, kThreads, 0);
-    else if constexpr (W < 128) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 8>, kThreads, 0);
+    if (r <= 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 1, NR>, kThreads, 0);
+    else if constexpr (W <= 128) {
+        if (r <= 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 2, NR>, kThreads, 0);
+    }
+    if constexpr (W <= 128 && NR == 1) {
+        if (r > 8 && r <= 16) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 4, NR>, kThreads, 0);
+        else if constexpr (W < 128) { if (r > 16) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<R, W, 8, NR>, kThreads, 0); }
+    }
     return per_sm;
 }
 
 }  // namespace
 
-// tile shapes: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128 (r <= 16)
-int sketch_tile_rows(int shape) { return shape == 0 ? 64 : shape == 1 ? 32 : 16; }
-int sketch_shape_ok(int shape, int r) { return shape != 2 || r <= 16; }
+// tile shapes R x W (load rounds): 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128 (r <= 16),
+// 3 = 32 x 256 in 4 rounds of 8 rows (r <= 4), 4 = 32 x 128 in 2 rounds of 16 rows (r <= 8)
+int sketch_tile_rows(int shape) { return shape == 0 ? 64 : shape == 2 ? 16 : 32; }
+int sketch_tile_cols(int shape) { return shape == 0 ? 32 : shape == 1 ? 64 : shape == 3 ? 256 : 128; }
+int sketch_shape_ok(int shape, int r) {
+    return shape <= 1 || (shape == 2 && r <= 16) || (shape == 3 && r <= 4) || (shape == 4 && r <= 8);
+}
 
 void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s) {
-    if (a.shape == 0) launch_rw<64, 32>(a, s);
-    else if (a.shape == 1) launch_rw<32, 64>(a, s);
-    else launch_rw<16, 128>(a, s);
+    switch (a.shape) {
+        case 0: launch_rw<64, 32>(a, s); break;
+        case 1: launch_rw<32, 64>(a, s); break;
+        case 2: launch_rw<16, 128>(a, s); break;
+        case 3: launch_rw<32, 256, 4>(a, s); break;
+        default: launch_rw<32, 128, 2>(a, s); break;
+    }
 }
 
 int ef_sketch_resident_ctas(int r, int shape) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int per_sm = shape == 0 ? occupancy_rw<64, 32>(r) : shape == 1 ? occupancy_rw<32, 64>(r) : occupancy_rw<16, 128>(r);
+    int per_sm = shape == 0 ? occupancy_rw<64, 32>(r)
+                 : shape == 1 ? occupancy_rw<32, 64>(r)
+                 : shape == 2 ? occupancy_rw<16, 128>(r)
+                 : shape == 3 ? occupancy_rw<32, 256, 4>(r)
+                              : occupancy_rw<32, 128, 2>(r);
     if (per_sm < 1) per_sm = 1;
     return sms * per_sm;
 }

@@ -1,0 +1,316 @@
+// Ceiling of the sketch pass's HBM traffic mix: read grad, g, h and write h
+// (3 reads : 1 write, in place), d floats each, versus a plain copy (1 : 1)
+// and pure reads.  Grid-stride float4 loops, several grid sizes / unrolls.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mb_stream tools/microbench_stream.cu
+#include <cstdio>
+#include <algorithm>
+
+template <int UN, bool CS>
+__global__ void k_mix(const float4* __restrict__ gr, const float4* __restrict__ g, float4* h, long long n4, float a,
+                      float b) {
+    const long long stride = (long long)gridDim.x * blockDim.x * UN;
+    for (long long base = (long long)blockIdx.x * blockDim.x * UN + threadIdx.x; base < n4; base += stride) {
+        float4 x[UN], y[UN], z[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const long long i = base + (long long)u * blockDim.x;
+            if (i < n4) {
+                x[u] = CS ? __ldcs(gr + i) : gr[i];
+                y[u] = CS ? __ldcs(g + i) : g[i];
+                z[u] = CS ? __ldcs(h + i) : h[i];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const long long i = base + (long long)u * blockDim.x;
+            if (i < n4) {
+                float4 o = make_float4(a * z[u].x + b * x[u].x - y[u].x, a * z[u].y + b * x[u].y - y[u].y,
+                                       a * z[u].z + b * x[u].z - y[u].z, a * z[u].w + b * x[u].w - y[u].w);
+                if (CS) __stcs(h + i, o); else h[i] = o;
+            }
+        }
+    }
+}
+
+template <int UN>
+__global__ void k_copy(const float4* __restrict__ s, float4* __restrict__ d, long long n4) {
+    const long long stride = (long long)gridDim.x * blockDim.x * UN;
+    for (long long base = (long long)blockIdx.x * blockDim.x * UN + threadIdx.x; base < n4; base += stride) {
+        float4 x[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const long long i = base + (long long)u * blockDim.x;
+            if (i < n4) x[u] = __ldcs(s + i);
+        }
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const long long i = base + (long long)u * blockDim.x;
+            if (i < n4) __stcs(d + i, x[u]);
+        }
+    }
+}
+
+template <int UN>
+__global__ void k_read3(const float4* __restrict__ a, const float4* __restrict__ b, const float4* __restrict__ c,
+                        long long n4, float* out) {
+    const long long stride = (long long)gridDim.x * blockDim.x * UN;
+    float acc = 0.f;
+    for (long long base = (long long)blockIdx.x * blockDim.x * UN + threadIdx.x; base < n4; base += stride) {
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const long long i = base + (long long)u * blockDim.x;
+            if (i < n4) {
+                const float4 x = __ldcs(a + i), y = __ldcs(b + i), z = __ldcs(c + i);
+                acc += x.x + y.y + z.z + x.w;
+            }
+        }
+    }
+    if (acc == 12345.f) out[0] = acc;
+}
+
+// the sketch kernel's access pattern: tiles of R full rows (n = 768), chunks of
+// R x W, each thread 2 float4 per array per chunk; DEPTH chunks in registers
+template <int R, int W, int DEPTH>
+__global__ void __launch_bounds__(256) k_tiled(const float* __restrict__ gr, const float* __restrict__ g, float* h, int n,
+                                               int ntiles, float a, float b) {
+    constexpr int NE4 = R * W / 4 / 256;       // float4 per thread per array per chunk
+    constexpr int LPR = W / 4;                 // lanes per row segment
+    const int nch = n / W;
+    const int tid = threadIdx.x;
+    const long long total = (long long)ntiles * nch;   // chunks
+    float4 x[DEPTH][NE4], y[DEPTH][NE4], z[DEPTH][NE4];
+    auto addr = [&](long long c, int k) {
+        const long long tile = c / nch; const int ch = (int)(c % nch);
+        const int q = tid + 256 * k;           // float4 index in chunk
+        const int row = q / LPR, col = 4 * (q % LPR);
+        return (tile * R + row) * (long long)n + ch * W + col;
+    };
+    auto load = [&](int sl, long long c) {
+#pragma unroll
+        for (int k = 0; k < NE4; ++k) {
+            const long long e = addr(c, k);
+            x[sl][k] = __ldcs(reinterpret_cast<const float4*>(gr + e));
+            y[sl][k] = __ldcs(reinterpret_cast<const float4*>(g + e));
+            z[sl][k] = __ldcs(reinterpret_cast<const float4*>(h + e));
+        }
+    };
+    // contiguous range of chunks per CTA (like the persistent tile list)
+    const long long c0 = total * blockIdx.x / gridDim.x, c1 = total * (blockIdx.x + 1) / gridDim.x;
+#pragma unroll
+    for (int dd = 0; dd < DEPTH; ++dd)
+        if (c0 + dd < c1) load(dd, c0 + dd);
+    for (long long c = c0; c < c1; c += DEPTH) {
+#pragma unroll
+        for (int dd = 0; dd < DEPTH; ++dd) {
+            if (c + dd >= c1) break;
+            float4 o[NE4];
+#pragma unroll
+            for (int k = 0; k < NE4; ++k)
+                o[k] = make_float4(a * z[dd][k].x + b * x[dd][k].x - y[dd][k].x, a * z[dd][k].y + b * x[dd][k].y - y[dd][k].y,
+                                   a * z[dd][k].z + b * x[dd][k].z - y[dd][k].z, a * z[dd][k].w + b * x[dd][k].w - y[dd][k].w);
+#pragma unroll
+            for (int k = 0; k < NE4; ++k) __stcs(reinterpret_cast<float4*>(h + addr(c + dd, k)), o[k]);
+            if (c + dd + DEPTH < c1) load(dd, c + dd + DEPTH);
+        }
+    }
+}
+
+// the same pattern through TMA bulk copies into an S-stage shared-memory ring
+// (one mbarrier per stage; R x 3 row segments of W floats per chunk)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" :: "r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b,
+                                         unsigned long long pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol) : "memory");
+}
+
+template <int R, int W, int S>
+__global__ void __launch_bounds__(256) k_tma(const float* __restrict__ gr, const float* __restrict__ g, float* h, int n,
+                                             int ntiles, float a, float b) {
+    constexpr int DS = W + 4;
+    extern __shared__ __align__(128) float sm[];
+    float (*st)[3][R][DS] = reinterpret_cast<float (*)[3][R][DS]>(sm);
+    __shared__ __align__(8) unsigned long long full[S];
+    const int tid = threadIdx.x;
+    const int nch = n / W;
+    const long long total = (long long)ntiles * nch;
+    const long long c0 = total * blockIdx.x / gridDim.x, c1 = total * (blockIdx.x + 1) / gridDim.x;
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](long long c) {   // threads 0 .. 3R-1: one row segment each
+        const int sl = (int)((c - c0) % S);
+        const long long tile = c / nch; const int ch = (int)(c % nch);
+        if (tid == 0) mbar_expect_tx(&full[sl], 3u * R * W * 4);
+        if (tid < 3 * R) {
+            const int arr = tid / R, row = tid % R;
+            const float* src = (arr == 0 ? gr : arr == 1 ? (const float*)h : g) + (tile * R + row) * (long long)n + ch * W;
+            bulk_g2s(&st[sl][arr][row][0], src, W * 4, &full[sl], pol);
+        }
+    };
+    for (int i = 0; i < S - 1; ++i)
+        if (c0 + i < c1) issue(c0 + i);
+    constexpr int LPR = W / 4;
+    for (long long c = c0; c < c1; ++c) {
+        const int sl = (int)((c - c0) % S);
+        mbar_wait(&full[sl], (unsigned)(((c - c0) / S) & 1));
+        const long long tile = c / nch; const int ch = (int)(c % nch);
+#pragma unroll
+        for (int k = 0; k < R * W / 4 / 256; ++k) {
+            const int q = tid + 256 * k, row = q / LPR, col = 4 * (q % LPR);
+            const float4 x = *reinterpret_cast<const float4*>(&st[sl][0][row][col]);
+            const float4 z = *reinterpret_cast<const float4*>(&st[sl][1][row][col]);
+            float4* py = reinterpret_cast<float4*>(&st[sl][2][row][col]);
+            const float4 y = *py;
+            const float4 o = make_float4(a * z.x + b * x.x, a * z.y + b * x.y, a * z.z + b * x.z, a * z.w + b * x.w);
+            __stcs(reinterpret_cast<float4*>(h + (tile * R + row) * (long long)n + ch * W + col), o);
+            *py = make_float4(o.x - y.x, o.y - y.y, o.z - y.z, o.w - y.w);   // Delta in place
+        }
+        __syncthreads();
+        if (c + S - 1 < c1) issue(c + S - 1);
+    }
+}
+
+// the same pattern through cp.async (LDGSTS, 16 B per thread) into an S-stage ring
+template <int R, int W, int S>
+__global__ void __launch_bounds__(256) k_cpa(const float* __restrict__ gr, const float* __restrict__ g, float* h, int n,
+                                             int ntiles, float a, float b) {
+    constexpr int DS = W + 4;
+    constexpr int NE4 = R * W / 4 / 256;
+    constexpr int LPR = W / 4;
+    extern __shared__ __align__(128) float sm[];
+    float (*st)[3][R][DS] = reinterpret_cast<float (*)[3][R][DS]>(sm);
+    const int tid = threadIdx.x;
+    const int nch = n / W;
+    const long long total = (long long)ntiles * nch;
+    const long long c0 = total * blockIdx.x / gridDim.x, c1 = total * (blockIdx.x + 1) / gridDim.x;
+    auto issue = [&](long long c) {
+        const int sl = (int)((c - c0) % S);
+        const long long tile = c / nch; const int ch = (int)(c % nch);
+#pragma unroll
+        for (int k = 0; k < NE4; ++k) {
+            const int q = tid + 256 * k, row = q / LPR, col = 4 * (q % LPR);
+            const long long e = (tile * R + row) * (long long)n + ch * W + col;
+            asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(&st[sl][0][row][col])), "l"(gr + e), "l"(0ull));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&st[sl][1][row][col])), "l"(h + e));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&st[sl][2][row][col])), "l"(g + e));
+        }
+    };
+    for (int i = 0; i < S - 1; ++i) {
+        if (c0 + i < c1) issue(c0 + i);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (long long c = c0; c < c1; ++c) {
+        const int sl = (int)((c - c0) % S);
+        asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
+        __syncthreads();
+        // refill the stage consumed in the previous iteration
+        if (c + S - 1 < c1) issue(c + S - 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const long long tile = c / nch; const int ch = (int)(c % nch);
+#pragma unroll
+        for (int k = 0; k < NE4; ++k) {
+            const int q = tid + 256 * k, row = q / LPR, col = 4 * (q % LPR);
+            const float4 x = *reinterpret_cast<const float4*>(&st[sl][0][row][col]);
+            const float4 z = *reinterpret_cast<const float4*>(&st[sl][1][row][col]);
+            float4* py = reinterpret_cast<float4*>(&st[sl][2][row][col]);
+            const float4 y = *py;
+            const float4 o = make_float4(a * z.x + b * x.x, a * z.y + b * x.y, a * z.z + b * x.z, a * z.w + b * x.w);
+            __stcs(reinterpret_cast<float4*>(h + (tile * R + row) * (long long)n + ch * W + col), o);
+            *py = make_float4(o.x - y.x, o.y - y.y, o.z - y.z, o.w - y.w);
+        }
+    }
+}
+
+int main() {
+    const long long d = 124439808LL, n4 = d / 4;
+    float *gr, *g, *h, *o;
+    cudaMalloc(&gr, d * 4); cudaMalloc(&g, d * 4); cudaMalloc(&h, d * 4); cudaMalloc(&o, 64);
+    cudaMemset(gr, 0, d * 4); cudaMemset(g, 0, d * 4); cudaMemset(h, 0, d * 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    auto timeit = [&](auto launch) {
+        for (int w = 0; w < 3; ++w) launch();
+        float best = 1e9;
+        for (int rep = 0; rep < 20; ++rep) {
+            cudaEventRecord(e0);
+            launch();
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1);
+            best = std::min(best, ms);
+        }
+        return best;
+    };
+    const double B4 = 4.0 * d * 4, B2 = 2.0 * d * 4, B3 = 3.0 * d * 4;
+    for (int grid : {148, 296, 592, 1184, 2368}) {
+        for (int th : {256, 512}) {
+            float t1 = timeit([&] { k_mix<4, true><<<grid, th>>>((float4*)gr, (float4*)g, (float4*)h, n4, 0.9f, 0.1f); });
+            float t2 = timeit([&] { k_mix<4, false><<<grid, th>>>((float4*)gr, (float4*)g, (float4*)h, n4, 0.9f, 0.1f); });
+            float t3 = timeit([&] { k_mix<2, true><<<grid, th>>>((float4*)gr, (float4*)g, (float4*)h, n4, 0.9f, 0.1f); });
+            float t4 = timeit([&] { k_copy<4><<<grid, th>>>((float4*)gr, (float4*)g, n4); });
+            float t5 = timeit([&] { k_read3<4><<<grid, th>>>((float4*)gr, (float4*)g, (float4*)h, n4, o); });
+            printf("grid %5d x %3d: mix3r1w cs/UN4 %7.1f us %6.0f GB/s | plain/UN4 %6.0f | cs/UN2 %6.0f || copy %6.0f | read3 %6.0f GB/s\n",
+                   grid, th, t1 * 1e3, B4 / (t1 * 1e-3) / 1e9, B4 / (t2 * 1e-3) / 1e9, B4 / (t3 * 1e-3) / 1e9,
+                   B2 / (t4 * 1e-3) / 1e9, B3 / (t5 * 1e-3) / 1e9);
+        }
+    }
+    const int n = 768, ntiles = (int)(d / n / 32);
+    const double BT = 4.0 * (double)ntiles * 32 * n * 4;
+    for (int grid : {296, 592}) {
+        float t1 = timeit([&] { k_tiled<32, 64, 1><<<grid, 256>>>(gr, g, h, n, ntiles, 0.9f, 0.1f); });
+        float t2 = timeit([&] { k_tiled<32, 64, 2><<<grid, 256>>>(gr, g, h, n, ntiles, 0.9f, 0.1f); });
+        float t3 = timeit([&] { k_tiled<32, 64, 4><<<grid, 256>>>(gr, g, h, n, ntiles, 0.9f, 0.1f); });
+        float t4 = timeit([&] { k_tiled<8, 256, 1><<<grid, 256>>>(gr, g, h, n, ntiles * 4, 0.9f, 0.1f); });
+        float t5 = timeit([&] { k_tiled<8, 256, 2><<<grid, 256>>>(gr, g, h, n, ntiles * 4, 0.9f, 0.1f); });
+        float t6 = timeit([&] { k_tiled<4, 512, 2><<<grid, 256>>>(gr, g, h, 1536, ntiles * 4, 0.9f, 0.1f); });
+        printf("tiled grid %d: 32x64 depth1 %6.0f | depth2 %6.0f | depth4 %6.0f || 8x256 d1 %6.0f | d2 %6.0f || 4x512 d2 %6.0f GB/s\n", grid,
+               BT / (t1 * 1e-3) / 1e9, BT / (t2 * 1e-3) / 1e9, BT / (t3 * 1e-3) / 1e9, BT / (t4 * 1e-3) / 1e9,
+               BT / (t5 * 1e-3) / 1e9, BT / (t6 * 1e-3) / 1e9);
+    }
+    for (int grid : {148, 296, 444}) {
+        auto run = [&](auto kern, int S, int R, int W, int nn, int nt) {
+            const int smem = S * 3 * R * (W + 4) * 4;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            float t = timeit([&] { kern<<<grid, 256, smem>>>(gr, g, h, nn, nt, 0.9f, 0.1f); });
+            cudaError_t e = cudaGetLastError();
+            return e == cudaSuccess ? BT / (t * 1e-3) / 1e9 : -1.0;
+        };
+        printf("tma grid %d: 32x64 S2 %6.0f | S3 %6.0f | S4 %6.0f | S6 %6.0f || 16x128 S3 %6.0f | S4 %6.0f || 8x256 S4 %6.0f GB/s\n", grid,
+               run(k_tma<32, 64, 2>, 2, 32, 64, n, ntiles), run(k_tma<32, 64, 3>, 3, 32, 64, n, ntiles),
+               run(k_tma<32, 64, 4>, 4, 32, 64, n, ntiles), run(k_tma<32, 64, 6>, 6, 32, 64, n, ntiles),
+               run(k_tma<16, 128, 3>, 3, 16, 128, n, ntiles * 2), run(k_tma<16, 128, 4>, 4, 16, 128, n, ntiles * 2),
+               run(k_tma<8, 256, 4>, 4, 8, 256, n, ntiles * 4));
+    }
+    for (int grid : {148, 296, 444}) {
+        auto run = [&](auto kern, int S, int R, int W, int nn, int nt) {
+            const int smem = S * 3 * R * (W + 4) * 4;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            float t = timeit([&] { kern<<<grid, 256, smem>>>(gr, g, h, nn, nt, 0.9f, 0.1f); });
+            cudaError_t e = cudaGetLastError();
+            return e == cudaSuccess ? BT / (t * 1e-3) / 1e9 : -1.0;
+        };
+        printf("cp.async grid %d: 32x64 S2 %6.0f | S3 %6.0f | S4 %6.0f | S6 %6.0f || 16x128 S3 %6.0f | S4 %6.0f || 8x256 S4 %6.0f GB/s\n", grid,
+               run(k_cpa<32, 64, 2>, 2, 32, 64, n, ntiles), run(k_cpa<32, 64, 3>, 3, 32, 64, n, ntiles),
+               run(k_cpa<32, 64, 4>, 4, 32, 64, n, ntiles), run(k_cpa<32, 64, 6>, 6, 32, 64, n, ntiles),
+               run(k_cpa<16, 128, 3>, 3, 16, 128, n, ntiles * 2), run(k_cpa<16, 128, 4>, 4, 16, 128, n, ntiles * 2),
+               run(k_cpa<8, 256, 4>, 4, 8, 256, n, ntiles * 4));
+    }
+    return 0;
+}
