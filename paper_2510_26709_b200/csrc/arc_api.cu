@@ -33,6 +33,10 @@ struct Nccl {
     ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
     ncclResult_t (*commUserRank)(const ncclComm_t, int*) = nullptr;
     ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
     bool ok = false;
 };
 
@@ -45,7 +49,12 @@ bool load_nccl(Nccl& n) {
     n.commCount = reinterpret_cast<decltype(n.commCount)>(dlsym(h, "ncclCommCount"));
     n.commUserRank = reinterpret_cast<decltype(n.commUserRank)>(dlsym(h, "ncclCommUserRank"));
     n.commGetAsyncError = reinterpret_cast<decltype(n.commGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
-    n.ok = n.allGather && n.allReduce && n.commCount && n.commUserRank && n.commGetAsyncError;
+    n.send = reinterpret_cast<decltype(n.send)>(dlsym(h, "ncclSend"));
+    n.recv = reinterpret_cast<decltype(n.recv)>(dlsym(h, "ncclRecv"));
+    n.groupStart = reinterpret_cast<decltype(n.groupStart)>(dlsym(h, "ncclGroupStart"));
+    n.groupEnd = reinterpret_cast<decltype(n.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+    n.ok = n.allGather && n.allReduce && n.commCount && n.commUserRank && n.commGetAsyncError && n.send && n.recv &&
+           n.groupStart && n.groupEnd;
     return n.ok;
 }
 
@@ -55,6 +64,7 @@ struct Plan {
     bool exchange = false;       // run the G>1 sequence
     bool keep_pnodes = false;
     int M = 0;                   // sum of ARC m_b (global ARC rows)
+    int64_t Ms = 0;              // exchange #1: rows per rank slice, ceil(M / G)
     int64_t sumK = 0, sumKn = 0, sum_nr = 0;
     int64_t num_segs = 0;        // gather / scatter row segments
     int num_slices = 0;          // selection slices (all blocks)
@@ -207,7 +217,8 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_cta = take(sizeof(int) * (kMaxGrid + 1));
     pl.o_selrows = take(sizeof(SelRow) * pl.num_segs);
     pl.o_V = take(sizeof(float) * sum_nr * 2);   // double-buffered by t parity
-    pl.o_sigma = take(sizeof(float) * std::max<int64_t>(M * nl, 1));
+    pl.Ms = (M + pl.G - 1) / pl.G;
+    pl.o_sigma = take(sizeof(float) * std::max<int64_t>(std::max<int64_t>(M * nl, pl.G * pl.Ms), 1));
     pl.o_sel = take(sizeof(int32_t) * sumK);
     pl.o_status = take(16);
     pl.o_hist1 = take(sizeof(unsigned) * kHist1Bins * nsb);
@@ -226,7 +237,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         pl.o_wire = take(sizeof(float) * pl.W * pl.L);
         pl.o_wire_all = pl.G > 1 ? take(sizeof(float) * pl.W * pl.L * pl.G) : 0;
     } else if (pl.exchange) {
-        pl.o_xrecv = pl.randk ? 0 : take(pn * pl.G);
+        pl.o_xrecv = pl.randk ? 0 : take(sizeof(float) * static_cast<size_t>(pl.Ms) * pl.L * p->r * pl.G);
         const bool ordered = p->value_reduce == ARC_REDUCE_ORDERED;
         pl.o_wire = take(sizeof(float) * sumKn * (ordered ? pl.L : 1));
         pl.o_wire_all = ordered ? take(sizeof(float) * sumKn * pl.L * pl.G) : 0;
@@ -641,17 +652,54 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     }
     ARC_MARK(2);
     // (DENSE blocks skip the sketch pass: the select/gather kernel applies their momentum.)
-    // Exchange #1 + S2 for G > 1 (Rand-K needs none: every rank draws the same keys)
-    if (pl.exchange && !pl.randk && pl.M > 0) {
-        const size_t cnt = static_cast<size_t>(pl.M) * L * c->p.r;
+    // Exchange #1 + S2 (Rand-K needs none: every rank draws the same keys).  Rank j
+    // owns rows [j Ms, (j+1) Ms) of the M ARC rows: an all-to-all brings it those
+    // rows' per-node sketches from every rank, k_sigma_slice sums them in global
+    // node order and forms Sigma, and an all-gather of the Sigma slices gives
+    // every rank all of Sigma.  (Several local nodes and no exchange: the select
+    // kernel forms Sigma from the per-node sketches itself, phase 0.)
+    const bool sigma_pass = (pl.exchange || L > 1) && !pl.randk && !pl.topk && pl.M > 0;
+    if (sigma_pass && pl.exchange) {
+        const int G = pl.G;
+        const int me = G > 1 ? c->p.rank : 0;
+        const int64_t Ms = pl.Ms;
+        const size_t row_floats = static_cast<size_t>(L) * c->p.r;
+        auto slice_rows = [&](int j) { return std::max<int64_t>(0, std::min<int64_t>(pl.M, (j + 1) * Ms) - j * Ms); };
         float* xs = c->at<float>(pl.o_pnodes);
-        float* xr = c->at<float>(pl.o_xrecv);
-        if (c->comm != nullptr) {
-            if (c->nccl.allGather(xs, xr, cnt, ncclFloat32, c->comm, s) != ncclSuccess) return ARC_ERR_NCCL;
-        } else {
-            ARC_CUDA(cudaMemcpyAsync(xr, xs, cnt * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        const float* x = xs;
+        if (pl.exchange && c->comm != nullptr) {
+            float* xr = c->at<float>(pl.o_xrecv);
+            if (c->nccl.groupStart() != ncclSuccess) return ARC_ERR_NCCL;
+            for (int j = 0; j < G; ++j) {
+                const size_t out = static_cast<size_t>(slice_rows(j)) * row_floats;
+                const size_t in = static_cast<size_t>(slice_rows(me)) * row_floats;
+                if (out > 0 && c->nccl.send(xs + j * Ms * row_floats, out, ncclFloat32, j, c->comm, s) != ncclSuccess) {
+                    c->nccl.groupEnd();
+                    return ARC_ERR_NCCL;
+                }
+                if (in > 0 && c->nccl.recv(xr + j * Ms * row_floats, in, ncclFloat32, j, c->comm, s) != ncclSuccess) {
+                    c->nccl.groupEnd();
+                    return ARC_ERR_NCCL;
+                }
+            }
+            if (c->nccl.groupEnd() != ncclSuccess) return ARC_ERR_NCCL;
+            x = xr;
         }
-        // (S2 itself — the ordered node sum and Sigma — is phase 0 of the selection kernel)
+        SigmaLaunch sl{};
+        sl.x = x;
+        sl.Ms = Ms;
+        sl.rows = slice_rows(me);
+        sl.G = G;
+        sl.L = L;
+        sl.r = c->p.r;
+        sl.Nf = c->Nf;
+        sl.sigma = sigma + me * Ms;
+        sl.status = status;
+        launch_sigma_slice(sl, s);
+        ARC_LAUNCHED();
+        if (pl.exchange && c->comm != nullptr &&
+            c->nccl.allGather(sigma + me * Ms, sigma, static_cast<size_t>(Ms), ncclFloat32, c->comm, s) != ncclSuccess)
+            return ARC_ERR_NCCL;
     }
     ARC_MARK(3);
     // S3 + S4 (+ S5, S6 when every node is local): one cooperative kernel
@@ -702,14 +750,11 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.stamps = c->stamps;
         sg.pdl = c->pdl && !c->timing && !(pl.exchange && pl.M > 0) ? 1 : 0;
         sg.early = c->early && ga.mode == 0 && ga.values == nullptr ? 1 : 0;
-        if ((pl.exchange || L > 1) && !pl.randk && !pl.topk && pl.M > 0) {
-            // S2 (ordered node sum, Sigma) as phase 0 of the selection kernel, from the
-            // all-gathered sketches (exchange) or this GPU's per-node sketches
-            sg.xrecv = pl.exchange ? c->at<float>(pl.o_xrecv) : c->at<float>(pl.o_pnodes);
+        sg.build_hist = sigma_pass ? 1 : 0;
+        if (sigma_pass && !pl.exchange) {
+            sg.xsk = c->at<float>(pl.o_pnodes);
             sg.sigma_w = sigma;
-            sg.G = pl.exchange ? pl.G : 1;
             sg.L = L;
-            sg.M = pl.M;
             sg.Nf = c->Nf;
             sg.status = status;
         }
@@ -901,15 +946,17 @@ arc_status arc_topk_sizes(const arc_topk_ctx* c, int64_t* sum_K, int64_t* sum_Kn
 
 int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     if (c == nullptr) return -1;
-    // steady state with consecutive t: V comes from the previous step (no k_vgen)
-    const int arc = c->pl.M > 0 ? (c->pl.items.empty() ? 2 : 1) : 0;
-    // vgen + ef_sketch, [sketch_reduce], select_gather, [scatter]; Top-K: no vgen, N merges
-    if (c->pl.topk) return (c->pl.M > 0 ? 1 : 0) + 1 + c->p.N;
-    if (c->pl.randk)
-        return (c->pl.M > 0 ? 1 : 0) + (c->pl.items.empty() ? 0 : 1) + (c->pl.dense_ids.empty() ? 0 : 1) +
-               (c->pl.exchange ? 1 : 0);
-    return arc + (c->pl.items.empty() ? 0 : 1) +
-           (c->pl.dense_ids.empty() ? 0 : 1) + (c->pl.exchange ? 1 : 0);
+    // steady state with consecutive t: V comes from the previous step's select
+    // kernel (k_vgen only when there is none)
+    const Plan& pl = c->pl;
+    const int sketch = pl.M > 0 ? 1 : 0;
+    const int sel = pl.items.empty() ? 0 : 1;
+    if (pl.topk) return sketch + sel + c->p.N;   // + N ordered merges
+    const int vgen = (pl.M > 0 && pl.items.empty() && !pl.randk) ? 1 : 0;
+    const int sigma = pl.exchange && !pl.randk && pl.M > 0 ? 1 : 0;
+    const int dense = pl.dense_ids.empty() ? 0 : 1;
+    const int scatter = pl.exchange ? (pl.segs_real.empty() ? 0 : 1) + dense : 0;
+    return vgen + sketch + sigma + sel + dense + scatter;
 }
 
 arc_status arc_topk_set_timing(arc_topk_ctx* c, int32_t enable) {

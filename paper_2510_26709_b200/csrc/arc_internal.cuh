@@ -96,10 +96,14 @@ struct SelectGatherLaunch {
     int pdl;                       // launch with programmatic stream serialization
     int early;                     // mode 0 without values: gather the certainly selected rows
                                    // (digit 1 above the boundary bin) before barrier 1 completes
-    // exchange path: Sigma computed here from the all-gathered sketches (else nullptr)
-    const float* xrecv;            // [G][M][L][r]
+    // Sigma not formed by the streaming pass: the kernel builds the digit-1
+    // histogram itself, behind one more grid barrier (phase 0) -- from s.sigma
+    // (k_sigma_slice + all-gather, exchange path) or, when xsk != nullptr, after
+    // forming Sigma from this GPU's per-node sketches (several local nodes)
+    int build_hist;
+    const float* xsk;              // [M][L][r] per-node sketches, or nullptr
     float* sigma_w;                // Sigma written for queries
-    int G, L, M;
+    int L;
     float Nf;
     unsigned* status;
 };
@@ -183,6 +187,19 @@ struct ScatterLaunch {
     float* values;          // optional A/N
 };
 void launch_scatter(const ScatterLaunch& a, cudaStream_t s);
+
+// S2 on this rank's row slice (after the all-to-all of exchange #1, or on the
+// per-node sketches of one GPU with several local nodes).
+struct SigmaLaunch {
+    const float* x;      // [G][Ms][L][r] per-node sketches of the slice's rows, by source rank
+    long long Ms;        // rows per slice (the source-rank stride)
+    long long rows;      // rows of this slice
+    int G, L, r;
+    float Nf;
+    float* sigma;        // Sigma of the slice's rows
+    unsigned* status;
+};
+void launch_sigma_slice(const SigmaLaunch& a, cudaStream_t s);
 
 // DENSE blocks with every node on this GPU: one streaming pass (identity compressor).
 struct DenseLaunch {

@@ -5,13 +5,15 @@
 // fixes (R9, R11), so results are bit-identical to the plain definition; the
 // library is also built with -fmad=false -ftz=false -prec-div=true.
 //
-// Kernels (DESIGN.md §5 has the roofline of each):
-//   k_vgen          S0  V_b = Gaussian(seed, t, b)                  P:229-230, Alg.1 l.3
-//   k_ef_sketch     S1+S2  h' = (1-eta)h + eta grad; Delta = h' - g;  eq:ef21m-1 P:325,
-//                      P_i = (1/sqrt r) Delta V; (G==1) P, Sigma      P:231-237, Alg.1 l.4-6
-//   k_select        S3  I_b = argtop_K(Sigma), cluster radix select  zn28373 P:236-237
-//   k_gather_ef     S4 (+S5+S6 when G==1)                            2zn20 P:241-243, eq:ef21m-2
-//   k_scatter       S6 (G>1)                                         eq:ef21m-3 P:327
+// Kernels here (DESIGN.md §5 has the roofline of each; the two big ones,
+// k_ef_sketch and k_select_gather, have their own files):
+//   k_vgen          S0  V_b = Gaussian(seed, t, b)                     P:229-230, Alg.1 l.3
+//   k_sigma_slice   S2 on a row slice: S = sum of the nodes' P_i in    P:232, zn28373 P:236
+//                   global node order, P = S / N, Sigma = sum_j P_j^2   (R3, R9, R21)
+//   k_dense         S1+S4..S6 of DENSE blocks (identity compressor)    P:510, R11, R20
+//   k_scatter       S6 after exchange #2                               eq:ef21m-3 P:327
+//   k_dense_scatter S6 of DENSE blocks after exchange #2
+//   k_topk_merge    Top-K baseline: merge of the all-gathered payloads  Table I "Top-K"
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -249,6 +251,41 @@ __global__ void __launch_bounds__(256) k_dense_scatter(const DenseScatterLaunch 
     }
 }
 
+// S2 for the rows of one slice: x holds, for every source rank g and local node
+// l, the slice's per-node sketches P_{gL+l} ([G][Ms][L][r]); the sum runs in
+// ascending global node id g L + l (R9, R21).  One thread per row.
+__global__ void __launch_bounds__(256) k_sigma_slice(const SigmaLaunch a) {
+    const long long p = blockIdx.x * 256LL + threadIdx.x;
+    if (p >= a.rows) return;
+    const int L = a.L, r = a.r;
+    float sig = 0.0f;
+    if (r == 4) {
+        float4 S = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int g = 0; g < a.G; ++g)
+            for (int l = 0; l < L; ++l) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(a.x + ((g * a.Ms + p) * L + l) * 4));
+                if (g == 0 && l == 0) S = v;
+                else { S.x = fadd(S.x, v.x); S.y = fadd(S.y, v.y); S.z = fadd(S.z, v.z); S.w = fadd(S.w, v.w); }
+            }
+        const float P[4] = {__fdiv_rn(S.x, a.Nf), __fdiv_rn(S.y, a.Nf), __fdiv_rn(S.z, a.Nf), __fdiv_rn(S.w, a.Nf)};   // R3
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sig = fadd(sig, fmul(P[j], P[j]));                       // zn28373
+    } else {
+        for (int j = 0; j < r; ++j) {
+            float S = 0.0f;
+            for (int g = 0; g < a.G; ++g)
+                for (int l = 0; l < L; ++l) {
+                    const float v = __ldcs(a.x + ((g * a.Ms + p) * L + l) * r + j);
+                    S = (g == 0 && l == 0) ? v : fadd(S, v);
+                }
+            const float P = __fdiv_rn(S, a.Nf);
+            sig = fadd(sig, fmul(P, P));
+        }
+    }
+    a.sigma[p] = sig;
+    if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
+}
+
 }  // namespace
 
 // ---- launchers ---------------------------------------------------------------
@@ -282,6 +319,10 @@ void launch_dense_scatter(const DenseScatterLaunch& a, cudaStream_t s) {
 
 void launch_topk_merge(const MergeLaunch& a, cudaStream_t s) {
     k_topk_merge<<<rows_grid(a.num_rows), 256, 0, s>>>(a);
+}
+
+void launch_sigma_slice(const SigmaLaunch& a, cudaStream_t s) {
+    if (a.rows > 0) k_sigma_slice<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(a);
 }
 
 void launch_scatter(const ScatterLaunch& a, cudaStream_t s) {

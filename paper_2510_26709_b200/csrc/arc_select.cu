@@ -398,81 +398,96 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     unsigned* ccount = s.cand_count + par * s.num_blocks;                 // this step's counters
     unsigned* cand = s.cand + (static_cast<long long>(par) * s.num_blocks + bb) * (2 * kCandCap);
 
-    // ------------------------------------------------ phase 0 (exchange path)
-    // S2 after exchange #1: Sigma of this slice's rows from the all-gathered
-    // per-node sketches (sum in global node order, R9, R21), its digit-1
-    // histogram, then a grid barrier so the block's histogram is complete.
+    // ------------------------------------------------ phase 0
+    // Sigma was not formed by the streaming pass: either the kernel forms it here
+    // from this GPU's per-node sketches ([M][L][r], several local nodes, no
+    // exchange: S2 summed in node order, R9, R21), or k_sigma_slice + the Sigma
+    // all-gather left it in s.sigma (exchange path).  Then the slice's keys, the
+    // block's digit-1 histogram, and a grid barrier so the histogram is complete.
     if constexpr (kPhase0) {
-        if (B.kind == ARC_BLOCK_ARC) {   // every ARC block gets its Sigma (queries); K < m ones select
+        if (B.kind == ARC_BLOCK_ARC && (arc || s.xsk != nullptr)) {   // every ARC block gets its Sigma
             for (int i = tid; i < kHist1Bins; i += kThreads) sh[i] = 0;
             __syncthreads();
-            const long long M = s.M;
-            const int GL = s.G * s.L;                // global node id = g L + l
-            auto finish = [&](int i, const float* S) {
-                const long long p = B.row_base + lo + i;
-                float sig = 0.0f;
-                for (int j = 0; j < s.r; ++j) {
-                    const float pv = __fdiv_rn(S[j], s.Nf);                // R3
-                    sig = fadd(sig, fmul(pv, pv));                         // zn28373
-                }
-                s.sigma_w[p] = sig;
+            auto finish = [&](int i, float sig) {
                 const unsigned key = order_key(sig);
                 s_keys[i] = key;
                 atomicAdd(&sh[key >> kHist1Shift], 1u);
-                if (!isfinite(sig)) atomicOr(s.status, kStatusNonfinite);
             };
-            if (s.r == 4) {
-                // 4 rows per thread, 4 nodes per round: 16 float4 loads in flight
+            if (s.xsk == nullptr) {
+                const float* __restrict__ sg = s.sigma + B.row_base + lo;
                 for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {
-                    float S[4][4];
-                    for (int n0 = 0; n0 < GL; n0 += 4) {
-                        float4 v[4][4];
+                    float v[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int i = i0 + u * kThreads + tid;
-                            const long long p = B.row_base + lo + i;
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const int node = n0 + k;
-                                if (i < nk && node < GL) {
-                                    const long long g = node / s.L, l = node % s.L;
-                                    v[u][k] = __ldcg(reinterpret_cast<const float4*>(s.xrecv + ((g * M + p) * s.L + l) * 4));
-                                }
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                if (n0 + k >= GL) continue;
-                                const float4 w = v[u][k];
-                                if (n0 + k == 0) { S[u][0] = w.x; S[u][1] = w.y; S[u][2] = w.z; S[u][3] = w.w; }
-                                else {                                                   // R9 node order
-                                    S[u][0] = fadd(S[u][0], w.x); S[u][1] = fadd(S[u][1], w.y);
-                                    S[u][2] = fadd(S[u][2], w.z); S[u][3] = fadd(S[u][3], w.w);
-                                }
-                            }
+                    for (int k = 0; k < 4; ++k) {
+                        const int i = i0 + k * kThreads + tid;
+                        v[k] = i < nk ? __ldcg(sg + i) : 0.0f;
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int i = i0 + u * kThreads + tid;
-                        if (i < nk) finish(i, S[u]);
+                    for (int k = 0; k < 4; ++k) {
+                        const int i = i0 + k * kThreads + tid;
+                        if (i < nk) finish(i, v[k]);
                     }
                 }
             } else {
-                for (int i = tid; i < nk; i += kThreads) {
-                    const long long p = B.row_base + lo + i;
-                    float S[32];
+                const int L = s.L;
+                auto sigma_of = [&](int i, const float* S) {
+                    float sig = 0.0f;
                     for (int j = 0; j < s.r; ++j) {
-                        float a = 0.0f;
-                        for (int node = 0; node < GL; ++node) {
-                            const long long g = node / s.L, l = node % s.L;
-                            const float v = __ldcg(s.xrecv + ((g * M + p) * s.L + l) * s.r + j);
-                            a = node == 0 ? v : fadd(a, v);
-                        }
-                        S[j] = a;
+                        const float pv = __fdiv_rn(S[j], s.Nf);                // R3
+                        sig = fadd(sig, fmul(pv, pv));                         // zn28373
                     }
-                    finish(i, S);
+                    s.sigma_w[B.row_base + lo + i] = sig;
+                    if (!isfinite(sig)) atomicOr(s.status, kStatusNonfinite);
+                    finish(i, sig);
+                };
+                if (s.r == 4) {
+                    // 4 rows per thread, 4 nodes per round: 16 float4 loads in flight
+                    for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {
+                        float S[4][4];
+                        for (int n0 = 0; n0 < L; n0 += 4) {
+                            float4 v[4][4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int i = i0 + u * kThreads + tid;
+                                const long long p = B.row_base + lo + i;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    if (i < nk && n0 + k < L)
+                                        v[u][k] = __ldcg(reinterpret_cast<const float4*>(s.xsk + (p * L + n0 + k) * 4));
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    if (n0 + k >= L) continue;
+                                    const float4 w = v[u][k];
+                                    if (n0 + k == 0) { S[u][0] = w.x; S[u][1] = w.y; S[u][2] = w.z; S[u][3] = w.w; }
+                                    else {                                               // R9 node order
+                                        S[u][0] = fadd(S[u][0], w.x); S[u][1] = fadd(S[u][1], w.y);
+                                        S[u][2] = fadd(S[u][2], w.z); S[u][3] = fadd(S[u][3], w.w);
+                                    }
+                                }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = i0 + u * kThreads + tid;
+                            if (i < nk) sigma_of(i, S[u]);
+                        }
+                    }
+                } else {
+                    for (int i = tid; i < nk; i += kThreads) {
+                        const long long p = B.row_base + lo + i;
+                        float S[32];
+                        for (int j = 0; j < s.r; ++j) {
+                            float a = 0.0f;
+                            for (int l = 0; l < L; ++l) {
+                                const float v = __ldcg(s.xsk + (p * L + l) * s.r + j);
+                                a = l == 0 ? v : fadd(a, v);
+                            }
+                            S[j] = a;
+                        }
+                        sigma_of(i, S);
+                    }
                 }
             }
             if (arc) flush_hist(sh, s.hist1 + bb * kHist1Bins, kHist1Bins);
@@ -767,7 +782,7 @@ cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = s.pdl ? 2 : 1;
-    if (s.xrecv != nullptr) return cudaLaunchKernelEx(&cfg, k_select_gather<true>, s, ga);
+    if (s.build_hist) return cudaLaunchKernelEx(&cfg, k_select_gather<true>, s, ga);
     return cudaLaunchKernelEx(&cfg, k_select_gather<false>, s, ga);
 }
 

@@ -29,12 +29,15 @@ def comm_entries(method: str, m: int, n: int, N: int, K: int, r: int = 4) -> int
 def arc_bus_bytes(sum_m: int, sum_Kn: int, r: int, G: int, nodes_local: int = 1,
                   reduce: str = "nccl") -> dict:
     """Bytes each GPU sends over NVLink per step in this build's schedule:
-    exchange #1 = all-gather of the per-node sketches (sum_m x nodes_local x r fp32),
-    exchange #2 = ncclAllReduce of the K rows (ring bus bytes 2(G-1)/G) or, in
-    ordered mode, an all-gather of the per-node rows."""
+    exchange #1 = all-to-all of row slices of the per-node sketches
+    ((G-1) slices of ceil(sum_m/G) rows x nodes_local x r fp32) plus an
+    all-gather of the Sigma slices ((G-1) x ceil(sum_m/G) fp32 received, one
+    slice sent per peer); exchange #2 = ncclAllReduce of the K rows (ring bus
+    bytes 2(G-1)/G) or, in ordered mode, an all-gather of the per-node rows."""
     if G <= 1:
         return {"sketch": 0, "values": 0, "total": 0}
-    sk = (G - 1) * sum_m * nodes_local * r * 4
+    Ms = -(-sum_m // G)
+    sk = (G - 1) * Ms * nodes_local * r * 4 + (G - 1) * Ms * 4
     if reduce == "nccl":
         vals = int(2 * (G - 1) / G * sum_Kn * 4)
     else:

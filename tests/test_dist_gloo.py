@@ -2,8 +2,10 @@
 
 1. Parameter consistency across ranks (SPMD contract of arc_topk_create).
 2. The exchange protocol of the multi-GPU path (reading R21):
-   every rank exports its nodes' sketches P_i, all-gathers them, and sums them
-   in ascending GLOBAL node id; the selection is then identical on every rank
+   every rank exports its nodes' sketches P_i; an all-to-all of row slices
+   gives rank j all nodes' sketches of its rows, which it sums in ascending
+   GLOBAL node id into its slice of Sigma; an all-gather of the slices gives
+   every rank all of Sigma.  The selection is then identical on every rank
    and equal to the single-process oracle's, bit for bit, for any placement of
    the N nodes on G ranks.  Exchange #2 in "ordered" mode (all-gather of the
    per-node rows) is bit-exact too; in "nccl" mode (an All-Reduce with
@@ -67,7 +69,7 @@ def _worker_protocol(rank, world, port, L, reduce, steps, q):
     import oracle
     from synth import GradientSource, flat_blocks
     N = world * L
-    d, n, K, r, eta, seed = 6000, 30, 13, 4, 0.1, 9
+    d, n, K, r, eta, seed = 6030, 30, 13, 4, 0.1, 9   # m = 201: uneven row slices
     blocks = flat_blocks(d, n, K=K)
     m = blocks[0].m
     src = GradientSource(d, blocks, N, seed=seed)
@@ -88,15 +90,31 @@ def _worker_protocol(rank, world, port, L, reduce, steps, q):
             h[l] = (one_m_eta * h[l] + np.float32(eta) * all_grads[i]).astype(np.float32)
             D.append((h[l] - g[l]).astype(np.float32))
             Pi.append(oracle.arc_round([D[-1]], n=n, K=K, V=V)["P_nodes"][0])      # (1/sqrt r) Delta_i V
-        # exchange #1: all-gather per-node sketches, sum in global node order
-        mine = torch.from_numpy(np.stack(Pi))
-        got = [torch.empty_like(mine) for _ in range(world)]
-        dist.all_gather(got, mine)
-        per_node = [x.numpy()[l] for x in got for l in range(L)]                    # global node order
+        # exchange #1: rank j owns rows [j Ms, (j+1) Ms); an
+        # all-to-all (send/recv) brings it those rows' per-node sketches from every
+        # rank, it sums them in global node order and forms its Sigma slice, and an
+        # all-gather of the (padded) slices gives every rank all of Sigma
+        Ms = -(-m // world)
+        mine = np.zeros((world * Ms, L, r), np.float32)
+        mine[:m] = np.stack(Pi, axis=1)                                              # [m][L][r]
+        recv = [torch.empty((Ms, L, r)) for _ in range(world)]
+        reqs = []
+        for j in range(world):
+            if j == rank:
+                recv[j].copy_(torch.from_numpy(mine[j * Ms:(j + 1) * Ms]))
+                continue
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(mine[j * Ms:(j + 1) * Ms])), j))
+            reqs.append(dist.irecv(recv[j], j))
+        for q_ in reqs:
+            q_.wait()
+        per_node = [recv[gr].numpy()[:, l, :] for gr in range(world) for l in range(L)]   # global node order
         P = (_f32_seq_sum(per_node) / Nf).astype(np.float32)
-        sig = np.zeros(m, np.float32)
+        sig_slice = np.zeros(Ms, np.float32)
         for j in range(r):
-            sig = (sig + P[:, j] * P[:, j]).astype(np.float32)
+            sig_slice = (sig_slice + P[:, j] * P[:, j]).astype(np.float32)
+        got = [torch.empty(Ms) for _ in range(world)]
+        dist.all_gather(got, torch.from_numpy(sig_slice))
+        sig = np.concatenate([x.numpy() for x in got])[:m]
         I = oracle.argtop_k(sig, K)
         # compaction + local EF update
         C = [Dl.reshape(m, n)[I] for Dl in D]
@@ -173,6 +191,12 @@ def test_ledger_closed_forms():
     assert comm_entries("arc", 4, 3, 1, 1) == 0
     # r = 1 reduces ARC to 2Kn + 2m
     assert comm_entries("arc", 100, 8, 4, 5, r=1) == 2 * 5 * 8 + 2 * 100
+    # this build's NVLink bytes per GPU: all-to-all of sketch row slices + Sigma
+    # all-gather (G = 2, m = 10 -> slices of 5 rows), ring All-Reduce of K n values
+    from paper_2510_26709_b200.ledger import arc_bus_bytes
+    b = arc_bus_bytes(10, 30, r=4, G=2)
+    assert b["sketch"] == 5 * 4 * 4 + 5 * 4 and b["values"] == 30 * 4
+    assert arc_bus_bytes(10, 30, r=4, G=1)["total"] == 0
 
 
 def test_node_placement():
