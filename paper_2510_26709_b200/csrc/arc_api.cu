@@ -480,9 +480,10 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         for (const BlockDev& B : c->pl.bdev)
             if (B.kind == ARC_BLOCK_ARC) { all_vec = all_vec && B.vec; min_n = std::min(min_n, B.n); }
         (void)all_vec;
-        // 32 x 64 measured best on C3 (n = 768) and C5 (n = 1024); 32 x 256 in
-        // 8-row rounds (1 KB row segments) on the LLaMA layout (n >= 2048)
-        c->shape = min_n >= 2048 && sketch_shape_ok(3, c->p.r) ? 3 : min_n >= 64 ? 1 : 0;
+        // 32 x 256 in 8-row rounds (1 KB row segments) measured best for rows of
+        // >= 1024 (C5, the LLaMA layout), 32 x 64 for shorter rows (C2, C3 tie)
+        //
+        c->shape = min_n >= 1024 && sketch_shape_ok(3, c->p.r) ? 3 : min_n >= 64 ? 1 : 0;
         if (const char* e = getenv("ARC_SKETCH_SHAPE")) {
             const int v = atoi(e);
             if (v >= 0 && v <= 4) c->shape = v;

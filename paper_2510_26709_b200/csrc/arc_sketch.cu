@@ -72,8 +72,9 @@ __device__ __forceinline__ void fetch_tile(const TileDesc* tiles, int li, TileDe
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(d), "l"(src) : "memory");
     }
 }
+template <int kPending>
 __device__ __forceinline__ void fetch_wait() {
-    if (threadIdx.x < 4) asm volatile("cp.async.wait_all;" ::: "memory");
+    if (threadIdx.x < 4) asm volatile("cp.async.wait_group %0;" ::"n"(kPending) : "memory");
 }
 
 // valid columns of tile row `row` (0 for rows beyond the tile): the last row of
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
     __shared__ __align__(16) float Ds[NB][R][DS];
     __shared__ __align__(16) float Vs[NB][W * VS];
     __shared__ unsigned hist[kHist1Bins];       // digit-1 histogram of this CTA's Sigma (mode 0)
-    __shared__ TileDesc s_tile[2];              // tile descriptors: list position parity
+    __shared__ TileDesc s_tile[3];              // tile descriptors, list position mod 3
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int crow = tid >> 2, jl = tid & 3;    // chain role (threads < 4R)
@@ -106,9 +107,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
     if (list_begin >= list_end) return;
     const int r = a.r;
     for (int i = tid; i < kHist1Bins; i += kThreads) hist[i] = 0;
-    fetch_tile(a.tiles, list_begin, &s_tile[0]);
-    if (list_begin + 1 < list_end) fetch_tile(a.tiles, list_begin + 1, &s_tile[1]);
-    fetch_wait();
+    for (int k = 0; k < 3 && list_begin + k < list_end; ++k) fetch_tile(a.tiles, list_begin + k, &s_tile[k]);
+    fetch_wait<0>();
     __syncthreads();
     grid_dependency_wait();   // the previous kernel (g, V, histogram reset) is complete
     // (the first __syncthreads of the main loop orders this before any use)
@@ -132,12 +132,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
     float xv[NV];                                // this thread's V entries of the chunk
 
 
-    auto load_chunk = [&](const TileRegs& t, int node, int chunk, int rnd) {
-        const float* __restrict__ pg = a.nodes.grad[node];
-        const float* __restrict__ ph = a.nodes.h[node];
-        const float* __restrict__ pgg = a.nodes.g[node];
+    // A load round is NP parts of 4 elements per thread per stream; part 0 also
+    // carries the thread's V entries of the chunk (round 0).  Staging part p of
+    // the current round frees its registers, which immediately take part p of
+    // the next round: one round stays in flight without a gap at the barrier.
+    constexpr int NP = NE / 4;
+    auto load_part = [&](const TileRegs& t, int chunk, int rnd, int part) {
+        const float* __restrict__ pg = a.nodes.grad[t.node];
+        const float* __restrict__ ph = a.nodes.h[t.node];
+        const float* __restrict__ pgg = a.nodes.g[t.node];
         const int c0 = chunk * W;
-        if (rnd == 0) {   // V rows [c0, c0 + W) of the block, r values each -> stride VS (zero padded)
+        if (rnd == 0 && part == 0) {   // V rows [c0, c0 + W) of the block, r values each -> stride VS (zero padded)
             const float* __restrict__ Vb = a.V + t.v_off;
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
@@ -146,32 +151,30 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
             }
         }
         if (t.vec) {
+            const int e4 = 4 * part;
+            const int row = rnd * RR + vrow(e4), col = c0 + vcol(e4);
+            const int nv = row_cols(t, row);
+            const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
+            if (col + 3 < nv) {
+                const float4 vg = __ldcs(reinterpret_cast<const float4*>(pg + e));
+                const float4 vh = __ldcs(reinterpret_cast<const float4*>(ph + e));
+                const float4 vd = __ldcs(reinterpret_cast<const float4*>(pgg + e));
+                xg[e4] = vg.x; xg[e4 + 1] = vg.y; xg[e4 + 2] = vg.z; xg[e4 + 3] = vg.w;
+                xh[e4] = vh.x; xh[e4 + 1] = vh.y; xh[e4 + 2] = vh.z; xh[e4 + 3] = vh.w;
+                xd[e4] = vd.x; xd[e4 + 1] = vd.y; xd[e4 + 2] = vd.z; xd[e4 + 3] = vd.w;
+            } else {
 #pragma unroll
-            for (int e4 = 0; e4 < NE; e4 += 4) {
-                const int row = rnd * RR + vrow(e4), col = c0 + vcol(e4);
-                const int nv = row_cols(t, row);
-                const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
-                if (col + 3 < nv) {
-                    const float4 vg = __ldcs(reinterpret_cast<const float4*>(pg + e));
-                    const float4 vh = __ldcs(reinterpret_cast<const float4*>(ph + e));
-                    const float4 vd = __ldcs(reinterpret_cast<const float4*>(pgg + e));
-                    xg[e4] = vg.x; xg[e4 + 1] = vg.y; xg[e4 + 2] = vg.z; xg[e4 + 3] = vg.w;
-                    xh[e4] = vh.x; xh[e4 + 1] = vh.y; xh[e4 + 2] = vh.z; xh[e4 + 3] = vh.w;
-                    xd[e4] = vd.x; xd[e4 + 1] = vd.y; xd[e4 + 2] = vd.z; xd[e4 + 3] = vd.w;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (col + k < nv) {
-                            xg[e4 + k] = __ldcs(pg + e + k);
-                            xh[e4 + k] = __ldcs(ph + e + k);
-                            xd[e4 + k] = __ldcs(pgg + e + k);
-                        }
+                for (int k = 0; k < 4; ++k) {
+                    if (col + k < nv) {
+                        xg[e4 + k] = __ldcs(pg + e + k);
+                        xh[e4 + k] = __ldcs(ph + e + k);
+                        xd[e4 + k] = __ldcs(pgg + e + k);
                     }
                 }
             }
         } else {
 #pragma unroll
-            for (int e1 = 0; e1 < NE; ++e1) {
+            for (int e1 = 4 * part; e1 < 4 * part + 4; ++e1) {
                 const int row = rnd * RR + srow(e1), col = c0 + scol(e1);
                 const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
                 if (col < row_cols(t, row)) {
@@ -183,33 +186,31 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         }
     };
 
-    auto stage_chunk = [&](const TileRegs& t, int node, int chunk, int rnd, int buf) {
-        float* __restrict__ ph = a.nodes.h[node];
+    auto stage_part = [&](const TileRegs& t, int chunk, int rnd, int part, int buf) {
+        float* __restrict__ ph = a.nodes.h[t.node];
         const int c0 = chunk * W;
         if (t.vec) {
+            const int e4 = 4 * part;
+            const int row = rnd * RR + vrow(e4), cl = vcol(e4), col = c0 + cl;
+            const int nv = row_cols(t, row);
+            const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
+            float hn[4], dl[4];
 #pragma unroll
-            for (int e4 = 0; e4 < NE; e4 += 4) {
-                const int row = rnd * RR + vrow(e4), cl = vcol(e4), col = c0 + cl;
-                const int nv = row_cols(t, row);
-                const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
-                float hn[4], dl[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    hn[k] = fadd(fmul(a.ome, xh[e4 + k]), fmul(a.eta, xg[e4 + k]));   // R11
-                    dl[k] = fsub(hn[k], xd[e4 + k]);                                   // R4
-                }
-                if (col + 3 < nv) {
-                    __stcs(reinterpret_cast<float4*>(ph + e), make_float4(hn[0], hn[1], hn[2], hn[3]));
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (col + k < nv) ph[e + k] = hn[k];
-                }
-                *reinterpret_cast<float4*>(&Ds[buf][row][cl]) = make_float4(dl[0], dl[1], dl[2], dl[3]);
+            for (int k = 0; k < 4; ++k) {
+                hn[k] = fadd(fmul(a.ome, xh[e4 + k]), fmul(a.eta, xg[e4 + k]));   // R11
+                dl[k] = fsub(hn[k], xd[e4 + k]);                                   // R4
             }
+            if (col + 3 < nv) {
+                __stcs(reinterpret_cast<float4*>(ph + e), make_float4(hn[0], hn[1], hn[2], hn[3]));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (col + k < nv) ph[e + k] = hn[k];
+            }
+            *reinterpret_cast<float4*>(&Ds[buf][row][cl]) = make_float4(dl[0], dl[1], dl[2], dl[3]);
         } else {
 #pragma unroll
-            for (int e1 = 0; e1 < NE; ++e1) {
+            for (int e1 = 4 * part; e1 < 4 * part + 4; ++e1) {
                 const int row = rnd * RR + srow(e1), cl = scol(e1), col = c0 + cl;
                 const long long e = t.off + static_cast<long long>(t.row0 + row) * t.n + col;
                 const float hn = fadd(fmul(a.ome, xh[e1]), fmul(a.eta, xg[e1]));
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
                 Ds[buf][row][cl] = fsub(hn, xd[e1]);
             }
         }
-        if (rnd == 0) {   // V, loaded with the chunk
+        if (rnd == 0 && part == 0) {   // V, loaded with the chunk
 #pragma unroll
             for (int k = 0; k < NV; ++k)
                 if (tid + k * kThreads < W * VS) Vs[buf][tid + k * kThreads] = xv[k];
@@ -228,37 +229,48 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
 #pragma unroll
     for (int s = 0; s < RPT; ++s) { acc[s] = 0.0f; S[s] = 0.0f; }
 
-    int li = list_begin, chunk = 0;
-    TileRegs tc = tile_regs<W>(s_tile[0]); // tile of the chunk being staged / chained
-    TileRegs tl = tc;                      // tile of the chunk being loaded
-    load_chunk(tc, tc.node, chunk, 0);
+    // the unit = one load round (tile li, chunk, round); cursor on the unit being
+    // staged, its successor's loads issued part by part while it is staged
+    int li = list_begin, chunk = 0, rnd = 0;
+    TileRegs tc = tile_regs<W>(s_tile[0]); // tile of the unit being staged / chained
+#pragma unroll
+    for (int p = 0; p < NP; ++p) load_part(tc, 0, 0, p);
     int buf = 0;
+    bool first = true;
     while (true) {
-        // NR rounds of RR rows; each round's loads fly while the previous one is staged
-        if (NB == 1) __syncthreads();      // the single Delta buffer is free again
-#pragma unroll 1
-        for (int k = 0; k < NR; ++k) {
-            stage_chunk(tc, tc.node, chunk, k, buf);
-            if (k + 1 < NR) {
-                if (NR > 1 && (k + 1) * RR >= tc.m_rows) break;   // rounds past the tile's rows
-                load_chunk(tc, tc.node, chunk, k + 1);
+        int nli = li, nchunk = chunk, nrnd = rnd + 1;
+        if (nrnd == NR || nrnd * RR >= tc.m_rows) {   // (rounds past the tile's rows are skipped)
+            nrnd = 0;
+            if (++nchunk == tc.nchunks) {
+                nchunk = 0;
+                ++nli;
             }
-        }
-        fetch_wait();                      // (the descriptor fetched one tile ahead)
-        __syncthreads();
-        // advance the load cursor and issue the next chunk's loads
-        int nli = li, nchunk = chunk + 1;
-        if (nchunk == tc.nchunks) {
-            nchunk = 0;
-            ++nli;
         }
         const bool more = nli < list_end;
-        if (more) {
-            if (nli != li) {
-                tl = tile_regs<W>(s_tile[(nli - list_begin) & 1]);
-                if (nli + 1 < list_end) fetch_tile(a.tiles, nli + 1, &s_tile[(nli + 1 - list_begin) & 1]);
-            }
-            load_chunk(tl, tl.node, nchunk, 0);
+        TileRegs tl = tc;                  // tile of the successor unit
+        if (more && nli != li) {
+            tl = tile_regs<W>(s_tile[(nli - list_begin) % 3]);
+            if (nli + 2 < list_end) fetch_tile(a.tiles, nli + 2, &s_tile[(nli + 2 - list_begin) % 3]);
+        }
+        if (NB == 1 && rnd == 0 && !first) __syncthreads();   // the single Delta buffer is free again
+        first = false;
+        // Several rounds per chunk: the successor's loads go out part by part as
+        // this round is staged.  One round per chunk: after the barrier, all at
+        // once (measured faster for 32 x 64 on C3 / C4 / C5).
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            stage_part(tc, chunk, rnd, p, buf);
+            if (NR > 1 && more) load_part(tl, nchunk, nrnd, p);
+        }
+        if (more && nrnd != 0) {           // the chunk has more rounds
+            rnd = nrnd;
+            continue;
+        }
+        fetch_wait<1>();                   // (descriptors go two tiles ahead: the latest may fly on)
+        __syncthreads();
+        if (NR == 1 && more) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) load_part(tl, nchunk, nrnd, p);
         }
         const int node = tc.node;
 
@@ -355,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ef_sketch(const SketchLaunch a)
         if (nli != li) tc = tl;
         li = nli;
         chunk = nchunk;
+        rnd = 0;
         buf ^= NB - 1;
     }
 }
