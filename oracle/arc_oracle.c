@@ -6,29 +6,36 @@
  * The product path (paper_2510_26709_b200/) never imports, links or calls it,
  * and this file includes nothing from the product (no shared headers, tables
  * or helpers).  Its only shared source is the text of the paper plus the
- * readings written down in DESIGN.md §3 ("Readings").
+ * readings written down in DESIGN.md §3 ("Readings"), which take SURVEY.md
+ * §8(c)'s ARC-NUM v1 / ARC-RNG v1 wherever the paper is silent.
  *
  * What it computes (PAPER.md = /root/reference/PAPER.md, "P:n" = line n):
  *   EF21M, eq:ef21m-1..3, with the compressor C_local / C realised
  *   by ARC-Top-K, Algorithm 1 alg:ar_topk:
  *     reshape g -> G (m x n)                 z72habsd00111, Alg.1 l.2
  *     V in R^{n x r}, vec(V) ~ N(0, I)       P:229-230,     Alg.1 l.3
- *     P_i = (1/sqrt r) G_i V                 P:231-233,     Alg.1 l.4
- *     P   = (1/N) sum_i P_i    (All-Reduce)  P:232,         Alg.1 l.5
- *     Sigma = diag(P P^T), I = argtop_K      zn28373 P:236-237, Alg.1 l.6
+ *     P'_i = G_i V                           P:231-233,     Alg.1 l.4
+ *     S    = sum_i P'_i        (All-Reduce)  P:232,         Alg.1 l.5
+ *     Sigma = diag(S S^T), I = argtop_K      zn28373 P:236-237, Alg.1 l.6
  *     C_local(G_i) = [G_i]_{I,:}             2zn20 P:241-243, Alg.1 l.7
  *     C = (1/N) sum_i C_local (All-Reduce)   P:242, Alg.1 l.8
+ *   The factors 1/sqrt(r) and 1/N of P scale every row's Sigma by the
+ *   same 1/(r N^2), which leaves argtop_K unchanged in exact arithmetic, so
+ *   the selection is computed unscaled [R2, R3].
  *
  * Precision.  The selection I is an argtop (an integer decided by floating
  * point), and h, g feed the next step's Sigma, so every value on that chain is
- * computed in IEEE binary32 — the kernel's precision — with each operation
- * rounded once (no FMA contraction: built with -ffp-contract=off), in the
- * plain left-to-right order in which the formulas are written.  The places
- * where the paper is silent (summation order, tie-break, generator, NaN) follow
- * DESIGN.md §3; each is cited below as "[Rn]".
+ * computed in IEEE binary32 — the kernel's precision — each + and * rounded
+ * once (built with -ffp-contract=off) and fused multiply-adds only where
+ * ARC-NUM v1 writes fmaf: the momentum (O2), the sketch dot products (O6) and
+ * Sigma (O8).  The sketch's order over q is ARC-NUM v1's O6 (1024-column
+ * chunks, 32 lanes, a butterfly, chunks left to right — o6_dot below,
+ * simulated lane by lane); every other sum runs left to right in the order it
+ * is written.  The places where the paper is silent (summation order,
+ * tie-break, generator, NaN) follow DESIGN.md §3; each is cited as "[Rn]".
  *
- * The plain definitions are written out with plain loops; nothing is blocked,
- * fused or reordered.  It is deliberately slow.
+ * The definitions are written out with plain loops; nothing is blocked, fused
+ * or reordered beyond what ARC-NUM v1 fixes.  It is deliberately slow.
  */
 #include <math.h>
 #include <stdint.h>
@@ -237,71 +244,97 @@ static int64_t row_len(int64_t len, int64_t n, int64_t p)
 }
 
 /*
+ * ARC-NUM v1 O6 [R9]: the dot product sum_{q < nv} x[q] * y[q * ys] in the
+ * canonical order.  Row chunk c holds columns [1024 c, 1024 c + 1024); in it,
+ * lane l (0..31) starts from a_l = +0 and, for s = 0..7 then e = 0..3, with
+ * q = 1024 c + 128 s + 4 l + e < nv, sets a_l <- fma(x[q], y[q ys], a_l).  A
+ * butterfly (o = 16, 8, 4, 2, 1: every lane a_l <- a_l + a_{l xor o}, all
+ * lanes from the previous values) leaves the chunk value w_c = a_0, and the
+ * result is (((w_0 + w_1) + w_2) + ...), left to right.  The 32 lanes are
+ * simulated literally.
+ */
+static float o6_dot(const float* x, const float* y, int64_t ys, int64_t nv)
+{
+    float P = 0.0f;
+    for (int64_t c = 0; c * 1024 < nv; c++) {
+        float a[32], b[32];
+        for (int l = 0; l < 32; l++) {
+            a[l] = 0.0f;
+            for (int s = 0; s < 8; s++)
+                for (int e = 0; e < 4; e++) {
+                    int64_t q = 1024 * c + 128 * s + 4 * l + e;
+                    if (q < nv) a[l] = fmaf(x[q], y[q * ys], a[l]);
+                }
+        }
+        for (int o = 16; o >= 1; o >>= 1) {
+            for (int l = 0; l < 32; l++) b[l] = a[l] + a[l ^ o];
+            memcpy(a, b, sizeof a);
+        }
+        P = (c == 0) ? a[0] : P + a[0];
+    }
+    return P;
+}
+
+/*
  * orc_arc_round — Algorithm 1 on N node-local m x n matrices.
  *   G[i]      : node i's block as flat floats (len of them), read-only
  *   V         : n x r projection (row-major)
  *   exact     : 0 = Gaussian sketch (the paper); 1 = test mode, Sigma_p =
- *               || (1/N) sum_i G_i[p,:] ||^2 exactly (the quantity the sketch
- *               estimates, z72ena P:254-261)
+ *               O6 sum of fma(S_q, S_q, .) with S_q = sum_i G_i[p][q] in node
+ *               order: || sum_i G_i[p,:] ||^2, the quantity the sketch
+ *               estimates up to the factor N^2 (z72ena P:254-261)
  * Outputs (each optional except sel):
- *   P_nodes [N][m][r] : P_i = (1/sqrt r) G_i V
- *   P_avg   [m][r]    : P   = (1/N) sum_i P_i
- *   sigma   [m]       : Sigma = diag(P P^T)
+ *   P_nodes [N][m][r] : P'_i = G_i V, each entry an O6 dot product
+ *   S_out   [m][r]    : S = ((P'_0 + P'_1) + ...) + P'_{N-1}, node order [R9]
+ *   sigma   [m]       : Sigma_p: s = +0; s <- fma(S_pj, S_pj, s), j = 0..r-1 (O8)
  *   sel     [K]       : I, ascending
  *   C_local [N][K][n] : [G_i]_{I,:}, compact rows in I order, +0 in padding
- *   C_glob  [K][n]    : (1/N) sum_i C_local_i
+ *   C_glob  [K][n]    : (1/N) sum_i C_local_i = A / N, A summed in node order
  */
 void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int32_t r,
                    const float* const* G, const float* V, int32_t exact,
-                   float* P_nodes, float* P_avg, float* sigma, int32_t* sel,
+                   float* P_nodes, float* S_out, float* sigma, int32_t* sel,
                    float* C_local, float* C_glob)
 {
     float* Pn = (float*)malloc((size_t)N * (size_t)m * (size_t)r * sizeof(float));
-    float* Pa = (float*)malloc((size_t)m * (size_t)r * sizeof(float));
+    float* Sa = (float*)malloc((size_t)m * (size_t)r * sizeof(float));
     float* Sg = (float*)calloc((size_t)m, sizeof(float));
-    const float inv_sqrt_r = 1.0f / sqrtf((float)r);       /* [R2] */
     const float Nf = (float)N;
 
     if (!exact) {
-        /* Alg.1 l.4: P_i = (1/sqrt r) G_i V; each entry a plain left-to-right
-         * sum over q [R9]. */
-        for (int32_t i = 0; i < N; i++) {
+        /* Alg.1 l.4: P'_i = G_i V, entry (p, j) the O6 dot product of row p
+         * with column j of V [R2, R9]. */
+        for (int32_t i = 0; i < N; i++)
             for (int64_t p = 0; p < m; p++) {
                 int64_t nv = row_len(len, n, p);
-                for (int32_t j = 0; j < r; j++) {
-                    float acc = 0.0f;
-                    for (int64_t q = 0; q < nv; q++)
-                        acc = acc + G[i][p * n + q] * V[q * r + j];
-                    Pn[((size_t)i * m + p) * r + j] = inv_sqrt_r * acc;
-                }
+                for (int32_t j = 0; j < r; j++)
+                    Pn[((size_t)i * m + p) * r + j] = o6_dot(G[i] + p * n, V + j, r, nv);
             }
-        }
-        /* Alg.1 l.5: P = (1/N) sum_i P_i, the node sum in ascending node id [R9]. */
-        for (int64_t p = 0; p < m; p++) {
+        /* Alg.1 l.5: S = sum_i P'_i, the node sum in ascending node id [R9]. */
+        for (int64_t p = 0; p < m; p++)
             for (int32_t j = 0; j < r; j++) {
                 float s = Pn[(size_t)p * r + j];
                 for (int32_t i = 1; i < N; i++) s = s + Pn[((size_t)i * m + p) * r + j];
-                Pa[(size_t)p * r + j] = s / Nf;
+                Sa[(size_t)p * r + j] = s;
             }
-        }
-        /* Alg.1 l.6: Sigma = diag(P P^T): Sigma_p = sum_j P_pj^2 [R9]. */
+        /* Alg.1 l.6: Sigma = diag(S S^T) (O8) [R3]. */
         for (int64_t p = 0; p < m; p++) {
             float s = 0.0f;
-            for (int32_t j = 0; j < r; j++) s = s + Pa[(size_t)p * r + j] * Pa[(size_t)p * r + j];
+            for (int32_t j = 0; j < r; j++) s = fmaf(Sa[(size_t)p * r + j], Sa[(size_t)p * r + j], s);
             Sg[p] = s;
         }
     } else {
+        float* row = (float*)malloc((size_t)(n > 0 ? n : 1) * sizeof(float));
         for (int64_t p = 0; p < m; p++) {
             int64_t nv = row_len(len, n, p);
-            float s = 0.0f;
             for (int64_t q = 0; q < nv; q++) {
                 float a = G[0][p * n + q];
                 for (int32_t i = 1; i < N; i++) a = a + G[i][p * n + q];
-                float u = a / Nf;
-                s = s + u * u;
+                row[q] = a;
             }
-            Sg[p] = s;
+            Sg[p] = o6_dot(row, row, 1, nv);
         }
+        free(row);
     }
     /* Alg.1 l.6: I = argtop_K(Sigma) */
     orc_argtop_k(Sg, m, K, sel);
@@ -322,9 +355,9 @@ void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int3
     }
 
     if (P_nodes && !exact) memcpy(P_nodes, Pn, (size_t)N * m * r * sizeof(float));
-    if (P_avg && !exact) memcpy(P_avg, Pa, (size_t)m * r * sizeof(float));
+    if (S_out && !exact) memcpy(S_out, Sa, (size_t)m * r * sizeof(float));
     if (sigma) memcpy(sigma, Sg, (size_t)m * sizeof(float));
-    free(Pn); free(Pa); free(Sg);
+    free(Pn); free(Sa); free(Sg);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -375,10 +408,11 @@ int orc_step(const orc_cfg* cfg, int64_t t,
     const float eta = cfg->eta;
     const float one_minus_eta = 1.0f - eta;
 
-    /* eq:ef21m-1: h_t = (1 - eta) h_{t-1} + eta grad */
+    /* eq:ef21m-1: h_t = (1 - eta) h_{t-1} + eta grad, as
+     * fma(eta, grad, (1 - eta) h) (ARC-NUM v1 O1, O2) [R11] */
     for (int32_t i = 0; i < N; i++)
         for (int64_t e = 0; e < cfg->d; e++)
-            h[i][e] = one_minus_eta * h[i][e] + eta * grad[i][e];
+            h[i][e] = fmaf(eta, grad[i][e], one_minus_eta * h[i][e]);
 
     int64_t sel_pos = 0, val_pos = 0, V_pos = 0, sig_pos = 0;
     for (int32_t b = 0; b < cfg->num_blocks; b++) {
@@ -486,7 +520,7 @@ int orc_step_topk(const orc_cfg* cfg, int64_t t,
     const float one_minus_eta = 1.0f - eta;
     for (int32_t i = 0; i < N; i++)
         for (int64_t e = 0; e < cfg->d; e++)
-            h[i][e] = one_minus_eta * h[i][e] + eta * grad[i][e];
+            h[i][e] = fmaf(eta, grad[i][e], one_minus_eta * h[i][e]);   /* [R11] */
 
     int64_t sumK = 0, sumKn = 0;
     for (int32_t b = 0; b < cfg->num_blocks; b++) { sumK += cfg->blocks[b].K; sumKn += cfg->blocks[b].K * cfg->blocks[b].n; }
@@ -499,17 +533,18 @@ int orc_step_topk(const orc_cfg* cfg, int64_t t,
         float* Cl = (float*)malloc((size_t)N * K * n * sizeof(float));
         float* norms = (float*)malloc((size_t)m * sizeof(float));
         for (int32_t i = 0; i < N; i++) {
-            /* node-local row norms of Delta_i = h - g */
+            /* node-local row norms ||Delta_i[p,:]||^2, Delta_i = h - g, in the
+             * O6 order (the exact sketch of one node) */
+            float* row = (float*)malloc((size_t)n * sizeof(float));
             for (int64_t p = 0; p < m; p++) {
                 int64_t nv = row_len(len, n, p);
-                float s = 0.0f;
                 for (int64_t q = 0; q < nv; q++) {
                     int64_t e = B->offset + p * n + q;
-                    float dlt = h[i][e] - g[i][e];
-                    s = s + dlt * dlt;
+                    row[q] = h[i][e] - g[i][e];
                 }
-                norms[p] = s;
+                norms[p] = o6_dot(row, row, 1, nv);
             }
+            free(row);
             if (B->kind == 0) orc_argtop_k(norms, m, K, sel + (size_t)i * K);
             else for (int64_t k = 0; k < K; k++) sel[(size_t)i * K + k] = (int32_t)k;
             for (int64_t k = 0; k < K; k++) {
@@ -541,6 +576,25 @@ int orc_step_topk(const orc_cfg* cfg, int64_t t,
         free(sel); free(Cl); free(norms);
     }
     return 0;
+}
+
+/* eq:ef21m-1 on one vector: h <- fma(eta, grad, (1 - eta) h) [R11] (used by
+ * the multi-process protocol tests). */
+void orc_momentum(float* h, const float* grad, int64_t d, float eta)
+{
+    const float one_minus_eta = 1.0f - eta;
+    for (int64_t e = 0; e < d; e++) h[e] = fmaf(eta, grad[e], one_minus_eta * h[e]);
+}
+
+/* O8 on given node sums: sigma[p] = s, s = +0; s <- fma(S[p][j], S[p][j], s)
+ * for j = 0..r-1 (used by the multi-process protocol tests on row slices). */
+void orc_sigma_rows(const float* S, int64_t rows, int32_t r, float* sigma)
+{
+    for (int64_t p = 0; p < rows; p++) {
+        float s = 0.0f;
+        for (int32_t j = 0; j < r; j++) s = fmaf(S[p * r + j], S[p * r + j], s);
+        sigma[p] = s;
+    }
 }
 
 /* Array forms of the generator's scalar functions (used by the exhaustive

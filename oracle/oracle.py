@@ -18,7 +18,8 @@ _SRC = os.path.join(_HERE, "arc_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "libarc_oracle.so")
 
 # Plain IEEE binary32: every operation rounded once, no contraction into FMA,
-# no fast-math.  (The only FMAs are the explicit fmaf() calls of the generator.)
+# no fast-math.  (The only FMAs are the explicit fmaf() calls ARC-NUM v1 and
+# ARC-RNG v1 prescribe: the momentum, the O6 sketch order, Sigma, ln/sincos.)
 CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
           "-fexcess-precision=standard", "-Wall"]
 
@@ -57,6 +58,8 @@ def lib():
                                     ctypes.c_int32] + [ctypes.c_void_p] * 6
         L.orc_randk_keys.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p]
         L.orc_ln_array.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.orc_sigma_rows.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
+        L.orc_momentum.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_float]
         L.orc_sincos2pi_array.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_step.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 8
         L.orc_step.restype = ctypes.c_int
@@ -149,6 +152,22 @@ def randk_keys(seed: int, t: int, b: int, m: int) -> np.ndarray:
     return k
 
 
+def momentum(h, grad, eta: float) -> np.ndarray:
+    """eq:ef21m-1 on one vector (returns the new h; the input is not modified)."""
+    out = np.array(h, dtype=np.float32, copy=True)
+    g = np.ascontiguousarray(grad, dtype=np.float32)
+    lib().orc_momentum(_ptr(out), _ptr(g), out.size, float(eta))
+    return out
+
+
+def sigma_rows(S) -> np.ndarray:
+    """O8: Sigma of each row of the node sums S [rows, r] (fma chain over j)."""
+    S = np.ascontiguousarray(S, dtype=np.float32)
+    out = np.zeros(S.shape[0], np.float32)
+    lib().orc_sigma_rows(_ptr(S), S.shape[0], S.shape[1], _ptr(out))
+    return out
+
+
 def sigma_key(s: float) -> int:
     return int(lib().orc_sigma_key(float(s)))
 
@@ -167,8 +186,10 @@ def _ptr_array(arrs):
 def arc_round(G_nodes, n: int, K: int, V=None, r: int | None = None, exact: bool = False, m: int | None = None):
     """Algorithm 1 on N local flat blocks (each ``len`` floats viewed as m x n).
 
-    Returns dict with P_nodes [N,m,r], P_avg [m,r], sigma [m], sel [K],
-    C_local [N,K,n], C [K,n]."""
+    Returns dict with P_nodes [N,m,r] (P'_i = G_i V, unscaled), S [m,r] (their
+    node-order sum), sigma [m] (diag(S S^T)), sel [K], C_local [N,K,n], C [K,n].
+    The paper's reported P = (1/N)(1/sqrt r) S and its Sigma = sigma / (r N^2)
+    differ from these by selection-invariant factors (reading R2/R3)."""
     G = [_f32(x).ravel() for x in G_nodes]
     N = len(G)
     length = G[0].size
@@ -179,12 +200,12 @@ def arc_round(G_nodes, n: int, K: int, V=None, r: int | None = None, exact: bool
         V = np.zeros((n, r or 1), dtype=np.float32)
     V = _f32(V)
     r = V.shape[1]
-    out = dict(P_nodes=np.zeros((N, m, r), np.float32), P_avg=np.zeros((m, r), np.float32),
+    out = dict(P_nodes=np.zeros((N, m, r), np.float32), S=np.zeros((m, r), np.float32),
                sigma=np.zeros(m, np.float32), sel=np.zeros(K, np.int32),
                C_local=np.zeros((N, K, n), np.float32), C=np.zeros((K, n), np.float32))
     Gp = _ptr_array(G)
     lib().orc_arc_round(N, length, m, n, K, r, ctypes.cast(Gp, ctypes.c_void_p), _ptr(V), int(bool(exact)),
-                        _ptr(out["P_nodes"]), _ptr(out["P_avg"]), _ptr(out["sigma"]), _ptr(out["sel"]),
+                        _ptr(out["P_nodes"]), _ptr(out["S"]), _ptr(out["sigma"]), _ptr(out["sel"]),
                         _ptr(out["C_local"]), _ptr(out["C"]))
     return out
 
@@ -247,4 +268,5 @@ class OracleEF21M:
 
 
 __all__ = ["Block", "OracleEF21M", "arc_round", "argtop_k", "build", "gaussian_V", "ln", "ln_array", "lib",
-           "philox4x32_10", "randk_keys", "sigma_key", "sincos2pi", "sincos2pi_array", "uniform"]
+           "momentum", "philox4x32_10", "randk_keys", "sigma_key", "sigma_rows", "sincos2pi", "sincos2pi_array",
+           "uniform"]

@@ -78,7 +78,6 @@ def _worker_protocol(rank, world, port, L, reduce, steps, q):
     g = [np.zeros(d, np.float32) for _ in nodes]
     gbar = np.zeros(d, np.float32)
     ref = oracle.OracleEF21M(d, blocks, N=N, eta=eta, r=r, seed=seed)
-    one_m_eta = np.float32(1) - np.float32(eta)
     Nf = np.float32(N)
     out = []
     for t in range(steps):
@@ -87,9 +86,9 @@ def _worker_protocol(rank, world, port, L, reduce, steps, q):
         V = oracle.gaussian_V(seed, t, 0, n, r)
         Pi, D = [], []
         for l, i in enumerate(nodes):
-            h[l] = (one_m_eta * h[l] + np.float32(eta) * all_grads[i]).astype(np.float32)
+            h[l] = oracle.momentum(h[l], all_grads[i], eta)
             D.append((h[l] - g[l]).astype(np.float32))
-            Pi.append(oracle.arc_round([D[-1]], n=n, K=K, V=V)["P_nodes"][0])      # (1/sqrt r) Delta_i V
+            Pi.append(oracle.arc_round([D[-1]], n=n, K=K, V=V)["P_nodes"][0])      # P'_i = Delta_i V
         # exchange #1: rank j owns rows [j Ms, (j+1) Ms); an
         # all-to-all (send/recv) brings it those rows' per-node sketches from every
         # rank, it sums them in global node order and forms its Sigma slice, and an
@@ -108,10 +107,8 @@ def _worker_protocol(rank, world, port, L, reduce, steps, q):
         for q_ in reqs:
             q_.wait()
         per_node = [recv[gr].numpy()[:, l, :] for gr in range(world) for l in range(L)]   # global node order
-        P = (_f32_seq_sum(per_node) / Nf).astype(np.float32)
-        sig_slice = np.zeros(Ms, np.float32)
-        for j in range(r):
-            sig_slice = (sig_slice + P[:, j] * P[:, j]).astype(np.float32)
+        S = _f32_seq_sum(per_node)
+        sig_slice = oracle.sigma_rows(S)                                             # O8 on the slice
         got = [torch.empty(Ms) for _ in range(world)]
         dist.all_gather(got, torch.from_numpy(sig_slice))
         sig = np.concatenate([x.numpy() for x in got])[:m]
@@ -156,7 +153,18 @@ def _spawn(fn, world, *args):
     procs = [ctx.Process(target=fn, args=(r, world, port, *args, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=300) for _ in procs]
+    import queue
+    import time
+    res, t0 = [], time.time()
+    while len(res) < len(procs):
+        try:
+            res.append(q.get(timeout=1))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead or time.time() - t0 > 300:
+                for p in procs:
+                    p.kill()
+                raise AssertionError(f"worker failed (exit codes {[p.exitcode for p in procs]})")
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

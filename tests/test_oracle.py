@@ -113,13 +113,15 @@ def test_row_major_reshape(orc):
 
 
 def test_sketch_spec_examples(orc):
-    """S:130-132, P_i = (1/sqrt r) G_i V."""
+    """S:130-132, P_i = (1/sqrt r) G_i V.  The oracle keeps P'_i = G_i V
+    (reading R2); the reported P = P' * fl(1/sqrt r) * (1/N) matches S's values."""
     out = orc.arc_round([np.array([[1, 0], [0, 1]], np.float32)], n=2, K=1,
                         V=np.array([[2], [0]], np.float32))
-    assert out["P_nodes"][0].tolist() == [[2.0], [0.0]]
+    assert out["P_nodes"][0].tolist() == [[2.0], [0.0]]            # r = 1: P = P'
     out = orc.arc_round([np.array([[1, 1]], np.float32)], n=2, K=1,
                         V=np.array([[1, 1], [1, -1]], np.float32))
-    P = out["P_avg"].astype(np.float64)
+    assert out["S"].tolist() == [[2.0, 0.0]]
+    P = (out["S"] * (np.float32(1) / np.sqrt(np.float32(2)))).astype(np.float64)
     assert abs(P[0, 0] - 2 / math.sqrt(2)) <= 2 * np.spacing(np.float32(1.41421356))
     assert P[0, 1] == 0.0
     out = orc.arc_round([np.zeros((3, 2), np.float32)], n=2, K=1, V=np.ones((2, 4), np.float32))
@@ -129,7 +131,8 @@ def test_sketch_spec_examples(orc):
 @pytest.mark.parametrize("N,m,n,r", [(1, 40, 300, 4), (3, 33, 129, 3), (4, 17, 1, 4), (2, 9, 1000, 1)])
 def test_sketch_within_rounding_bound_of_exact_product(orc, N, m, n, r):
     """The fp32 sketch agrees with the binary64 matrix product (numpy) within the
-    classical bound |fl(sum) - sum| <= gamma_k sum |terms|, gamma_k = k u / (1 - k u).
+    classical bound |fl(sum) - sum| <= gamma_k sum |terms|, gamma_k = k u / (1 - k u),
+    k = n + 5 covering any O6 order (lane chain, butterfly, chunk sum).
     A dropped term, a wrong index or a transposed operand breaks it by orders of magnitude."""
     rng = np.random.default_rng(11 * m + n)
     G = [(rng.standard_normal((m, n)) * np.exp(rng.standard_normal((m, 1)))).astype(np.float32) for _ in range(N)]
@@ -137,18 +140,46 @@ def test_sketch_within_rounding_bound_of_exact_product(orc, N, m, n, r):
     out = orc.arc_round(G, n=n, K=max(1, m // 4), V=V)
     u = 2.0 ** -24
     gam = lambda k: k * u / (1 - k * u)
-    c = np.float32(1.0) / np.sqrt(np.float32(r))
     G64 = [x.astype(np.float64) for x in G]
     V64 = V.astype(np.float64)
     for i in range(N):
-        exact = float(c) * (G64[i] @ V64)
-        bound = gam(n + 1) * float(c) * (np.abs(G64[i]) @ np.abs(V64)) + 1e-300
+        exact = G64[i] @ V64
+        bound = gam(n + 5) * (np.abs(G64[i]) @ np.abs(V64)) + 1e-300
         assert np.all(np.abs(out["P_nodes"][i] - exact) <= bound)
-    Pavg = sum(out["P_nodes"].astype(np.float64)) / N
-    absP = sum(np.abs(out["P_nodes"].astype(np.float64))) / N
-    assert np.all(np.abs(out["P_avg"] - Pavg) <= gam(N + 1) * absP + 1e-300)
-    sig = (out["P_avg"].astype(np.float64) ** 2).sum(1)
+    S = sum(out["P_nodes"].astype(np.float64))
+    absS = sum(np.abs(out["P_nodes"].astype(np.float64)))
+    assert np.all(np.abs(out["S"] - S) <= gam(N + 1) * absS + 1e-300)
+    sig = (out["S"].astype(np.float64) ** 2).sum(1)
     assert np.all(np.abs(out["sigma"] - sig) <= gam(r + 2) * sig + 1e-300)
+
+
+def test_o6_order_is_the_lane_chunk_order(orc):
+    """ARC-NUM v1 O6 pinned on a row where the order shows.  n = 1100
+    (two chunks), V = 1.  Terms 2^25 at q = 0 (lane 0), 2 at q = 4 (lane 1) and 2 at
+    q = 12 (lane 3): the butterfly pairs lanes 1 and 3 at o = 2 (2 + 2 = 4), then lane 0
+    with lane 1 at o = 1: 2^25 + 4, exact.  A left-to-right sum rounds 2^25 + 2 to even
+    twice and gives 2^25.  A term in chunk 1 is added after chunk 0's butterfly."""
+    n = 1100
+    x = np.zeros(n, np.float32)
+    x[0], x[4], x[12] = 2.0 ** 25, 2.0, 2.0
+    V = np.ones((n, 1), np.float32)
+    assert orc.arc_round([x], n=n, K=1, V=V)["P_nodes"][0][0, 0] == np.float32(2.0 ** 25 + 4)
+    lr = np.float32(0)
+    for q in range(n):
+        lr = np.float32(lr + x[q])
+    assert lr == np.float32(2.0 ** 25)                     # the plain order differs
+    x[1024] = -(2.0 ** 25)
+    assert orc.arc_round([x], n=n, K=1, V=V)["P_nodes"][0][0, 0] == np.float32(4.0)
+    # the lane chain is a fused multiply-add: the product (1 + 2^-12)(1 - 2^-12 + 2^-24) 2^-24
+    # = 2^-24 (1 + 2^-36) rounds to 2^-24 on its own, and 1 + 2^-24 is a tie (-> 1.0);
+    # fma rounds 1 + 2^-24 (1 + 2^-36) once, above the tie (-> 1 + 2^-23)
+    y = np.zeros(8, np.float32)
+    y[0], y[1] = 1.0, 1.0 + 2.0 ** -12
+    W = np.ones((8, 1), np.float32)
+    W[1, 0] = (1.0 - 2.0 ** -12 + 2.0 ** -24) * 2.0 ** -24
+    assert np.float32(np.float32(y[1] * W[1, 0]) + np.float32(1.0)) == np.float32(1.0)
+    got = orc.arc_round([y], n=8, K=1, V=W)["P_nodes"][0][0, 0]
+    assert got == np.float32(1.0 + 2.0 ** -23)
 
 
 # ---------------------------------------------------------------- selection (R5, R15)
@@ -156,7 +187,7 @@ def test_sketch_within_rounding_bound_of_exact_product(orc, N, m, n, r):
 def test_selection_spec_examples(orc):
     """S:139-141 / zn28373 (P:236-237)."""
     out = orc.arc_round([np.array([[1, 2], [0, 3]], np.float32)], n=2, K=1, V=np.eye(2, dtype=np.float32))
-    # with V = I (r=2), P = G/sqrt(2): Sigma = [5, 9]/2 -> I = {1}
+    # with V = I (r = 2): S = G, Sigma = [5, 9] (the paper's P = G/sqrt 2 halves both) -> I = {1}
     assert out["sel"].tolist() == [1]
     assert orc.argtop_k(np.array([5, 9], np.float32), 1).tolist() == [1]
     assert orc.argtop_k(np.array([1, 1], np.float32), 1).tolist() == [0]      # tie -> smaller index
@@ -216,7 +247,8 @@ def _monte_carlo_sigma(orc, G, r, seeds, N=1):
     out = []
     for s in range(seeds):
         V = orc.gaussian_V(1000 + s, 0, 0, n, r)
-        out.append(orc.arc_round([G] * N, n=n, K=1, V=V)["sigma"].astype(np.float64))
+        # reported Sigma = sigma / (r N^2) (reading R2/R3: selection-invariant factors)
+        out.append(orc.arc_round([G] * N, n=n, K=1, V=V)["sigma"].astype(np.float64) / (r * N * N))
     return np.array(out)
 
 

@@ -273,6 +273,10 @@ int main() {
     }
     const int n = 768, ntiles = (int)(d / n / 32);
     const double BT = 4.0 * (double)ntiles * 32 * n * 4;
+    for (int grid : {148 * 4, 148 * 5, 148 * 6, 148 * 8}) {
+        float t0 = timeit([&] { k_tiled<32, 64, 1><<<grid, 256>>>(gr, g, h, n, ntiles, 0.9f, 0.1f); });
+        printf("tiled 32x64 depth1 grid %d (%d/SM): %6.0f GB/s\n", grid, grid / 148, BT / (t0 * 1e-3) / 1e9);
+    }
     for (int grid : {296, 592}) {
         float t1 = timeit([&] { k_tiled<32, 64, 1><<<grid, 256>>>(gr, g, h, n, ntiles, 0.9f, 0.1f); });
         float t2 = timeit([&] { k_tiled<32, 64, 2><<<grid, 256>>>(gr, g, h, n, ntiles, 0.9f, 0.1f); });
