@@ -145,10 +145,12 @@ arc_status arc_topk_step_host(arc_topk_ctx* ctx, int64_t t,
 
 /* Debug read-back of the last step's intermediates (device dst, async). */
 typedef enum {
-    ARC_Q_V = 0,        /* float [sum_ARC n_b * r]       V_b row-major, blocks in order        */
-    ARC_Q_SIGMA = 1,    /* float [sum_ARC m_b]           Sigma per ARC block row               */
+    ARC_Q_V = 0,        /* float [sum_ARC n_b * r]       V_b transposed, [r][n_b] (column j of
+                           V_b contiguous, the layout the sketch reads), blocks in order      */
+    ARC_Q_SIGMA = 1,    /* float [sum_ARC m_b]           Sigma per ARC block row (unscaled, R2) */
     ARC_Q_SEL = 2,      /* int32 [sum_b K_b]             I_b                                   */
-    ARC_Q_P_NODES = 3,  /* float [sum_ARC m_b][nodes_local][r]  P_i (needs DEBUG_SKETCH, or G>1) */
+    ARC_Q_P_NODES = 3,  /* float [sum_ARC m_b][nodes_local][r]  P'_i = G_i V, unscaled (needs
+                           DEBUG_SKETCH, or G > 1, or nodes_local > 1)                         */
     ARC_Q_CANDIDATES = 4 /* uint32 [num_blocks] rows sharing the boundary bin of the last selection */
 } arc_query;
 arc_status arc_topk_query(arc_topk_ctx* ctx, int32_t what, void* dst, size_t bytes, void* stream);

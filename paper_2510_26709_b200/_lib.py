@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libarctopk.so")
+# ARC_LIB_PATH: an alternative build of the same library (A/B timing experiments)
+LIB_PATH = os.environ.get("ARC_LIB_PATH") or os.path.join(_PKG, "libarctopk.so")
 
 ABI_VERSION = 1
 MAX_NODES_LOCAL = 16

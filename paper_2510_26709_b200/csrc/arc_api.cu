@@ -358,8 +358,8 @@ struct arc_topk_ctx {
     Nccl nccl;
     ncclComm_t comm = nullptr;
     unsigned char* ws = nullptr;
-    int grid = 0, num_tiles = 0, shape = 0;
-    float ome = 0.f, c_r = 0.f, Nf = 0.f;
+    int grid = 0, num_tiles = 0, shape = 0, vs_cap = 0;
+    float ome = 0.f, Nf = 0.f;
     cudaStream_t last = nullptr;
     // per-phase timing
     bool timing = false;
@@ -474,23 +474,25 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     // static tables
     std::vector<Tile> tiles;
     std::vector<int> cta_begin;
-    {   // tile shape of the streaming pass: wide chunks for long aligned rows
-        bool all_vec = true;
-        int min_n = INT32_MAX;
-        for (const BlockDev& B : c->pl.bdev)
-            if (B.kind == ARC_BLOCK_ARC) { all_vec = all_vec && B.vec; min_n = std::min(min_n, B.n); }
-        (void)all_vec;
-        // 32 x 256 in 8-row rounds (1 KB row segments) measured best for rows of
-        // >= 1024 (C5, the LLaMA layout), 32 x 64 for shorter rows (C2, C3 tie)
-        //
-        c->shape = min_n >= 1024 && sketch_shape_ok(3, c->p.r) ? 3 : min_n >= 64 ? 1 : 0;
+    {   // streaming-pass variant: 0 = 4 row segments per batch (>= 3 CTAs/SM),
+        // 1 = 2 segments per batch at 4 CTAs/SM (ARC_SKETCH_SHAPE, experiments)
+        c->shape = 0;
         if (const char* e = getenv("ARC_SKETCH_SHAPE")) {
             const int v = atoi(e);
-            if (v >= 0 && v <= 4) c->shape = v;
+            if (sketch_shape_ok(v, c->p.r)) c->shape = v;
         }
-        if (!sketch_shape_ok(c->shape, c->p.r)) c->shape = 1;
     }
-    plan_tiles(c->pl, ef_sketch_resident_ctas(c->p.r, c->shape), sketch_tile_rows(c->shape),
+    {
+        int max_n = 0;
+        for (const BlockDev& B : c->pl.bdev)
+            if (B.kind == ARC_BLOCK_ARC) max_n = std::max(max_n, B.n);
+        c->vs_cap = sketch_vs_cap(c->p.r, max_n);
+        // blocks whose V does not fit read it from global memory; stage the largest that fits
+        if (c->vs_cap == 0)
+            for (const BlockDev& B : c->pl.bdev)
+                if (B.kind == ARC_BLOCK_ARC) c->vs_cap = std::max(c->vs_cap, sketch_vs_cap(c->p.r, B.n));
+    }
+    plan_tiles(c->pl, ef_sketch_resident_ctas(c->p.r, c->shape, c->vs_cap), sketch_tile_rows(c->shape),
                sketch_tile_cols(c->shape), tiles, cta_begin, c->grid);
     c->num_tiles = static_cast<int>(tiles.size());
     std::vector<TileDesc> tdesc(tiles.size());
@@ -544,7 +546,6 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     if (const char* e = getenv("ARC_PDL")) c->pdl = e[0] != '0';
     if (const char* e = getenv("ARC_EARLY")) c->early = e[0] != '0';
     c->ome = 1.0f - c->p.eta;                       // R11, fp32
-    c->c_r = 1.0f / sqrtf(static_cast<float>(c->p.r));   // R2: fl(1 / sqrt_rn(r))
     c->Nf = static_cast<float>(c->p.N);             // R3
 
     if (G > 1) {   // every rank checks that all ranks passed identical params
@@ -630,7 +631,6 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.r = c->p.r;
         a.eta = c->p.eta;
         a.ome = c->ome;
-        a.c_r = c->c_r;
         a.Nf = c->Nf;
         a.V = V_t;
         a.sigma = sigma;
@@ -643,6 +643,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.M = pl.M;
         a.num_blocks = c->p.num_blocks;
         a.shape = c->shape;
+        a.vs_cap = c->vs_cap;
         a.pdl = c->pdl && !c->timing ? 1 : 0;
         a.status = status;
         ARC_MARK(1);

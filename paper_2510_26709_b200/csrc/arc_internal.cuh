@@ -126,7 +126,7 @@ struct SketchLaunch {
     int grid;
     NodePtrs nodes;
     int nodes_local, N, r;
-    float eta, ome, c_r, Nf;
+    float eta, ome, Nf;
     const float* V;
     float* sigma;      // mode 0: written
     unsigned* hist1;   // [num_blocks][kHist1Bins] digit-1 histogram of Sigma (mode 0)
@@ -138,12 +138,14 @@ struct SketchLaunch {
     uint2 key;         // Rand-K: Philox key (seed)
     unsigned t_lo, t_hi;             // ARC rows (stride of the per-node sigma in mode 2)
     int num_blocks;
-    int shape;         // tile shape R x W: 0 = 64 x 32, 1 = 32 x 64, 2 = 16 x 128, 3 = 32 x 256, 4 = 32 x 128
+    int shape;         // variant (arc_sketch.cu)
+    int vs_cap;        // floats of dynamic shared memory for V_b^T (0: V from global memory)
     int pdl;           // launch with programmatic stream serialization (overlap the launch)
     unsigned* status;
 };
 void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s);
-int ef_sketch_resident_ctas(int r, int shape);   // SMs x occupancy
+int ef_sketch_resident_ctas(int r, int shape, int vs_cap);   // SMs x occupancy
+int sketch_vs_cap(int r, int max_n);   // floats of V_b^T the streaming pass stages in shared memory
 int sketch_tile_rows(int shape);
 int sketch_tile_cols(int shape);
 int sketch_shape_ok(int shape, int r);

@@ -31,7 +31,8 @@ using namespace dev;
 using namespace rng;
 
 // V_b[q][j]: one thread per (q, jj) of block b = blockIdx.y; counter
-// (q*R4 + jj, b, lo32 t, hi32 t), key (lo32 seed, hi32 seed).
+// (q*R4 + jj, b, lo32 t, hi32 t), key (lo32 seed, hi32 seed).  V_b is stored
+// transposed ([r][n_b], column j contiguous: the streaming pass reads it so).
 __global__ void __launch_bounds__(256) k_vgen(const BlockDev* __restrict__ blocks, int r, uint2 key,
                                               unsigned t_lo, unsigned t_hi, float* __restrict__ V) {
     const int b = blockIdx.y;
@@ -48,10 +49,10 @@ __global__ void __launch_bounds__(256) k_vgen(const BlockDev* __restrict__ block
         box_muller(x.z, x.w, z[2], z[3]);
         const long long q = it / R4;
         const int j0 = 4 * static_cast<int>(it - q * R4);
-        float* dst = V + v_off + q * r + j0;
+        float* dst = V + v_off + q;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (j0 + k < r) dst[k] = z[k];
+            if (j0 + k < r) dst[static_cast<long long>(j0 + k) * n] = z[k];
     }
 }
 
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
                 float hn[4], gn[4], c4[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    hn[k] = fadd(fmul(a.ome, h4[k]), fmul(a.eta, r4[k]));   // R11
+                    hn[k] = ffma(a.eta, r4[k], fmul(a.ome, h4[k]));   // O2, R11
                     c4[k] = fsub(hn[k], g4[k]);                              // R4
                     gn[k] = fadd(g4[k], c4[k]);                              // R12
                     A[k] = (i == 0) ? c4[k] : fadd(A[k], c4[k]);             // R9 node order
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
             const long long e = B.off + q;
             float A = 0.0f;
             for (int i = 0; i < a.nodes_local; ++i) {
-                const float hn = fadd(fmul(a.ome, a.nodes.h[i][e]), fmul(a.eta, a.nodes.grad[i][e]));
+                const float hn = ffma(a.eta, a.nodes.grad[i][e], fmul(a.ome, a.nodes.h[i][e]));   // O2, R11
                 a.nodes.h[i][e] = hn;
                 const float gv = a.nodes.g[i][e];
                 const float c = fsub(hn, gv);
@@ -267,9 +268,9 @@ __global__ void __launch_bounds__(256) k_sigma_slice(const SigmaLaunch a) {
                 if (g == 0 && l == 0) S = v;
                 else { S.x = fadd(S.x, v.x); S.y = fadd(S.y, v.y); S.z = fadd(S.z, v.z); S.w = fadd(S.w, v.w); }
             }
-        const float P[4] = {__fdiv_rn(S.x, a.Nf), __fdiv_rn(S.y, a.Nf), __fdiv_rn(S.z, a.Nf), __fdiv_rn(S.w, a.Nf)};   // R3
+        const float P[4] = {S.x, S.y, S.z, S.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sig = fadd(sig, fmul(P[j], P[j]));                       // zn28373
+        for (int j = 0; j < 4; ++j) sig = ffma(P[j], P[j], sig);                             // O8, zn28373
     } else {
         for (int j = 0; j < r; ++j) {
             float S = 0.0f;
@@ -278,8 +279,7 @@ __global__ void __launch_bounds__(256) k_sigma_slice(const SigmaLaunch a) {
                     const float v = __ldcs(a.x + ((g * a.Ms + p) * L + l) * r + j);
                     S = (g == 0 && l == 0) ? v : fadd(S, v);
                 }
-            const float P = __fdiv_rn(S, a.Nf);
-            sig = fadd(sig, fmul(P, P));
+            sig = ffma(S, S, sig);                                                             // O8
         }
     }
     a.sigma[p] = sig;

@@ -131,10 +131,11 @@ static __device__ __forceinline__ void gen_V_item(const BlockDev* __restrict__ b
     box_muller(x.z, x.w, z[2], z[3]);
     const long long q = local / R4;
     const int j0 = 4 * static_cast<int>(local - q * R4);
-    float* dst = V + blocks[b].v_off + q * r + j0;
+    const int n = blocks[b].n;
+    float* dst = V + blocks[b].v_off + q;   // V_b stored transposed: column j at j * n
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-        if (j0 + k < r) dst[k] = z[k];
+        if (j0 + k < r) dst[static_cast<long long>(j0 + k) * n] = z[k];
 }
 
 }  // namespace rng

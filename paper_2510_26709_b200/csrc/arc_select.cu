@@ -204,7 +204,7 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                         const Quad hv = load_quad(ph + e[u], v4[u], cnt[u]);
                         const Quad gr = load_quad(a.nodes.grad[i] + e[u], v4[u], cnt[u]);
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) hq[u].v[kk] = fadd(fmul(a.ome, hv.v[kk]), fmul(a.eta, gr.v[kk]));
+                        for (int kk = 0; kk < 4; ++kk) hq[u].v[kk] = ffma(a.eta, gr.v[kk], fmul(a.ome, hv.v[kk]));   // O2
                         store_quad(ph + e[u], hq[u], v4[u], cnt[u]);
                     } else {
                         hq[u] = load_quad(ph + e[u], v4[u], cnt[u]);
@@ -433,8 +433,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
                 auto sigma_of = [&](int i, const float* S) {
                     float sig = 0.0f;
                     for (int j = 0; j < s.r; ++j) {
-                        const float pv = __fdiv_rn(S[j], s.Nf);                // R3
-                        sig = fadd(sig, fmul(pv, pv));                         // zn28373
+                        sig = ffma(S[j], S[j], sig);                           // O8, zn28373
                     }
                     s.sigma_w[B.row_base + lo + i] = sig;
                     if (!isfinite(sig)) atomicOr(s.status, kStatusNonfinite);

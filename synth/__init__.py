@@ -86,6 +86,9 @@ CONFIGS = {
     "C5_1e6": dict(d=1_000_000, n=1024, mu_bp=100, N=1),
     "C5_1e8": dict(d=100_000_000, n=1024, mu_bp=100, N=1),
     "C5_1e9": dict(d=1_000_000_000, n=1024, mu_bp=100, N=1),
+    # probes (not BASELINE configs): one flat block with the LLaMA row lengths
+    "P_n2048": dict(d=2048 * 48_828, n=2048, mu_bp=10, N=1),
+    "P_n5461": dict(d=5461 * 18_311, n=5461, mu_bp=10, N=1),
 }
 
 

@@ -238,6 +238,110 @@ __global__ void __launch_bounds__(256) k_cpa(const float* __restrict__ gr, const
     }
 }
 
+// warp-per-row streaming (the O6 lane mapping): each warp walks rows of n floats,
+// UN segments of 128 columns per batch (lane l: columns 128 s + 4 l .. +3);
+// SYNC: the CTA's 8 warps meet at a barrier after every batch (lockstep rows)
+template <int UN, bool SYNC>
+__global__ void __launch_bounds__(256) k_warprow(const float* __restrict__ gr, const float* __restrict__ g, float* h,
+                                                int n, long long m, float a, float b, float* sink) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long rows_per_cta = (m + gridDim.x - 1) / gridDim.x;
+    const long long r0 = blockIdx.x * rows_per_cta, r1 = min(m, r0 + rows_per_cta);
+    const int nseg = n / 128;
+    float acc = 0.f;
+    for (long long base_row = r0; base_row < r1; base_row += 8) {
+        const long long row = base_row + warp;
+        const bool live = row < r1;
+        for (int k0 = 0; k0 < nseg; k0 += UN) {
+            float4 x[UN], y[UN], z[UN];
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                const long long e = row * n + 128 * (k0 + u) + 4 * lane;
+                if (live && k0 + u < nseg) {
+                    x[u] = __ldcs(reinterpret_cast<const float4*>(gr + e));
+                    y[u] = __ldcs(reinterpret_cast<const float4*>(g + e));
+                    z[u] = __ldcs(reinterpret_cast<const float4*>(h + e));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                const long long e = row * n + 128 * (k0 + u) + 4 * lane;
+                if (live && k0 + u < nseg) {
+                    const float4 o = make_float4(a * z[u].x + b * x[u].x, a * z[u].y + b * x[u].y, a * z[u].z + b * x[u].z, a * z[u].w + b * x[u].w);
+                    __stcs(reinterpret_cast<float4*>(h + e), o);
+                    acc += (o.x - y[u].x) + (o.y - y[u].y);
+                }
+            }
+            if (SYNC) __syncthreads();
+        }
+    }
+    if (acc == 1234.5f) sink[0] = acc;
+}
+
+// warp-per-row streaming through a per-lane cp.async ring: every lane copies the
+// 16-byte pieces it will itself consume into its own shared-memory slots
+// (S stages of UN segments x 3 arrays), so only cp.async.wait_group orders them
+template <int UN, int S>
+__global__ void __launch_bounds__(256) k_warprow_cpa(const float* __restrict__ gr, const float* __restrict__ g, float* h,
+                                                    int n, long long m, float a, float b, float* sink) {
+    extern __shared__ __align__(16) float4 ring[];   // [8 warps][S][UN][3][32 lanes]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float4* my = ring + (size_t)warp * S * UN * 3 * 32;
+    const long long rows_per_cta = (m + gridDim.x - 1) / gridDim.x;
+    const long long r0 = blockIdx.x * rows_per_cta, r1 = min(m, r0 + rows_per_cta);
+    const int nseg = n / 128;
+    const int nb_row = (nseg + UN - 1) / UN;
+    // the warp's batches: rows r0 + warp, r0 + warp + 8, ...; batch index -> (row, k0)
+    long long nrows_w = (r1 - r0 - warp + 7) / 8;
+    if (r1 - r0 <= warp) nrows_w = 0;
+    const long long nbatch = nrows_w * nb_row;
+    auto issue = [&](long long bi) {
+        if (bi < nbatch) {
+            const long long row = r0 + warp + 8 * (bi / nb_row);
+            const int k0 = (int)(bi % nb_row) * UN;
+            float4* st = my + (size_t)(bi % S) * UN * 3 * 32;
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                if (k0 + u >= nseg) break;
+                const long long e = row * n + 128 * (k0 + u) + 4 * lane;
+                const unsigned d0 = (unsigned)__cvta_generic_to_shared(st + (u * 3 + 0) * 32 + lane);
+                const unsigned d1 = (unsigned)__cvta_generic_to_shared(st + (u * 3 + 1) * 32 + lane);
+                const unsigned d2 = (unsigned)__cvta_generic_to_shared(st + (u * 3 + 2) * 32 + lane);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d0), "l"(gr + e));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d1), "l"(g + e));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d2), "l"(h + e));
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int i = 0; i < S - 1; ++i) issue(i);
+    float acc = 0.f;
+    for (long long bi = 0; bi < nbatch; ++bi) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
+        const long long row = r0 + warp + 8 * (bi / nb_row);
+        const int k0 = (int)(bi % nb_row) * UN;
+        float4* st = my + (size_t)(bi % S) * UN * 3 * 32;
+        float4 x[UN], y[UN], z[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            x[u] = st[(u * 3 + 0) * 32 + lane];
+            y[u] = st[(u * 3 + 1) * 32 + lane];
+            z[u] = st[(u * 3 + 2) * 32 + lane];
+        }
+        issue(bi + S - 1);                 // refill the slot consumed one batch ago... (this one is read)
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            if (k0 + u >= nseg) break;
+            const long long e = row * n + 128 * (k0 + u) + 4 * lane;
+            const float4 o = make_float4(a * z[u].x + b * x[u].x, a * z[u].y + b * x[u].y, a * z[u].z + b * x[u].z, a * z[u].w + b * x[u].w);
+            __stcs(reinterpret_cast<float4*>(h + e), o);
+            acc += (o.x - y[u].x) + (o.y - y[u].y);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (acc == 1234.5f) sink[0] = acc;
+}
+
 int main() {
     const long long d = 124439808LL, n4 = d / 4;
     float *gr, *g, *h, *o;
@@ -315,6 +419,37 @@ int main() {
                run(k_cpa<32, 64, 4>, 4, 32, 64, n, ntiles), run(k_cpa<32, 64, 6>, 6, 32, 64, n, ntiles),
                run(k_cpa<16, 128, 3>, 3, 16, 128, n, ntiles * 2), run(k_cpa<16, 128, 4>, 4, 16, 128, n, ntiles * 2),
                run(k_cpa<8, 256, 4>, 4, 8, 256, n, ntiles * 4));
+    }
+    {
+        const long long m = d / n;
+        const double BW = 4.0 * (double)m * n * 4;
+        for (int grid : {148 * 4, 148 * 6, 148 * 8}) {
+            float t1 = timeit([&] { k_warprow<2, false><<<grid, 256>>>(gr, g, h, n, m, 0.9f, 0.1f, o); });
+            float t2 = timeit([&] { k_warprow<2, true><<<grid, 256>>>(gr, g, h, n, m, 0.9f, 0.1f, o); });
+            float t3 = timeit([&] { k_warprow<3, false><<<grid, 256>>>(gr, g, h, n, m, 0.9f, 0.1f, o); });
+            float t4 = timeit([&] { k_warprow<3, true><<<grid, 256>>>(gr, g, h, n, m, 0.9f, 0.1f, o); });
+            float t5 = timeit([&] { k_warprow<1, false><<<grid, 256>>>(gr, g, h, n, m, 0.9f, 0.1f, o); });
+            printf("warprow n=768 grid %d: UN2 %6.0f | UN2 sync %6.0f | UN3 %6.0f | UN3 sync %6.0f | UN1 %6.0f GB/s\n", grid,
+                   BW / (t1 * 1e-3) / 1e9, BW / (t2 * 1e-3) / 1e9, BW / (t3 * 1e-3) / 1e9, BW / (t4 * 1e-3) / 1e9,
+                   BW / (t5 * 1e-3) / 1e9);
+        }
+    }
+    {
+        const long long m = d / n;
+        const double BW = 4.0 * (double)m * n * 4;
+        auto run = [&](auto kern, int S, int UN, int grid) {
+            const int smem = 8 * S * UN * 3 * 32 * 16;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            float t = timeit([&] { kern<<<grid, 256, smem>>>(gr, g, h, n, m, 0.9f, 0.1f, o); });
+            return cudaGetLastError() == cudaSuccess ? BW / (t * 1e-3) / 1e9 : -1.0;
+        };
+        for (int per : {2, 3, 4}) {
+            const int grid = 148 * per;
+            printf("warprow cp.async grid %d: UN2 S3 %6.0f | UN2 S4 %6.0f | UN1 S6 %6.0f | UN3 S3 %6.0f | UN1 S8 %6.0f GB/s\n", grid,
+                   run(k_warprow_cpa<2, 3>, 3, 2, grid), run(k_warprow_cpa<2, 4>, 4, 2, grid),
+                   run(k_warprow_cpa<1, 6>, 6, 1, grid), run(k_warprow_cpa<3, 3>, 3, 3, grid),
+                   run(k_warprow_cpa<1, 8>, 8, 1, grid));
+        }
     }
     return 0;
 }
