@@ -131,9 +131,7 @@ __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int r
         if (lane == 0) {
             const float sig = P[0];
             a.sigma[static_cast<long long>(node) * a.M + row_base + p] = sig;
-            atomicAdd(&a.hist1[(static_cast<long long>(node) * a.num_blocks + b) * kHist1Bins +
-                               (order_key_dev(sig) >> kHist1Shift)],
-                      1u);
+            atomicAdd(&s_hist[order_key_dev(sig) >> kHist1Shift], 1u);   // slot (node, block)
             if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
         }
     } else {
@@ -180,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
     const float eta = a.eta, ome = a.ome;
     const int mode = a.mode;
     const bool sketch = mode <= 1;
-    const bool cta_hist = mode == 0 || mode == 3;
+    const bool cta_hist = true;                 // every mode histograms its keys in shared memory first
     auto flush_hist = [&](int b) {
         unsigned* gh = a.hist1 + static_cast<long long>(b) * kHist1Bins;
         for (int i = tid; i < kHist1Bins; i += kThreads) {
@@ -192,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         return li - list_begin < kTileCache ? &s_tile[li - list_begin] : a.tiles + li;
     };
 
-    int cur_b = -1;
+    int cur_b = -1;                             // histogram slot of the current tile: block (mode 2: node, block)
     bool v_smem = false;
     for (int li = list_begin; li < list_end; ++li) {
         const TileDesc* Tp = tile(li);
@@ -200,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         const int T_n = Tp->n, T_row0 = Tp->row0, T_rows = Tp->rows, T_row_base = Tp->row_base, T_b = Tp->b;
         const bool T_vec = Tp->vec != 0;
         const int node = Tp->node;
-        if (T_b != cur_b && (sketch || cta_hist)) {
+        const int hslot = mode == 2 ? node * a.num_blocks + T_b : T_b;
+        if (hslot != cur_b) {
             __syncthreads();
             if (cta_hist && cur_b >= 0) flush_hist(cur_b);
             const int nvf = r * T_n;
@@ -216,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
             }
             __syncthreads();
         }
-        cur_b = T_b;
+        cur_b = hslot;
         const float* __restrict__ pg = a.nodes.grad[node];
         float* __restrict__ ph = a.nodes.h[node];
         const float* __restrict__ pgg = a.nodes.g[node];
