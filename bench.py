@@ -198,7 +198,8 @@ def run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, str
     * nccl_allreduce_d (G > 1): a bare ncclAllReduce of d fp32 per GPU;
     * allgather_topk: vanilla EF21M with per-node row Top-K, whose
       exchange is an All-Gather of K values rows plus K indices per node;
-    * randk_shared_seed: Rand-K — the same path with data-independent rows."""
+    * randk_shared_seed: Rand-K (P:92) — the same path with data-independent rows;
+    * noef_msgd: Table II's "(without EF)" compressed momentum SGD on the same selection."""
     import torch
     import torch.distributed as dist
 
@@ -255,6 +256,14 @@ def run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, str
     out["randk_shared_seed"] = timed(lambda t: ctx.step(t, pool[t % pool_n], hs, gs, gb))
     out["randk_shared_seed"]["note"] = "Rand-K rows from a shared seed (Table I row Rand-K), same EF21M path, no sketch"
     ctx.close()
+    try:
+        ctx = ArcTopK(d, blocks, N=N, eta=0.9, r=4, seed=20251030, nodes_local=L, pg=pg, rank=rank, method="noef_msgd")
+        out["noef_msgd"] = timed(lambda t: ctx.step(t, pool[t % pool_n], None, None, gb))
+        out["noef_msgd"]["note"] = ("compressed momentum SGD without EF (Table II rows without EF): the ARC selection "
+                                    "on the gradients, u = 0.9 u + C; 12 B per element instead of 16")
+        ctx.close()
+    except Exception as e:
+        out["noef_msgd"] = {"unavailable": str(e)[:200]}
     return out
 
 

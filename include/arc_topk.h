@@ -76,7 +76,18 @@ typedef enum {
  * (R16): each block keeps K_b uniformly random rows, the same on every node
  * (row p's key is Philox(seed; p, b | 2^31, t) >> 2, the K_b largest keys win),
  * with the same EF21M update and index-free value All-Reduce as ARC-Top-K. */
-typedef enum { ARC_METHOD_ARC = 0, ARC_METHOD_TOPK_ALLGATHER = 1, ARC_METHOD_RANDK = 2 } arc_method;
+/* ARC_METHOD_NOEF_MSGD is Table II's "(without EF)" baseline (SPEC
+ * compressed_msgd_step): compressed momentum SGD with the shared ARC-Top-K
+ * selection applied to the gradients themselves, c_i = C_local(grad_i), and the
+ * replicated heavy-ball momentum u_t = beta u_{t-1} + (1/N) sum_i c_i kept in
+ * `gbar` (beta = params.eta, 0 <= beta < 1): u <- beta (x) u everywhere, then
+ * u[I] <- u[I] (+) A (/) N.  There is no (h, g) state: h and g may be NULL. */
+typedef enum {
+    ARC_METHOD_ARC = 0,
+    ARC_METHOD_TOPK_ALLGATHER = 1,
+    ARC_METHOD_RANDK = 2,
+    ARC_METHOD_NOEF_MSGD = 3
+} arc_method;
 
 /* flags */
 #define ARC_FLAG_HOST_STAGING   0x1u  /* reserve device staging for arc_topk_step_host          */
@@ -103,7 +114,7 @@ typedef struct {
     int32_t  r;             /* sketch width, 1..32 (paper: 4)                         */
     int32_t  num_blocks;    /* >= 1                                                   */
     const arc_block* blocks;/* host array, copied at create                           */
-    float    eta;           /* EF21M momentum, 0 < eta <= 1                           */
+    float    eta;           /* EF21M momentum, 0 < eta <= 1 (NOEF_MSGD: beta, [0, 1)) */
     int32_t  value_reduce;  /* arc_reduce_mode                                        */
     uint64_t seed;          /* shared base seed (R7), identical on every rank         */
     uint32_t flags;         /* ARC_FLAG_*                                             */

@@ -502,6 +502,72 @@ int orc_step(const orc_cfg* cfg, int64_t t,
 }
 
 /* ------------------------------------------------------------------------- */
+/* Baseline: compressed momentum SGD without error feedback (Table II rows     */
+/* "(without EF)"; SPEC compressed_msgd_step).  The shared          */
+/* ARC-Top-K selection is applied to the gradients themselves,                 */
+/* c_i = C_local(grad_i), and the replicated heavy-ball momentum is            */
+/*   u_t = beta u_{t-1} + (1/N) sum_i c_i,   beta = cfg->eta [R22]:            */
+/* u <- beta * u for every element, then u[I] <- u[I] + A / N.                 */
+/* ------------------------------------------------------------------------- */
+int orc_step_noef(const orc_cfg* cfg, int64_t t, const float* const* grad, float* u,
+                  int32_t* sel_out, float* values_out, float* V_out, float* sigma_out)
+{
+    const int32_t N = cfg->N;
+    const float beta = cfg->eta;
+    for (int64_t e = 0; e < cfg->d; e++) u[e] = beta * u[e];
+
+    int64_t sel_pos = 0, val_pos = 0, V_pos = 0, sig_pos = 0;
+    const float** G = (const float**)malloc((size_t)N * sizeof(float*));
+    for (int32_t b = 0; b < cfg->num_blocks; b++) {
+        const orc_block* B = &cfg->blocks[b];
+        const int64_t m = B->m, n = B->n, K = B->K, len = B->len;
+        for (int32_t i = 0; i < N; i++) G[i] = grad[i] + B->offset;
+        int32_t* sel = (int32_t*)malloc((size_t)K * sizeof(int32_t));
+        float* Cg = (float*)malloc((size_t)K * n * sizeof(float));
+        if (B->kind == 0) {
+            float* V = (float*)malloc((size_t)n * cfg->r * sizeof(float));
+            orc_gaussian_V(cfg->seed, t, b, n, cfg->r, V);
+            float* sg = (float*)malloc((size_t)m * sizeof(float));
+            orc_arc_round(N, len, m, n, K, cfg->r, G, V, 0, NULL, NULL, sg, sel, NULL, Cg);
+            if (V_out) memcpy(V_out + V_pos, V, (size_t)n * cfg->r * sizeof(float));
+            if (sigma_out) memcpy(sigma_out + sig_pos, sg, (size_t)m * sizeof(float));
+            V_pos += n * cfg->r;
+            sig_pos += m;
+            free(V); free(sg);
+        } else {
+            /* DENSE block: identity compressor, I = all rows [R20] */
+            for (int64_t k = 0; k < K; k++) {
+                sel[k] = (int32_t)k;
+                int64_t nv = row_len(len, n, k);
+                for (int64_t q = 0; q < n; q++) {
+                    float a = 0.0f;
+                    for (int32_t i = 0; i < N; i++) {
+                        float c = (q < nv) ? G[i][k * n + q] : 0.0f;
+                        a = (i == 0) ? c : a + c;
+                    }
+                    Cg[(size_t)k * n + q] = a / (float)N;
+                }
+            }
+        }
+        for (int64_t k = 0; k < K; k++) {
+            int64_t p = sel[k];
+            int64_t nv = row_len(len, n, p);
+            for (int64_t q = 0; q < nv; q++) {
+                int64_t e = B->offset + p * n + q;
+                u[e] = u[e] + Cg[(size_t)k * n + q];
+            }
+        }
+        if (sel_out) memcpy(sel_out + sel_pos, sel, (size_t)K * sizeof(int32_t));
+        if (values_out) memcpy(values_out + val_pos, Cg, (size_t)K * n * sizeof(float));
+        sel_pos += K;
+        val_pos += K * n;
+        free(sel); free(Cg);
+    }
+    free(G);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
 /* Baseline: vanilla EF21M with per-node row Top-K (Table I row "Top-K",      */
 /* P:91): node i keeps the K rows of its own residual   */
 /* with the largest ||row||^2 (ties -> smaller index), and the global update  */

@@ -65,6 +65,8 @@ def lib():
         L.orc_step.restype = ctypes.c_int
         L.orc_step_topk.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 6
         L.orc_step_topk.restype = ctypes.c_int
+        L.orc_step_noef.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 6
+        L.orc_step_noef.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -235,6 +237,8 @@ class OracleEF21M:
         self.sum_nr_arc = sum(b.n * self.r for b in self.blocks if b.kind == 0)
 
     def step(self, t: int, grads, debug: bool = False):
+        if self.method == "noef_msgd":
+            return self.step_noef(t, grads, debug)
         grads = [_f32(x).ravel() for x in grads]
         assert len(grads) == self.N and all(x.size == self.d for x in grads)
         sel = np.zeros(self.sum_K, np.int32)
@@ -247,6 +251,24 @@ class OracleEF21M:
                             ctypes.cast(_ptr_array(self.g), ctypes.c_void_p),
                             _ptr(self.gbar), _ptr(sel), _ptr(vals),
                             _ptr(V) if debug else None, _ptr(sig) if debug else None)
+        assert rc == 0
+        out = dict(sel=sel, values=vals)
+        if debug:
+            out.update(V=V, sigma=sig)
+        return out
+
+    def step_noef(self, t: int, grads, debug: bool = False):
+        """Compressed MSGD without EF (Table II "(without EF)"): gbar is the momentum
+        u, eta is beta; h and g are untouched."""
+        grads = [_f32(x).ravel() for x in grads]
+        assert len(grads) == self.N and all(x.size == self.d for x in grads)
+        sel = np.zeros(self.sum_K, np.int32)
+        vals = np.zeros(self.sum_Kn, np.float32)
+        V = np.zeros(self.sum_nr_arc, np.float32) if debug else None
+        sig = np.zeros(self.sum_m_arc, np.float32) if debug else None
+        rc = lib().orc_step_noef(ctypes.byref(self._cfg), int(t), ctypes.cast(_ptr_array(grads), ctypes.c_void_p),
+                                 _ptr(self.gbar), _ptr(sel), _ptr(vals),
+                                 _ptr(V) if debug else None, _ptr(sig) if debug else None)
         assert rc == 0
         out = dict(sel=sel, values=vals)
         if debug:

@@ -25,7 +25,7 @@ REDUCE_NCCL, REDUCE_ORDERED = 0, 1
 # flags
 FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE = 0x1, 0x2, 0x4
 # arc_method
-METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK = 0, 1, 2
+METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK, METHOD_NOEF_MSGD = 0, 1, 2, 3
 # arc_query
 Q_V, Q_SIGMA, Q_SEL, Q_P_NODES, Q_CANDIDATES = 0, 1, 2, 3, 4
 

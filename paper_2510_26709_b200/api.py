@@ -80,7 +80,9 @@ def _stream_handle(stream) -> int:
     return int(stream.cuda_stream)
 
 
-def _ptrs(ts) -> ctypes.Array:
+def _ptrs(ts) -> ctypes.Array | None:
+    if ts is None:      # (NOEF_MSGD: no h / g state)
+        return None
     return (ctypes.c_void_p * len(ts))(*[int(x.data_ptr()) for x in ts])
 
 
@@ -115,7 +117,7 @@ class ArcTopK:
                                   {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED}[reduce],
                                   int(seed) & (2**64 - 1), flags,
                                   {"arc": L.METHOD_ARC, "topk_allgather": L.METHOD_TOPK_ALLGATHER,
-                                   "randk": L.METHOD_RANDK}[method])
+                                   "randk": L.METHOD_RANDK, "noef_msgd": L.METHOD_NOEF_MSGD}[method])
         self.method = method
         nbytes = ctypes.c_size_t()
         L.check(self.lib.arc_topk_workspace_bytes(ctypes.byref(self.params), ctypes.byref(nbytes)),
@@ -148,7 +150,11 @@ class ArcTopK:
     # ------------------------------------------------------------------ step
     def _check_state(self, grads, h, g, gbar):
         nl = self.nodes_local
-        if not (len(grads) == len(h) == len(g) == nl):
+        if self.method == "noef_msgd" and h is None and g is None:   # no (h, g) state without EF
+            h = g = []
+            if len(grads) != nl:
+                raise ValueError(f"expected {nl} gradient tensors")
+        elif not (len(grads) == len(h) == len(g) == nl):
             raise ValueError(f"expected {nl} node tensors each")
         for x in list(h) + list(g) + [gbar]:
             if not (x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.numel() == self.d):
@@ -156,7 +162,8 @@ class ArcTopK:
 
     def step(self, t: int, grads, h, g, gbar, sel_out: torch.Tensor | None = None,
              values_out: torch.Tensor | None = None, stream=None) -> None:
-        """One EF21M + ARC-Top-K step: updates h, g, gbar in place (async)."""
+        """One EF21M + ARC-Top-K step: updates h, g, gbar in place (async).  For
+        method="noef_msgd" pass h = g = None; gbar is the momentum u."""
         self._check_state(grads, h, g, gbar)
         for x in grads:
             if not (x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.numel() == self.d):

@@ -75,6 +75,7 @@ struct Plan {
     std::vector<BlockDev> bdev;      // the caller's blocks
     bool topk = false;               // ARC_METHOD_TOPK_ALLGATHER baseline
     bool randk = false;              // ARC_METHOD_RANDK: data-independent shared selection
+    bool noef = false;               // ARC_METHOD_NOEF_MSGD: sketch the gradient, u = gbar (no h, g)
     int64_t W = 0;                   // Top-K: payload words per node (sum K n values + sum K indices)
     std::vector<BlockDev> sbdev;     // selection blocks: bdev, or (Top-K) one copy per local node
     std::vector<SelRow> segs;        // gather segments over sbdev
@@ -96,11 +97,14 @@ arc_status validate(const arc_topk_params* p) {
     const int G = p->N / p->nodes_local;
     if (p->rank < 0 || p->rank >= G) return ARC_ERR_INVALID_ARG;
     if (p->d < 1 || p->r < 1 || p->r > 32) return ARC_ERR_INVALID_ARG;
-    if (!(p->eta > 0.0f && p->eta <= 1.0f)) return ARC_ERR_INVALID_ARG;
+    // eta: the EF21M momentum, 0 < eta <= 1; without EF it is the heavy-ball beta, 0 <= beta < 1
+    if (p->method == ARC_METHOD_NOEF_MSGD ? !(p->eta >= 0.0f && p->eta < 1.0f) : !(p->eta > 0.0f && p->eta <= 1.0f))
+        return ARC_ERR_INVALID_ARG;
     if (p->value_reduce != ARC_REDUCE_NCCL && p->value_reduce != ARC_REDUCE_ORDERED) return ARC_ERR_INVALID_ARG;
     if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
     if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE)) return ARC_ERR_INVALID_ARG;
-    if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER && p->method != ARC_METHOD_RANDK)
+    if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER && p->method != ARC_METHOD_RANDK &&
+        p->method != ARC_METHOD_NOEF_MSGD)
         return ARC_ERR_INVALID_ARG;
     int64_t pos = 0, M = 0, sumK = 0;
     for (int b = 0; b < p->num_blocks; ++b) {
@@ -128,6 +132,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.G = p->N / p->nodes_local;
     pl.exchange = pl.G > 1 || (p->flags & ARC_FLAG_FORCE_EXCHANGE);
     pl.randk = p->method == ARC_METHOD_RANDK;
+    pl.noef = p->method == ARC_METHOD_NOEF_MSGD;
     pl.keep_pnodes = !pl.randk && (pl.exchange || pl.L > 1 || (p->flags & ARC_FLAG_DEBUG_SKETCH));
     pl.bdev.resize(p->num_blocks);
     int64_t M = 0, sumK = 0, sumKn = 0, sum_nr = 0;
@@ -243,7 +248,8 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         pl.o_wire_all = ordered ? take(sizeof(float) * sumKn * pl.L * pl.G) : 0;
     }
     if (p->flags & ARC_FLAG_HOST_STAGING) {
-        pl.o_staging = take(sizeof(float) * static_cast<size_t>(p->d) * pl.L);
+        // each node's staged gradient starts 256-byte aligned (the kernels' 16-byte loads)
+        pl.o_staging = take(sizeof(float) * static_cast<size_t>((p->d + 63) / 64 * 64) * pl.L);
         pl.o_vals = take(sizeof(float) * sumKn);
     }
     pl.total = off;
@@ -593,11 +599,14 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     const int L = pl.L;
     NodePtrs np{};
     for (int i = 0; i < L; ++i) {
-        if (grad[i] == nullptr || h[i] == nullptr || g[i] == nullptr) return ARC_ERR_INVALID_ARG;
+        if (grad[i] == nullptr) return ARC_ERR_INVALID_ARG;
         np.grad[i] = grad[i];
+        if (pl.noef) continue;   // without EF there is no (h, g) state: h, g may be NULL
+        if (h == nullptr || g == nullptr || h[i] == nullptr || g[i] == nullptr) return ARC_ERR_INVALID_ARG;
         np.h[i] = h[i];
         np.g[i] = g[i];
     }
+    if (gbar == nullptr) return ARC_ERR_INVALID_ARG;
     c->last = s;
     const BlockDev* blocks = c->at<BlockDev>(pl.o_blocks);
     float* V = c->at<float>(pl.o_V);
@@ -647,6 +656,8 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.pdl = c->pdl && !c->timing ? 1 : 0;
         a.status = status;
         ARC_MARK(1);
+        a.noef = pl.noef ? 1 : 0;
+        a.gbar = gbar;
         launch_ef_sketch(a, s);
         ARC_LAUNCHED();
     } else {
@@ -717,6 +728,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ga.Nf = c->Nf;
     ga.N_int = c->p.N;
     ga.sum_Kn = pl.sumKn;
+    ga.noef = pl.noef ? 1 : 0;
     const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
     float* wire = (pl.exchange || pl.topk) ? c->at<float>(pl.o_wire) : nullptr;
     ga.blocks = sblocks;
@@ -792,6 +804,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         dl.gbar = gbar;
         dl.sel = sel;
         dl.mode = !pl.exchange ? 0 : (ordered ? 2 : 1);
+        dl.noef = pl.noef ? 1 : 0;
         dl.values = !pl.exchange ? values_out : wire;
         dl.sum_Kn = pl.sumKn;
         launch_dense(dl, s);
@@ -881,13 +894,13 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
 
 arc_status arc_topk_step(arc_topk_ctx* c, int64_t t, const float* const* grad, float* const* h, float* const* g,
                          float* gbar, int32_t* sel_out, float* values_out, void* stream) {
-    if (c == nullptr || grad == nullptr || h == nullptr || g == nullptr || gbar == nullptr) return ARC_ERR_INVALID_ARG;
+    if (c == nullptr || grad == nullptr || gbar == nullptr) return ARC_ERR_INVALID_ARG;   // (h, g: checked per method)
     return run_step(c, t, grad, h, g, gbar, sel_out, values_out, static_cast<cudaStream_t>(stream));
 }
 
 arc_status arc_topk_step_host(arc_topk_ctx* c, int64_t t, const float* const* grad_host, float* const* h,
                               float* const* g, float* gbar, int32_t* sel_host, float* values_host, void* stream) {
-    if (c == nullptr || grad_host == nullptr || h == nullptr || g == nullptr || gbar == nullptr) return ARC_ERR_INVALID_ARG;
+    if (c == nullptr || grad_host == nullptr || gbar == nullptr) return ARC_ERR_INVALID_ARG;
     if (!(c->p.flags & ARC_FLAG_HOST_STAGING)) return ARC_ERR_INVALID_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int L = c->pl.L;
@@ -895,7 +908,7 @@ arc_status arc_topk_step_host(arc_topk_ctx* c, int64_t t, const float* const* gr
     float* stage = c->at<float>(c->pl.o_staging);
     for (int i = 0; i < L; ++i) {
         if (grad_host[i] == nullptr) return ARC_ERR_INVALID_ARG;
-        float* dst = stage + static_cast<size_t>(i) * c->p.d;
+        float* dst = stage + static_cast<size_t>(i) * ((c->p.d + 63) / 64 * 64);
         ARC_CUDA(cudaMemcpyAsync(dst, grad_host[i], sizeof(float) * c->p.d, cudaMemcpyHostToDevice, s));
         dgrad[i] = dst;
     }

@@ -140,6 +140,8 @@ struct SketchLaunch {
     int num_blocks;
     int shape;         // variant (arc_sketch.cu)
     int vs_cap;        // floats of dynamic shared memory for V_b^T (0: V from global memory)
+    int noef;          // compressed MSGD without EF: sketch the gradient, u = gbar <- eta u
+    float* gbar;       // (noef) the replicated momentum u
     int pdl;           // launch with programmatic stream serialization (overlap the launch)
     unsigned* status;
 };
@@ -172,6 +174,7 @@ struct GatherLaunch {
     int mode;           // 0 = fused local (G==1); 1 = wire pre-sum; 2 = wire per node [nodes_local][sumKn];
                         // 3 = Top-K baseline: node B.node only, wire values at B.val_base
     long long sum_Kn;
+    int noef;           // without EF: C_i = grad_i rows, no h / g (u = gbar, scaled by the sketch pass)
 };
 
 struct ScatterLaunch {
@@ -217,6 +220,7 @@ struct DenseLaunch {
     int32_t* sel;               // identity selection written here
     int mode;                   // 0 = fused local; 1 = payload = local node sum; 2 = payload per node
     long long sum_Kn;           // mode 2: per-node payload stride
+    int noef;                   // without EF: C_i = grad_i, u = gbar <- eta u (+ A / N in mode 0)
 };
 void launch_dense(const DenseLaunch& a, cudaStream_t s);
 

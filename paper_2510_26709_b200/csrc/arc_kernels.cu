@@ -164,8 +164,17 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
             const long long e = B.off + 4 * f;
             float A[4];
             for (int i = 0; i < a.nodes_local; ++i) {
-                const float4 hv = *reinterpret_cast<const float4*>(a.nodes.h[i] + e);
                 const float4 gr = __ldcs(reinterpret_cast<const float4*>(a.nodes.grad[i] + e));
+                if (a.noef) {   // without EF: C_i = grad_i (identity compressor), no h / g
+                    const float r4[4] = {gr.x, gr.y, gr.z, gr.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) A[k] = (i == 0) ? r4[k] : fadd(A[k], r4[k]);
+                    if (a.mode == 2)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) *out_at(4 * f + k, i) = r4[k];
+                    continue;
+                }
+                const float4 hv = *reinterpret_cast<const float4*>(a.nodes.h[i] + e);
                 const float4 gv = *reinterpret_cast<const float4*>(a.nodes.g[i] + e);
                 const float h4[4] = {hv.x, hv.y, hv.z, hv.w}, r4[4] = {gr.x, gr.y, gr.z, gr.w}, g4[4] = {gv.x, gv.y, gv.z, gv.w};
                 float hn[4], gn[4], c4[4];
@@ -182,6 +191,11 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) *out_at(4 * f + k, i) = c4[k];
             }
+            if (a.noef && a.mode != 0) {   // u <- eta u here; the scatter adds A / N
+                const float4 bv = *reinterpret_cast<const float4*>(a.gbar + e);
+                *reinterpret_cast<float4*>(a.gbar + e) =
+                    make_float4(fmul(a.eta, bv.x), fmul(a.eta, bv.y), fmul(a.eta, bv.z), fmul(a.eta, bv.w));
+            }
             if (a.mode == 1) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) *out_at(4 * f + k, 0) = A[k];
@@ -189,7 +203,10 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
             }
             if (a.mode == 2) continue;
             const float4 bv = *reinterpret_cast<const float4*>(a.gbar + e);
-            const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
+            float b4[4] = {bv.x, bv.y, bv.z, bv.w};
+            if (a.noef)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) b4[k] = fmul(a.eta, b4[k]);   // u <- eta u
             float v[4], bn[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -215,6 +232,20 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
             }
             const long long e = B.off + q;
             float A = 0.0f;
+            if (a.noef) {   // without EF: C_i = grad_i, u <- eta u (+ A / N in mode 0)
+                for (int i = 0; i < a.nodes_local; ++i) {
+                    const float c = a.nodes.grad[i][e];
+                    A = (i == 0) ? c : fadd(A, c);
+                    if (a.mode == 2) *out_at(q, i) = c;
+                }
+                const float us = fmul(a.eta, a.gbar[e]);
+                if (a.mode == 1) *out_at(q, 0) = A;
+                if (a.mode != 0) { a.gbar[e] = us; continue; }
+                const float v = pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf);
+                a.gbar[e] = fadd(us, v);
+                if (a.values != nullptr) a.values[B.val_base + q] = v;
+                continue;
+            }
             for (int i = 0; i < a.nodes_local; ++i) {
                 const float hn = ffma(a.eta, a.nodes.grad[i][e], fmul(a.ome, a.nodes.h[i][e]));   // O2, R11
                 a.nodes.h[i][e] = hn;

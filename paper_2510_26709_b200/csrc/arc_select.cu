@@ -192,14 +192,15 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
         // Top-K baseline (mode 3): a selection block belongs to one node (nd)
         const bool per_node = a.mode == 3;
         for (int i = 0; i < a.nodes_local; ++i) {
-            float* __restrict__ ph = a.nodes.h[i];
+            // (without EF the compressed rows are the gradient's: C_i = grad_i, no g)
+            float* __restrict__ ph = a.noef ? const_cast<float*>(a.nodes.grad[i]) : a.nodes.h[i];
             float* __restrict__ pg = a.nodes.g[i];
             Quad hq[UN], gq[UN];
 #pragma unroll
             for (int u = 0; u < UN; ++u) {
                 if (i == 0 && a.mode == 0 && cnt[u] > 0) gb[u] = load_quad(a.gbar + e[u], v4[u], cnt[u]);
                 if (cnt[u] > 0 && (!per_node || nd[u] == i)) {
-                    gq[u] = load_quad(pg + e[u], v4[u], cnt[u]);
+                    if (!a.noef) gq[u] = load_quad(pg + e[u], v4[u], cnt[u]);
                     if (dense[u]) {   // DENSE block: eq:ef21m-1 here (R11, R20)
                         const Quad hv = load_quad(ph + e[u], v4[u], cnt[u]);
                         const Quad gr = load_quad(a.nodes.grad[i] + e[u], v4[u], cnt[u]);
@@ -217,11 +218,11 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                 Quad c, gn;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    c.v[kk] = kk < cnt[u] ? fsub(hq[u].v[kk], gq[u].v[kk]) : 0.0f;   // C_i (+0 padding)
-                    gn.v[kk] = fadd(gq[u].v[kk], c.v[kk]);                             // R12
+                    c.v[kk] = kk < cnt[u] ? (a.noef ? hq[u].v[kk] : fsub(hq[u].v[kk], gq[u].v[kk])) : 0.0f;   // C_i (+0 padding)
+                    gn.v[kk] = a.noef ? 0.0f : fadd(gq[u].v[kk], c.v[kk]);                             // R12
                     A[u].v[kk] = (i == 0 || per_node) ? c.v[kk] : fadd(A[u].v[kk], c.v[kk]);   // R9 node order
                 }
-                if (cnt[u] > 0) store_quad(pg + e[u], gn, v4[u], cnt[u]);
+                if (cnt[u] > 0 && !a.noef) store_quad(pg + e[u], gn, v4[u], cnt[u]);
                 if (a.mode == 2)
                     store_quad(a.values + static_cast<long long>(i) * a.sum_Kn + o[u], c,
                                ov4[u] && (a.sum_Kn % 4 == 0), ocnt[u]);
@@ -277,14 +278,15 @@ __device__ void gather_rows_local(const GatherLaunch& a, const BlockDev& B, int 
         }
         Quad A[UN], gb[UN];
         for (int i = 0; i < a.nodes_local; ++i) {
-            float* __restrict__ ph = a.nodes.h[i];
+            // (without EF the compressed rows are the gradient's: C_i = grad_i, no g)
+            float* __restrict__ ph = a.noef ? const_cast<float*>(a.nodes.grad[i]) : a.nodes.h[i];
             float* __restrict__ pg = a.nodes.g[i];
             Quad hq[UN], gq[UN];
 #pragma unroll
             for (int u = 0; u < UN; ++u) {
                 if (nv[u] == 0) continue;
                 if (i == 0) gb[u] = load_quad(a.gbar + e[u], v4[u], nv[u]);
-                gq[u] = load_quad(pg + e[u], v4[u], nv[u]);
+                if (!a.noef) gq[u] = load_quad(pg + e[u], v4[u], nv[u]);
                 hq[u] = load_quad(ph + e[u], v4[u], nv[u]);
             }
 #pragma unroll
@@ -293,11 +295,11 @@ __device__ void gather_rows_local(const GatherLaunch& a, const BlockDev& B, int 
                 Quad gn;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    const float c = fsub(hq[u].v[kk], gq[u].v[kk]);               // C_i
-                    gn.v[kk] = fadd(gq[u].v[kk], c);                               // R12
+                    const float c = a.noef ? hq[u].v[kk] : fsub(hq[u].v[kk], gq[u].v[kk]);   // C_i
+                    gn.v[kk] = a.noef ? 0.0f : fadd(gq[u].v[kk], c);                       // R12
                     A[u].v[kk] = i == 0 ? c : fadd(A[u].v[kk], c);                 // R9 node order
                 }
-                store_quad(pg + e[u], gn, v4[u], nv[u]);
+                if (!a.noef) store_quad(pg + e[u], gn, v4[u], nv[u]);
             }
         }
 #pragma unroll

@@ -61,19 +61,31 @@ constexpr int kVsMax = 12288;              // floats of V_b^T staged at most (48
 // One segment (columns q..q+3 of lane l) of one row: momentum, residual, the
 // h' store and the lane's O6 fma chains; at the end of a 1024-column chunk the
 // butterfly folds the lane sums into P (left to right over chunks).
-template <int RJ>
+template <int RJ, bool NOEF>
 __device__ __forceinline__ void segment(const SketchLaunch& a, int k, int nseg, int q, int nv, long long base, bool vec,
                                         int n, const float* Vb, bool V_vec, bool v_smem, bool sketch, float* ph,
                                         const float (&gx)[4], const float (&hx)[4], const float (&dx)[4], float eta,
                                         float ome, int r, float (&acc)[RJ], float (&P)[RJ]) {
     const long long e = base + q;
     float hn[4], dl[4];
+    if (NOEF) {
+        // compressed MSGD without EF: the sketch sees the gradient itself; the
+        // replicated momentum u (kept in gbar) decays, u <- beta u (eta = beta),
+        // once per element (node-0 tiles, ph == gbar; others ph == nullptr)
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-        hn[kk] = ffma(eta, gx[kk], fmul(ome, hx[kk]));   // O2, R11
-        dl[kk] = fsub(hn[kk], dx[kk]);                   // O3, R4
+        for (int kk = 0; kk < 4; ++kk) {
+            hn[kk] = fmul(eta, hx[kk]);
+            dl[kk] = gx[kk];
+        }
+    } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            hn[kk] = ffma(eta, gx[kk], fmul(ome, hx[kk]));   // O2, R11
+            dl[kk] = fsub(hn[kk], dx[kk]);                   // O3, R4
+        }
     }
-    if (q + 3 < nv && vec) {
+    if (NOEF && ph == nullptr) {
+    } else if (q + 3 < nv && vec) {
         __stcs(reinterpret_cast<float4*>(ph + e), make_float4(hn[0], hn[1], hn[2], hn[3]));
     } else {
 #pragma unroll
@@ -157,7 +169,7 @@ __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int r
 // The register path: the same per-segment arithmetic with the batch loaded
 // straight into registers (UN segments, 3 UN float4 per lane), warps streaming
 // their rows independently; V_b^T staged in shared memory as above.
-template <int RJ, int UN, int MINB>
+template <int RJ, int UN, int MINB, bool NOEF>
 __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch a) {
     __shared__ TileDesc s_tile[kTileCache];
     __shared__ unsigned s_hist[kHist1Bins];     // digit-1 histogram of this CTA's Sigma (modes 0, 3)
@@ -217,8 +229,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         }
         cur_b = hslot;
         const float* __restrict__ pg = a.nodes.grad[node];
-        float* __restrict__ ph = a.nodes.h[node];
-        const float* __restrict__ pgg = a.nodes.g[node];
+        // (without EF: h is the replicated momentum u = gbar, read and scaled by node 0 only; no g)
+        float* __restrict__ ph = NOEF ? (node == 0 ? a.gbar : nullptr) : a.nodes.h[node];
+        const float* __restrict__ pgg = NOEF ? nullptr : a.nodes.g[node];
         const float* Vb = v_smem ? Vs : a.V + T_voff;
         const bool V_vec = T_vec && (v_smem || (T_voff & 3) == 0);
 
@@ -238,16 +251,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
                     const long long e = base + q;
                     if (q + 3 < nv && T_vec) {
                         xg[u] = __ldcs(reinterpret_cast<const float4*>(pg + e));
-                        xh[u] = __ldcs(reinterpret_cast<const float4*>(ph + e));
-                        xd[u] = __ldcs(reinterpret_cast<const float4*>(pgg + e));
+                        xh[u] = (!NOEF || ph != nullptr) ? __ldcs(reinterpret_cast<const float4*>(ph + e))
+                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                        xd[u] = !NOEF ? __ldcs(reinterpret_cast<const float4*>(pgg + e)) : make_float4(0.f, 0.f, 0.f, 0.f);
                     } else {
                         float tg[4] = {0.f, 0.f, 0.f, 0.f}, th[4] = {0.f, 0.f, 0.f, 0.f}, td[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             if (q + k < nv) {
                                 tg[k] = __ldcs(pg + e + k);
-                                th[k] = __ldcs(ph + e + k);
-                                td[k] = __ldcs(pgg + e + k);
+                                if (!NOEF || ph != nullptr) th[k] = __ldcs(ph + e + k);
+                                if (!NOEF) td[k] = __ldcs(pgg + e + k);
                             }
                         xg[u] = make_float4(tg[0], tg[1], tg[2], tg[3]);
                         xh[u] = make_float4(th[0], th[1], th[2], th[3]);
@@ -261,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
                     const float gx[4] = {xg[u].x, xg[u].y, xg[u].z, xg[u].w};
                     const float hx[4] = {xh[u].x, xh[u].y, xh[u].z, xh[u].w};
                     const float dx[4] = {xd[u].x, xd[u].y, xd[u].z, xd[u].w};
-                    segment<RJ>(a, k, nseg, 128 * k + 4 * lane, nv, base, T_vec, T_n, Vb, V_vec, v_smem, sketch, ph,
+                    segment<RJ, NOEF>(a, k, nseg, 128 * k + 4 * lane, nv, base, T_vec, T_n, Vb, V_vec, v_smem, sketch, ph,
                                 gx, hx, dx, eta, ome, r, acc, P);
                 }
             }
@@ -274,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
     }
 }
 
-template <int RJ, int UN, int MINB>
+template <int RJ, int UN, int MINB, bool NOEF = false>
 void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(a.grid);
@@ -283,7 +297,7 @@ void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     cfg.stream = s;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sizeof(float) * kVsMax));
         attr_set = true;
     }
@@ -292,14 +306,14 @@ void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, k_ef_sketch<RJ, UN, MINB>, a);
+    cudaLaunchKernelEx(&cfg, k_ef_sketch<RJ, UN, MINB, NOEF>, a);
 }
-template <int RJ, int UN, int MINB>
+template <int RJ, int UN, int MINB, bool NOEF = false>
 int occupancy_reg(int vs_cap) {
-    cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(float) * kVsMax));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB>, kThreads, sizeof(float) * vs_cap);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB, NOEF>, kThreads, sizeof(float) * vs_cap);
     return per_sm;
 }
 
@@ -307,6 +321,10 @@ int occupancy_reg(int vs_cap) {
 // 2 = 4 / 2, 3 = 1 / 5 (r <= 8; wider sketches get fewer CTAs)
 template <int RJ>
 void launch_rj(const SketchLaunch& a, cudaStream_t s) {
+    if (a.noef) {   // (the without-EF baseline: one variant)
+        launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2), true>(a, s);
+        return;
+    }
     switch (a.shape) {
         case 1: launch_reg<RJ, 2, (RJ <= 8 ? 4 : 2)>(a, s); break;
         case 2: launch_reg<RJ, 4, 2>(a, s); break;

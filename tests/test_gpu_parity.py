@@ -51,6 +51,7 @@ def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, 
                   debug_sketch=check_debug, force_exchange=force_exchange, host_staging=host, pg=pg,
                   method=method)
     o = orc.OracleEF21M(d, blocks, N=N, eta=eta, r=r, seed=seed, method=method)
+    noef = method == "noef_msgd"      # no (h, g) state: gbar is the momentum u
     h = [torch.zeros(d, device=DEV) for _ in range(N)]
     g = [torch.zeros(d, device=DEV) for _ in range(N)]
     gbar = torch.zeros(d, device=DEV)
@@ -61,13 +62,14 @@ def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, 
             gh = [torch.from_numpy(x).pin_memory() for x in gr]
             sel = torch.empty(ctx.sum_K, dtype=torch.int32).pin_memory()
             vals = torch.empty(ctx.sum_Kn, dtype=torch.float32).pin_memory()
-            ctx.step_host(t, gh, h, g, gbar, sel, vals)
+            ctx.step_host(t, gh, None if noef else h, None if noef else g, gbar, sel, vals)
         else:
             # values are requested on every other step: without them the select
             # kernel takes its early-gather path (mode 0), with them the segment path
             sel = torch.empty(ctx.sum_K, dtype=torch.int32, device=DEV)
             vals = torch.empty(ctx.sum_Kn, dtype=torch.float32, device=DEV) if t % 2 else None
-            ctx.step(t, [torch.from_numpy(x).to(DEV) for x in gr], h, g, gbar, sel, vals)
+            ctx.step(t, [torch.from_numpy(x).to(DEV) for x in gr], None if noef else h, None if noef else g, gbar,
+                     sel, vals)
         ref = o.step(t, gr, debug=check_debug)
         torch.cuda.synchronize()
         if check_debug and method == "arc":
@@ -338,6 +340,27 @@ def test_randk_multiblock_and_exchange(orc):
         off += m * n
     run_parity(orc, off, blocks, N=2, steps=3, method="randk")
     run_parity(orc, off, blocks, N=2, steps=3, method="randk", force_exchange=True, reduce="ordered")
+
+
+# ------------------------------------------------------------------ without EF (Table II)
+
+@pytest.mark.parametrize("N,d,n,K,beta", [(1, 50_000, 100, 7, 0.9), (4, 60_000, 96, 12, 0.9), (3, 4_097, 3, 40, 0.0)])
+def test_noef_msgd(orc, N, d, n, K, beta):
+    """Compressed momentum SGD without error feedback (Table II "(without EF)"):
+    the shared selection on the gradients, u = beta u + C; selection, values and u
+    bit-exact against the oracle."""
+    run_parity(orc, d, flat_blocks(d, n, K=K), N=N, steps=4, eta=beta, method="noef_msgd")
+
+
+def test_noef_msgd_multiblock_and_exchange(orc):
+    shapes = [(300, 64, 5, 0), (13, 100, 13, 1), (77, 33, 4, 0)]
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n, m, n, K, kind))
+        off += m * n
+    run_parity(orc, off, blocks, N=2, steps=3, eta=0.5, method="noef_msgd")
+    run_parity(orc, off, blocks, N=2, steps=3, eta=0.5, method="noef_msgd", force_exchange=True, reduce="ordered")
+    run_parity(orc, off, blocks, N=2, steps=3, eta=0.5, method="noef_msgd", host=True, check_debug=False)
 
 
 # ------------------------------------------------------------------ randomized sweep

@@ -587,3 +587,59 @@ def test_randk_values_are_node_average_of_rows(orc):
     rows = np.stack([x.reshape(-1, n) for x in gr])[:, res["sel"]].astype(np.float64)
     mean, mag = rows.mean(0), np.abs(rows).mean(0)
     assert np.all(np.abs(res["values"].reshape(K, n) - mean) <= N * 2 ** -24 * mag + 1e-30)
+
+
+# ---------------------------------------------------------------- without EF (Table II, SPEC compressed_msgd_step)
+
+def test_noef_identity_compressor_is_msgd(orc):
+    """K = m: the compressor is the identity, so the step is heavy-ball momentum SGD on
+    the node average (SPEC "K=m -> exact MSGD"): u_t = beta u_{t-1} + mean_i grad_i,
+    checked against a plain numpy recursion in binary64 within the rounding of a few
+    fp32 operations per step."""
+    rng = np.random.default_rng(8)
+    d, N, beta = 600, 3, 0.9
+    o = orc.OracleEF21M(d, flat_blocks(d, 20, K=30), N=N, eta=beta, r=4, seed=2, method="noef_msgd")
+    u = np.zeros(d)
+    for t in range(12):
+        gr = [rng.standard_normal(d).astype(np.float32) for _ in range(N)]
+        o.step(t, gr)
+        u = beta * u + sum(x.astype(np.float64) for x in gr) / N
+        assert np.all(np.abs(o.gbar - u) <= 1e-5 * (np.abs(u) + 1))
+        assert not any(x.any() for x in o.h) and not any(x.any() for x in o.g)   # no EF state
+
+
+def test_noef_beta0_identity_is_gradient_average(orc):
+    """beta = 0, K = m: plain (averaged) gradient descent direction (SPEC)."""
+    rng = np.random.default_rng(9)
+    d, N = 256, 4
+    o = orc.OracleEF21M(d, flat_blocks(d, 16, K=16), N=N, eta=0.0, r=4, seed=3, method="noef_msgd")
+    gr = [rng.integers(-8, 9, d).astype(np.float32) for _ in range(N)]   # exact sums
+    o.step(0, gr)
+    assert np.array_equal(o.gbar, (sum(x.astype(np.float64) for x in gr) / N).astype(np.float32))
+
+
+def test_noef_prop1_shared_selection_keeps_signal(orc):
+    """Prop. 1 inputs without EF: per-node Top-K would average to C(g) = 0,
+    the shared ARC selection (n = 1) keeps index 1: u = [0, 0.1] exactly (beta = 0)."""
+    g1 = np.array([-1.0, 0.1], np.float32)
+    g2 = np.array([1.0, 0.1], np.float32)
+    o = orc.OracleEF21M(2, flat_blocks(2, 1, K=1), N=2, eta=0.0, r=4, seed=1, method="noef_msgd")
+    o.step(0, [g1, g2])
+    assert o.gbar.tolist() == [0.0, np.float32(0.1)]
+
+
+def test_noef_rows_outside_selection_only_decay(orc):
+    """Rows outside I: u <- beta u exactly; rows in I: u <- beta u + values."""
+    rng = np.random.default_rng(10)
+    d, n, K, beta = 400, 10, 7, 0.75
+    o = orc.OracleEF21M(d, flat_blocks(d, n, K=K), N=2, eta=beta, r=4, seed=4, method="noef_msgd")
+    o.gbar[:] = rng.standard_normal(d).astype(np.float32)
+    before = o.gbar.copy()
+    out = o.step(0, [rng.standard_normal(d).astype(np.float32) for _ in range(2)])
+    scaled = (np.float32(beta) * before).astype(np.float32)
+    mask = np.zeros(d // n, bool)
+    mask[out["sel"]] = True
+    rows = o.gbar.reshape(-1, n)
+    assert np.array_equal(rows[~mask], scaled.reshape(-1, n)[~mask])
+    want = (scaled.reshape(-1, n)[mask] + out["values"].reshape(K, n)).astype(np.float32)
+    assert np.array_equal(rows[mask], want)
