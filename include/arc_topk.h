@@ -156,8 +156,10 @@ arc_status arc_topk_step_host(arc_topk_ctx* ctx, int64_t t,
 
 /* Debug read-back of the last step's intermediates (device dst, async). */
 typedef enum {
-    ARC_Q_V = 0,        /* float [sum_ARC n_b * r]       V_b transposed, [r][n_b] (column j of
-                           V_b contiguous, the layout the sketch reads), blocks in order      */
+    ARC_Q_V = 0,        /* float [sum_ARC ldv_b * r]     V_b transposed, [r][ldv_b] with
+                           ldv_b = round_up(n_b, 4) (column j of V_b contiguous and 16-byte
+                           aligned, the layout the sketch reads; padding undefined), blocks
+                           in order                                                        */
     ARC_Q_SIGMA = 1,    /* float [sum_ARC m_b]           Sigma per ARC block row (unscaled, R2) */
     ARC_Q_SEL = 2,      /* int32 [sum_b K_b]             I_b                                   */
     ARC_Q_P_NODES = 3,  /* float [sum_ARC m_b][nodes_local][r]  P'_i = G_i V, unscaled (needs

@@ -157,7 +157,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         D.pad_ = 0;
         if (B.kind == ARC_BLOCK_ARC) {
             M += B.m;
-            sum_nr += B.n * p->r;
+            sum_nr += (B.n + 3) / 4 * 4 * p->r;   // V_b^T rows padded to 16 bytes
             pl.max_nR4 = std::max<int64_t>(pl.max_nR4, B.n * R4);
             max_tiles += static_cast<int>((B.m + kMinTileRows - 1) / kMinTileRows) *
                          (p->method == ARC_METHOD_TOPK_ALLGATHER || p->nodes_local > 1 ? p->nodes_local : 1);
@@ -548,7 +548,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
 #undef UPLOAD
 
     for (const BlockDev& B : c->pl.bdev)
-        if (B.kind == ARC_BLOCK_ARC) c->v_items += static_cast<int64_t>(B.n) * ((c->p.r + 3) / 4);
+        if (B.kind == ARC_BLOCK_ARC) c->v_items += static_cast<int64_t>((B.n + 3) / 4 * 4) * ((c->p.r + 3) / 4);
     if (const char* e = getenv("ARC_PDL")) c->pdl = e[0] != '0';
     if (const char* e = getenv("ARC_EARLY")) c->early = e[0] != '0';
     c->ome = 1.0f - c->p.eta;                       // R11, fp32

@@ -50,9 +50,10 @@ __global__ void __launch_bounds__(256) k_vgen(const BlockDev* __restrict__ block
         const long long q = it / R4;
         const int j0 = 4 * static_cast<int>(it - q * R4);
         float* dst = V + v_off + q;
+        const int ldv = (n + 3) & ~3;   // rows of V_b^T padded to 16 bytes
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (j0 + k < r) dst[static_cast<long long>(j0 + k) * n] = z[k];
+            if (j0 + k < r) dst[static_cast<long long>(j0 + k) * ldv] = z[k];
     }
 }
 

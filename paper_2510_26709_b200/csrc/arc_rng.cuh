@@ -118,7 +118,7 @@ static __device__ __forceinline__ void gen_V_item(const BlockDev* __restrict__ b
     int lo = 0, hi = num_blocks - 1, b = -1;
     while (lo <= hi) {   // last ARC block whose first item is <= it
         const int mid = (lo + hi) >> 1;
-        const long long first = (blocks[mid].v_off / r) * R4;
+        const long long first = (blocks[mid].v_off / r) * R4;   // (v_off = sum of r * ldv)
         if (first <= it) { b = mid; lo = mid + 1; } else hi = mid - 1;
     }
     while (b >= 0 && blocks[b].kind != ARC_BLOCK_ARC) --b;   // DENSE blocks own no items
@@ -131,11 +131,11 @@ static __device__ __forceinline__ void gen_V_item(const BlockDev* __restrict__ b
     box_muller(x.z, x.w, z[2], z[3]);
     const long long q = local / R4;
     const int j0 = 4 * static_cast<int>(local - q * R4);
-    const int n = blocks[b].n;
-    float* dst = V + blocks[b].v_off + q;   // V_b stored transposed: column j at j * n
+    const int ldv = (blocks[b].n + 3) & ~3;
+    float* dst = V + blocks[b].v_off + q;   // V_b stored transposed: column j at j * ldv
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-        if (j0 + k < r) dst[static_cast<long long>(j0 + k) * n] = z[k];
+        if (j0 + k < r) dst[static_cast<long long>(j0 + k) * ldv] = z[k];
 }
 
 }  // namespace rng

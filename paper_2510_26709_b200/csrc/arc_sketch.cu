@@ -97,7 +97,7 @@ __device__ __forceinline__ void segment(const SketchLaunch& a, int k, int nseg, 
 #pragma unroll
         for (int j = 0; j < RJ; ++j) {
             if (j >= r) break;
-            const float* vj = Vb + static_cast<long long>(j) * n + q;
+            const float* vj = Vb + static_cast<long long>(j) * ((n + 3) & ~3) + q;   // V_b^T rows padded
             float v[4];
             if (q + 3 < nv && V_vec) {
                 const float4 t4 = v_smem ? *reinterpret_cast<const float4*>(vj) : __ldg(reinterpret_cast<const float4*>(vj));
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         if (hslot != cur_b) {
             __syncthreads();
             if (cta_hist && cur_b >= 0) flush_hist(cur_b);
-            const int nvf = r * T_n;
+            const int nvf = r * ((T_n + 3) & ~3);
             v_smem = sketch && nvf <= a.vs_cap;
             if (v_smem) {
                 const float* __restrict__ src = a.V + T_voff;
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         float* __restrict__ ph = NOEF ? (node == 0 ? a.gbar : nullptr) : a.nodes.h[node];
         const float* __restrict__ pgg = NOEF ? nullptr : a.nodes.g[node];
         const float* Vb = v_smem ? Vs : a.V + T_voff;
-        const bool V_vec = T_vec && (v_smem || (T_voff & 3) == 0);
+        const bool V_vec = true;   // V_b^T rows start 16-byte aligned (padded to ldv = round_up(n, 4))
 
         for (int rr = warp; rr < T_rows; rr += kWarps) {
             const int p = T_row0 + rr;
@@ -358,7 +358,7 @@ void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s) {
 }
 
 int sketch_vs_cap(int r, int max_n) {
-    const long long need = static_cast<long long>(r) * max_n;
+    const long long need = static_cast<long long>(r) * ((max_n + 3) / 4 * 4);   // padded V_b^T rows
     return static_cast<int>(need <= kVsMax ? need : 0) & ~3;   // 0: V read from global memory
 }
 
