@@ -89,6 +89,7 @@ CONFIGS = {
     # probes (not BASELINE configs): one flat block with the LLaMA row lengths
     "P_n2048": dict(d=2048 * 48_828, n=2048, mu_bp=10, N=1),
     "P_n5461": dict(d=5461 * 18_311, n=5461, mu_bp=10, N=1),
+    "P_n5460": dict(d=5460 * 18_315, n=5460, mu_bp=10, N=1),
 }
 
 
