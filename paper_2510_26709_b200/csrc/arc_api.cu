@@ -268,16 +268,24 @@ void plan_tiles(const Plan& pl, int resident, int tile_rows_max, int W, std::vec
     Cand best;
     resident = std::max(1, std::min(resident, kMaxGrid));
     const int nodes = pl.topk || pl.L > 1 ? pl.L : 1;
+    // Tile height: 8 rows (one per warp, the finest balance of the last round:
+    // -1 % on C3, -1.7 % on C5 d = 1e8, -6 % on C2 against 32 rows) when the
+    // layout has few blocks and the CTAs' tile lists stay in the kernel's shared
+    // descriptor cache; 32 rows otherwise (many blocks: fewer block changes per
+    // CTA, each restaging V; C4 +5 % and C5 d = 1e9 +0.4 % with 8-row tiles).
+    {
+        int arc_blocks = 0;
+        int64_t tiles8 = 0;
+        for (const BlockDev& B : pl.bdev)
+            if (B.kind == ARC_BLOCK_ARC) { ++arc_blocks; tiles8 += (B.m + 7) / 8 * nodes; }
+        if (arc_blocks <= 8 && tiles8 <= static_cast<int64_t>(resident) * 96) tile_rows_max = std::min(tile_rows_max, 8);
+    }
     const int64_t floor_rows = (tile_rows_max * 6 + 9) / 10;
-    // Full-height tiles are the cheapest per element (measured on C3: 32-row
-    // tiles 94 %, 30 rows 93 %, 24 rows 90 % of HBM peak; on C2 8-row tiles ran
-    // instruction-bound at 36 %), and a bandwidth-bound grid absorbs a ragged
-    // last round well, so the tile height is always the shape's.
     const int R_pick = tile_rows_max;
     int R_lo = R_pick, R_hi = R_pick;
     if (const char* e = getenv("ARC_TILE_ROWS")) {   // debug knob: one tile height
         const int v = atoi(e);
-        if (v >= 1 && v <= tile_rows_max) R_lo = R_hi = v;
+        if (v >= 1 && v <= 32) R_lo = R_hi = v;
     }
     for (int R = R_hi; R >= R_lo; --R) {
         std::vector<Tile> ts;

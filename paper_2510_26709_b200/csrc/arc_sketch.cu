@@ -20,7 +20,7 @@
 // friendly).  Delta stays in registers and meets V_b^T (stored transposed,
 // [r][n], staged in shared memory per block when it fits) in the lane's fma
 // chain.  UN segments are loaded per batch (3 UN float4 per lane in flight).
-// A CTA walks a host-balanced list of tiles (<= 32 rows of one block for one
+// A CTA walks a host-balanced list of tiles (8 or 32 rows of one block for one
 // node); warp w takes rows w, w + 8, ... of each tile, independently of the
 // other warps; the CTA meets at a barrier only when the block changes, to
 // publish its shared histogram and stage the next block's V.
@@ -38,7 +38,7 @@ using namespace dev;
 
 constexpr int kThreads = kSketchThreads;   // 256 = 8 warps
 constexpr int kWarps = kThreads / 32;
-constexpr int kTileCache = 64;             // tile descriptors cached in shared memory
+constexpr int kTileCache = 128;            // tile descriptors cached in shared memory
 
 // valid columns of row p of a block (the last row of a padded flat block is short, R14)
 __device__ __forceinline__ int row_cols(long long len, int n, int p) {
@@ -344,7 +344,7 @@ int occupancy_rj(int shape, int vs_cap) {
 
 }  // namespace
 
-int sketch_tile_rows(int) { return 32; }
+int sketch_tile_rows(int) { return 32; }   // (plan_tiles takes 8 for small single-block layouts)
 int sketch_tile_cols(int) { return 128; }
 int sketch_shape_ok(int shape, int) { return shape >= 0 && shape <= 3; }
 
