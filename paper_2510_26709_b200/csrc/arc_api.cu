@@ -86,7 +86,8 @@ struct Plan {
     size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
            o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
            o_vals = 0, o_hash = 0, o_hist1 = 0, o_hist2 = 0, o_hist3 = 0, o_slice_gt = 0, o_slice_eq = 0,
-           o_items = 0, o_cand = 0, o_cand_count = 0, o_sblocks = 0, o_segs_real = 0, o_dense_ids = 0, total = 0;
+           o_items = 0, o_cand = 0, o_cand_count = 0, o_sblocks = 0, o_segs_real = 0, o_dense_ids = 0, total = 0,
+           o_b1s = 0;
 };
 
 arc_status validate(const arc_topk_params* p) {
@@ -234,6 +235,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_items = take(sizeof(SliceItem) * pl.items.size());
     pl.o_cand = take(sizeof(unsigned) * 2 * 2 * kCandCap * nsb);
     pl.o_cand_count = take(sizeof(unsigned) * 2 * nsb);
+    pl.o_b1s = take(sizeof(unsigned) * nsb);
     pl.o_hash = take(sizeof(uint64_t) * (pl.G + 1));
     const size_t pn = sizeof(float) * static_cast<size_t>(M) * pl.L * p->r;
     pl.o_pnodes = pl.keep_pnodes ? take(pn) : 0;
@@ -737,6 +739,8 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ga.N_int = c->p.N;
     ga.sum_Kn = pl.sumKn;
     ga.noef = pl.noef ? 1 : 0;
+    ga.sigma = sigma;
+    ga.b1s = c->at<unsigned>(pl.o_b1s);
     const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
     float* wire = (pl.exchange || pl.topk) ? c->at<float>(pl.o_wire) : nullptr;
     ga.blocks = sblocks;

@@ -153,7 +153,7 @@ __device__ __forceinline__ float div_N(float A, float Nf, float invN, bool pow2)
     return pow2 ? fmul(A, invN) : __fdiv_rn(A, Nf);
 }
 
-template <int UN>
+template <int UN, bool FILTER = false>
 __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const SelRow* pre) {
     const int items = (seg1 - seg0) * kSegQuads;
     const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
@@ -174,7 +174,13 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                 const BlockDev& B = a.blocks[R.b];
                 const int f = R.q0 + item % kSegQuads;
                 const int q = 4 * f;
-                if (q < B.n) {
+                bool done = false;
+                if (FILTER && q < B.n) {   // updated before barrier 1 (early mode)
+                    const unsigned b1 = __ldcg(a.b1s + R.b);
+                    const int p = __ldcg(a.sel + B.sel_base + R.k);
+                    done = b1 == 0xFFFFFFFFu || (order_key(__ldcg(a.sigma + B.row_base + p)) >> 21) > b1;
+                }
+                if (q < B.n && !done) {
                     const int p = __ldcg(a.sel + B.sel_base + R.k);
                     const int nv = row_valid_cols(B, p);
                     cnt[u] = max(0, min(4, nv - q));
@@ -724,11 +730,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
         for (int p = lo + tid; p < hi; p += kThreads) out[p] = p;
     }
     STAMP(5);
-    if (s.early) {
+    if (s.early && !overflow) {
         if (arc) {
             __syncthreads();
             gather_rows_local<4>(ga, B, lo, s_rows, s_nb);
         }
+        STAMP(6);
+        STAMP(7);
+        return;
+    }
+    if (s.early) {
+        // a candidate overflow (massive ties): the selected boundary rows may crowd
+        // a few slices, so they are spread over the grid like the non-early path,
+        // skipping the rows each slice updated before barrier 1
+        if (it.c == 0 && tid == 0) ga.b1s[bb] = arc ? b1 : 0xFFFFFFFFu;
+        __threadfence();
+        grid.sync();                                 // ---------------- b1 of every block published
+        constexpr int UN = 4;
+        const long long S = ga.num_rows;
+        const int seg0 = static_cast<int>(S * blockIdx.x / gridDim.x);
+        const int seg1 = static_cast<int>(S * (blockIdx.x + 1) / gridDim.x);
+        gather_segments<UN, true>(ga, seg0, seg1, nullptr);
         STAMP(6);
         STAMP(7);
         return;
