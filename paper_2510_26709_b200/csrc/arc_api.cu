@@ -87,7 +87,7 @@ struct Plan {
            o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
            o_vals = 0, o_hash = 0, o_hist1 = 0, o_hist2 = 0, o_hist3 = 0, o_slice_gt = 0, o_slice_eq = 0,
            o_items = 0, o_cand = 0, o_cand_count = 0, o_sblocks = 0, o_segs_real = 0, o_dense_ids = 0, total = 0,
-           o_b1s = 0;
+           o_bnd = 0, o_bnd_count = 0;
 };
 
 arc_status validate(const arc_topk_params* p) {
@@ -235,7 +235,8 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_items = take(sizeof(SliceItem) * pl.items.size());
     pl.o_cand = take(sizeof(unsigned) * 2 * 2 * kCandCap * nsb);
     pl.o_cand_count = take(sizeof(unsigned) * 2 * nsb);
-    pl.o_b1s = take(sizeof(unsigned) * nsb);
+    pl.o_bnd = take(sizeof(int) * 2 * std::max<int64_t>(sumK, 1));
+    pl.o_bnd_count = take(sizeof(unsigned) * 2);
     pl.o_hash = take(sizeof(uint64_t) * (pl.G + 1));
     const size_t pn = sizeof(float) * static_cast<size_t>(M) * pl.L * p->r;
     pl.o_pnodes = pl.keep_pnodes ? take(pn) : 0;
@@ -545,6 +546,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
             UPLOAD(c->pl.o_selrows, rows);
             UPLOAD(c->pl.o_items, c->pl.items);
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_cand_count, 0, sizeof(unsigned) * 2 * c->pl.sbdev.size(), s));
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_bnd_count, 0, sizeof(unsigned) * 2, s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist2, 0, sizeof(unsigned) * 2048 * c->pl.sbdev.size(), s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist3, 0, sizeof(unsigned) * 1024 * c->pl.sbdev.size(), s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_status, 0, 16, s));
@@ -739,8 +741,8 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ga.N_int = c->p.N;
     ga.sum_Kn = pl.sumKn;
     ga.noef = pl.noef ? 1 : 0;
-    ga.sigma = sigma;
-    ga.b1s = c->at<unsigned>(pl.o_b1s);
+    ga.bnd = c->at<int2>(pl.o_bnd);
+    ga.bnd_count = c->at<unsigned>(pl.o_bnd_count);
     const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
     float* wire = (pl.exchange || pl.topk) ? c->at<float>(pl.o_wire) : nullptr;
     ga.blocks = sblocks;

@@ -175,10 +175,8 @@ struct GatherLaunch {
                         // 3 = Top-K baseline: node B.node only, wire values at B.val_base
     long long sum_Kn;
     int noef;           // without EF: C_i = grad_i rows, no h / g (u = gbar, scaled by the sketch pass)
-    // early mode after a candidate overflow: rows already updated before barrier 1
-    // (digit 1 above the block's boundary bin b1s[b]; 0xFFFFFFFF: every row) are skipped
-    const float* sigma;
-    unsigned* b1s;
+    int2* bnd;          // early mode after an overflow: selected boundary rows (block, row)
+    unsigned* bnd_count;   // [2] by step parity
 };
 
 struct ScatterLaunch {

@@ -153,7 +153,7 @@ __device__ __forceinline__ float div_N(float A, float Nf, float invN, bool pow2)
     return pow2 ? fmul(A, invN) : __fdiv_rn(A, Nf);
 }
 
-template <int UN, bool FILTER = false>
+template <int UN>
 __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const SelRow* pre) {
     const int items = (seg1 - seg0) * kSegQuads;
     const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
@@ -174,13 +174,7 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                 const BlockDev& B = a.blocks[R.b];
                 const int f = R.q0 + item % kSegQuads;
                 const int q = 4 * f;
-                bool done = false;
-                if (FILTER && q < B.n) {   // updated before barrier 1 (early mode)
-                    const unsigned b1 = __ldcg(a.b1s + R.b);
-                    const int p = __ldcg(a.sel + B.sel_base + R.k);
-                    done = b1 == 0xFFFFFFFFu || (order_key(__ldcg(a.sigma + B.row_base + p)) >> 21) > b1;
-                }
-                if (q < B.n && !done) {
+                if (q < B.n) {
                     const int p = __ldcg(a.sel + B.sel_base + R.k);
                     const int nv = row_valid_cols(B, p);
                     cnt[u] = max(0, min(4, nv - q));
@@ -315,6 +309,37 @@ __device__ void gather_rows_local(const GatherLaunch& a, const BlockDev& B, int 
             for (int kk = 0; kk < 4; ++kk) gb[u].v[kk] = fadd(gb[u].v[kk], div_N(A[u].v[kk], a.Nf, invN, pow2));   // R3, R13
             store_quad(a.gbar + e[u], gb[u], v4[u], nv[u]);
         }
+    }
+}
+
+// S4 + S5 + S6 of one selected row (mode 0, no values output) by one warp: lane
+// l takes columns 4l, 4l + 128, ...; the same arithmetic as gather_rows_local.
+__device__ __forceinline__ void gather_row_warp(const GatherLaunch& a, const BlockDev& B, int p, int lane) {
+    const int nvr = row_valid_cols(B, p);
+    const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
+    const float invN = 1.0f / a.Nf;
+    for (int q = 4 * lane; q < nvr; q += 128) {
+        const int nv = min(4, nvr - q);
+        const long long e = B.off + static_cast<long long>(p) * B.n + q;
+        const bool v4 = B.vec && nv == 4;
+        Quad A, gb = load_quad(a.gbar + e, v4, nv);
+        for (int i = 0; i < a.nodes_local; ++i) {
+            float* __restrict__ ph = a.noef ? const_cast<float*>(a.nodes.grad[i]) : a.nodes.h[i];
+            float* __restrict__ pg = a.nodes.g[i];
+            const Quad hq = load_quad(ph + e, v4, nv);
+            Quad gq, gn;
+            if (!a.noef) gq = load_quad(pg + e, v4, nv);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const float c = a.noef ? hq.v[kk] : fsub(hq.v[kk], gq.v[kk]);   // C_i
+                gn.v[kk] = a.noef ? 0.0f : fadd(gq.v[kk], c);                 // R12
+                A.v[kk] = i == 0 ? c : fadd(A.v[kk], c);                      // R9 node order
+            }
+            if (!a.noef) store_quad(pg + e, gn, v4, nv);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) gb.v[kk] = fadd(gb.v[kk], div_N(A.v[kk], a.Nf, invN, pow2));   // R3, R13
+        store_quad(a.gbar + e, gb, v4, nv);
     }
 }
 
@@ -741,16 +766,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     }
     if (s.early) {
         // a candidate overflow (massive ties): the selected boundary rows may crowd
-        // a few slices, so they are spread over the grid like the non-early path,
-        // skipping the rows each slice updated before barrier 1
-        if (it.c == 0 && tid == 0) ga.b1s[bb] = arc ? b1 : 0xFFFFFFFFu;
+        // a few slices, so every slice appends them to one list and, after a
+        // barrier, the grid's warps take them row by row
+        if (arc && tid == 0) s_abv = s_nb > 0 ? static_cast<int>(atomicAdd(ga.bnd_count + par, static_cast<unsigned>(s_nb))) : 0;
+        if (blockIdx.x == 0 && tid == 0) ga.bnd_count[par ^ 1] = 0;   // the next step's counter
+        __syncthreads();
+        if (arc)
+            for (int i = tid; i < s_nb; i += kThreads) ga.bnd[s_abv + i] = make_int2(static_cast<int>(bb), lo + s_rows[i]);
         __threadfence();
-        grid.sync();                                 // ---------------- b1 of every block published
-        constexpr int UN = 4;
-        const long long S = ga.num_rows;
-        const int seg0 = static_cast<int>(S * blockIdx.x / gridDim.x);
-        const int seg1 = static_cast<int>(S * (blockIdx.x + 1) / gridDim.x);
-        gather_segments<UN, true>(ga, seg0, seg1, nullptr);
+        grid.sync();                                 // ---------------- the boundary list is complete
+        const int total = static_cast<int>(__ldcg(ga.bnd_count + par));
+        const int lane = tid & 31, warps = kThreads / 32;
+        for (int j = blockIdx.x * warps + (tid >> 5); j < total; j += gridDim.x * warps) {
+            const int2 br = __ldcg(ga.bnd + j);
+            gather_row_warp(ga, ga.blocks[br.x], br.y, lane);
+        }
         STAMP(6);
         STAMP(7);
         return;

@@ -13,7 +13,7 @@ run --config C5_1e6
 run --config C5_1e8 --mu-bp 10 --pool 4
 run --config C5_1e8 --pool 4
 run --config C5_1e8 --mu-bp 1000 --pool 4
-run --config C5_1e9 --mu-bp 10 --pool 1
-run --config C5_1e9 --pool 1
-run --config C5_1e9 --mu-bp 1000 --pool 1
+run --config C5_1e9 --mu-bp 10 --pool 2
+run --config C5_1e9 --pool 2
+run --config C5_1e9 --mu-bp 1000 --pool 2
 } > ${out}.jsonl
