@@ -83,6 +83,7 @@ struct Plan {
     bool dense_fast = false;         // DENSE blocks handled by the streaming k_dense (not Top-K)
     std::vector<int> dense_ids;
     // workspace offsets (bytes)
+    size_t o_cta_w = 0;
     size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
            o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
            o_vals = 0, o_hash = 0, o_hist1 = 0, o_hist2 = 0, o_hist3 = 0, o_slice_gt = 0, o_slice_eq = 0,
@@ -221,6 +222,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_dense_ids = take(sizeof(int) * pl.dense_ids.size());
     pl.o_tiles = take(sizeof(TileDesc) * pl.max_tiles);
     pl.o_cta = take(sizeof(int) * (kMaxGrid + 1));
+    pl.o_cta_w = take(sizeof(int) * (kMaxGrid + 1));
     pl.o_selrows = take(sizeof(SelRow) * pl.num_segs);
     pl.o_V = take(sizeof(float) * sum_nr * 2);   // double-buffered by t parity
     pl.Ms = (M + pl.G - 1) / pl.G;
@@ -265,8 +267,8 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
 // are live (masked rows still run the load and staging code), so a tile of r
 // rows is charged nchunks * max(r, 0.6 R_shape); tiles go longest-first to the
 // least-loaded CTA (LPT).
-void plan_tiles(const Plan& pl, int resident, int tile_rows_max, int W, std::vector<Tile>& tiles,
-                std::vector<int>& cta_begin, int& grid) {
+void plan_tiles(const Plan& pl, const std::vector<char>& use, int resident, int tile_rows_max, int W,
+                std::vector<Tile>& tiles, std::vector<int>& cta_begin, int& grid) {
     struct Cand { int64_t makespan = INT64_MAX; std::vector<Tile> tiles; std::vector<int> begin; int grid = 0; };
     Cand best;
     resident = std::max(1, std::min(resident, kMaxGrid));
@@ -279,8 +281,8 @@ void plan_tiles(const Plan& pl, int resident, int tile_rows_max, int W, std::vec
     {
         int arc_blocks = 0;
         int64_t tiles8 = 0;
-        for (const BlockDev& B : pl.bdev)
-            if (B.kind == ARC_BLOCK_ARC) { ++arc_blocks; tiles8 += (B.m + 7) / 8 * nodes; }
+        for (size_t b = 0; b < pl.bdev.size(); ++b)
+            if (pl.bdev[b].kind == ARC_BLOCK_ARC && use[b]) { ++arc_blocks; tiles8 += (pl.bdev[b].m + 7) / 8 * nodes; }
         if (arc_blocks <= 8 && tiles8 <= static_cast<int64_t>(resident) * 96) tile_rows_max = std::min(tile_rows_max, 8);
     }
     const int64_t floor_rows = (tile_rows_max * 6 + 9) / 10;
@@ -295,7 +297,7 @@ void plan_tiles(const Plan& pl, int resident, int tile_rows_max, int W, std::vec
         std::vector<int64_t> cost;
         for (size_t b = 0; b < pl.bdev.size(); ++b) {
             const BlockDev& B = pl.bdev[b];
-            if (B.kind != ARC_BLOCK_ARC) continue;
+            if (B.kind != ARC_BLOCK_ARC || !use[b]) continue;
             const int Rb = std::min(R, B.m);
             const int nt = (B.m + Rb - 1) / Rb;
             const int64_t nch = (B.n + W - 1) / W;
@@ -376,6 +378,7 @@ struct arc_topk_ctx {
     ncclComm_t comm = nullptr;
     unsigned char* ws = nullptr;
     int grid = 0, num_tiles = 0, shape = 0, vs_cap = 0;
+    int grid_w = 0, vs_cap_w = 0, tiles_w0 = 0;   // the wide blocks' ranged launch (grid_w == 0: none)
     float ome = 0.f, Nf = 0.f;
     cudaStream_t last = nullptr;
     // per-phase timing
@@ -490,7 +493,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
 
     // static tables
     std::vector<Tile> tiles;
-    std::vector<int> cta_begin;
+    std::vector<int> cta_begin, cta_begin_w;
     {   // streaming-pass variant: 0 = 4 row segments per batch (>= 3 CTAs/SM),
         // 1 = 2 segments per batch at 4 CTAs/SM (ARC_SKETCH_SHAPE, experiments)
         c->shape = 0;
@@ -500,17 +503,39 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         }
     }
     {
-        int max_n = 0;
-        for (const BlockDev& B : c->pl.bdev)
-            if (B.kind == ARC_BLOCK_ARC) max_n = std::max(max_n, B.n);
-        c->vs_cap = sketch_vs_cap(c->p.r, max_n);
-        // blocks whose V does not fit read it from global memory; stage the largest that fits
-        if (c->vs_cap == 0)
-            for (const BlockDev& B : c->pl.bdev)
-                if (B.kind == ARC_BLOCK_ARC) c->vs_cap = std::max(c->vs_cap, sketch_vs_cap(c->p.r, B.n));
+        // blocks whose V_b^T fits the shared-memory stage stream in one launch; the
+        // wider ones (methods with a sketch) in a second, ranged launch
+        const bool sketches = !c->pl.topk && !c->pl.randk;
+        std::vector<char> narrow(c->pl.bdev.size(), 1), wide(c->pl.bdev.size(), 0);
+        c->vs_cap = 0;
+        bool any_wide = false;
+        for (size_t b = 0; b < c->pl.bdev.size(); ++b) {
+            const BlockDev& B = c->pl.bdev[b];
+            if (B.kind != ARC_BLOCK_ARC) continue;
+            const int cap = sketch_vs_cap(c->p.r, B.n);
+            if (cap == 0 && sketches && sketch_ranged_cap(c->p.r) > 0) {
+                narrow[b] = 0;
+                wide[b] = 1;
+                any_wide = true;
+            } else {
+                c->vs_cap = std::max(c->vs_cap, cap);
+            }
+        }
+        plan_tiles(c->pl, narrow, ef_sketch_resident_ctas(c->p.r, c->shape, c->vs_cap), sketch_tile_rows(c->shape),
+                   sketch_tile_cols(c->shape), tiles, cta_begin, c->grid);
+        c->grid_w = 0;
+        if (any_wide) {
+            c->vs_cap_w = sketch_ranged_cap(c->p.r);
+            std::vector<Tile> tw;
+            std::vector<int> cbw;
+            plan_tiles(c->pl, wide, ef_sketch_resident_ctas_ranged(c->p.r, c->vs_cap_w), 32, sketch_tile_cols(c->shape),
+                       tw, cbw, c->grid_w);
+            c->tiles_w0 = static_cast<int>(tiles.size());
+            for (int& x : cbw) x += c->tiles_w0;
+            tiles.insert(tiles.end(), tw.begin(), tw.end());
+            cta_begin_w = std::move(cbw);
+        }
     }
-    plan_tiles(c->pl, ef_sketch_resident_ctas(c->p.r, c->shape, c->vs_cap), sketch_tile_rows(c->shape),
-               sketch_tile_cols(c->shape), tiles, cta_begin, c->grid);
     c->num_tiles = static_cast<int>(tiles.size());
     std::vector<TileDesc> tdesc(tiles.size());
     for (size_t i = 0; i < tiles.size(); ++i) {
@@ -543,6 +568,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
             UPLOAD(c->pl.o_dense_ids, c->pl.dense_ids);
             UPLOAD(c->pl.o_tiles, tdesc);
             UPLOAD(c->pl.o_cta, cta_begin);
+            UPLOAD(c->pl.o_cta_w, cta_begin_w);
             UPLOAD(c->pl.o_selrows, rows);
             UPLOAD(c->pl.o_items, c->pl.items);
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_cand_count, 0, sizeof(unsigned) * 2 * c->pl.sbdev.size(), s));
@@ -670,8 +696,18 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         ARC_MARK(1);
         a.noef = pl.noef ? 1 : 0;
         a.gbar = gbar;
-        launch_ef_sketch(a, s);
-        ARC_LAUNCHED();
+        if (c->grid > 0) {
+            launch_ef_sketch(a, s);
+            ARC_LAUNCHED();
+        }
+        if (c->grid_w > 0) {   // blocks with V_b^T wider than the stage
+            a.cta_begin = c->at<int>(pl.o_cta_w);
+            a.grid = c->grid_w;
+            a.vs_cap = c->vs_cap_w;
+            a.ranged = 1;
+            launch_ef_sketch(a, s);
+            ARC_LAUNCHED();
+        }
     } else {
         ARC_MARK(1);
     }
@@ -978,7 +1014,7 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     // steady state with consecutive t: V comes from the previous step's select
     // kernel (k_vgen only when there is none)
     const Plan& pl = c->pl;
-    const int sketch = pl.M > 0 ? 1 : 0;
+    const int sketch = pl.M > 0 ? (c->grid > 0 ? 1 : 0) + (c->grid_w > 0 ? 1 : 0) : 0;
     const int sel = pl.items.empty() ? 0 : 1;
     if (pl.topk) return sketch + sel + c->p.N;   // + N ordered merges
     const int vgen = (pl.M > 0 && pl.items.empty() && !pl.randk) ? 1 : 0;

@@ -141,13 +141,16 @@ struct SketchLaunch {
     int shape;         // variant (arc_sketch.cu)
     int vs_cap;        // floats of dynamic shared memory for V_b^T (0: V from global memory)
     int noef;          // compressed MSGD without EF: sketch the gradient, u = gbar <- eta u
+    int ranged;        // the launch over blocks whose V_b^T exceeds the stage (ranges of vs_cap / r columns)
     float* gbar;       // (noef) the replicated momentum u
     int pdl;           // launch with programmatic stream serialization (overlap the launch)
     unsigned* status;
 };
 void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s);
 int ef_sketch_resident_ctas(int r, int shape, int vs_cap);   // SMs x occupancy
-int sketch_vs_cap(int r, int max_n);   // floats of V_b^T the streaming pass stages in shared memory
+int sketch_vs_cap(int r, int max_n);   // floats of V_b^T the streaming pass stages in shared memory (0: too wide)
+int sketch_ranged_cap(int r);          // floats staged per range by the wide blocks' launch
+int ef_sketch_resident_ctas_ranged(int r, int vs_cap);
 int sketch_tile_rows(int shape);
 int sketch_tile_cols(int shape);
 int sketch_shape_ok(int shape, int r);

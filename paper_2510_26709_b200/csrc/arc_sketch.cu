@@ -63,7 +63,7 @@ constexpr int kVsMax = 12288;              // floats of V_b^T staged at most (48
 // butterfly folds the lane sums into P (left to right over chunks).
 template <int RJ, bool NOEF>
 __device__ __forceinline__ void segment(const SketchLaunch& a, int k, int nseg, int q, int nv, long long base, bool vec,
-                                        int n, const float* Vb, bool V_vec, bool v_smem, bool sketch, float* ph,
+                                        int vld, int vc0, const float* Vb, bool V_vec, bool v_smem, bool sketch, float* ph,
                                         const float (&gx)[4], const float (&hx)[4], const float (&dx)[4], float eta,
                                         float ome, int r, float (&acc)[RJ], float (&P)[RJ]) {
     const long long e = base + q;
@@ -97,7 +97,7 @@ __device__ __forceinline__ void segment(const SketchLaunch& a, int k, int nseg, 
 #pragma unroll
         for (int j = 0; j < RJ; ++j) {
             if (j >= r) break;
-            const float* vj = Vb + static_cast<long long>(j) * ((n + 3) & ~3) + q;   // V_b^T rows padded
+            const float* vj = Vb + static_cast<long long>(j) * vld + (q - vc0);   // V_b^T [r][vld] from column vc0
             float v[4];
             if (q + 3 < nv && V_vec) {
                 const float4 t4 = v_smem ? *reinterpret_cast<const float4*>(vj) : __ldg(reinterpret_cast<const float4*>(vj));
@@ -169,10 +169,14 @@ __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int r
 // The register path: the same per-segment arithmetic with the batch loaded
 // straight into registers (UN segments, 3 UN float4 per lane), warps streaming
 // their rows independently; V_b^T staged in shared memory as above.
-template <int RJ, int UN, int MINB, bool NOEF>
+// RANGED: the launch over the blocks whose V_b^T does not fit the stage; V is
+// staged in ranges of whole 1024-column chunks and every row carries its P'
+// across ranges in shared memory (the O6 order is unchanged)
+template <int RJ, int UN, int MINB, bool NOEF, bool RANGED>
 __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch a) {
     __shared__ TileDesc s_tile[kTileCache];
     __shared__ unsigned s_hist[kHist1Bins];     // digit-1 histogram of this CTA's Sigma (modes 0, 3)
+    __shared__ float s_P[RANGED ? 32 : 1][RJ];  // (RANGED) the tile rows' running P' between ranges
     extern __shared__ __align__(16) float4 dyn[];   // V_b^T
     float* Vs = reinterpret_cast<float*>(dyn);
 
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
             __syncthreads();
             if (cta_hist && cur_b >= 0) flush_hist(cur_b);
             const int nvf = r * ((T_n + 3) & ~3);
-            v_smem = sketch && nvf <= a.vs_cap;
+            v_smem = !RANGED && sketch && nvf <= a.vs_cap;
             if (v_smem) {
                 const float* __restrict__ src = a.V + T_voff;
                 if ((T_voff & 3) == 0 && (nvf & 3) == 0) {
@@ -235,6 +239,80 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         const float* Vb = v_smem ? Vs : a.V + T_voff;
         const bool V_vec = true;   // V_b^T rows start 16-byte aligned (padded to ldv = round_up(n, 4))
 
+        if constexpr (RANGED) {
+            const int ldv = (T_n + 3) & ~3;
+            const int range_w = (a.vs_cap / r) / 1024 * 1024;
+            for (int c0 = 0; c0 < T_n; c0 += range_w) {
+                __syncthreads();                         // stage V_b^T[:, c0 : c0 + range_w)
+                const int w = min(range_w, ldv - c0);
+                for (int i = tid; i < r * (w >> 2); i += kThreads) {
+                    const int j = i / (w >> 2), f = i - j * (w >> 2);
+                    reinterpret_cast<float4*>(Vs + j * range_w)[f] =
+                        __ldg(reinterpret_cast<const float4*>(a.V + T_voff + static_cast<long long>(j) * ldv + c0) + f);
+                }
+                __syncthreads();
+                for (int rr = warp; rr < T_rows; rr += kWarps) {
+                    const int p = T_row0 + rr;
+                    const int nv = row_cols(T_len, T_n, p);
+                    const long long base = T_off + static_cast<long long>(p) * T_n;
+                    const int nseg = (nv + 127) >> 7;
+                    const int kb = c0 >> 7, ke = min(nseg, (c0 + range_w) >> 7);
+                    if (kb >= ke) continue;              // (a short last row ends in an earlier range)
+                    float acc[RJ], P[RJ];
+#pragma unroll
+                    for (int j = 0; j < RJ; ++j) { acc[j] = 0.0f; P[j] = c0 > 0 ? s_P[rr][j] : 0.0f; }
+                    for (int k0 = kb; k0 < ke; k0 += UN) {
+                        float4 xg[UN], xh[UN], xd[UN];
+#pragma unroll
+                        for (int u = 0; u < UN; ++u) {
+                            const int q = 128 * (k0 + u) + 4 * lane;
+                            const long long e = base + q;
+                            float tg[4] = {0.f, 0.f, 0.f, 0.f}, th[4] = {0.f, 0.f, 0.f, 0.f}, td[4] = {0.f, 0.f, 0.f, 0.f};
+                            if (k0 + u < ke && q + 3 < nv && T_vec) {
+                                const float4 g4 = __ldcs(reinterpret_cast<const float4*>(pg + e));
+                                tg[0] = g4.x; tg[1] = g4.y; tg[2] = g4.z; tg[3] = g4.w;
+                                if (!NOEF || ph != nullptr) {
+                                    const float4 h4 = __ldcs(reinterpret_cast<const float4*>(ph + e));
+                                    th[0] = h4.x; th[1] = h4.y; th[2] = h4.z; th[3] = h4.w;
+                                }
+                                if (!NOEF) {
+                                    const float4 d4 = __ldcs(reinterpret_cast<const float4*>(pgg + e));
+                                    td[0] = d4.x; td[1] = d4.y; td[2] = d4.z; td[3] = d4.w;
+                                }
+                            } else if (k0 + u < ke) {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    if (q + k < nv) {
+                                        tg[k] = __ldcs(pg + e + k);
+                                        if (!NOEF || ph != nullptr) th[k] = __ldcs(ph + e + k);
+                                        if (!NOEF) td[k] = __ldcs(pgg + e + k);
+                                    }
+                            }
+                            xg[u] = make_float4(tg[0], tg[1], tg[2], tg[3]);
+                            xh[u] = make_float4(th[0], th[1], th[2], th[3]);
+                            xd[u] = make_float4(td[0], td[1], td[2], td[3]);
+                        }
+#pragma unroll
+                        for (int u = 0; u < UN; ++u) {
+                            const int k = k0 + u;
+                            if (k >= ke) break;
+                            const float gx[4] = {xg[u].x, xg[u].y, xg[u].z, xg[u].w};
+                            const float hx[4] = {xh[u].x, xh[u].y, xh[u].z, xh[u].w};
+                            const float dx[4] = {xd[u].x, xd[u].y, xd[u].z, xd[u].w};
+                            segment<RJ, NOEF>(a, k, nseg, 128 * k + 4 * lane, nv, base, T_vec, range_w, c0, Vs, true, true,
+                                              sketch, ph, gx, hx, dx, eta, ome, r, acc, P);
+                        }
+                    }
+                    if (ke < nseg) {                     // the row continues in the next range
+                        if (lane == 0)
+#pragma unroll
+                            for (int j = 0; j < RJ; ++j) s_P[rr][j] = P[j];
+                        continue;
+                    }
+                    row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
+                }
+            }
+        } else {
         for (int rr = warp; rr < T_rows; rr += kWarps) {
             const int p = T_row0 + rr;
             const int nv = row_cols(T_len, T_n, p);
@@ -275,11 +353,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
                     const float gx[4] = {xg[u].x, xg[u].y, xg[u].z, xg[u].w};
                     const float hx[4] = {xh[u].x, xh[u].y, xh[u].z, xh[u].w};
                     const float dx[4] = {xd[u].x, xd[u].y, xd[u].z, xd[u].w};
-                    segment<RJ, NOEF>(a, k, nseg, 128 * k + 4 * lane, nv, base, T_vec, T_n, Vb, V_vec, v_smem, sketch, ph,
+                    segment<RJ, NOEF>(a, k, nseg, 128 * k + 4 * lane, nv, base, T_vec, (T_n + 3) & ~3, 0, Vb, V_vec, v_smem, sketch, ph,
                                 gx, hx, dx, eta, ome, r, acc, P);
                 }
             }
             row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
+        }
         }
     }
     if (cta_hist) {
@@ -288,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
     }
 }
 
-template <int RJ, int UN, int MINB, bool NOEF = false>
+template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false>
 void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(a.grid);
@@ -297,7 +376,7 @@ void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     cfg.stream = s;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sizeof(float) * kVsMax));
         attr_set = true;
     }
@@ -306,14 +385,14 @@ void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, k_ef_sketch<RJ, UN, MINB, NOEF>, a);
+    cudaLaunchKernelEx(&cfg, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, a);
 }
-template <int RJ, int UN, int MINB, bool NOEF = false>
+template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false>
 int occupancy_reg(int vs_cap) {
-    cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(float) * kVsMax));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB, NOEF>, kThreads, sizeof(float) * vs_cap);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, kThreads, sizeof(float) * vs_cap);
     return per_sm;
 }
 
@@ -321,6 +400,11 @@ int occupancy_reg(int vs_cap) {
 // 2 = 4 / 2, 3 = 1 / 5 (r <= 8; wider sketches get fewer CTAs)
 template <int RJ>
 void launch_rj(const SketchLaunch& a, cudaStream_t s) {
+    if (a.ranged) {   // the wide blocks' launch (one variant)
+        if (a.noef) launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2), true, true>(a, s);
+        else launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2), false, true>(a, s);
+        return;
+    }
     if (a.noef) {   // (the without-EF baseline: one variant)
         launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2), true>(a, s);
         return;
@@ -360,6 +444,19 @@ void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s) {
 int sketch_vs_cap(int r, int max_n) {
     const long long need = static_cast<long long>(r) * ((max_n + 3) / 4 * 4);   // padded V_b^T rows
     return static_cast<int>(need <= kVsMax ? need : 0) & ~3;   // 0: V read from global memory
+}
+
+int sketch_ranged_cap(int r) { return kVsMax / (1024 * r) * (1024 * r); }
+
+int ef_sketch_resident_ctas_ranged(int r, int vs_cap) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = r <= 4 ? occupancy_reg<4, 3, 3, false, true>(vs_cap)
+                       : r <= 8 ? occupancy_reg<8, 3, 3, false, true>(vs_cap)
+                       : r <= 16 ? occupancy_reg<16, 3, 2, false, true>(vs_cap)
+                                 : occupancy_reg<32, 3, 2, false, true>(vs_cap);
+    return sms * (per_sm < 1 ? 1 : per_sm);
 }
 
 int ef_sketch_resident_ctas(int r, int shape, int vs_cap) {

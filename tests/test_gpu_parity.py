@@ -344,6 +344,26 @@ def test_randk_multiblock_and_exchange(orc):
     run_parity(orc, off, blocks, N=2, steps=3, method="randk", force_exchange=True, reduce="ordered")
 
 
+# ------------------------------------------------------------------ wide blocks (V staged in ranges)
+
+@pytest.mark.parametrize("r,exchange", [(4, False), (8, False), (4, True)])
+def test_wide_blocks_ranged_launch(orc, r, exchange):
+    """Blocks whose V_b^T exceeds the streaming kernel's shared-memory stage (r n > 12288
+    floats) go through the second, ranged launch (V staged in 1024-column ranges, P'
+    carried across ranges); mixed with narrow blocks, a ragged wide last row and an
+    unaligned row length."""
+    shapes = [(37, 3500, 5), (20, 1000, 3), (9, 7777, 2)]
+    blocks, off = [], 0
+    for m, n, K in shapes:
+        blocks.append(Block(off, m * n, m, n, K, 0))
+        off += m * n
+    last = Block(off, 6 * 4100 - 57, 6, 4100, 2, 0)            # ragged last row
+    blocks.append(last)
+    off += last.len
+    run_parity(orc, off, blocks, N=2, steps=3, r=r, force_exchange=exchange,
+               reduce="ordered" if exchange else "nccl")
+
+
 # ------------------------------------------------------------------ without EF (Table II)
 
 @pytest.mark.parametrize("N,d,n,K,beta", [(1, 50_000, 100, 7, 0.9), (4, 60_000, 96, 12, 0.9), (3, 4_097, 3, 40, 0.0)])
