@@ -436,7 +436,9 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "k_ef_sketch", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": ab["ef_sketch"], "peak_source": peak_src,
-                         "launch_ms": sk_ms},
+                         "launch_ms": sk_ms,
+                         # also against the nominal HBM3e figure (HGX B200, 7.7 TB/s)
+                         "nominal_peak": 7700.0, "nominal_frac": achieved / 7700.0},
             "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
                               "hbm_bytes": ab["total"], "nvlink_bus_bytes": bus["total"]},
             "phases_ms": phase_ms,
