@@ -86,6 +86,29 @@ def test_workspace_bytes_rejects_invalid(L, blocks, kw):
     assert st == L.ERR_INVALID_ARG
 
 
+def test_workspace_bytes_multi_gpu_and_methods(L):
+    """Host-only plan checks of the G > 1 layout (no GPU needed): the exchange buffers
+    (all-to-all receive [G][ceil(M/G)][L][r], the K-row wire) appear once G > 1 and
+    stay O(M r + K n) as G grows; the method-specific momentum ranges validate."""
+    blocks = [(0, 100_000, 1000, 100, 10, 0)]
+    st1, n1 = _ws(L, _params(L, blocks, N=1, nodes_local=1))
+    st2, n2 = _ws(L, _params(L, blocks, N=2, nodes_local=1, rank=1))
+    st8, n8 = _ws(L, _params(L, blocks, N=8, nodes_local=1, rank=7))
+    assert st1 == st2 == st8 == L.OK
+    M, r, Kn = 1000, 4, 10 * 100
+    assert n2 > n1                                             # exchange buffers
+    assert n8 - n1 <= 4 * (2 * 8 * (-(-M // 8)) * r + 8 * M + 2 * Kn) + 64 * 1024   # O(M r + K n)
+    p = _params(L, blocks, N=1, nodes_local=1, eta=0.0)
+    p.method = L.METHOD_NOEF_MSGD                               # beta = 0 is a valid heavy-ball constant
+    assert _ws(L, p)[0] == L.OK
+    p = _params(L, blocks, N=1, nodes_local=1, eta=1.0)
+    p.method = L.METHOD_NOEF_MSGD                               # beta = 1 never decays: rejected
+    assert _ws(L, p)[0] == L.ERR_INVALID_ARG
+    p = _params(L, blocks, N=1, nodes_local=1)
+    p.method = 9
+    assert _ws(L, p)[0] == L.ERR_INVALID_ARG
+
+
 def test_null_arguments_rejected(L):
     lib = L.lib()
     assert lib.arc_topk_workspace_bytes(None, None) == L.ERR_INVALID_ARG
