@@ -414,3 +414,34 @@ def test_randomized_configurations(orc, case):
     reduce = str(rng.choice(["nccl", "ordered"]))
     run_parity(orc, d, blocks, N=N, steps=2, eta=eta, r=r, seed=case, method=method,
                force_exchange=fx, reduce=reduce)
+
+
+# ------------------------------------------------------------------ selection vs torch.sort
+
+@pytest.mark.parametrize("cfg,mu_bp", [("C5_1e8", 100), ("C5_1e8", 1000), ("C3", 10)])
+def test_selection_matches_torch_stable_sort(cfg, mu_bp):
+    """the GPU selection against torch.sort(stable) of the same Sigma's
+    order keys (larger key first, ties -> smaller row, NaN above +Inf) at full size,
+    independently of the oracle."""
+    from paper_2510_26709_b200 import ArcTopK
+    from paper_2510_26709_b200 import _lib as L
+    d, blocks = config_blocks(cfg, mu_bp)
+    src = GradientSource(d, blocks, 1, seed=31, device=DEV)
+    h, g, gbar = [torch.zeros(d, device=DEV)], [torch.zeros(d, device=DEV)], torch.zeros(d, device=DEV)
+    ctx = ArcTopK(d, blocks, N=1, eta=0.1, r=4, seed=31, debug_sketch=True)
+    for t in range(3):
+        sel = torch.empty(ctx.sum_K, dtype=torch.int32, device=DEV)
+        ctx.step(t, src.grads(t), h, g, gbar, sel)
+    sig = ctx.query(L.Q_SIGMA)
+    key = sig.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    key = torch.where(torch.isnan(sig), torch.full_like(key, 0xFFFFFFFF), key)
+    base = 0
+    for b in blocks:
+        if b.kind != 0:
+            continue
+        kb = key[base:base + b.m]
+        order = torch.sort(-kb, stable=True).indices           # stable: ties keep the smaller row first
+        want = torch.sort(order[:b.K]).values.to(torch.int32)
+        assert torch.equal(sel[sum(x.K for x in blocks[:blocks.index(b)]):][:b.K], want)
+        base += b.m
+    ctx.close()
