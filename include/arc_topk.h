@@ -20,7 +20,8 @@
  *
  * Conventions
  *   - Device pointers unless a name ends in _host.  All base pointers 16-byte
- *     aligned (torch's allocator gives 512); rows inside a block may be
+ *     aligned (torch's allocator gives 512; step returns ARC_ERR_INVALID_ARG
+ *     otherwise, before enqueueing anything); rows inside a block may be
  *     unaligned (n % 4 != 0) and are handled.
  *   - Every GPU call enqueues on `stream` (a cudaStream_t; NULL = legacy
  *     default stream) and returns without blocking the host, except create

@@ -636,15 +636,20 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     const Plan& pl = c->pl;
     const int L = pl.L;
     NodePtrs np{};
+    // base pointers must be 16-byte aligned (the kernels' vector accesses; the ABI)
+    auto misaligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) != 0; };
     for (int i = 0; i < L; ++i) {
-        if (grad[i] == nullptr) return ARC_ERR_INVALID_ARG;
+        if (grad[i] == nullptr || misaligned(grad[i])) return ARC_ERR_INVALID_ARG;
         np.grad[i] = grad[i];
         if (pl.noef) continue;   // without EF there is no (h, g) state: h, g may be NULL
         if (h == nullptr || g == nullptr || h[i] == nullptr || g[i] == nullptr) return ARC_ERR_INVALID_ARG;
+        if (misaligned(h[i]) || misaligned(g[i])) return ARC_ERR_INVALID_ARG;
         np.h[i] = h[i];
         np.g[i] = g[i];
     }
-    if (gbar == nullptr) return ARC_ERR_INVALID_ARG;
+    if (gbar == nullptr || misaligned(gbar)) return ARC_ERR_INVALID_ARG;
+    if ((sel_out != nullptr && (reinterpret_cast<uintptr_t>(sel_out) & 3u)) || (values_out != nullptr && misaligned(values_out)))
+        return ARC_ERR_INVALID_ARG;
     c->last = s;
     const BlockDev* blocks = c->at<BlockDev>(pl.o_blocks);
     float* V = c->at<float>(pl.o_V);

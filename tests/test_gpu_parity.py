@@ -445,3 +445,24 @@ def test_selection_matches_torch_stable_sort(cfg, mu_bp):
         assert torch.equal(sel[sum(x.K for x in blocks[:blocks.index(b)]):][:b.K], want)
         base += b.m
     ctx.close()
+
+
+def test_misaligned_pointers_rejected():
+    """T5: base pointers must be 16-byte aligned; a misaligned one is rejected before
+    anything is enqueued (the state stays untouched)."""
+    from paper_2510_26709_b200 import ArcTopK
+    d, blocks = 4_000, flat_blocks(4_000, 40, K=3)
+    ctx = ArcTopK(d, blocks, N=1, eta=0.1, r=4, seed=1)
+    big = torch.zeros(d + 4, device=DEV)
+    h, g, gbar = [torch.zeros(d, device=DEV)], [torch.zeros(d, device=DEV)], torch.zeros(d, device=DEV)
+    grad = [torch.ones(d, device=DEV)]
+    with pytest.raises(Exception):
+        ctx.step(0, [big[1:d + 1]], h, g, gbar)           # 4-byte aligned only
+    with pytest.raises(Exception):
+        ctx.step(0, grad, [big[2:d + 2]], g, gbar)
+    torch.cuda.synchronize()
+    assert not h[0].any() and not g[0].any() and not gbar.any()
+    ctx.step(0, grad, h, g, gbar)                        # aligned: fine
+    torch.cuda.synchronize()
+    assert h[0].any()
+    ctx.close()
