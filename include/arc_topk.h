@@ -3,15 +3,17 @@
  * on B200 (sm_100a).
  *
  * What one arc_topk_step computes (PAPER.md = arXiv 2510.26709 LaTeX, "P:n" =
- * line n; readings R1..R21 are in DESIGN.md §3):
+ * line n; readings R1..R22 are in DESIGN.md §3, the arithmetic is SURVEY.md
+ * §8(c)'s ARC-NUM v1):
  *   for every node i held by this GPU, every block b (an m_b x n_b row-major
  *   view of the flat vector, R1):
- *     h_i   <- (1-eta) h_i + eta grad_i                      eq:ef21m-1, P:325 (R11)
+ *     h_i   <- fma(eta, grad_i, (1-eta) h_i)                 eq:ef21m-1, P:325 (R11)
  *     Delta_i = h_i - g_i                                     R4
  *     V_b   ~ N(0, I), n_b x r, from (seed, t, b)             P:229-230, Alg.1 l.3 (R7, R8)
- *     P_i   = (1/sqrt r) G_i V_b                              P:231-233, Alg.1 l.4 (R2)
- *     P     = (1/N) sum_i P_i        (exchange #1)            P:232, Alg.1 l.5 (R3, R9, R21)
- *     Sigma = diag(P P^T); I_b = argtop_{K_b}(Sigma)          zn28373 P:236-237, Alg.1 l.6 (R5, R15)
+ *     P'_i  = G_i V_b  (the O6 lane/chunk order, fma)         P:231-233, Alg.1 l.4 (R2, R9)
+ *     S     = sum_i P'_i   (exchange #1, node order)          P:232, Alg.1 l.5 (R3, R9, R21)
+ *     Sigma = diag(S S^T); I_b = argtop_{K_b}(Sigma)          zn28373 P:236-237, Alg.1 l.6 (R5, R15)
+ *     (the paper's 1/sqrt(r) and 1/N scale every Sigma alike: not applied, R2/R3)
  *     C_i   = [Delta_i]_{I_b,:}                               2zn20 P:241-243, Alg.1 l.7
  *     g_i[I_b] <- g_i[I_b] + C_i                              eq:ef21m-2, P:326 (R12)
  *     C     = (1/N) sum_i C_i        (exchange #2)            P:242, P:278 (index-free All-Reduce)
