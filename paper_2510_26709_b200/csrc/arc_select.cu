@@ -4,22 +4,26 @@
 //
 // S3  I_b = argtop_{K_b}(Sigma_b)  (zn28373 P:236-237; ties -> smaller row,
 //     R5; NaN above +Inf, R15): an MSB-first radix select on the 32-bit order
-//     keys with digits key[31:21] | key[20:10] | key[9:0].  Every CTA owns a
-//     slice of `slice_rows` consecutive rows of one block and keeps its keys in
-//     shared memory; the per-digit histograms of a block are summed in global
-//     memory with one atomic per nonzero bin per slice, and a grid-wide barrier
-//     separates the digits.  Digit 1 was histogrammed by the pass that produced
-//     Sigma, so the kernel needs three barriers.  Every slice derives the same
-//     threshold key T and tie quota need_eq; the selected rows of a slice are
-//     key > T, or key == T among the first need_eq rows with key == T in row
-//     order (per-slice counts give the running offsets).  No step is serial in
-//     the number of tied keys.
-// S4  each slice then writes its selected rows in ascending order at its
-//     prefix offset and applies, for every selected row k (row p) and node i,
+//     keys, digits key[31:21] | key[20:10] | key[9:0].  Every CTA owns a slice
+//     of consecutive rows of one block and keeps its keys in shared memory.
+//     Digit 1 was histogrammed by the pass that produced Sigma (phase 0 here
+//     when Sigma came from the exchange or several local nodes), so each slice
+//     knows the boundary bin b1 at once: it counts its keys above b1 and appends
+//     its keys in b1 (the candidates) to a per-block list.  After ONE grid
+//     barrier every CTA resolves the K-th key T and the tie cutoff P_eq from the
+//     candidate list in shared memory (digit 2, then a rank count); a block
+//     whose boundary bin overflows the list takes the digit-by-digit path
+//     (digits 2 and 3 through global histograms, two more barriers).  Nothing
+//     is serial in the number of tied keys.
+// S4  each slice writes its selected rows in ascending order at its prefix
+//     offset and applies, for every selected row k (row p) and node i,
 //       C_i = h_i - g_i ; g_i <- g_i + C_i                      eq:ef21m-2 (R12)
 //     and, when every node is on this GPU (mode 0),
 //       A = C_0 + C_1 + ... ; val = A / N ; gbar <- gbar + val  P:242, R3, R13
-//     or writes the exchange payload (modes 1, 2).
+//     or writes the exchange payload (modes 1, 2; mode 3: the Top-K baseline).
+//     Early mode (mode 0, no values requested): the rows above b1 are updated
+//     between the arrive and the wait of barrier 1, the selected boundary rows
+//     after the resolution — no second barrier.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
