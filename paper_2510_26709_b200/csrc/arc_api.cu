@@ -5,6 +5,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -495,8 +496,19 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     std::vector<Tile> tiles;
     std::vector<int> cta_begin, cta_begin_w;
     {   // streaming-pass variant: 0 = 4 row segments per batch (>= 3 CTAs/SM),
-        // 1 = 2 segments per batch at 4 CTAs/SM (ARC_SKETCH_SHAPE, experiments)
-        c->shape = 0;
+        // 1 = 2 segments per batch at 4 CTAs/SM, 2 = 4 segments at 2 CTAs/SM
+        // (ARC_SKETCH_SHAPE, experiments).  A row of n columns is ceil(n/128)
+        // segments; the batch size that leaves fewer padded slots (weighted by
+        // the blocks' bytes) wins: 3 for n = 768 (C3), 4 for n = 512, 1024,
+        // 2048 (C2 -6 %, C5 -3 %, LLaMA layout -1 %, measured).
+        double waste3 = 0.0, waste4 = 0.0;
+        for (const BlockDev& B : c->pl.bdev) {
+            if (B.kind != ARC_BLOCK_ARC) continue;
+            const double nseg = static_cast<double>((B.n + 127) / 128);
+            waste3 += static_cast<double>(B.len) * (1.0 - nseg / (std::ceil(nseg / 3.0) * 3.0));
+            waste4 += static_cast<double>(B.len) * (1.0 - nseg / (std::ceil(nseg / 4.0) * 4.0));
+        }
+        c->shape = waste4 <= waste3 ? 2 : 0;
         if (const char* e = getenv("ARC_SKETCH_SHAPE")) {
             const int v = atoi(e);
             if (sketch_shape_ok(v, c->p.r)) c->shape = v;
