@@ -397,7 +397,8 @@ int occupancy_reg(int vs_cap) {
 }
 
 // variant (a.shape): UN segments per batch / CTAs per SM: 0 = 3 / 3, 1 = 2 / 4,
-// 2 = 4 / 2, 3 = 1 / 5 (r <= 8; wider sketches get fewer CTAs)
+// 2 = 4 / 2, 3 = 6 / 2 (r <= 8; wider sketches get fewer CTAs).  0 and 2 are chosen per
+// layout (arc_api.cu); 1 and 3 measured no better (C3: 3 / 3 325.7 us, 6 / 2 326.3 us)
 template <int RJ>
 void launch_rj(const SketchLaunch& a, cudaStream_t s) {
     if (a.ranged) {   // the wide blocks' launch (one variant)
@@ -412,7 +413,7 @@ void launch_rj(const SketchLaunch& a, cudaStream_t s) {
     switch (a.shape) {
         case 1: launch_reg<RJ, 2, (RJ <= 8 ? 4 : 2)>(a, s); break;
         case 2: launch_reg<RJ, 4, 2>(a, s); break;
-        case 3: launch_reg<RJ, 1, (RJ <= 8 ? 5 : 3)>(a, s); break;
+        case 3: launch_reg<RJ, (RJ <= 8 ? 6 : 2), 2>(a, s); break;
         default: launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2)>(a, s); break;
     }
 }
@@ -421,7 +422,7 @@ int occupancy_rj(int shape, int vs_cap) {
     switch (shape) {
         case 1: return occupancy_reg<RJ, 2, (RJ <= 8 ? 4 : 2)>(vs_cap);
         case 2: return occupancy_reg<RJ, 4, 2>(vs_cap);
-        case 3: return occupancy_reg<RJ, 1, (RJ <= 8 ? 5 : 3)>(vs_cap);
+        case 3: return occupancy_reg<RJ, (RJ <= 8 ? 6 : 2), 2>(vs_cap);
         default: return occupancy_reg<RJ, 3, (RJ <= 8 ? 3 : 2)>(vs_cap);
     }
 }
