@@ -299,7 +299,7 @@ void plan_tiles(const Plan& pl, const std::vector<char>& use, int resident, int 
         for (size_t b = 0; b < pl.bdev.size(); ++b) {
             const BlockDev& B = pl.bdev[b];
             if (B.kind != ARC_BLOCK_ARC || !use[b]) continue;
-            const int Rb = std::min(R, B.m);
+            const int Rb = std::min(B.n <= 4 ? 256 : R, B.m);   // (rows of <= 4 columns: one per thread)
             const int nt = (B.m + Rb - 1) / Rb;
             const int64_t nch = (B.n + W - 1) / W;
             for (int l = 0; l < nodes; ++l)
@@ -516,7 +516,8 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     }
     {
         // blocks whose V_b^T fits the shared-memory stage stream in one launch; the
-        // wider ones (methods with a sketch) in a second, ranged launch
+        // wider ones (methods with a sketch) and blocks of rows of <= 4 columns (one
+        // row per thread) in a second launch, so the main kernel carries neither path
         const bool sketches = !c->pl.topk && !c->pl.randk;
         std::vector<char> narrow(c->pl.bdev.size(), 1), wide(c->pl.bdev.size(), 0);
         c->vs_cap = 0;
@@ -525,7 +526,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
             const BlockDev& B = c->pl.bdev[b];
             if (B.kind != ARC_BLOCK_ARC) continue;
             const int cap = sketch_vs_cap(c->p.r, B.n);
-            if (cap == 0 && sketches && sketch_ranged_cap(c->p.r) > 0) {
+            if (((cap == 0 && sketches) || B.n <= 4) && sketch_ranged_cap(c->p.r) > 0) {
                 narrow[b] = 0;
                 wide[b] = 1;
                 any_wide = true;

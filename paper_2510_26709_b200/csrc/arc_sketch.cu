@@ -240,6 +240,76 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         const bool V_vec = true;   // V_b^T rows start 16-byte aligned (padded to ldv = round_up(n, 4))
 
         if constexpr (RANGED) {
+          if (T_n <= 4) {
+            // rows of at most 4 columns (e.g. n = 1): one row per THREAD (tiles of up
+            // to 256 rows).  In O6 terms only lane 0 holds data, so the butterfly
+            // yields a_0 (+) (+0): the lane's own fma chain with -0 turned into +0.
+            const int rr = tid;
+            if (rr < T_rows) {
+                const int p = T_row0 + rr;
+                const int nv = row_cols(T_len, T_n, p);
+                const long long base = T_off + static_cast<long long>(p) * T_n;
+                const int ldv = (T_n + 3) & ~3;   // (V_b^T read from global: r x 4 floats)
+                float P[RJ];
+#pragma unroll
+                for (int j = 0; j < RJ; ++j) P[j] = 0.0f;
+                for (int e = 0; e < nv; ++e) {
+                    const long long x = base + e;
+                    const float gv = __ldcs(pg + x);
+                    float dl;
+                    if (NOEF) {
+                        if (ph != nullptr) ph[x] = fmul(eta, ph[x]);          // u <- beta u (node 0)
+                        dl = gv;
+                    } else {
+                        const float hn = ffma(eta, gv, fmul(ome, __ldcs(ph + x)));   // O2, R11
+                        __stcs(ph + x, hn);
+                        dl = fsub(hn, __ldcs(pgg + x));                       // O3, R4
+                    }
+                    if (sketch) {
+#pragma unroll
+                        for (int j = 0; j < RJ; ++j)
+                            if (j < r) P[j] = ffma(dl, Vb[static_cast<long long>(j) * ldv + e], P[j]);   // O6 lane 0
+                    } else if (mode == 2) {
+                        P[0] = ffma(dl, dl, P[0]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < RJ; ++j) P[j] = fadd(P[j], 0.0f);    // the butterfly with idle lanes
+                if (mode == 3) {
+                    if (node == 0) {
+                        const uint4 x = rng::philox4x32_10(
+                            make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(T_b) | 0x80000000u, a.t_lo, a.t_hi),
+                            a.key);
+                        const float sig = __uint_as_float(x.x >> 2);
+                        a.sigma[T_row_base + p] = sig;
+                        atomicAdd(&s_hist[order_key_dev(sig) >> kHist1Shift], 1u);
+                    }
+                } else if (mode == 2) {
+                    const float sig = P[0];
+                    a.sigma[static_cast<long long>(node) * a.M + T_row_base + p] = sig;
+                    atomicAdd(&s_hist[order_key_dev(sig) >> kHist1Shift], 1u);
+                    if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
+                } else {
+                    if (a.pnodes != nullptr)
+                        for (int j = 0; j < r; ++j) {
+                            float v = P[0];
+#pragma unroll
+                            for (int jj = 1; jj < RJ; ++jj)
+                                if (jj == j) v = P[jj];
+                            a.pnodes[(static_cast<long long>(T_row_base + p) * a.nodes_local + node) * r + j] = v;
+                        }
+                    if (mode == 0) {
+                        float sig = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < RJ; ++j)
+                            if (j < r) sig = ffma(P[j], P[j], sig);                   // O8
+                        a.sigma[T_row_base + p] = sig;
+                        atomicAdd(&s_hist[order_key_dev(sig) >> kHist1Shift], 1u);
+                        if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
+                    }
+                }
+            }
+          } else {
             const int ldv = (T_n + 3) & ~3;
             const int range_w = (a.vs_cap / r) / 1024 * 1024;
             for (int c0 = 0; c0 < T_n; c0 += range_w) {
@@ -312,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
                     row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
                 }
             }
+          }
         } else {
         for (int rr = warp; rr < T_rows; rr += kWarps) {
             const int p = T_row0 + rr;

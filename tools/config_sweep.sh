@@ -5,6 +5,7 @@ out=${1:-gpurun_out/sweep}
 mkdir -p $(dirname $out)
 run() { timeout 600 python bench.py --steps ${STEPS:-100} --warmup 10 --e2e-steps 2 --no-cpu-baseline --no-baselines "$@" 2>&1 | grep '^{' ; }
 {
+run --config C1 --nodes-per-gpu 4 --pool 2
 run --config C2 --nodes-per-gpu 8 --pool 2
 run --config C2 --nodes-per-gpu 1
 run --config C3
