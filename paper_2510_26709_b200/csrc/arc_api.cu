@@ -177,7 +177,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.sumK = sumK;
     pl.sumKn = sumKn;
     pl.sum_nr = sum_nr;
-    pl.max_tiles = std::max(max_tiles, 1);
+    pl.max_tiles = max_tiles + 2 * kMaxGrid;   // (+ plan_tiles' balancing of a single block, per launch)
     // selection blocks: one per (local node, block) for the Top-K baseline, whose
     // nodes rank their own rows; the node's payload is [values | indices]
     pl.topk = p->method == ARC_METHOD_TOPK_ALLGATHER;
@@ -269,7 +269,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
 // rows is charged nchunks * max(r, 0.6 R_shape); tiles go longest-first to the
 // least-loaded CTA (LPT).
 void plan_tiles(const Plan& pl, const std::vector<char>& use, int resident, int tile_rows_max, int W,
-                std::vector<Tile>& tiles, std::vector<int>& cta_begin, int& grid) {
+                std::vector<Tile>& tiles, std::vector<int>& cta_begin, int& grid, int tiny_rows = 0) {
     struct Cand { int64_t makespan = INT64_MAX; std::vector<Tile> tiles; std::vector<int> begin; int grid = 0; };
     Cand best;
     resident = std::max(1, std::min(resident, kMaxGrid));
@@ -284,7 +284,8 @@ void plan_tiles(const Plan& pl, const std::vector<char>& use, int resident, int 
         int64_t tiles8 = 0;
         for (size_t b = 0; b < pl.bdev.size(); ++b)
             if (pl.bdev[b].kind == ARC_BLOCK_ARC && use[b]) { ++arc_blocks; tiles8 += (pl.bdev[b].m + 7) / 8 * nodes; }
-        if (arc_blocks <= 8 && tiles8 <= static_cast<int64_t>(resident) * 96) tile_rows_max = std::min(tile_rows_max, 8);
+        if (tiny_rows == 0 && arc_blocks <= 8 && tiles8 <= static_cast<int64_t>(resident) * 96)
+            tile_rows_max = std::min(tile_rows_max, 8);
     }
     const int64_t floor_rows = (tile_rows_max * 6 + 9) / 10;
     const int R_pick = tile_rows_max;
@@ -293,14 +294,24 @@ void plan_tiles(const Plan& pl, const std::vector<char>& use, int resident, int 
         const int v = atoi(e);
         if (v >= 1 && v <= 32) R_lo = R_hi = v;
     }
+    int used_blocks = 0;
+    for (size_t b = 0; b < pl.bdev.size(); ++b) used_blocks += pl.bdev[b].kind == ARC_BLOCK_ARC && use[b];
+    // variant 1 (one block in the second launch): raise the tile count to a multiple of the resident
+    // CTAs, so every CTA streams the same number of rows (e.g. m = 18,315 rows
+    // of 8 over 444 CTAs is 5.16 tiles per CTA: the last wave would be 16 % idle)
+    for (int variant = 0; variant < (used_blocks == 1 && tiny_rows > 0 ? 2 : 1); ++variant)
     for (int R = R_hi; R >= R_lo; --R) {
         std::vector<Tile> ts;
         std::vector<int64_t> cost;
         for (size_t b = 0; b < pl.bdev.size(); ++b) {
             const BlockDev& B = pl.bdev[b];
             if (B.kind != ARC_BLOCK_ARC || !use[b]) continue;
-            const int Rb = std::min(B.n <= 4 ? 256 : R, B.m);   // (rows of <= 4 columns: one per thread)
-            const int nt = (B.m + Rb - 1) / Rb;
+            const int Rb = std::min(B.n <= 4 && tiny_rows > 0 ? tiny_rows : R, B.m);   // (<= 4 columns: a row per thread)
+            int nt = (B.m + Rb - 1) / Rb;
+            if (variant == 1) {
+                const int64_t want = (static_cast<int64_t>(nt) * nodes + resident - 1) / resident * resident;
+                nt = static_cast<int>(std::min<int64_t>(B.m, (want + nodes - 1) / nodes));
+            }
             const int64_t nch = (B.n + W - 1) / W;
             for (int l = 0; l < nodes; ++l)
                 for (int i = 0; i < nt; ++i) {   // rows spread evenly over the block's tiles
@@ -538,11 +549,19 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
                    sketch_tile_cols(c->shape), tiles, cta_begin, c->grid);
         c->grid_w = 0;
         if (any_wide) {
-            c->vs_cap_w = sketch_ranged_cap(c->p.r);
+            // shared memory: the widest fully staged V_b^T, or the range stage
+            // (rows of <= 4 columns read V from global memory)
+            const int cap_w = sketch_ranged_cap(c->p.r);
+            c->vs_cap_w = 0;
+            for (size_t b = 0; b < c->pl.bdev.size(); ++b) {
+                const BlockDev& B = c->pl.bdev[b];
+                if (wide[b] && B.n > 4)
+                    c->vs_cap_w = std::max<int>(c->vs_cap_w, std::min<int64_t>(cap_w, c->p.r * ((B.n + 3) / 4 * 4)));
+            }
             std::vector<Tile> tw;
             std::vector<int> cbw;
             plan_tiles(c->pl, wide, ef_sketch_resident_ctas_ranged(c->p.r, c->vs_cap_w), 32, sketch_tile_cols(c->shape),
-                       tw, cbw, c->grid_w);
+                       tw, cbw, c->grid_w, sketch_wide_threads(c->p.r));
             c->tiles_w0 = static_cast<int>(tiles.size());
             for (int& x : cbw) x += c->tiles_w0;
             tiles.insert(tiles.end(), tw.begin(), tw.end());

@@ -151,6 +151,7 @@ int ef_sketch_resident_ctas(int r, int shape, int vs_cap);   // SMs x occupancy
 int sketch_vs_cap(int r, int max_n);   // floats of V_b^T the streaming pass stages in shared memory (0: too wide)
 int sketch_ranged_cap(int r);          // floats staged per range by the wide blocks' launch
 int ef_sketch_resident_ctas_ranged(int r, int vs_cap);
+int sketch_wide_threads(int r);        // threads per CTA of that launch (tiles of <= 4-column rows: one row per thread)
 int sketch_tile_rows(int shape);
 int sketch_tile_cols(int shape);
 int sketch_shape_ok(int shape, int r);

@@ -37,7 +37,6 @@ namespace {
 using namespace dev;
 
 constexpr int kThreads = kSketchThreads;   // 256 = 8 warps
-constexpr int kWarps = kThreads / 32;
 constexpr int kTileCache = 128;            // tile descriptors cached in shared memory
 
 // valid columns of row p of a block (the last row of a padded flat block is short, R14)
@@ -57,6 +56,13 @@ __device__ __forceinline__ float butterfly(float a) {
 // fits (a.vs_cap floats), so the lane chains read it with conflict-free 16-byte
 // loads next to the streaming traffic instead of through L1/L2.
 constexpr int kVsMax = 12288;              // floats of V_b^T staged at most (48 KB)
+// The second launch (RANGED instantiation: blocks whose V_b^T exceeds kVsMax,
+// and blocks of rows of <= 4 columns) runs one CTA per SM with the warps of
+// two main-kernel CTAs, so the whole of V_b^T up to 196 KB is staged once per
+// block; only wider V is staged in ranges.
+constexpr int kVsBig = 50176;
+__host__ __device__ constexpr int wide_threads(int rj) { return rj <= 16 ? 512 : 256; }
+__host__ __device__ constexpr int wide_un(int rj) { return rj <= 8 ? 4 : 3; }
 
 // One segment (columns q..q+3 of lane l) of one row: momentum, residual, the
 // h' store and the lane's O6 fma chains; at the end of a 1024-column chunk the
@@ -173,7 +179,8 @@ __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int r
 // staged in ranges of whole 1024-column chunks and every row carries its P'
 // across ranges in shared memory (the O6 order is unchanged)
 template <int RJ, int UN, int MINB, bool NOEF, bool RANGED>
-__global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch a) {
+__global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_ef_sketch(const SketchLaunch a) {
+    constexpr int NT = RANGED ? wide_threads(RJ) : kThreads, NW = NT / 32;
     __shared__ TileDesc s_tile[kTileCache];
     __shared__ unsigned s_hist[kHist1Bins];     // digit-1 histogram of this CTA's Sigma (modes 0, 3)
     __shared__ float s_P[RANGED ? 32 : 1][RJ];  // (RANGED) the tile rows' running P' between ranges
@@ -184,9 +191,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
     const int list_begin = a.cta_begin[blockIdx.x], list_end = a.cta_begin[blockIdx.x + 1];
     if (list_begin >= list_end) return;
     const int ntile = list_end - list_begin;
-    for (int i = tid; i < min(ntile, kTileCache) * 4; i += kThreads)
+    for (int i = tid; i < min(ntile, kTileCache) * 4; i += NT)
         reinterpret_cast<uint4*>(s_tile)[i] = __ldg(reinterpret_cast<const uint4*>(a.tiles + list_begin) + i);
-    for (int i = tid; i < kHist1Bins; i += kThreads) s_hist[i] = 0;
+    for (int i = tid; i < kHist1Bins; i += NT) s_hist[i] = 0;
     __syncthreads();
     grid_dependency_wait();   // the previous kernel (g, V, histogram reset) is complete
 
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
     const bool cta_hist = true;                 // every mode histograms its keys in shared memory first
     auto flush_hist = [&](int b) {
         unsigned* gh = a.hist1 + static_cast<long long>(b) * kHist1Bins;
-        for (int i = tid; i < kHist1Bins; i += kThreads) {
+        for (int i = tid; i < kHist1Bins; i += NT) {
             const unsigned v = s_hist[i];
             if (v) { atomicAdd(gh + i, v); s_hist[i] = 0; }
         }
@@ -206,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         return li - list_begin < kTileCache ? &s_tile[li - list_begin] : a.tiles + li;
     };
 
+    int carry = warp;                           // (RANGED) this warp's first row of the next tile
     int cur_b = -1;                             // histogram slot of the current tile: block (mode 2: node, block)
     bool v_smem = false;
     for (int li = list_begin; li < list_end; ++li) {
@@ -219,14 +227,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
             __syncthreads();
             if (cta_hist && cur_b >= 0) flush_hist(cur_b);
             const int nvf = r * ((T_n + 3) & ~3);
-            v_smem = !RANGED && sketch && nvf <= a.vs_cap;
+            v_smem = sketch && nvf <= a.vs_cap;
             if (v_smem) {
                 const float* __restrict__ src = a.V + T_voff;
                 if ((T_voff & 3) == 0 && (nvf & 3) == 0) {
-                    for (int i = tid; i < (nvf >> 2); i += kThreads)
+                    for (int i = tid; i < (nvf >> 2); i += NT)
                         reinterpret_cast<float4*>(Vs)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
                 } else {
-                    for (int i = tid; i < nvf; i += kThreads) Vs[i] = __ldg(src + i);
+                    for (int i = tid; i < nvf; i += NT) Vs[i] = __ldg(src + i);
                 }
             }
             __syncthreads();
@@ -239,7 +247,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
         const float* Vb = v_smem ? Vs : a.V + T_voff;
         const bool V_vec = true;   // V_b^T rows start 16-byte aligned (padded to ldv = round_up(n, 4))
 
+        bool streamed = false;                  // (RANGED) tile done by the per-thread or ranged path
         if constexpr (RANGED) {
+          streamed = T_n <= 4 || !v_smem;
           if (T_n <= 4) {
             // rows of at most 4 columns (e.g. n = 1): one row per THREAD (tiles of up
             // to 256 rows).  In O6 terms only lane 0 holds data, so the butterfly
@@ -309,19 +319,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
                     }
                 }
             }
-          } else {
+          } else if (!v_smem) {
             const int ldv = (T_n + 3) & ~3;
             const int range_w = (a.vs_cap / r) / 1024 * 1024;
             for (int c0 = 0; c0 < T_n; c0 += range_w) {
                 __syncthreads();                         // stage V_b^T[:, c0 : c0 + range_w)
                 const int w = min(range_w, ldv - c0);
-                for (int i = tid; i < r * (w >> 2); i += kThreads) {
+                for (int i = tid; i < r * (w >> 2); i += NT) {
                     const int j = i / (w >> 2), f = i - j * (w >> 2);
                     reinterpret_cast<float4*>(Vs + j * range_w)[f] =
                         __ldg(reinterpret_cast<const float4*>(a.V + T_voff + static_cast<long long>(j) * ldv + c0) + f);
                 }
                 __syncthreads();
-                for (int rr = warp; rr < T_rows; rr += kWarps) {
+                for (int rr = warp; rr < T_rows; rr += NW) {
                     const int p = T_row0 + rr;
                     const int nv = row_cols(T_len, T_n, p);
                     const long long base = T_off + static_cast<long long>(p) * T_n;
@@ -383,8 +393,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
                 }
             }
           }
-        } else {
-        for (int rr = warp; rr < T_rows; rr += kWarps) {
+        }
+        if (!streamed) {
+        // (RANGED: the CTA's warps take its rows round-robin across tiles, so a
+        // tile height that is not a multiple of the warp count idles no warp)
+        int rr = RANGED ? carry : warp;
+        for (; rr < T_rows; rr += NW) {
             const int p = T_row0 + rr;
             const int nv = row_cols(T_len, T_n, p);
             const long long base = T_off + static_cast<long long>(p) * T_n;
@@ -430,6 +444,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_ef_sketch(const SketchLaunch
             }
             row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
         }
+        if constexpr (RANGED) carry = rr - T_rows;
         }
     }
     if (cta_hist) {
@@ -442,13 +457,13 @@ template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false>
 void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(a.grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(RANGED ? wide_threads(RJ) : kThreads);
     cfg.dynamicSmemBytes = sizeof(float) * a.vs_cap;
     cfg.stream = s;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sizeof(float) * kVsMax));
+                             static_cast<int>(sizeof(float) * (RANGED ? kVsBig : kVsMax)));
         attr_set = true;
     }
     cudaLaunchAttribute attr[1];
@@ -461,9 +476,10 @@ void launch_reg(const SketchLaunch& a, cudaStream_t s) {
 template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false>
 int occupancy_reg(int vs_cap) {
     cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(float) * kVsMax));
+                         static_cast<int>(sizeof(float) * (RANGED ? kVsBig : kVsMax)));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, kThreads, sizeof(float) * vs_cap);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>,
+                                                  RANGED ? wide_threads(RJ) : kThreads, sizeof(float) * vs_cap);
     return per_sm;
 }
 
@@ -473,8 +489,8 @@ int occupancy_reg(int vs_cap) {
 template <int RJ>
 void launch_rj(const SketchLaunch& a, cudaStream_t s) {
     if (a.ranged) {   // the wide blocks' launch (one variant)
-        if (a.noef) launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2), true, true>(a, s);
-        else launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2), false, true>(a, s);
+        if (a.noef) launch_reg<RJ, wide_un(RJ), 1, true, true>(a, s);
+        else launch_reg<RJ, wide_un(RJ), 1, false, true>(a, s);
         return;
     }
     if (a.noef) {   // (the without-EF baseline: one variant)
@@ -518,16 +534,17 @@ int sketch_vs_cap(int r, int max_n) {
     return static_cast<int>(need <= kVsMax ? need : 0) & ~3;   // 0: V read from global memory
 }
 
-int sketch_ranged_cap(int r) { return kVsMax / (1024 * r) * (1024 * r); }
+int sketch_ranged_cap(int r) { return kVsBig / (1024 * r) * (1024 * r); }
+int sketch_wide_threads(int r) { return wide_threads(r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 32); }
 
 int ef_sketch_resident_ctas_ranged(int r, int vs_cap) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int per_sm = r <= 4 ? occupancy_reg<4, 3, 3, false, true>(vs_cap)
-                       : r <= 8 ? occupancy_reg<8, 3, 3, false, true>(vs_cap)
-                       : r <= 16 ? occupancy_reg<16, 3, 2, false, true>(vs_cap)
-                                 : occupancy_reg<32, 3, 2, false, true>(vs_cap);
+    const int per_sm = r <= 4 ? occupancy_reg<4, wide_un(4), 1, false, true>(vs_cap)
+                       : r <= 8 ? occupancy_reg<8, wide_un(8), 1, false, true>(vs_cap)
+                       : r <= 16 ? occupancy_reg<16, wide_un(16), 1, false, true>(vs_cap)
+                                 : occupancy_reg<32, wide_un(32), 1, false, true>(vs_cap);
     return sms * (per_sm < 1 ? 1 : per_sm);
 }
 

@@ -364,6 +364,35 @@ def test_wide_blocks_ranged_launch(orc, r, exchange):
                reduce="ordered" if exchange else "nccl")
 
 
+@pytest.mark.parametrize("r", [4, 32])
+def test_wide_blocks_beyond_the_full_stage(orc, r):
+    """The second launch stages a wide block's whole V_b^T (up to 196 KB) once per
+    block; wider ones (r = 4: n > 12288; r = 32: n > 1024) still go in ranges,
+    next to fully staged wide blocks, narrow blocks and rows of <= 4 columns."""
+    shapes = [(5, 13001, 2), (7, 5000, 1), (40, 300, 4), (6, 1100, 2), (90, 2, 9)]
+    blocks, off = [], 0
+    for m, n, K in shapes:
+        blocks.append(Block(off, m * n, m, n, K, 0))
+        off += m * n
+    run_parity(orc, off, blocks, N=2, steps=3, r=r)
+
+
+@pytest.mark.parametrize("method", ["arc", "randk", "noef_msgd"])
+def test_rows_of_at_most_four_columns(orc, method):
+    """Blocks of rows with n <= 4 (biases, norms) run one row per thread in the
+    second launch (tiles of up to 512 rows); mixed with a normal block, several
+    nodes and a ragged last row."""
+    shapes = [(700, 1, 7), (301, 3, 5), (1000, 4, 9), (50, 200, 3)]
+    blocks, off = [], 0
+    for m, n, K in shapes:
+        blocks.append(Block(off, m * n, m, n, K, 0))
+        off += m * n
+    last = Block(off, 3 * 129 - 2, 129, 3, 4, 0)                 # ragged last row
+    blocks.append(last)
+    off += last.len
+    run_parity(orc, off, blocks, N=3, steps=3, method=method, eta=0.5 if method == "noef_msgd" else 0.1)
+
+
 # ------------------------------------------------------------------ without EF (Table II)
 
 @pytest.mark.parametrize("N,d,n,K,beta", [(1, 50_000, 100, 7, 0.9), (4, 60_000, 96, 12, 0.9), (3, 4_097, 3, 40, 0.0)])
