@@ -275,7 +275,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
     ap.add_argument("--nodes-per-gpu", type=int, default=1)
-    ap.add_argument("--reduce", default="nccl", choices=["nccl", "ordered"])
+    ap.add_argument("--reduce", default="nccl", choices=["nccl", "ordered", "lsa"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--pool", type=int, default=8, help="distinct gradient sets cycled in the timed loop")
@@ -303,8 +303,11 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or (args.force_exchange and args.reduce == "lsa"):
+        # (one GPU, lsa: a real 1-rank communicator owns the symmetric window)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         pg = dist.group.WORLD
     L = args.nodes_per_gpu
     d, blocks, N = workload(args.config, L, world, args.mu_bp)

@@ -66,7 +66,18 @@ typedef enum { ARC_BLOCK_ARC = 0, ARC_BLOCK_DENSE = 1 } arc_block_kind;
 
 typedef enum {
     ARC_REDUCE_NCCL = 0,     /* exchange #2 = ncclAllReduce(sum): gbar within tolerance (G > 1) */
-    ARC_REDUCE_ORDERED = 1   /* exchange #2 = all-gather + ascending node-id sum: bit-exact gbar */
+    ARC_REDUCE_ORDERED = 1,  /* exchange #2 = all-gather + ascending node-id sum: bit-exact gbar */
+    ARC_REDUCE_LSA = 2       /* exchange #2 fused with S6: each rank's per-node
+                                payload sits in an NCCL symmetric window (ncclMemAlloc +
+                                ncclCommWindowRegister, library-owned, made at create — a collective);
+                                one kernel per block kind meets the peers at an LSA barrier, reads
+                                every node's payload from its owner over NVLink (ncclGetLsaPointer),
+                                sums in ascending node id (bit-exact gbar, like ORDERED) and adds
+                                A/N into gbar.  Needs the exchange path (G > 1 or
+                                ARC_FLAG_FORCE_EXCHANGE with a comm), every rank in one LSA team
+                                (one NVLink domain, <= 72 ranks) and NCCL >= 2.28; otherwise create
+                                returns ARC_ERR_UNSUPPORTED (ARC_ERR_INVALID_ARG without a comm).
+                                Not for ARC_METHOD_TOPK_ALLGATHER (UNSUPPORTED). */
 } arc_reduce_mode;
 
 /* Compressor.  ARC_METHOD_TOPK_ALLGATHER is the baseline of Table I row "Top-K"

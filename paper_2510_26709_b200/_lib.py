@@ -21,7 +21,7 @@ OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_PARAM_MISMATCH, ERR_CUDA, ERR_NCCL, ER
 # arc_block_kind
 BLOCK_ARC, BLOCK_DENSE = 0, 1
 # arc_reduce_mode
-REDUCE_NCCL, REDUCE_ORDERED = 0, 1
+REDUCE_NCCL, REDUCE_ORDERED, REDUCE_LSA = 0, 1, 2
 # flags
 FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE = 0x1, 0x2, 0x4
 # arc_method

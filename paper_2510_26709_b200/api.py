@@ -114,7 +114,7 @@ class ArcTopK:
                 (L.FLAG_FORCE_EXCHANGE if force_exchange else 0)
         self.params = L.ArcParams(L.ABI_VERSION, self.N, self.nodes_local, int(rank), self.d, int(r),
                                   len(self.blocks), self._cblocks, float(eta),
-                                  {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED}[reduce],
+                                  {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED, "lsa": L.REDUCE_LSA}[reduce],
                                   int(seed) & (2**64 - 1), flags,
                                   {"arc": L.METHOD_ARC, "topk_allgather": L.METHOD_TOPK_ALLGATHER,
                                    "randk": L.METHOD_RANDK, "noef_msgd": L.METHOD_NOEF_MSGD}[method])

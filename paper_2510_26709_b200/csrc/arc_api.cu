@@ -16,6 +16,7 @@
 
 #include "arc_internal.cuh"
 #include "nccl.h"   // types only (torch wheel's NCCL 2.28); functions are resolved with dlsym
+#include "nccl_device.h"   // ncclDevComm / requirements types (ARC_REDUCE_LSA)
 
 using namespace arc;
 
@@ -38,6 +39,14 @@ struct Nccl {
     ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*groupStart)() = nullptr;
     ncclResult_t (*groupEnd)() = nullptr;
+    // symmetric windows + device communicator (ARC_REDUCE_LSA; NCCL >= 2.28)
+    ncclResult_t (*memAlloc)(void**, size_t) = nullptr;
+    ncclResult_t (*memFree)(void*) = nullptr;
+    ncclResult_t (*winRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+    ncclResult_t (*winDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+    ncclResult_t (*devCommCreate)(ncclComm_t, const ncclDevCommRequirements_t*, ncclDevComm_t*) = nullptr;
+    ncclResult_t (*devCommDestroy)(ncclComm_t, const ncclDevComm_t*) = nullptr;
+    ncclTeam_t (*teamLsa)(ncclComm_t) = nullptr;
     bool ok = false;
 };
 
@@ -54,6 +63,13 @@ bool load_nccl(Nccl& n) {
     n.recv = reinterpret_cast<decltype(n.recv)>(dlsym(h, "ncclRecv"));
     n.groupStart = reinterpret_cast<decltype(n.groupStart)>(dlsym(h, "ncclGroupStart"));
     n.groupEnd = reinterpret_cast<decltype(n.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+    n.memAlloc = reinterpret_cast<decltype(n.memAlloc)>(dlsym(h, "ncclMemAlloc"));
+    n.memFree = reinterpret_cast<decltype(n.memFree)>(dlsym(h, "ncclMemFree"));
+    n.winRegister = reinterpret_cast<decltype(n.winRegister)>(dlsym(h, "ncclCommWindowRegister"));
+    n.winDeregister = reinterpret_cast<decltype(n.winDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
+    n.devCommCreate = reinterpret_cast<decltype(n.devCommCreate)>(dlsym(h, "ncclDevCommCreate"));
+    n.devCommDestroy = reinterpret_cast<decltype(n.devCommDestroy)>(dlsym(h, "ncclDevCommDestroy"));
+    n.teamLsa = reinterpret_cast<decltype(n.teamLsa)>(dlsym(h, "ncclTeamLsa"));
     n.ok = n.allGather && n.allReduce && n.commCount && n.commUserRank && n.commGetAsyncError && n.send && n.recv &&
            n.groupStart && n.groupEnd;
     return n.ok;
@@ -103,7 +119,8 @@ arc_status validate(const arc_topk_params* p) {
     // eta: the EF21M momentum, 0 < eta <= 1; without EF it is the heavy-ball beta, 0 <= beta < 1
     if (p->method == ARC_METHOD_NOEF_MSGD ? !(p->eta >= 0.0f && p->eta < 1.0f) : !(p->eta > 0.0f && p->eta <= 1.0f))
         return ARC_ERR_INVALID_ARG;
-    if (p->value_reduce != ARC_REDUCE_NCCL && p->value_reduce != ARC_REDUCE_ORDERED) return ARC_ERR_INVALID_ARG;
+    if (p->value_reduce != ARC_REDUCE_NCCL && p->value_reduce != ARC_REDUCE_ORDERED && p->value_reduce != ARC_REDUCE_LSA)
+        return ARC_ERR_INVALID_ARG;
     if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
     if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE)) return ARC_ERR_INVALID_ARG;
     if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER && p->method != ARC_METHOD_RANDK &&
@@ -249,8 +266,11 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         pl.o_wire_all = pl.G > 1 ? take(sizeof(float) * pl.W * pl.L * pl.G) : 0;
     } else if (pl.exchange) {
         pl.o_xrecv = pl.randk ? 0 : take(sizeof(float) * static_cast<size_t>(pl.Ms) * pl.L * p->r * pl.G);
+        // ORDERED and LSA carry per-node payloads; LSA's live in the library's
+        // symmetric window instead of the workspace
         const bool ordered = p->value_reduce == ARC_REDUCE_ORDERED;
-        pl.o_wire = take(sizeof(float) * sumKn * (ordered ? pl.L : 1));
+        const bool lsa = p->value_reduce == ARC_REDUCE_LSA;
+        pl.o_wire = lsa ? 0 : take(sizeof(float) * sumKn * (ordered ? pl.L : 1));
         pl.o_wire_all = ordered ? take(sizeof(float) * sumKn * pl.L * pl.G) : 0;
     }
     if (p->flags & ARC_FLAG_HOST_STAGING) {
@@ -404,6 +424,13 @@ struct arc_topk_ctx {
     bool early = true;           // early gather of the certain rows in the select kernel (ARC_EARLY=0: off)
     int64_t last_t = 0;
     int64_t v_items = 0;
+    // ARC_REDUCE_LSA: library-owned symmetric window and device communicator
+    bool lsa = false;
+    void* win_buf = nullptr;
+    ncclWindow_t win = nullptr;
+    bool dev_comm_ok = false;
+    ncclDevComm dev_comm{};
+    ncclDevComm* dev_comm_d = nullptr;
 
     template <class T> T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
 };
@@ -419,6 +446,48 @@ struct arc_topk_ctx {
             return ARC_ERR_CUDA;                                     \
         }                                                            \
     } while (0)
+
+// ARC_REDUCE_LSA (collective: every rank calls it at create, after the params
+// check).  The payload window [L][sum_Kn] floats comes from ncclMemAlloc and is
+// registered as a symmetric window; the device communicator carries one LSA
+// barrier per CTA of the fused scatter kernels (arc_lsa.cu).
+static void lsa_release(arc_topk_ctx* c) {
+    if (c->dev_comm_ok && c->nccl.devCommDestroy) c->nccl.devCommDestroy(c->comm, &c->dev_comm);
+    if (c->win && c->nccl.winDeregister) c->nccl.winDeregister(c->comm, c->win);
+    if (c->win_buf && c->nccl.memFree) c->nccl.memFree(c->win_buf);
+    if (c->dev_comm_d) cudaFree(c->dev_comm_d);
+    c->dev_comm_ok = false;
+    c->win = nullptr;
+    c->win_buf = nullptr;
+    c->dev_comm_d = nullptr;
+    c->lsa = false;
+}
+
+static arc_status lsa_setup(arc_topk_ctx* c, cudaStream_t s) {
+    const Plan& pl = c->pl;
+    if (pl.topk || c->comm == nullptr) return pl.topk ? ARC_ERR_UNSUPPORTED : ARC_ERR_INVALID_ARG;
+    Nccl& n = c->nccl;
+    if (!n.memAlloc || !n.memFree || !n.winRegister || !n.winDeregister || !n.devCommCreate || !n.devCommDestroy ||
+        !n.teamLsa)
+        return ARC_ERR_UNSUPPORTED;   // NCCL older than 2.28
+    const ncclTeam_t team = n.teamLsa(c->comm);
+    if (team.nRanks != pl.G || pl.G > 72) return ARC_ERR_UNSUPPORTED;   // every rank in one NVLink domain
+    if (cudaStreamSynchronize(s) != cudaSuccess) return ARC_ERR_CUDA;
+    size_t bytes = sizeof(float) * static_cast<size_t>(std::max<int64_t>(pl.sumKn, 1)) * pl.L;
+    bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    if (n.memAlloc(&c->win_buf, bytes) != ncclSuccess) return ARC_ERR_NCCL;
+    if (n.winRegister(c->comm, c->win_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) return ARC_ERR_NCCL;
+    ncclDevCommRequirements_t reqs;
+    std::memset(&reqs, 0, sizeof(reqs));
+    reqs.lsaBarrierCount = arc::kLsaCtas;
+    if (n.devCommCreate(c->comm, &reqs, &c->dev_comm) != ncclSuccess) return ARC_ERR_NCCL;
+    c->dev_comm_ok = true;
+    if (cudaMalloc(&c->dev_comm_d, sizeof(ncclDevComm)) != cudaSuccess ||
+        cudaMemcpy(c->dev_comm_d, &c->dev_comm, sizeof(ncclDevComm), cudaMemcpyHostToDevice) != cudaSuccess)
+        return ARC_ERR_CUDA;
+    c->lsa = true;
+    return ARC_OK;
+}
 
 extern "C" {
 
@@ -638,6 +707,10 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         for (uint64_t x : all)
             if (x != mine) { delete c; return ARC_ERR_PARAM_MISMATCH; }
     }
+    if (c->p.value_reduce == ARC_REDUCE_LSA && (c->pl.exchange || c->pl.topk)) {
+        const arc_status ls = lsa_setup(c, s);
+        if (ls != ARC_OK) { lsa_release(c); delete c; return ls; }
+    }
     if (const char* e = getenv("ARC_DEBUG_STAMPS")) {
         if (e[0] == '1' && cudaMalloc(&c->stamps, sizeof(unsigned long long) * 8 * c->pl.items.size()) != cudaSuccess)
             c->stamps = nullptr;
@@ -816,8 +889,9 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ga.noef = pl.noef ? 1 : 0;
     ga.bnd = c->at<int2>(pl.o_bnd);
     ga.bnd_count = c->at<unsigned>(pl.o_bnd_count);
-    const bool ordered = c->p.value_reduce == ARC_REDUCE_ORDERED;
-    float* wire = (pl.exchange || pl.topk) ? c->at<float>(pl.o_wire) : nullptr;
+    const bool ordered = c->p.value_reduce != ARC_REDUCE_NCCL;   // ORDERED and LSA: per-node payloads
+    float* wire = c->lsa ? static_cast<float*>(c->win_buf)
+                         : ((pl.exchange || pl.topk) ? c->at<float>(pl.o_wire) : nullptr);
     ga.blocks = sblocks;
     if (pl.topk) {   // baseline: each node's payload [values | indices] in the wire
         ga.mode = 3;
@@ -917,6 +991,41 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             ml.N_int = c->p.N;
             ml.gbar = gbar;
             launch_topk_merge(ml, s);
+            ARC_LAUNCHED();
+        }
+    } else if (pl.exchange && c->lsa) {   // exchange #2 fused with S6 over peer memory
+        LsaScatter x{};
+        x.dev_comm = c->dev_comm_d;
+        x.win = c->win;
+        x.G = pl.G;
+        x.L = L;
+        x.N = c->p.N;
+        x.sum_Kn = pl.sumKn;
+        if (!pl.segs_real.empty()) {
+            ScatterLaunch sa{};
+            sa.blocks = blocks;
+            sa.rows = c->at<SelRow>(pl.o_segs_real);
+            sa.num_rows = static_cast<int>(pl.segs_real.size());
+            sa.sel = sel;
+            sa.sum_Kn = pl.sumKn;
+            sa.Nf = c->Nf;
+            sa.N_int = c->p.N;
+            sa.gbar = gbar;
+            sa.values = values_out;
+            launch_lsa_scatter(sa, x, s);
+            ARC_LAUNCHED();
+        }
+        if (!pl.dense_ids.empty()) {
+            DenseScatterLaunch ds{};
+            ds.blocks = blocks;
+            ds.dense_ids = c->at<int>(pl.o_dense_ids);
+            ds.num_dense = static_cast<int>(pl.dense_ids.size());
+            ds.sum_Kn = pl.sumKn;
+            ds.Nf = c->Nf;
+            ds.N_int = c->p.N;
+            ds.gbar = gbar;
+            ds.values = values_out;
+            launch_lsa_dense_scatter(ds, x, s);
             ARC_LAUNCHED();
         }
     } else if (pl.exchange) {   // exchange #2 + S6
@@ -1112,6 +1221,7 @@ arc_status arc_topk_destroy(arc_topk_ctx* c) {
     cudaStreamSynchronize(c->last);
     if (c->stamps) cudaFree(c->stamps);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    lsa_release(c);
     delete c;
     return ARC_OK;
 }

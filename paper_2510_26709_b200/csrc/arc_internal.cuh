@@ -6,6 +6,9 @@
 
 #include "arc_topk.h"
 
+struct ncclDevComm;
+struct ncclWindow_vidmem;
+
 namespace arc {
 
 // Per-block descriptor in device memory (built once at create).
@@ -246,6 +249,18 @@ struct DenseScatterLaunch {
     float* values;              // optional A/N
 };
 void launch_dense_scatter(const DenseScatterLaunch& a, cudaStream_t s);
+
+// Exchange #2 fused with S6 over peer memory (ARC_REDUCE_LSA, arc_lsa.cu):
+// the per-node payloads live in an NCCL symmetric window on every rank.
+constexpr int kLsaCtas = 296;   // grid cap = LSA barriers requested at create (2 per SM)
+struct LsaScatter {
+    const ncclDevComm* dev_comm;   // device copy of the ncclDevComm (library-owned)
+    ncclWindow_vidmem* win;        // window of [L][sum_Kn] floats per rank
+    int G, L, N;                   // ranks (= LSA team), local nodes, global nodes
+    long long sum_Kn;
+};
+void launch_lsa_scatter(const ScatterLaunch& a, const LsaScatter& x, cudaStream_t s);
+void launch_lsa_dense_scatter(const DenseScatterLaunch& a, const LsaScatter& x, cudaStream_t s);
 
 // Top-K baseline merge of one node's gathered payload: gbar[I_j] += C_j / N.
 struct MergeLaunch {

@@ -33,7 +33,9 @@ def arc_bus_bytes(sum_m: int, sum_Kn: int, r: int, G: int, nodes_local: int = 1,
     ((G-1) slices of ceil(sum_m/G) rows x nodes_local x r fp32) plus an
     all-gather of the Sigma slices ((G-1) x ceil(sum_m/G) fp32 received, one
     slice sent per peer); exchange #2 = ncclAllReduce of the K rows (ring bus
-    bytes 2(G-1)/G) or, in ordered mode, an all-gather of the per-node rows."""
+    bytes 2(G-1)/G) or, in ordered mode, an all-gather of the per-node rows;
+    in lsa mode every rank loads the (G-1) peers' per-node rows over NVLink
+    (the same bytes as the ordered all-gather, read instead of pushed)."""
     if G <= 1:
         return {"sketch": 0, "values": 0, "total": 0}
     Ms = -(-sum_m // G)

@@ -191,7 +191,7 @@ def test_exchange_kernels_single_gpu(orc, reduce):
     run_parity(orc, 50_000, flat_blocks(50_000, 96, K=40), N=4, steps=3, reduce=reduce, force_exchange=True)
 
 
-@pytest.mark.parametrize("reduce", ["nccl", "ordered"])
+@pytest.mark.parametrize("reduce", ["nccl", "ordered", "lsa"])
 def test_exchange_through_nccl_one_rank(orc, reduce):
     """The exchange path with a real NCCL communicator borrowed from a 1-rank torch
     ProcessGroupNCCL (dlopen'd libnccl, ncclAllGather of the per-node sketches and
@@ -207,6 +207,55 @@ def test_exchange_through_nccl_one_rank(orc, reduce):
                    pg=dist.group.WORLD)
     finally:
         pass
+
+
+def _world_pg():
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    return dist.group.WORLD
+
+
+@pytest.mark.parametrize("method", ["arc", "randk", "noef_msgd"])
+def test_lsa_fused_scatter_multiblock(orc, method):
+    """reduce="lsa" (exchange #2 fused with S6 over an NCCL symmetric window, LSA
+    barriers, peer loads) through a real 1-rank communicator:
+    per-tensor ARC blocks (aligned, unaligned, wide enough for the ranged launch), a
+    DENSE block, several local nodes — gbar, g, h, selection and values bit-exact
+    against the oracle, like the ORDERED mode it replaces."""
+    pg = _world_pg()
+    shapes = [(300, 128, 5, 0), (77, 127, 3, 0), (64, 64, 64, 0), (1000, 3, 17, 0), (13, 100, 13, 1),
+              (9, 7777, 2, 0), (129, 2048, 2, 0)]
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n, m, n, K, kind))
+        off += m * n
+    eta = 0.5 if method == "noef_msgd" else 0.1
+    for N in (1, 3, 4):
+        run_parity(orc, off, blocks, N=N, steps=3, eta=eta, method=method, force_exchange=True, reduce="lsa", pg=pg)
+
+
+def test_lsa_flat_many_steps(orc):
+    """The window and the LSA barrier epochs are reused step after step (the
+    barrier that ends each scatter guards the next step's payload writes)."""
+    pg = _world_pg()
+    run_parity(orc, 200_000, flat_blocks(200_000, 768, K=3), N=2, steps=8, reduce="lsa", force_exchange=True, pg=pg)
+
+
+def test_lsa_create_errors():
+    """reduce="lsa" needs a communicator (INVALID_ARG without one) and is not offered
+    for the All-Gather Top-K baseline (UNSUPPORTED); nothing is left allocated."""
+    from paper_2510_26709_b200 import ArcTopK
+    pg = _world_pg()
+    blocks = flat_blocks(4096, 64, K=4)
+    with pytest.raises(RuntimeError):
+        ArcTopK(4096, blocks, N=2, eta=0.1, nodes_local=2, reduce="lsa", force_exchange=True, device=DEV)
+    with pytest.raises(RuntimeError):
+        ArcTopK(4096, blocks, N=2, eta=0.1, nodes_local=2, reduce="lsa", force_exchange=True, method="topk_allgather",
+                pg=pg, device=DEV)
 
 
 def test_nonconsecutive_steps(orc):

@@ -9,6 +9,9 @@ run --config C1 --nodes-per-gpu 4 --pool 2
 run --config C2 --nodes-per-gpu 8 --pool 2
 run --config C2 --nodes-per-gpu 1
 run --config C3
+run --config C3 --force-exchange --reduce nccl
+run --config C3 --force-exchange --reduce ordered
+run --config C3 --force-exchange --reduce lsa
 run --config C4 --pool 2
 run --config C5_1e6
 run --config C5_1e8 --mu-bp 10 --pool 4
