@@ -95,7 +95,8 @@ class ArcTopK:
       nodes when > 1).  eta: EF21M momentum.  r: sketch width.  seed: shared
       base seed.  pg: torch process group (NCCL) when N / nodes_local > 1.
       rank: this GPU's rank in pg.  reduce: "nccl" (All-Reduce of the K rows)
-      or "ordered" (bit-exact node-ordered sum).
+      or "ordered" (bit-exact node-ordered sum) or "lsa" (both exchanges
+      fused into the library's kernels over NCCL symmetric windows, bit-exact).
     """
 
     def __init__(self, d: int, blocks: Sequence, N: int, eta: float, r: int = 4, seed: int = 20251030,

@@ -431,6 +431,15 @@ struct arc_topk_ctx {
     bool dev_comm_ok = false;
     ncclDevComm dev_comm{};
     ncclDevComm* dev_comm_d = nullptr;
+    // exchange #1 over peer memory: P' ([M][L][r]) and Sigma in one more window
+    bool lsa1 = false;
+    void* sk_buf = nullptr;
+    ncclWindow_t sk_win = nullptr;
+    size_t sk_sigma_off = 0;
+    float* pnodes_ptr() const { return lsa1 ? static_cast<float*>(sk_buf) : at<float>(pl.o_pnodes); }
+    float* sigma_ptr() const {
+        return lsa1 ? reinterpret_cast<float*>(static_cast<unsigned char*>(sk_buf) + sk_sigma_off) : at<float>(pl.o_sigma);
+    }
 
     template <class T> T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
 };
@@ -453,6 +462,11 @@ struct arc_topk_ctx {
 // barrier per CTA of the fused scatter kernels (arc_lsa.cu).
 static void lsa_release(arc_topk_ctx* c) {
     if (c->dev_comm_ok && c->nccl.devCommDestroy) c->nccl.devCommDestroy(c->comm, &c->dev_comm);
+    if (c->sk_win && c->nccl.winDeregister) c->nccl.winDeregister(c->comm, c->sk_win);
+    if (c->sk_buf && c->nccl.memFree) c->nccl.memFree(c->sk_buf);
+    c->sk_win = nullptr;
+    c->sk_buf = nullptr;
+    c->lsa1 = false;
     if (c->win && c->nccl.winDeregister) c->nccl.winDeregister(c->comm, c->win);
     if (c->win_buf && c->nccl.memFree) c->nccl.memFree(c->win_buf);
     if (c->dev_comm_d) cudaFree(c->dev_comm_d);
@@ -477,6 +491,15 @@ static arc_status lsa_setup(arc_topk_ctx* c, cudaStream_t s) {
     bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
     if (n.memAlloc(&c->win_buf, bytes) != ncclSuccess) return ARC_ERR_NCCL;
     if (n.winRegister(c->comm, c->win_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) return ARC_ERR_NCCL;
+    if (pl.exchange && pl.keep_pnodes && !pl.randk && pl.M > 0) {   // exchange #1 window: [P' | Sigma]
+        const size_t pn = sizeof(float) * static_cast<size_t>(pl.M) * pl.L * c->p.r;
+        c->sk_sigma_off = (pn + 255) / 256 * 256;
+        size_t sb = c->sk_sigma_off + sizeof(float) * static_cast<size_t>(std::max<int64_t>(pl.M, pl.G * pl.Ms));
+        sb = (sb + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+        if (n.memAlloc(&c->sk_buf, sb) != ncclSuccess) return ARC_ERR_NCCL;
+        if (n.winRegister(c->comm, c->sk_buf, sb, &c->sk_win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) return ARC_ERR_NCCL;
+        c->lsa1 = true;
+    }
     ncclDevCommRequirements_t reqs;
     std::memset(&reqs, 0, sizeof(reqs));
     reqs.lsaBarrierCount = arc::kLsaCtas;
@@ -758,7 +781,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     c->last = s;
     const BlockDev* blocks = c->at<BlockDev>(pl.o_blocks);
     float* V = c->at<float>(pl.o_V);
-    float* sigma = c->at<float>(pl.o_sigma);
+    float* sigma = c->sigma_ptr();
     int32_t* sel = c->at<int32_t>(pl.o_sel);
     unsigned* status = c->at<unsigned>(pl.o_status);
     unsigned* hist1 = c->at<unsigned>(pl.o_hist1);
@@ -792,7 +815,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.V = V_t;
         a.sigma = sigma;
         a.hist1 = hist1;
-        a.pnodes = pl.keep_pnodes ? c->at<float>(pl.o_pnodes) : nullptr;
+        a.pnodes = pl.keep_pnodes ? c->pnodes_ptr() : nullptr;
         a.mode = pl.topk ? 2 : pl.randk ? 3 : ((pl.exchange || L > 1) ? 1 : 0);
         a.key = make_uint2(static_cast<unsigned>(c->p.seed), static_cast<unsigned>(c->p.seed >> 32));
         a.t_lo = static_cast<unsigned>(static_cast<uint64_t>(t));
@@ -830,7 +853,22 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     // every rank all of Sigma.  (Several local nodes and no exchange: the select
     // kernel forms Sigma from the per-node sketches itself, phase 0.)
     const bool sigma_pass = (pl.exchange || L > 1) && !pl.randk && !pl.topk && pl.M > 0;
-    if (sigma_pass && pl.exchange) {
+    if (sigma_pass && pl.exchange && c->lsa1) {   // exchange #1 + S2 over peer memory
+        LsaSigma ls{};
+        ls.dev_comm = c->dev_comm_d;
+        ls.win = c->sk_win;
+        ls.sigma_off = c->sk_sigma_off;
+        ls.sigma = sigma;
+        ls.Ms = pl.Ms;
+        ls.M = pl.M;
+        ls.G = pl.G;
+        ls.me = pl.G > 1 ? c->p.rank : 0;
+        ls.L = L;
+        ls.r = c->p.r;
+        ls.status = status;
+        launch_lsa_sigma(ls, s);
+        ARC_LAUNCHED();
+    } else if (sigma_pass && pl.exchange) {
         const int G = pl.G;
         const int me = G > 1 ? c->p.rank : 0;
         const int64_t Ms = pl.Ms;
@@ -927,7 +965,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.early = c->early && ga.mode == 0 && ga.values == nullptr ? 1 : 0;
         sg.build_hist = sigma_pass ? 1 : 0;
         if (sigma_pass && !pl.exchange) {
-            sg.xsk = c->at<float>(pl.o_pnodes);
+            sg.xsk = c->pnodes_ptr();
             sg.sigma_w = sigma;
             sg.L = L;
             sg.Nf = c->Nf;
@@ -1141,7 +1179,10 @@ arc_status arc_topk_query(arc_topk_ctx* c, int32_t what, void* dst, size_t bytes
     }
     if (bytes < need) return ARC_ERR_INVALID_ARG;
     if (need == 0) return ARC_OK;
-    ARC_CUDA(cudaMemcpyAsync(dst, c->ws + off, need, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+    const void* src = c->ws + off;
+    if (what == ARC_Q_SIGMA) src = c->sigma_ptr();
+    if (what == ARC_Q_P_NODES) src = c->pnodes_ptr();
+    ARC_CUDA(cudaMemcpyAsync(dst, src, need, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
     return ARC_OK;
 }
 

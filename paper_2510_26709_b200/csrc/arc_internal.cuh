@@ -252,7 +252,7 @@ void launch_dense_scatter(const DenseScatterLaunch& a, cudaStream_t s);
 
 // Exchange #2 fused with S6 over peer memory (ARC_REDUCE_LSA, arc_lsa.cu):
 // the per-node payloads live in an NCCL symmetric window on every rank.
-constexpr int kLsaCtas = 296;   // grid cap = LSA barriers requested at create (2 per SM)
+constexpr int kLsaCtas = 592;   // grid cap = LSA barriers requested at create (4 per SM)
 struct LsaScatter {
     const ncclDevComm* dev_comm;   // device copy of the ncclDevComm (library-owned)
     ncclWindow_vidmem* win;        // window of [L][sum_Kn] floats per rank
@@ -260,6 +260,19 @@ struct LsaScatter {
     long long sum_Kn;
 };
 void launch_lsa_scatter(const ScatterLaunch& a, const LsaScatter& x, cudaStream_t s);
+// Exchange #1 over peer memory: every rank's per-node sketches P' ([M][L][r])
+// and Sigma ([G * Ms]) live in one symmetric window (P' at byte 0, Sigma at
+// sigma_off).  CTA b of every rank owns sub-range b of every rank's row slice.
+struct LsaSigma {
+    const ncclDevComm* dev_comm;
+    ncclWindow_vidmem* win;
+    size_t sigma_off;      // bytes
+    float* sigma;          // this rank's Sigma (the window's local address + sigma_off)
+    long long Ms, M;       // rows per slice, rows in total
+    int G, me, L, r;
+    unsigned* status;
+};
+void launch_lsa_sigma(const LsaSigma& a, cudaStream_t s);
 void launch_lsa_dense_scatter(const DenseScatterLaunch& a, const LsaScatter& x, cudaStream_t s);
 
 // Top-K baseline merge of one node's gathered payload: gbar[I_j] += C_j / N.

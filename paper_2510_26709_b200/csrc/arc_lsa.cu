@@ -18,7 +18,7 @@
 //      payload) while a peer is still reading it.
 // This replaces the all-gather into a staging buffer and the separate scatter
 // launch of the ORDERED mode: the payload crosses NVLink once and lands in
-// registers, not in HBM.
+// registers, not in HBM.  k_lsa_sigma does the same for exchange #1 (below).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -76,6 +76,31 @@ __global__ void __launch_bounds__(256) k_lsa_scatter(const ScatterLaunch a, cons
         const long long e0 = B.off + static_cast<long long>(p) * B.n;
         const long long o0 = B.val_base + static_cast<long long>(R.k) * B.n;
         const int cnt = max(0, min(4, nv - q)), ocnt = min(4, B.n - q);
+        if (ocnt == 4 && (((o0 + q) | x.sum_Kn) & 3) == 0) {   // 16-byte payload loads
+            float4 A = __ldcg(reinterpret_cast<const float4*>(pb.p[0] + o0 + q));
+            for (int i = 1; i < x.N; ++i) {
+                const int g = i / x.L, l = i - g * x.L;
+                const float4 c = __ldcg(reinterpret_cast<const float4*>(pb.p[g] + static_cast<long long>(l) * x.sum_Kn + o0 + q));
+                A.x = fadd(A.x, c.x); A.y = fadd(A.y, c.y); A.z = fadd(A.z, c.z); A.w = fadd(A.w, c.w);
+            }
+            const float Av[4] = {A.x, A.y, A.z, A.w};
+            float val[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) val[k] = k < cnt ? (pow2 ? fmul(Av[k], invN) : __fdiv_rn(Av[k], a.Nf)) : 0.0f;
+            if (B.vec && cnt == 4) {
+                float4* gp = reinterpret_cast<float4*>(a.gbar + e0 + q);
+                float4 gb = *gp;
+                gb.x = fadd(gb.x, val[0]); gb.y = fadd(gb.y, val[1]); gb.z = fadd(gb.z, val[2]); gb.w = fadd(gb.w, val[3]);
+                *gp = gb;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < cnt) a.gbar[e0 + q + k] = fadd(a.gbar[e0 + q + k], val[k]);
+            }
+            if (a.values != nullptr)
+                *reinterpret_cast<float4*>(a.values + o0 + q) = make_float4(val[0], val[1], val[2], val[3]);
+            continue;
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (k >= ocnt) continue;
@@ -110,7 +135,80 @@ __global__ void __launch_bounds__(256) k_lsa_dense_scatter(const DenseScatterLau
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
 }
 
+// Exchange #1 + S2 over peer memory (replaces the all-to-all of P' slices,
+// k_sigma_slice and the all-gather of Sigma): after barrier 1 (every rank's
+// sketch pass has completed) CTA b forms Sigma of sub-range b of this rank's
+// slice from every node's P' rows read in the owners' windows, summed in
+// ascending global node id and squared-summed with the O8 fma chain (R9, R21;
+// the k_sigma_slice order); after barrier 2 it copies sub-range b of every
+// other rank's Sigma slice from that rank's window (CTA b of that rank wrote
+// it); barrier 3 keeps every rank's P' and Sigma unchanged until all peers have
+// read them.
+__global__ void __launch_bounds__(256) k_lsa_sigma(const LsaSigma a) {
+    __shared__ const float* pk[kLsaMaxPeers];   // peers' P' (window offset 0)
+    __shared__ const float* ps[kLsaMaxPeers];   // peers' Sigma
+    for (int g = threadIdx.x; g < a.G; g += blockDim.x) {
+        pk[g] = static_cast<const float*>(ncclGetLsaPointer(a.win, 0, g));
+        ps[g] = static_cast<const float*>(ncclGetLsaPointer(a.win, a.sigma_off, g));
+    }
+    __syncthreads();
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), *a.dev_comm, ncclTeamTagLsa(), blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    const long long chunk = (a.Ms + gridDim.x - 1) / gridDim.x;
+    const long long lo = blockIdx.x * chunk, hi = min(a.Ms, lo + chunk);
+    const int L = a.L, r = a.r;
+    const long long base = a.me * a.Ms;
+    for (long long p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+        const long long row = base + p;
+        if (row >= a.M) break;
+        float sig = 0.0f;
+        if (r == 4) {   // one 16-byte load per node (P' rows are 16-byte aligned: r = 4)
+            float4 S = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int g = 0; g < a.G; ++g)
+                for (int l = 0; l < L; ++l) {
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>(pk[g] + (row * L + l) * 4));
+                    if (g == 0 && l == 0) S = v;
+                    else { S.x = fadd(S.x, v.x); S.y = fadd(S.y, v.y); S.z = fadd(S.z, v.z); S.w = fadd(S.w, v.w); }
+                }
+            const float P[4] = {S.x, S.y, S.z, S.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sig = ffma(P[j], P[j], sig);                         // O8
+            a.sigma[row] = sig;
+            if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
+            continue;
+        }
+        for (int j = 0; j < r; ++j) {
+            float S = 0.0f;
+            for (int g = 0; g < a.G; ++g)
+                for (int l = 0; l < L; ++l) {
+                    const float v = __ldcg(pk[g] + (row * L + l) * r + j);
+                    S = (g == 0 && l == 0) ? v : fadd(S, v);
+                }
+            sig = ffma(S, S, sig);                                                             // O8
+        }
+        a.sigma[row] = sig;
+        if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
+    }
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    for (int g = 0; g < a.G; ++g) {
+        if (g == a.me) continue;
+        const long long gb = g * a.Ms;
+        for (long long p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+            if (gb + p >= a.M) break;
+            a.sigma[gb + p] = __ldcg(ps[g] + gb + p);
+        }
+    }
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
 }  // namespace
+
+void launch_lsa_sigma(const LsaSigma& a, cudaStream_t s) {
+    long long grid = (a.Ms + 255) / 256;
+    if (grid > kLsaCtas) grid = kLsaCtas;
+    if (grid < 1) grid = 1;
+    k_lsa_sigma<<<static_cast<int>(grid), 256, 0, s>>>(a);
+}
 
 void launch_lsa_scatter(const ScatterLaunch& a, const LsaScatter& x, cudaStream_t s) {
     const long long quads = static_cast<long long>(a.num_rows) * kSegQuads;
