@@ -673,3 +673,38 @@ void orc_sincos2pi_array(const float* u, int64_t n, float* s, float* c)
 {
     for (int64_t i = 0; i < n; i++) orc_sincos2pi(u[i], &s[i], &c[i]);
 }
+
+/* ---------------------------------------------------------------------------
+ * The model update that consumes gbar (readings R23, R24).
+ * ------------------------------------------------------------------------- */
+
+/* eq:ef21m-3: x_{t+1} = x_t - (gamma/N) sum_i g_i^{(t)} = x_t - gamma gbar_t,
+ * gbar being the replicated (1/N) sum_i g_i the step maintains [R13].  Per
+ * element, each operation rounded once [R23]: x <- x - (gamma * gbar). */
+void orc_apply_sgd(float* x, const float* gbar, int64_t d, float gamma)
+{
+    for (int64_t e = 0; e < d; e++) x[e] = x[e] - gamma * gbar[e];
+}
+
+/* "standard Adam" (Kingma & Ba, Algorithm 1; no weight decay) driven by the
+ * EF21M direction gbar, as in the paper's GLUE and C4 experiments (P:572,
+ * P:578) [R24].  t >= 1 is Adam's step count.  Per element:
+ *   m <- fma(1-b1, gbar, b1 * m)            (the O2 form of eq:ef21m-1)
+ *   v <- fma(1-b2, gbar * gbar, b2 * v)
+ *   mhat = m / bc1,  vhat = v / bc2,   bc_k = fl32(1 - b_k^t) (pow in double)
+ *   x <- x - gamma * (mhat / (sqrt(vhat) + eps))                               */
+void orc_apply_adam(float* x, float* m, float* v, const float* gbar, int64_t d, int64_t t,
+                    float gamma, float beta1, float beta2, float eps)
+{
+    const float om1 = 1.0f - beta1, om2 = 1.0f - beta2;
+    const float bc1 = (float)(1.0 - pow((double)beta1, (double)t));
+    const float bc2 = (float)(1.0 - pow((double)beta2, (double)t));
+    for (int64_t e = 0; e < d; e++) {
+        const float gb = gbar[e];
+        m[e] = fmaf(om1, gb, beta1 * m[e]);
+        v[e] = fmaf(om2, gb * gb, beta2 * v[e]);
+        const float mhat = m[e] / bc1;
+        const float vhat = v[e] / bc2;
+        x[e] = x[e] - gamma * (mhat / (sqrtf(vhat) + eps));
+    }
+}

@@ -67,6 +67,8 @@ def lib():
         L.orc_step_topk.restype = ctypes.c_int
         L.orc_step_noef.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 6
         L.orc_step_noef.restype = ctypes.c_int
+        L.orc_apply_sgd.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_float]
+        L.orc_apply_adam.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64] + [ctypes.c_float] * 4
         _lib = L
     return _lib
 
@@ -289,6 +291,25 @@ class OracleEF21M:
         return dict(sel=sel.reshape(self.N, self.sum_K), values=vals.reshape(self.N, self.sum_Kn))
 
 
-__all__ = ["Block", "OracleEF21M", "arc_round", "argtop_k", "build", "gaussian_V", "ln", "ln_array", "lib",
+__all__ = ["Block", "OracleEF21M", "apply_adam", "apply_sgd", "arc_round", "argtop_k", "build", "gaussian_V", "ln", "ln_array", "lib",
            "momentum", "philox4x32_10", "randk_keys", "sigma_key", "sigma_rows", "sincos2pi", "sincos2pi_array",
            "uniform"]
+
+
+def apply_sgd(x, gbar, gamma: float) -> np.ndarray:
+    """eq:ef21m-3: x - gamma * gbar, per element [R23]; returns the new x."""
+    x = _f32(x).copy()
+    gbar = _f32(gbar)
+    lib().orc_apply_sgd(_ptr(x), _ptr(gbar), x.size, float(gamma))
+    return x
+
+
+def apply_adam(x, m, v, gbar, t: int, gamma: float, beta1: float = 0.9, beta2: float = 0.999,
+               eps: float = 1e-8):
+    """Adam step t >= 1 on the EF21M direction gbar (P:572, P:578) [R24];
+    returns the new (x, m, v)."""
+    x, m, v = _f32(x).copy(), _f32(m).copy(), _f32(v).copy()
+    gbar = _f32(gbar)
+    lib().orc_apply_adam(_ptr(x), _ptr(m), _ptr(v), _ptr(gbar), x.size, int(t), float(gamma),
+                         float(beta1), float(beta2), float(eps))
+    return x, m, v
