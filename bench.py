@@ -264,6 +264,28 @@ def run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, str
         ctx.close()
     except Exception as e:
         out["noef_msgd"] = {"unavailable": str(e)[:200]}
+    # the model update that consumes gbar: not part of the
+    # compression step, timed on its own against the HBM roofline
+    try:
+        from paper_2510_26709_b200 import apply_update
+        peak, _ = _peaks()
+        x = torch.zeros(d, device=dev)
+        mom = torch.zeros(d, device=dev)
+        var = torch.zeros(d, device=dev)
+        gb = pool[0][0]
+        for name, nbytes, fn in [
+                ("update_sgd", 12, lambda t: apply_update(x, gb, 1e-3, stream=stream)),
+                ("update_adam", 28, lambda t: apply_update(x, gb, 1e-3, optimizer="adam", t=t + 1, m=mom, v=var,
+                                                           stream=stream))]:
+            r = timed(fn)
+            gbs = nbytes * d / (r["ms_per_step"] * 1e-3) / 1e9
+            out[name] = {"ms_per_step": r["ms_per_step"], "value": gbs, "unit": "GB/s", "steps": r["steps"],
+                         "frac_of_hbm_peak": gbs / peak, "bytes_per_element": nbytes,
+                         "note": "k_apply_%s over d (eq:ef21m-3 / Adam on gbar), algorithmic bytes / CUDA-event time"
+                                 % name.split("_")[1]}
+        del x, mom, var
+    except Exception as e:
+        out["update"] = {"unavailable": str(e)[:200]}
     return out
 
 

@@ -211,6 +211,33 @@ arc_status arc_topk_read_timing(arc_topk_ctx* ctx, float* ms, int32_t n_phases, 
  * min(n, grid * 8) uint64 values into host memory (synchronises). */
 arc_status arc_topk_debug_stamps(arc_topk_ctx* ctx, uint64_t* stamps_host, int64_t n, int32_t* grid);
 
+/* The model update that consumes gbar (R23,
+ * R24).  Context-free: one HBM-streaming kernel over d elements, enqueued on
+ * `stream` (call it after arc_topk_step on the same stream, so it reads the
+ * step's gbar).
+ *   ARC_OPT_SGD  : x <- x - gamma * gbar                  eq:ef21m-3, P:327 (R23)
+ *   ARC_OPT_ADAM : "standard Adam" on gbar, no weight decay (R24):
+ *                  m <- fma(1-b1, gbar, b1 m);  v <- fma(1-b2, gbar^2, b2 v)
+ *                  x <- x - gamma ((m / bc1) / (sqrt(v / bc2) + eps)),
+ *                  bc_k = (float)(1 - b_k^t) evaluated in double on the host
+ * Arguments: x (in/out), gbar (read-only), m and v (in/out, ADAM only; may be
+ * NULL for SGD): device float[d], base pointers 16-byte aligned, caller-owned.
+ * t is Adam's step count (>= 1; ignored by SGD).  d == 0 is a no-op.
+ * Errors (returned before anything is enqueued): ARC_ERR_INVALID_ARG for a
+ * NULL params, d < 0, NULL or unaligned pointers, t < 1 (ADAM), betas outside
+ * [0, 1), eps < 0 or a non-finite gamma; ARC_ERR_UNSUPPORTED for an unknown
+ * kind; ARC_ERR_CUDA if the launch fails.  Non-finite inputs propagate (IEEE). */
+typedef enum { ARC_OPT_SGD = 0, ARC_OPT_ADAM = 1 } arc_opt_kind;
+typedef struct {
+    uint32_t kind;      /* arc_opt_kind */
+    float    gamma;     /* step size                          */
+    float    beta1;     /* ADAM first-moment decay, [0, 1)    */
+    float    beta2;     /* ADAM second-moment decay, [0, 1)   */
+    float    eps;       /* ADAM denominator offset, >= 0      */
+} arc_opt_params;
+arc_status arc_topk_apply_update(const arc_opt_params* params, int64_t t, float* x, const float* gbar,
+                                 float* m, float* v, int64_t d, void* stream);
+
 /* Frees the host context (synchronises first).  Never frees caller memory. */
 arc_status arc_topk_destroy(arc_topk_ctx* ctx);
 

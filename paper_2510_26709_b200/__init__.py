@@ -4,6 +4,7 @@ Public surface:
 
 * :class:`ArcTopK` — one compression context (a C-ABI ``arc_topk_ctx``);
   ``step()`` runs one EF21M + ARC-Top-K iteration on CUDA tensors.
+* :func:`apply_update` — the SGD (eq:ef21m-3) or Adam update of x from gbar.
 * :class:`Block`, :func:`flat_layout` — the m x n block views of the flat
   gradient (per-tensor blocks P:130).
 
@@ -12,7 +13,7 @@ PyTorch supplies device memory, streams and the process group only.
 """
 from __future__ import annotations
 
-from .api import ArcTopK, Block, flat_layout, nccl_comm_ptr, per_tensor_layout  # noqa: F401
+from .api import ArcTopK, Block, apply_update, flat_layout, nccl_comm_ptr, per_tensor_layout  # noqa: F401
 from .ledger import comm_entries  # noqa: F401
 
-__all__ = ["ArcTopK", "Block", "flat_layout", "per_tensor_layout", "nccl_comm_ptr", "comm_entries"]
+__all__ = ["ArcTopK", "Block", "apply_update", "flat_layout", "per_tensor_layout", "nccl_comm_ptr", "comm_entries"]

@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libarctopk.so")
 SOURCES = [os.path.join(CSRC, "arc_kernels.cu"), os.path.join(CSRC, "arc_sketch.cu"),
            os.path.join(CSRC, "arc_select.cu"), os.path.join(CSRC, "arc_lsa.cu"),
-           os.path.join(CSRC, "arc_api.cu")]
+           os.path.join(CSRC, "arc_optim.cu"), os.path.join(CSRC, "arc_api.cu")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -26,6 +26,8 @@ REDUCE_NCCL, REDUCE_ORDERED, REDUCE_LSA = 0, 1, 2
 FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE = 0x1, 0x2, 0x4
 # arc_method
 METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK, METHOD_NOEF_MSGD = 0, 1, 2, 3
+# arc_opt_kind
+OPT_SGD, OPT_ADAM = 0, 1
 # arc_query
 Q_V, Q_SIGMA, Q_SEL, Q_P_NODES, Q_CANDIDATES = 0, 1, 2, 3, 4
 
@@ -33,7 +35,7 @@ EXPORTED = [
     "arc_topk_workspace_bytes", "arc_topk_create", "arc_topk_step", "arc_topk_step_host",
     "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_kernels_per_step",
     "arc_topk_destroy", "arc_topk_status_string", "arc_topk_set_timing", "arc_topk_read_timing",
-    "arc_topk_debug_stamps",
+    "arc_topk_debug_stamps", "arc_topk_apply_update",
 ]
 TIMING_PHASES = 6
 PHASE_NAMES = ["vgen", "ef_sketch", "exchange1_reduce", "select_gather", "exchange2_scatter", "copy_out"]
@@ -51,6 +53,11 @@ class ArcParams(ctypes.Structure):
                 ("num_blocks", ctypes.c_int32), ("blocks", ctypes.POINTER(ArcBlock)),
                 ("eta", ctypes.c_float), ("value_reduce", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("flags", ctypes.c_uint32), ("method", ctypes.c_uint32)]
+
+
+class ArcOptParams(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_uint32), ("gamma", ctypes.c_float), ("beta1", ctypes.c_float),
+                ("beta2", ctypes.c_float), ("eps", ctypes.c_float)]
 
 
 class ArcError(RuntimeError):
@@ -85,12 +92,13 @@ def lib():
         L.arc_topk_read_timing.argtypes = [vp, P(ctypes.c_float), i32, P(i32)]
         L.arc_topk_debug_stamps.argtypes = [vp, vp, i64, P(i32)]
         L.arc_topk_debug_stamps.restype = ctypes.c_int
+        L.arc_topk_apply_update.argtypes = [P(ArcOptParams), i64, vp, vp, vp, vp, i64, vp]
         L.arc_topk_destroy.argtypes = [vp]
         L.arc_topk_status_string.argtypes = [ctypes.c_int]
         L.arc_topk_status_string.restype = ctypes.c_char_p
         for name in ["arc_topk_workspace_bytes", "arc_topk_create", "arc_topk_step", "arc_topk_step_host",
                      "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_destroy",
-                     "arc_topk_set_timing", "arc_topk_read_timing"]:
+                     "arc_topk_set_timing", "arc_topk_read_timing", "arc_topk_apply_update"]:
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib

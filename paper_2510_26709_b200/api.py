@@ -239,3 +239,27 @@ class ArcTopK:
             self.close()
         except Exception:
             pass
+
+
+def apply_update(x: torch.Tensor, gbar: torch.Tensor, gamma: float, *, optimizer: str = "sgd",
+                 t: int = 1, m: torch.Tensor | None = None, v: torch.Tensor | None = None,
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, stream=None) -> None:
+    """The model update that consumes the step's gbar (include/arc_topk.h
+    ``arc_topk_apply_update``), in place on x (and m, v for Adam):
+
+    * ``"sgd"``:  x <- x - gamma * gbar   (eq:ef21m-3, P:327; R23)
+    * ``"adam"``: standard Adam on gbar, no weight decay (R24),
+      t >= 1 its step count, m and v its moment buffers.
+
+    Enqueued on ``stream`` (default: the current stream) — call it after
+    ``ArcTopK.step`` on the same stream."""
+    kind = {"sgd": L.OPT_SGD, "adam": L.OPT_ADAM}[optimizer]
+    ts = [x, gbar] + ([m, v] if kind == L.OPT_ADAM else [])
+    if any(u is None or u.dtype != torch.float32 or not u.is_cuda or not u.is_contiguous() for u in ts):
+        raise ValueError("x, gbar (and m, v for adam) must be contiguous float32 CUDA tensors")
+    if any(u.numel() != x.numel() for u in ts):
+        raise ValueError("x, gbar, m, v must have the same number of elements")
+    p = L.ArcOptParams(kind, float(gamma), float(beta1), float(beta2), float(eps))
+    ptr = lambda u: ctypes.c_void_p(u.data_ptr()) if u is not None else None
+    L.check(L.lib().arc_topk_apply_update(ctypes.byref(p), int(t), ptr(x), ptr(gbar), ptr(m), ptr(v),
+                                          int(x.numel()), _stream_handle(stream)), "arc_topk_apply_update")

@@ -124,3 +124,30 @@ def test_sass_is_sm100a(L):
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", L.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_apply_update_validation(L):
+    """arc_topk_apply_update validates before touching the GPU (host-only here)."""
+    import math
+    lib = L.lib()
+    fake = ctypes.c_void_p(1 << 20)          # 16-byte aligned, never dereferenced
+    odd = ctypes.c_void_p((1 << 20) + 4)     # not 16-byte aligned
+
+    def call(p, t=1, x=fake, gb=fake, m=fake, v=fake, d=1024):
+        return lib.arc_topk_apply_update(None if p is None else ctypes.byref(p), t, x, gb, m, v, d, None)
+
+    sgd = L.ArcOptParams(L.OPT_SGD, 0.1, 0.9, 0.999, 1e-8)
+    adam = L.ArcOptParams(L.OPT_ADAM, 0.1, 0.9, 0.999, 1e-8)
+    assert call(None) == L.ERR_INVALID_ARG
+    assert call(sgd, d=-1) == L.ERR_INVALID_ARG
+    assert call(sgd, d=0) == L.OK and call(adam, d=0) == L.OK          # no-op, nothing enqueued
+    assert call(sgd, x=None) == L.ERR_INVALID_ARG
+    assert call(sgd, gb=odd) == L.ERR_INVALID_ARG
+    assert call(adam, m=None) == L.ERR_INVALID_ARG
+    assert call(adam, v=odd) == L.ERR_INVALID_ARG
+    assert call(adam, t=0) == L.ERR_INVALID_ARG
+    assert call(L.ArcOptParams(L.OPT_ADAM, 0.1, 1.0, 0.999, 1e-8)) == L.ERR_INVALID_ARG
+    assert call(L.ArcOptParams(L.OPT_ADAM, 0.1, 0.9, -0.1, 1e-8)) == L.ERR_INVALID_ARG
+    assert call(L.ArcOptParams(L.OPT_ADAM, 0.1, 0.9, 0.999, -1.0)) == L.ERR_INVALID_ARG
+    assert call(L.ArcOptParams(L.OPT_SGD, math.inf, 0.9, 0.999, 1e-8)) == L.ERR_INVALID_ARG
+    assert call(L.ArcOptParams(7, 0.1, 0.9, 0.999, 1e-8)) == L.ERR_UNSUPPORTED
