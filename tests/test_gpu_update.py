@@ -121,3 +121,35 @@ def test_after_step_on_same_stream(orc, api):
     assert _same(x.cpu().numpy(), orc.apply_sgd(x0, gbar.cpu().numpy(), 0.5))
     assert int((gbar != 0).sum()) > 0
     ctx.close()
+
+
+def test_step_and_update_in_one_cuda_graph(orc, api):
+    """Step + SGD update captured together in one CUDA graph (the launch-bound
+    small-d case): one replay gives the oracle's x_{t+1} bit for bit."""
+    from paper_2510_26709_b200 import ArcTopK, flat_layout
+    d, n, N = 30_011, 50, 2
+    blocks = flat_layout(d, n, K=9)
+    rng = np.random.default_rng(21)
+    grads_np = [rng.standard_normal(d).astype(np.float32) for _ in range(N)]
+    x0 = rng.standard_normal(d).astype(np.float32)
+    ctx = ArcTopK(d, blocks, N=N, eta=0.1, seed=5)
+    h = [torch.zeros(d, device=DEV) for _ in range(N)]
+    g = [torch.zeros(d, device=DEV) for _ in range(N)]
+    gbar = torch.zeros(d, device=DEV)
+    grads = [_dev(a) for a in grads_np]
+    x = _dev(x0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            ctx.step(0, grads, h, g, gbar, stream=s)
+            api.apply_update(x, gbar, 0.125, stream=s)
+    graph.replay()
+    torch.cuda.synchronize()
+    ref = orc.OracleEF21M(d, [orc.Block(b.offset, b.len, b.m, b.n, b.K, b.kind) for b in blocks], N=N, eta=0.1,
+                          r=4, seed=5)
+    ref.step(0, grads_np)
+    assert gbar.cpu().numpy().tobytes() == ref.gbar.tobytes()
+    assert _same(x.cpu().numpy(), orc.apply_sgd(x0, ref.gbar, 0.125))
+    ctx.close()
