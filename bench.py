@@ -264,6 +264,15 @@ def run_baselines(args, d, blocks, L, N, world, rank, pg, pool, pool_n, dev, str
         ctx.close()
     except Exception as e:
         out["noef_msgd"] = {"unavailable": str(e)[:200]}
+    if world == 1:   # exact-sketch test mode (every node local): Sigma from exact row norms of the node sum
+        try:
+            ctx = ArcTopK(d, blocks, N=N, eta=0.1, r=4, seed=20251030, nodes_local=L, method="exact")
+            out["exact_sketch"] = timed(lambda t: ctx.step(t, pool[t % pool_n], hs, gs, gb))
+            out["exact_sketch"]["note"] = ("test mode (SURVEY 8(b) ARC_SKETCH_EXACT): the sketch pass plus "
+                                           "k_exact_sigma (re-reads h', g) instead of the Gaussian estimate")
+            ctx.close()
+        except Exception as e:
+            out["exact_sketch"] = {"unavailable": str(e)[:200]}
     # the model update that consumes gbar: not part of the
     # compression step, timed on its own against the HBM roofline
     try:

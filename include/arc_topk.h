@@ -100,7 +100,11 @@ typedef enum {
     ARC_METHOD_ARC = 0,
     ARC_METHOD_TOPK_ALLGATHER = 1,
     ARC_METHOD_RANDK = 2,
-    ARC_METHOD_NOEF_MSGD = 3
+    ARC_METHOD_NOEF_MSGD = 3,
+    ARC_METHOD_EXACT = 4      /* test mode (SURVEY 8(b) ARC_SKETCH_EXACT): the selection uses the
+                                 quantity the sketch estimates, Sigma_p = ||sum_i Delta_i[p,:]||^2
+                                 (z72ena P:254-261), the squares in the O6 order; every node on this
+                                 GPU (nodes_local == N, no FORCE_EXCHANGE), else ARC_ERR_UNSUPPORTED */
 } arc_method;
 
 /* flags */

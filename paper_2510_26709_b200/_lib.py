@@ -25,7 +25,7 @@ REDUCE_NCCL, REDUCE_ORDERED, REDUCE_LSA = 0, 1, 2
 # flags
 FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE = 0x1, 0x2, 0x4
 # arc_method
-METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK, METHOD_NOEF_MSGD = 0, 1, 2, 3
+METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK, METHOD_NOEF_MSGD, METHOD_EXACT = 0, 1, 2, 3, 4
 # arc_opt_kind
 OPT_SGD, OPT_ADAM = 0, 1
 # arc_query

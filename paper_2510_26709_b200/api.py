@@ -118,7 +118,8 @@ class ArcTopK:
                                   {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED, "lsa": L.REDUCE_LSA}[reduce],
                                   int(seed) & (2**64 - 1), flags,
                                   {"arc": L.METHOD_ARC, "topk_allgather": L.METHOD_TOPK_ALLGATHER,
-                                   "randk": L.METHOD_RANDK, "noef_msgd": L.METHOD_NOEF_MSGD}[method])
+                                   "randk": L.METHOD_RANDK, "noef_msgd": L.METHOD_NOEF_MSGD,
+                                   "exact": L.METHOD_EXACT}[method])
         self.method = method
         nbytes = ctypes.c_size_t()
         L.check(self.lib.arc_topk_workspace_bytes(ctypes.byref(self.params), ctypes.byref(nbytes)),

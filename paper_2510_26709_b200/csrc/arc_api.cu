@@ -92,6 +92,7 @@ struct Plan {
     std::vector<BlockDev> bdev;      // the caller's blocks
     bool topk = false;               // ARC_METHOD_TOPK_ALLGATHER baseline
     bool randk = false;              // ARC_METHOD_RANDK: data-independent shared selection
+    bool exact = false;              // ARC_METHOD_EXACT: Sigma = exact row norms of the node sum
     bool noef = false;               // ARC_METHOD_NOEF_MSGD: sketch the gradient, u = gbar (no h, g)
     int64_t W = 0;                   // Top-K: payload words per node (sum K n values + sum K indices)
     std::vector<BlockDev> sbdev;     // selection blocks: bdev, or (Top-K) one copy per local node
@@ -124,8 +125,10 @@ arc_status validate(const arc_topk_params* p) {
     if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
     if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE)) return ARC_ERR_INVALID_ARG;
     if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER && p->method != ARC_METHOD_RANDK &&
-        p->method != ARC_METHOD_NOEF_MSGD)
+        p->method != ARC_METHOD_NOEF_MSGD && p->method != ARC_METHOD_EXACT)
         return ARC_ERR_INVALID_ARG;
+    if (p->method == ARC_METHOD_EXACT && (p->nodes_local != p->N || (p->flags & ARC_FLAG_FORCE_EXCHANGE)))
+        return ARC_ERR_UNSUPPORTED;
     int64_t pos = 0, M = 0, sumK = 0;
     for (int b = 0; b < p->num_blocks; ++b) {
         const arc_block& B = p->blocks[b];
@@ -153,7 +156,8 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.exchange = pl.G > 1 || (p->flags & ARC_FLAG_FORCE_EXCHANGE);
     pl.randk = p->method == ARC_METHOD_RANDK;
     pl.noef = p->method == ARC_METHOD_NOEF_MSGD;
-    pl.keep_pnodes = !pl.randk && (pl.exchange || pl.L > 1 || (p->flags & ARC_FLAG_DEBUG_SKETCH));
+    pl.exact = p->method == ARC_METHOD_EXACT;
+    pl.keep_pnodes = !pl.randk && (pl.exchange || pl.L > 1 || pl.exact || (p->flags & ARC_FLAG_DEBUG_SKETCH));
     pl.bdev.resize(p->num_blocks);
     int64_t M = 0, sumK = 0, sumKn = 0, sum_nr = 0;
     int max_tiles = 0;
@@ -816,7 +820,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.sigma = sigma;
         a.hist1 = hist1;
         a.pnodes = pl.keep_pnodes ? c->pnodes_ptr() : nullptr;
-        a.mode = pl.topk ? 2 : pl.randk ? 3 : ((pl.exchange || L > 1) ? 1 : 0);
+        a.mode = pl.topk ? 2 : pl.randk ? 3 : ((pl.exchange || L > 1 || pl.exact) ? 1 : 0);
         a.key = make_uint2(static_cast<unsigned>(c->p.seed), static_cast<unsigned>(c->p.seed >> 32));
         a.t_lo = static_cast<unsigned>(static_cast<uint64_t>(t));
         a.t_hi = static_cast<unsigned>(static_cast<uint64_t>(t) >> 32);
@@ -852,7 +856,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     // node order and forms Sigma, and an all-gather of the Sigma slices gives
     // every rank all of Sigma.  (Several local nodes and no exchange: the select
     // kernel forms Sigma from the per-node sketches itself, phase 0.)
-    const bool sigma_pass = (pl.exchange || L > 1) && !pl.randk && !pl.topk && pl.M > 0;
+    const bool sigma_pass = (pl.exchange || L > 1 || pl.exact) && !pl.randk && !pl.topk && pl.M > 0;
     if (sigma_pass && pl.exchange && c->lsa1) {   // exchange #1 + S2 over peer memory
         LsaSigma ls{};
         ls.dev_comm = c->dev_comm_d;
@@ -910,6 +914,17 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             c->nccl.allGather(sigma + me * Ms, sigma, static_cast<size_t>(Ms), ncclFloat32, c->comm, s) != ncclSuccess)
             return ARC_ERR_NCCL;
     }
+    if (sigma_pass && pl.exact) {   // test mode: Sigma from the exact row norms of the node sum
+        ExactSigmaLaunch ex{};
+        ex.blocks = blocks;
+        ex.num_blocks = c->p.num_blocks;
+        ex.L = L;
+        ex.nodes = np;
+        ex.sigma = sigma;
+        ex.status = status;
+        launch_exact_sigma(ex, s);
+        ARC_LAUNCHED();
+    }
     ARC_MARK(3);
     // S3 + S4 (+ S5, S6 when every node is local): one cooperative kernel
     GatherLaunch ga{};
@@ -964,7 +979,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.pdl = c->pdl && !c->timing && !(pl.exchange && pl.M > 0) ? 1 : 0;
         sg.early = c->early && ga.mode == 0 && ga.values == nullptr ? 1 : 0;
         sg.build_hist = sigma_pass ? 1 : 0;
-        if (sigma_pass && !pl.exchange) {
+        if (sigma_pass && !pl.exchange && !pl.exact) {
             sg.xsk = c->pnodes_ptr();
             sg.sigma_w = sigma;
             sg.L = L;
@@ -1205,7 +1220,7 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     const int sel = pl.items.empty() ? 0 : 1;
     if (pl.topk) return sketch + sel + c->p.N;   // + N ordered merges
     const int vgen = (pl.M > 0 && pl.items.empty() && !pl.randk) ? 1 : 0;
-    const int sigma = pl.exchange && !pl.randk && pl.M > 0 ? 1 : 0;
+    const int sigma = (pl.exchange || pl.exact) && !pl.randk && pl.M > 0 ? 1 : 0;
     const int dense = pl.dense_ids.empty() ? 0 : 1;
     const int scatter = pl.exchange ? (pl.segs_real.empty() ? 0 : 1) + dense : 0;
     return vgen + sketch + sigma + sel + dense + scatter;

@@ -215,6 +215,17 @@ struct SigmaLaunch {
 };
 void launch_sigma_slice(const SigmaLaunch& a, cudaStream_t s);
 
+// ARC_METHOD_EXACT: Sigma_p = || sum_i (h'_i - g_i)[p, :] ||^2 for every ARC row.
+struct ExactSigmaLaunch {
+    const BlockDev* blocks;
+    int num_blocks;
+    int L;               // local nodes (== N)
+    NodePtrs nodes;      // h (already h'), g
+    float* sigma;        // [M], indexed by B.row_base + p
+    unsigned* status;
+};
+void launch_exact_sigma(const ExactSigmaLaunch& a, cudaStream_t s);
+
 // DENSE blocks with every node on this GPU: one streaming pass (identity compressor).
 struct DenseLaunch {
     const BlockDev* blocks;

@@ -318,6 +318,50 @@ __global__ void __launch_bounds__(256) k_sigma_slice(const SigmaLaunch a) {
     if (!isfinite(sig)) atomicOr(a.status, kStatusNonfinite);
 }
 
+// ARC_METHOD_EXACT (test mode, SURVEY 8(b) ARC_SKETCH_EXACT, 8(f) row 3): the
+// quantity the sketch estimates, Sigma_p = || sum_i Delta_i[p, :] ||^2
+// (z72ena P:254-261, up to the factor N^2).  Runs after the streaming pass has
+// stored h'_i, before the select kernel (which reads Sigma and histograms it).
+// Per element S_q = ((D_0 + D_1) + ...) + D_{N-1}, D_i = h'_i - g_i (node order,
+// R9); the squares summed in the O6 lane / chunk order with fma.  One warp per
+// row, lane l owns columns 1024 c + 128 s + 4 l + e.
+__global__ void __launch_bounds__(256) k_exact_sigma(const ExactSigmaLaunch a) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * 256LL + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * 256) >> 5;
+    for (int b = 0; b < a.num_blocks; ++b) {
+        const BlockDev& B = a.blocks[b];
+        if (B.kind != ARC_BLOCK_ARC) continue;
+        for (long long p = warp; p < B.m; p += nwarps) {
+            const long long base = B.off + p * B.n;
+            const long long rem = B.len - p * B.n;
+            const int nv = static_cast<int>(rem < B.n ? rem : B.n);
+            float P = 0.0f;
+            for (int c = 0; 1024 * c < nv; ++c) {
+                float acc = 0.0f;
+                for (int sgm = 0; sgm < 8; ++sgm)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int q = 1024 * c + 128 * sgm + 4 * lane + e;
+                        if (q < nv) {
+                            float S = fsub(a.nodes.h[0][base + q], a.nodes.g[0][base + q]);
+                            for (int i = 1; i < a.L; ++i)
+                                S = fadd(S, fsub(a.nodes.h[i][base + q], a.nodes.g[i][base + q]));
+                            acc = ffma(S, S, acc);                                  // O6
+                        }
+                    }
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) acc = fadd(acc, __shfl_xor_sync(kFull, acc, o));
+                P = (c == 0) ? acc : fadd(P, acc);
+            }
+            if (lane == 0) {
+                a.sigma[B.row_base + p] = P;
+                if (!isfinite(P)) atomicOr(a.status, kStatusNonfinite);
+            }
+        }
+    }
+}
+
 }  // namespace
 
 // ---- launchers ---------------------------------------------------------------
@@ -351,6 +395,10 @@ void launch_dense_scatter(const DenseScatterLaunch& a, cudaStream_t s) {
 
 void launch_topk_merge(const MergeLaunch& a, cudaStream_t s) {
     k_topk_merge<<<rows_grid(a.num_rows), 256, 0, s>>>(a);
+}
+
+void launch_exact_sigma(const ExactSigmaLaunch& a, cudaStream_t s) {
+    k_exact_sigma<<<148 * 8, 256, 0, s>>>(a);
 }
 
 void launch_sigma_slice(const SigmaLaunch& a, cudaStream_t s) {

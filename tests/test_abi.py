@@ -151,3 +151,17 @@ def test_apply_update_validation(L):
     assert call(L.ArcOptParams(L.OPT_ADAM, 0.1, 0.9, 0.999, -1.0)) == L.ERR_INVALID_ARG
     assert call(L.ArcOptParams(L.OPT_SGD, math.inf, 0.9, 0.999, 1e-8)) == L.ERR_INVALID_ARG
     assert call(L.ArcOptParams(7, 0.1, 0.9, 0.999, 1e-8)) == L.ERR_UNSUPPORTED
+
+
+def test_exact_method_validation(L):
+    """ARC_METHOD_EXACT (test mode) needs every node on this GPU and no forced exchange."""
+    blocks = [(0, 1000, 10, 100, 3, 0)]
+    p = _params(L, blocks, N=2, nodes_local=2)
+    p.method = L.METHOD_EXACT
+    assert _ws(L, p)[0] == L.OK
+    p = _params(L, blocks, N=4, nodes_local=2)
+    p.method = L.METHOD_EXACT
+    assert _ws(L, p)[0] == L.ERR_UNSUPPORTED
+    p = _params(L, blocks, N=2, nodes_local=2, flags=L.FLAG_FORCE_EXCHANGE)
+    p.method = L.METHOD_EXACT
+    assert _ws(L, p)[0] == L.ERR_UNSUPPORTED

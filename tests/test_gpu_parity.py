@@ -544,3 +544,56 @@ def test_misaligned_pointers_rejected():
     torch.cuda.synchronize()
     assert h[0].any()
     ctx.close()
+
+
+# ------------------------------------------------------------------ exact sketch (test mode)
+
+@pytest.mark.parametrize("N,d,n,K,mixed", [
+    (1, 100_003, 768, 13, False),      # N = 1: the exact sketch is row Top-K of Delta
+    (4, 65_536, 1, 656, False),        # C1 shape (n = 1: coordinate Top-K of the node sum)
+    (3, 40_000, 130, 17, False),       # n % 4 != 0, unaligned rows, ragged last row
+    (2, 3_000 * 2_500 + 7, 2_500, 9, False),   # rows of several 1024-column chunks
+    (4, 0, 0, 0, True),                # ARC blocks + a DENSE block
+])
+def test_exact_sketch_method(orc, N, d, n, K, mixed):
+    """method="exact" (SURVEY §8(b) ARC_SKETCH_EXACT, §8(f) row 3): Sigma_p =
+    ||sum_i Delta_i[p,:]||^2 with the squares in the O6 order — bit-exact
+    against the oracle's exact mode (OracleEF21M(exact=True)): Sigma, the
+    selection, values, h, g and gbar over several steps."""
+    from paper_2510_26709_b200 import ArcTopK
+    if mixed:
+        blocks = [Block(0, 96 * 300 + 5, 301, 96, 11, 0), Block(96 * 300 + 5, 640, 10, 64, 10, 1),
+                  Block(96 * 300 + 645, 50 * 77, 50, 77, 4, 0)]
+        d = 96 * 300 + 645 + 50 * 77
+    else:
+        blocks = flat_blocks(d, n, K=K)
+    src = GradientSource(d, blocks, N, seed=9)
+    ctx = ArcTopK(d, blocks, N=N, eta=0.1, r=4, seed=9, nodes_local=N, method="exact")
+    o = orc.OracleEF21M(d, blocks, N=N, eta=0.1, r=4, seed=9, exact=True)
+    h = [torch.zeros(d, device=DEV) for _ in range(N)]
+    g = [torch.zeros(d, device=DEV) for _ in range(N)]
+    gbar = torch.zeros(d, device=DEV)
+    for t in range(4):
+        gr = [x.numpy() for x in src.grads(t)]
+        sel = torch.empty(ctx.sum_K, dtype=torch.int32, device=DEV)
+        vals = torch.empty(ctx.sum_Kn, dtype=torch.float32, device=DEV) if t % 2 else None
+        ctx.step(t, [torch.from_numpy(x).to(DEV) for x in gr], h, g, gbar, sel, vals)
+        ref = o.step(t, gr, debug=True)
+        torch.cuda.synchronize()
+        assert_same_floats(ctx.query(1).cpu().numpy(), ref["sigma"], f"exact Sigma (t={t})")
+        assert np.array_equal(sel.cpu().numpy(), ref["sel"]), f"selection differs at t={t}"
+        if vals is not None:
+            assert_same_floats(vals.cpu().numpy(), ref["values"], f"values (t={t})")
+    for i in range(N):
+        assert_same_floats(h[i].cpu().numpy(), o.h[i], f"h[{i}]")
+        assert_same_floats(g[i].cpu().numpy(), o.g[i], f"g[{i}]")
+    assert_same_floats(gbar.cpu().numpy(), o.gbar, "gbar")
+    ctx.close()
+
+
+def test_exact_sketch_needs_all_nodes_local():
+    from paper_2510_26709_b200 import ArcTopK
+    from paper_2510_26709_b200._lib import ArcError
+    blocks = flat_blocks(4096, 64, K=4)
+    with pytest.raises(ArcError):
+        ArcTopK(4096, blocks, N=2, eta=0.1, nodes_local=2, method="exact", force_exchange=True, device=DEV)
