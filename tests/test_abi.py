@@ -165,3 +165,25 @@ def test_exact_method_validation(L):
     p = _params(L, blocks, N=2, nodes_local=2, flags=L.FLAG_FORCE_EXCHANGE)
     p.method = L.METHOD_EXACT
     assert _ws(L, p)[0] == L.ERR_UNSUPPORTED
+
+
+def test_product_never_touches_the_oracle():
+    """The product package (Python and CUDA sources) never imports, links or
+    names the oracle; the oracle includes nothing from the product."""
+    import glob
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2510_26709_b200")
+    srcs = glob.glob(os.path.join(pkg, "*.py")) + glob.glob(os.path.join(pkg, "csrc", "*"))
+    assert srcs
+    for p in srcs:
+        txt = open(p, encoding="utf-8", errors="replace").read()
+        assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), p
+        assert "arc_oracle" not in txt and "libarc_oracle" not in txt, p
+    orc = open(os.path.join(root, "oracle", "arc_oracle.c")).read()
+    for inc in re.findall(r'#include\s+[<"]([^>"]+)[>"]', orc):
+        assert not inc.startswith("arc_") or inc == "arc_oracle.h", inc
+    # the loaded product library does not depend on the oracle's shared object
+    import subprocess
+    from paper_2510_26709_b200 import _lib as L
+    out = subprocess.run(["ldd", L.LIB_PATH], capture_output=True, text=True).stdout
+    assert "arc_oracle" not in out
