@@ -187,3 +187,15 @@ def test_product_never_touches_the_oracle():
     from paper_2510_26709_b200 import _lib as L
     out = subprocess.run(["ldd", L.LIB_PATH], capture_output=True, text=True).stdout
     assert "arc_oracle" not in out
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: with the library absent the binding raises on first use."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import paper_2510_26709_b200._lib as L\n"
+            "try:\n    L.lib()\nexcept RuntimeError as e:\n    print('RAISED', 'missing' in str(e))\n")
+    env = dict(os.environ, ARC_LIB_PATH=str(tmp_path / "absent.so"), PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root)
+    assert "RAISED True" in out.stdout, out.stderr
