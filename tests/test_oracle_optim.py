@@ -111,3 +111,18 @@ def test_adam_pin_sensitivity(orc, bad):
     for t, gb in enumerate(gb_seq, 1):
         x, m, v = orc.apply_adam(x, m, v, gb.astype(np.float32), t, 1e-2, 0.9, 0.999, 1e-8)
     assert np.max(np.abs(x - good)) < 2e-5
+
+
+def test_adam_eps_outside_sqrt_and_bias_correction_dyadic(orc):
+    # beta1 = beta2 = 0.5, t = 1: bc1 = bc2 = 0.5, m = 0.5 g, v = 0.5 g^2, so
+    # mhat = g and vhat = g^2 exactly; with eps = 1 the step is g / (|g| + 1)
+    # (eps OUTSIDE the square root, Kingma & Ba Alg. 1): for g = 3 that is
+    # 3/4, and x = 1 - 0.5 * 0.75 = 0.625 exactly (inside it would be 3/sqrt(10))
+    x, m, v = orc.apply_adam(np.array([1.0, 1.0], np.float32), np.zeros(2, np.float32), np.zeros(2, np.float32),
+                             np.array([3.0, -1.0], np.float32), 1, 0.5, 0.5, 0.5, 1.0)
+    assert np.array_equal(x, np.array([0.625, 1.25], np.float32))
+    assert np.array_equal(m, np.array([1.5, -0.5], np.float32))
+    assert np.array_equal(v, np.array([4.5, 0.5], np.float32))
+    # t = 2 with the same g: m = 0.75 g, v = 0.75 g^2, bc = 0.75: mhat = g, vhat = g^2 again
+    x2, m2, v2 = orc.apply_adam(x, m, v, np.array([3.0, -1.0], np.float32), 2, 0.5, 0.5, 0.5, 1.0)
+    assert np.array_equal(x2, np.array([0.25, 1.5], np.float32))
