@@ -111,6 +111,8 @@ typedef enum {
 #define ARC_FLAG_HOST_STAGING   0x1u  /* reserve device staging for arc_topk_step_host          */
 #define ARC_FLAG_DEBUG_SKETCH   0x2u  /* keep P_i for arc_topk_query(ARC_Q_P_NODES)              */
 #define ARC_FLAG_FORCE_EXCHANGE 0x4u  /* G == 1: run the G > 1 kernel sequence (tests)           */
+#define ARC_FLAG_LOOPBACK_COMM  0x8u  /* nccl_comm is an arc_topk_loopback_comm() handle: G ranks   */
+                                      /* emulated in one process on one GPU (tests; not with LSA)  */
 
 /* One block: the m x n row-major view of flat elements [offset, offset+len),
  * (m-1) n < len <= m n (only the last row may be short, R14).  K rows kept,
@@ -182,7 +184,9 @@ typedef enum {
     ARC_Q_SEL = 2,      /* int32 [sum_b K_b]             I_b                                   */
     ARC_Q_P_NODES = 3,  /* float [sum_ARC m_b][nodes_local][r]  P'_i = G_i V, unscaled (needs
                            DEBUG_SKETCH, or G > 1, or nodes_local > 1)                         */
-    ARC_Q_CANDIDATES = 4 /* uint32 [num_blocks] rows sharing the boundary bin of the last selection */
+    ARC_Q_CANDIDATES = 4 /* uint32 [num_blocks] rows sharing the boundary bin of the last selection
+                            ([nodes_local][num_blocks] for ARC_METHOD_TOPK_ALLGATHER, whose
+                            nodes select separately); synchronises the step's stream first    */
 } arc_query;
 arc_status arc_topk_query(arc_topk_ctx* ctx, int32_t what, void* dst, size_t bytes, void* stream);
 
@@ -241,6 +245,32 @@ typedef struct {
 } arc_opt_params;
 arc_status arc_topk_apply_update(const arc_opt_params* params, int64_t t, float* x, const float* gbar,
                                  float* m, float* v, int64_t d, void* stream);
+
+/* Ledger audit (Table I): the floats this rank handed to the
+ * step's collectives since create, summed over steps.  out[0] = sketch entries
+ * sent to other ranks in exchange #1 (all-to-all of row slices of P'_i),
+ * out[1] = Sigma entries contributed to the Sigma all-gather, out[2] = value
+ * entries handed to exchange #2 (all-reduce: sum_b K_b n_b per step; ORDERED:
+ * nodes_local x that; Top-K baseline: its all-gathered payload), out[3] =
+ * collective calls, out[4] = steps.  n <= 8 slots are copied (the rest are 0).
+ * Host-only; ARC_ERR_INVALID_ARG for a NULL ctx / out or n outside [1, 8]. */
+arc_status arc_topk_comm_tally(const arc_topk_ctx* ctx, int64_t* out, int32_t n);
+
+/* In-process loopback communicator (tests without G GPUs): G ranks emulated in
+ * ONE process on the current GPU.  Each rank is a host thread with its own
+ * context (created with ARC_FLAG_LOOPBACK_COMM and the handle of
+ * arc_topk_loopback_comm as nccl_comm) and its own stream; the collectives meet
+ * at host barriers and order the ranks' streams with CUDA events only (no
+ * kernel waits on another rank).  The all-reduce sums the ranks in descending
+ * rank order (not the oracle's order: it stands in for NCCL's).  A barrier that
+ * waits more than 120 s fails the call with ARC_ERR_NCCL (and every later one).
+ *   create : G in [1, 64]; *group receives the group (library-owned)
+ *   comm   : *comm receives rank's handle (valid until destroy)
+ *   destroy: synchronises the device, frees the group (every context using it
+ *            must be destroyed first)                                         */
+arc_status arc_topk_loopback_create(int32_t G, void** group);
+arc_status arc_topk_loopback_comm(void* group, int32_t rank, void** comm);
+arc_status arc_topk_loopback_destroy(void* group);
 
 /* Frees the host context (synchronises first).  Never frees caller memory. */
 arc_status arc_topk_destroy(arc_topk_ctx* ctx);

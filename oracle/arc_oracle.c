@@ -36,11 +36,39 @@
  *
  * The definitions are written out with plain loops; nothing is blocked, fused
  * or reordered beyond what ARC-NUM v1 fixes.  It is deliberately slow.
+ *
+ * Threads.  Loops over independent rows (or elements) may be split across
+ * OpenMP threads (orc_set_threads; 1 thread unless asked): every row's or
+ * element's arithmetic is the same sequence of operations whichever thread
+ * runs it, so the results are bit-identical to one thread (pinned in
+ * tests/test_oracle.py).  No sum crosses rows, so nothing is reordered.
  */
 #include <math.h>
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
+
+/* Threads for the row-parallel loops (see the header); 1 = the plain oracle. */
+void orc_set_threads(int32_t n)
+{
+#ifdef _OPENMP
+    omp_set_num_threads(n > 0 ? n : 1);
+#else
+    (void)n;
+#endif
+}
+
+int32_t orc_get_threads(void)
+{
+#ifdef _OPENMP
+    return (int32_t)omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
 
 /* ------------------------------------------------------------------------- */
 /* Counter-based generator [R8]: Philox4x32-10 (Salmon et al., SC'11).        */
@@ -305,12 +333,14 @@ void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int3
         /* Alg.1 l.4: P'_i = G_i V, entry (p, j) the O6 dot product of row p
          * with column j of V [R2, R9]. */
         for (int32_t i = 0; i < N; i++)
+#pragma omp parallel for schedule(static)
             for (int64_t p = 0; p < m; p++) {
                 int64_t nv = row_len(len, n, p);
                 for (int32_t j = 0; j < r; j++)
                     Pn[((size_t)i * m + p) * r + j] = o6_dot(G[i] + p * n, V + j, r, nv);
             }
         /* Alg.1 l.5: S = sum_i P'_i, the node sum in ascending node id [R9]. */
+#pragma omp parallel for schedule(static)
         for (int64_t p = 0; p < m; p++)
             for (int32_t j = 0; j < r; j++) {
                 float s = Pn[(size_t)p * r + j];
@@ -318,6 +348,7 @@ void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int3
                 Sa[(size_t)p * r + j] = s;
             }
         /* Alg.1 l.6: Sigma = diag(S S^T) (O8) [R3]. */
+#pragma omp parallel for schedule(static)
         for (int64_t p = 0; p < m; p++) {
             float s = 0.0f;
             for (int32_t j = 0; j < r; j++) s = fmaf(Sa[(size_t)p * r + j], Sa[(size_t)p * r + j], s);
@@ -340,6 +371,7 @@ void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int3
     orc_argtop_k(Sg, m, K, sel);
 
     /* Alg.1 l.7-8: C_local(G_i) = [G_i]_{I,:};  C = (1/N) sum_i C_local(G_i). */
+#pragma omp parallel for schedule(static)
     for (int64_t k = 0; k < K; k++) {
         int64_t p = sel[k];
         int64_t nv = row_len(len, n, p);
@@ -411,6 +443,7 @@ int orc_step(const orc_cfg* cfg, int64_t t,
     /* eq:ef21m-1: h_t = (1 - eta) h_{t-1} + eta grad, as
      * fma(eta, grad, (1 - eta) h) (ARC-NUM v1 O1, O2) [R11] */
     for (int32_t i = 0; i < N; i++)
+#pragma omp parallel for schedule(static)
         for (int64_t e = 0; e < cfg->d; e++)
             h[i][e] = fmaf(eta, grad[i][e], one_minus_eta * h[i][e]);
 
@@ -423,6 +456,7 @@ int orc_step(const orc_cfg* cfg, int64_t t,
         float** D = (float**)malloc((size_t)N * sizeof(float*));
         for (int32_t i = 0; i < N; i++) {
             D[i] = (float*)malloc((size_t)len * sizeof(float));
+#pragma omp parallel for schedule(static)
             for (int64_t e = 0; e < len; e++) D[i][e] = h[i][B->offset + e] - g[i][B->offset + e];
         }
         int32_t* sel = (int32_t*)malloc((size_t)K * sizeof(int32_t));
@@ -480,7 +514,9 @@ int orc_step(const orc_cfg* cfg, int64_t t,
         }
 
         /* eq:ef21m-2: g_t = g_{t-1} + C_local(h_t - g_{t-1}); rows outside I
-         * receive + 0 and are left as they are [R12].  gbar += C [R13]. */
+         * receive + 0 and are left as they are [R12].  gbar += C [R13].
+         * (The rows of I are distinct, so rows may run on any thread.) */
+#pragma omp parallel for schedule(static)
         for (int64_t k = 0; k < K; k++) {
             int64_t p = sel[k];
             int64_t nv = row_len(len, n, p);

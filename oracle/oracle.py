@@ -21,7 +21,7 @@ _LIB_PATH = os.path.join(_HERE, "libarc_oracle.so")
 # no fast-math.  (The only FMAs are the explicit fmaf() calls ARC-NUM v1 and
 # ARC-RNG v1 prescribe: the momentum, the O6 sketch order, Sigma, ln/sincos.)
 CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
-          "-fexcess-precision=standard", "-Wall"]
+          "-fexcess-precision=standard", "-Wall", "-fopenmp"]
 
 
 def build(force: bool = False) -> str:
@@ -69,6 +69,9 @@ def lib():
         L.orc_step_noef.restype = ctypes.c_int
         L.orc_apply_sgd.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_float]
         L.orc_apply_adam.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64] + [ctypes.c_float] * 4
+        L.orc_set_threads.argtypes = [ctypes.c_int32]
+        L.orc_get_threads.restype = ctypes.c_int32
+        L.orc_set_threads(1)          # the plain oracle unless a caller asks for threads
         _lib = L
     return _lib
 
@@ -104,6 +107,15 @@ def _ptr(a: np.ndarray) -> int:
 def _f32(a) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.float32)
     return a
+
+
+def set_threads(n: int) -> None:
+    """Threads for the oracle's row-parallel loops (bit-identical to 1 thread)."""
+    lib().orc_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
 
 
 def philox4x32_10(ctr, key) -> np.ndarray:
@@ -291,7 +303,7 @@ class OracleEF21M:
         return dict(sel=sel.reshape(self.N, self.sum_K), values=vals.reshape(self.N, self.sum_Kn))
 
 
-__all__ = ["Block", "OracleEF21M", "apply_adam", "apply_sgd", "arc_round", "argtop_k", "build", "gaussian_V", "ln", "ln_array", "lib",
+__all__ = ["Block", "OracleEF21M", "get_threads", "set_threads", "apply_adam", "apply_sgd", "arc_round", "argtop_k", "build", "gaussian_V", "ln", "ln_array", "lib",
            "momentum", "philox4x32_10", "randk_keys", "sigma_key", "sigma_rows", "sincos2pi", "sincos2pi_array",
            "uniform"]
 

@@ -13,7 +13,8 @@ PyTorch supplies device memory, streams and the process group only.
 """
 from __future__ import annotations
 
-from .api import ArcTopK, Block, apply_update, flat_layout, nccl_comm_ptr, per_tensor_layout  # noqa: F401
+from .api import (ArcTopK, Block, LoopbackGroup, apply_update, flat_layout, nccl_comm_ptr,  # noqa: F401
+                  per_tensor_layout)
 from .ledger import comm_entries  # noqa: F401
 
-__all__ = ["ArcTopK", "Block", "apply_update", "flat_layout", "per_tensor_layout", "nccl_comm_ptr", "comm_entries"]
+__all__ = ["ArcTopK", "Block", "LoopbackGroup", "apply_update", "flat_layout", "per_tensor_layout", "nccl_comm_ptr", "comm_entries"]

@@ -16,7 +16,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libarctopk.so")
 SOURCES = [os.path.join(CSRC, "arc_kernels.cu"), os.path.join(CSRC, "arc_sketch.cu"),
            os.path.join(CSRC, "arc_select.cu"), os.path.join(CSRC, "arc_lsa.cu"),
-           os.path.join(CSRC, "arc_optim.cu"), os.path.join(CSRC, "arc_api.cu")]
+           os.path.join(CSRC, "arc_optim.cu"), os.path.join(CSRC, "arc_loopback.cu"),
+           os.path.join(CSRC, "arc_api.cu")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -48,7 +49,8 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = SOURCES + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "arc_topk.h")]
+    deps = SOURCES + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
+        [os.path.join(ROOT, "include", "arc_topk.h")]
     return any(os.path.getmtime(p) > t for p in deps)
 
 

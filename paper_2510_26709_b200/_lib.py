@@ -23,7 +23,7 @@ BLOCK_ARC, BLOCK_DENSE = 0, 1
 # arc_reduce_mode
 REDUCE_NCCL, REDUCE_ORDERED, REDUCE_LSA = 0, 1, 2
 # flags
-FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE = 0x1, 0x2, 0x4
+FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE, FLAG_LOOPBACK_COMM = 0x1, 0x2, 0x4, 0x8
 # arc_method
 METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK, METHOD_NOEF_MSGD, METHOD_EXACT = 0, 1, 2, 3, 4
 # arc_opt_kind
@@ -35,8 +35,10 @@ EXPORTED = [
     "arc_topk_workspace_bytes", "arc_topk_create", "arc_topk_step", "arc_topk_step_host",
     "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_kernels_per_step",
     "arc_topk_destroy", "arc_topk_status_string", "arc_topk_set_timing", "arc_topk_read_timing",
-    "arc_topk_debug_stamps", "arc_topk_apply_update",
+    "arc_topk_debug_stamps", "arc_topk_apply_update", "arc_topk_comm_tally",
+    "arc_topk_loopback_create", "arc_topk_loopback_comm", "arc_topk_loopback_destroy",
 ]
+TALLY_NAMES = ["sketch", "sigma", "values", "calls", "steps"]
 TIMING_PHASES = 6
 PHASE_NAMES = ["vgen", "ef_sketch", "exchange1_reduce", "select_gather", "exchange2_scatter", "copy_out"]
 
@@ -93,12 +95,18 @@ def lib():
         L.arc_topk_debug_stamps.argtypes = [vp, vp, i64, P(i32)]
         L.arc_topk_debug_stamps.restype = ctypes.c_int
         L.arc_topk_apply_update.argtypes = [P(ArcOptParams), i64, vp, vp, vp, vp, i64, vp]
+        L.arc_topk_comm_tally.argtypes = [vp, P(i64), i32]
+        L.arc_topk_loopback_create.argtypes = [i32, P(vp)]
+        L.arc_topk_loopback_comm.argtypes = [vp, i32, P(vp)]
+        L.arc_topk_loopback_destroy.argtypes = [vp]
         L.arc_topk_destroy.argtypes = [vp]
         L.arc_topk_status_string.argtypes = [ctypes.c_int]
         L.arc_topk_status_string.restype = ctypes.c_char_p
         for name in ["arc_topk_workspace_bytes", "arc_topk_create", "arc_topk_step", "arc_topk_step_host",
                      "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_destroy",
-                     "arc_topk_set_timing", "arc_topk_read_timing", "arc_topk_apply_update"]:
+                     "arc_topk_set_timing", "arc_topk_read_timing", "arc_topk_apply_update",
+                     "arc_topk_comm_tally", "arc_topk_loopback_create", "arc_topk_loopback_comm",
+                     "arc_topk_loopback_destroy"]:
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib

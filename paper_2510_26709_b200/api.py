@@ -97,12 +97,19 @@ class ArcTopK:
       rank: this GPU's rank in pg.  reduce: "nccl" (All-Reduce of the K rows)
       or "ordered" (bit-exact node-ordered sum) or "lsa" (both exchanges
       fused into the library's kernels over NCCL symmetric windows, bit-exact).
+      comm_group: an NCCL group over pg's ranks for the library's collectives
+      (``dist.private_nccl_group(pg, device)``), shared by several contexts;
+      default: a private group per context.
+      loopback: a :class:`LoopbackGroup` of G = N / nodes_local emulated ranks
+      (tests on one GPU; this context is rank ``rank`` of it, and must be
+      created and stepped from its own host thread, concurrently with the
+      other ranks'); no process group is used then.
     """
 
     def __init__(self, d: int, blocks: Sequence, N: int, eta: float, r: int = 4, seed: int = 20251030,
                  nodes_local: int | None = None, pg=None, rank: int = 0, reduce: str = "nccl",
                  host_staging: bool = False, debug_sketch: bool = False, force_exchange: bool = False,
-                 method: str = "arc", device=None, stream=None):
+                 method: str = "arc", device=None, stream=None, comm_group=None, loopback=None):
         self.lib = L.lib()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.d, self.N = int(d), int(N)
@@ -112,7 +119,7 @@ class ArcTopK:
         self._cblocks = (L.ArcBlock * len(self.blocks))(*[
             L.ArcBlock(int(b.offset), int(b.len), int(b.m), int(b.n), int(b.K), int(b.kind), 0) for b in self.blocks])
         flags = (L.FLAG_HOST_STAGING if host_staging else 0) | (L.FLAG_DEBUG_SKETCH if debug_sketch else 0) | \
-                (L.FLAG_FORCE_EXCHANGE if force_exchange else 0)
+                (L.FLAG_FORCE_EXCHANGE if force_exchange else 0) | (L.FLAG_LOOPBACK_COMM if loopback is not None else 0)
         self.params = L.ArcParams(L.ABI_VERSION, self.N, self.nodes_local, int(rank), self.d, int(r),
                                   len(self.blocks), self._cblocks, float(eta),
                                   {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED, "lsa": L.REDUCE_LSA}[reduce],
@@ -127,14 +134,21 @@ class ArcTopK:
         self.workspace = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=self.device)
         comm = None
         self._pg = None
-        if self.G > 1 or (pg is not None and force_exchange):
+        if loopback is not None:
+            if loopback.G != self.G:
+                raise ValueError(f"loopback group has {loopback.G} ranks, N / nodes_local = {self.G}")
+            comm = loopback.comm(int(rank))
+        elif self.G > 1 or (pg is not None and force_exchange):
             if pg is None:
                 raise ValueError("N / nodes_local > 1 needs an NCCL process group")
             from .dist import check_consistent, params_digest, private_nccl_group
             check_consistent(pg, params_digest(d, self.blocks, self.N, self.nodes_local, r, eta, seed, reduce))
             # the library's collectives get a communicator of their own, so they can
-            # never interleave with torch's collectives on the caller's group
-            self._pg = private_nccl_group(pg, self.device)
+            # never interleave with torch's collectives on the caller's group; several
+            # contexts (e.g. one per DDP bucket) may share one: comm_group, made once
+            # with dist.private_nccl_group (their steps are issued in the same order
+            # on every rank, NCCL's rule for a shared communicator)
+            self._pg = comm_group if comm_group is not None else private_nccl_group(pg, self.device)
             import torch.distributed as dist
             self.params.rank = dist.get_rank(self._pg)     # this GPU's rank in the library's communicator
             comm = nccl_comm_ptr(self._pg, self.device)
@@ -198,7 +212,8 @@ class ArcTopK:
         shapes = {L.Q_V: (self.sum_nr_arc, torch.float32), L.Q_SIGMA: (self.sum_m_arc, torch.float32),
                   L.Q_SEL: (self.sum_K, torch.int32),
                   L.Q_P_NODES: (self.sum_m_arc * self.nodes_local * self.r, torch.float32),
-                  L.Q_CANDIDATES: (len(self.blocks), torch.int32)}
+                  L.Q_CANDIDATES: (len(self.blocks) * (self.nodes_local if self.method == "topk_allgather" else 1),
+                                   torch.int32)}
         n, dt = shapes[what]
         out = torch.empty(max(n, 1), dtype=dt, device=self.device)
         L.check(self.lib.arc_topk_query(self.ctx, int(what), int(out.data_ptr()), out.numel() * out.element_size(),
@@ -225,6 +240,13 @@ class ArcTopK:
                 "arc_topk_read_timing")
         return {name: float(ms[k]) for k, name in enumerate(L.PHASE_NAMES)}, int(steps.value)
 
+    def comm_tally(self) -> dict:
+        """Floats this rank handed to the step's collectives since create (Table I
+        ledger audit): sketch (exchange #1), sigma, values (exchange #2), calls, steps."""
+        out = (ctypes.c_int64 * 8)()
+        L.check(self.lib.arc_topk_comm_tally(self.ctx, out, 8), "arc_topk_comm_tally")
+        return {name: int(out[k]) for k, name in enumerate(L.TALLY_NAMES)}
+
     @property
     def kernels_per_step(self) -> int:
         return int(self.lib.arc_topk_kernels_per_step(self.ctx))
@@ -240,6 +262,30 @@ class ArcTopK:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackGroup:
+    """G ranks emulated in one process on the current GPU (arc_topk_loopback_*):
+    the library's multi-GPU step sequence with stream-event-ordered copies in
+    place of NCCL, for tests on one GPU.  Each rank's ArcTopK lives in its own
+    host thread (ctypes releases the GIL during the library's calls)."""
+
+    def __init__(self, G: int):
+        self.lib = L.lib()
+        self.G = int(G)
+        h = ctypes.c_void_p()
+        L.check(self.lib.arc_topk_loopback_create(self.G, ctypes.byref(h)), "arc_topk_loopback_create")
+        self.handle = h
+
+    def comm(self, rank: int) -> int:
+        c = ctypes.c_void_p()
+        L.check(self.lib.arc_topk_loopback_comm(self.handle, int(rank), ctypes.byref(c)), "arc_topk_loopback_comm")
+        return int(c.value)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.arc_topk_loopback_destroy(self.handle)
+            self.handle = None
 
 
 def apply_update(x: torch.Tensor, gbar: torch.Tensor, gamma: float, *, optimizer: str = "sgd",

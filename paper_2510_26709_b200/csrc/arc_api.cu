@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "arc_internal.cuh"
+#include "arc_loopback.h"
 #include "nccl.h"   // types only (torch wheel's NCCL 2.28); functions are resolved with dlsym
 #include "nccl_device.h"   // ncclDevComm / requirements types (ARC_REDUCE_LSA)
 
@@ -75,6 +76,49 @@ bool load_nccl(Nccl& n) {
     return n.ok;
 }
 
+// ---- the step's collectives: NCCL, or the in-process loopback group ------------
+// (arc_loopback.cu: G emulated ranks on one GPU, for tests without G GPUs).
+// Every call also tallies the floats this rank hands to the collective, for the
+// Table I ledger audit (arc_topk_comm_tally).
+struct Comm {
+    const Nccl* nccl = nullptr;
+    ncclComm_t nc = nullptr;
+    LoopbackComm* lb = nullptr;
+    bool any() const { return nc != nullptr || lb != nullptr; }
+    arc_status all_gather_bytes(const void* send, void* recv, size_t bytes, cudaStream_t s) const {
+        if (lb) return loopback_all_gather(lb, send, recv, bytes, s);
+        return nccl->allGather(send, recv, bytes, ncclUint8, nc, s) == ncclSuccess ? ARC_OK : ARC_ERR_NCCL;
+    }
+    arc_status all_gather_f32(const float* send, float* recv, size_t count, cudaStream_t s) const {
+        if (lb) return loopback_all_gather(lb, send, recv, count * sizeof(float), s);
+        return nccl->allGather(send, recv, count, ncclFloat32, nc, s) == ncclSuccess ? ARC_OK : ARC_ERR_NCCL;
+    }
+    arc_status all_reduce_f32(const float* send, float* recv, size_t count, cudaStream_t s) const {
+        if (lb) return loopback_all_reduce_f32(lb, send, recv, count, s);
+        return nccl->allReduce(send, recv, count, ncclFloat32, ncclSum, nc, s) == ncclSuccess ? ARC_OK : ARC_ERR_NCCL;
+    }
+    // grouped point-to-point all-to-all (counts / displacements in floats, host arrays [G])
+    arc_status all_to_all_f32(const float* send, const size_t* scount, const size_t* sdispl, float* recv,
+                              const size_t* rcount, const size_t* rdispl, int G, cudaStream_t s) const {
+        if (lb) return loopback_all_to_all_f32(lb, send, scount, sdispl, recv, rcount, rdispl, s);
+        if (nccl->groupStart() != ncclSuccess) return ARC_ERR_NCCL;
+        for (int j = 0; j < G; ++j) {
+            if (scount[j] > 0 && nccl->send(send + sdispl[j], scount[j], ncclFloat32, j, nc, s) != ncclSuccess) {
+                nccl->groupEnd();
+                return ARC_ERR_NCCL;
+            }
+            if (rcount[j] > 0 && nccl->recv(recv + rdispl[j], rcount[j], ncclFloat32, j, nc, s) != ncclSuccess) {
+                nccl->groupEnd();
+                return ARC_ERR_NCCL;
+            }
+        }
+        return nccl->groupEnd() == ncclSuccess ? ARC_OK : ARC_ERR_NCCL;
+    }
+};
+
+// ledger tally slots (floats this rank handed to each collective, summed over steps)
+enum { kTallySketch = 0, kTallySigma = 1, kTallyValues = 2, kTallyCalls = 3, kTallySteps = 4, kTallyN = 8 };
+
 // ---- derived layout -----------------------------------------------------------
 struct Plan {
     int G = 1, L = 1;
@@ -123,7 +167,8 @@ arc_status validate(const arc_topk_params* p) {
     if (p->value_reduce != ARC_REDUCE_NCCL && p->value_reduce != ARC_REDUCE_ORDERED && p->value_reduce != ARC_REDUCE_LSA)
         return ARC_ERR_INVALID_ARG;
     if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
-    if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE)) return ARC_ERR_INVALID_ARG;
+    if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE | ARC_FLAG_LOOPBACK_COMM))
+        return ARC_ERR_INVALID_ARG;
     if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER && p->method != ARC_METHOD_RANDK &&
         p->method != ARC_METHOD_NOEF_MSGD && p->method != ARC_METHOD_EXACT)
         return ARC_ERR_INVALID_ARG;
@@ -399,7 +444,7 @@ uint64_t params_hash(const arc_topk_params* p) {
     h = fnv1a(h, &p->eta, sizeof p->eta);
     h = fnv1a(h, &p->value_reduce, sizeof p->value_reduce);
     h = fnv1a(h, &p->seed, sizeof p->seed);
-    const uint32_t f = p->flags & ~ARC_FLAG_HOST_STAGING;
+    const uint32_t f = p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_LOOPBACK_COMM);
     h = fnv1a(h, &f, sizeof f);
     return h;
 }
@@ -411,7 +456,10 @@ struct arc_topk_ctx {
     std::vector<arc_block> blocks;
     Plan pl;
     Nccl nccl;
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;       // NCCL communicator (borrowed), or
+    LoopbackComm* lb = nullptr;      // the loopback group's rank handle (ARC_FLAG_LOOPBACK_COMM)
+    Comm xc;                         // the step's collectives over either
+    int64_t tally[kTallyN] = {};
     unsigned char* ws = nullptr;
     int grid = 0, num_tiles = 0, shape = 0, vs_cap = 0;
     int grid_w = 0, vs_cap_w = 0, tiles_w0 = 0;   // the wide blocks' ranged launch (grid_w == 0: none)
@@ -421,7 +469,6 @@ struct arc_topk_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;   // (ARC_TIMING_PHASES + 1) per timed step
     int timed_steps = 0;
-    uint64_t step_count = 0;     // parity of the selection's double-buffered candidate counters
     unsigned long long* stamps = nullptr;   // debug (ARC_DEBUG_STAMPS=1): library-owned device buffer
     int64_t v_ready = -1;        // t whose V the previous step generated speculatively
     bool pdl = true;             // programmatic dependent launch between the step's kernels (ARC_PDL=0: off)
@@ -584,7 +631,17 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     c->last = s;
 
     const int G = c->pl.G;
-    if (G > 1) {
+    if ((params->flags & ARC_FLAG_LOOPBACK_COMM) != 0) {
+        // the in-process loopback group (tests: G emulated ranks on one GPU)
+        if (nccl_comm == nullptr) { delete c; return ARC_ERR_INVALID_ARG; }
+        if (params->value_reduce == ARC_REDUCE_LSA) { delete c; return ARC_ERR_UNSUPPORTED; }
+        c->lb = static_cast<LoopbackComm*>(nccl_comm);
+        if (loopback_nranks(c->lb) != G || loopback_rank(c->lb) != (G > 1 ? params->rank : 0)) {
+            delete c;
+            return ARC_ERR_INVALID_ARG;
+        }
+        c->xc.lb = c->lb;
+    } else if (G > 1) {
         if (nccl_comm == nullptr) { delete c; return ARC_ERR_INVALID_ARG; }
         if (!load_nccl(c->nccl)) { delete c; return ARC_ERR_NCCL; }
         c->comm = static_cast<ncclComm_t>(nccl_comm);
@@ -597,6 +654,10 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
     } else if (nccl_comm != nullptr) {
         if (!load_nccl(c->nccl)) { delete c; return ARC_ERR_NCCL; }
         c->comm = static_cast<ncclComm_t>(nccl_comm);
+    }
+    if (c->comm != nullptr) {
+        c->xc.nccl = &c->nccl;
+        c->xc.nc = c->comm;
     }
 
     // static tables
@@ -725,7 +786,7 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
         uint64_t* dh = c->at<uint64_t>(c->pl.o_hash);
         std::vector<uint64_t> all(G, 0);
         if (cudaMemcpyAsync(dh + G, &mine, 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-            c->nccl.allGather(dh + G, dh, 8, ncclUint8, c->comm, s) != ncclSuccess ||
+            c->xc.all_gather_bytes(dh + G, dh, 8, s) != ARC_OK ||
             cudaMemcpyAsync(all.data(), dh, 8 * G, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess) {
             delete c;
@@ -796,7 +857,11 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ARC_MARK(0);
     // S0 (skipped when the previous step already generated V for this t)
     float* V_t = V + static_cast<size_t>(t & 1) * pl.sum_nr;
-    if (pl.M > 0 && !pl.topk && !pl.randk && c->v_ready != t) {
+    // (a captured step always draws its own V: a replay must not depend on what
+    // eager steps between capture and replay left in the double buffer)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return ARC_ERR_CUDA;
+    if (pl.M > 0 && !pl.topk && !pl.randk && (c->v_ready != t || cap != cudaStreamCaptureStatusNone)) {
         launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V_t, s);
         ARC_LAUNCHED();
     }
@@ -880,22 +945,21 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         auto slice_rows = [&](int j) { return std::max<int64_t>(0, std::min<int64_t>(pl.M, (j + 1) * Ms) - j * Ms); };
         float* xs = c->at<float>(pl.o_pnodes);
         const float* x = xs;
-        if (pl.exchange && c->comm != nullptr) {
+        if (pl.exchange && c->xc.any()) {
+            // rank j owns rows [j Ms, (j+1) Ms): send it those rows' sketches of
+            // this GPU's nodes, receive this rank's rows from every rank
             float* xr = c->at<float>(pl.o_xrecv);
-            if (c->nccl.groupStart() != ncclSuccess) return ARC_ERR_NCCL;
+            std::vector<size_t> sc(G), sd(G), rc(G), rd(G);
             for (int j = 0; j < G; ++j) {
-                const size_t out = static_cast<size_t>(slice_rows(j)) * row_floats;
-                const size_t in = static_cast<size_t>(slice_rows(me)) * row_floats;
-                if (out > 0 && c->nccl.send(xs + j * Ms * row_floats, out, ncclFloat32, j, c->comm, s) != ncclSuccess) {
-                    c->nccl.groupEnd();
-                    return ARC_ERR_NCCL;
-                }
-                if (in > 0 && c->nccl.recv(xr + j * Ms * row_floats, in, ncclFloat32, j, c->comm, s) != ncclSuccess) {
-                    c->nccl.groupEnd();
-                    return ARC_ERR_NCCL;
-                }
+                sc[j] = static_cast<size_t>(slice_rows(j)) * row_floats;
+                sd[j] = static_cast<size_t>(j) * Ms * row_floats;
+                rc[j] = static_cast<size_t>(slice_rows(me)) * row_floats;
+                rd[j] = static_cast<size_t>(j) * Ms * row_floats;
+                if (j != me) c->tally[kTallySketch] += static_cast<int64_t>(sc[j]);
             }
-            if (c->nccl.groupEnd() != ncclSuccess) return ARC_ERR_NCCL;
+            const arc_status xs_st = c->xc.all_to_all_f32(xs, sc.data(), sd.data(), xr, rc.data(), rd.data(), G, s);
+            if (xs_st != ARC_OK) return xs_st;
+            ++c->tally[kTallyCalls];
             x = xr;
         }
         SigmaLaunch sl{};
@@ -910,9 +974,12 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sl.status = status;
         launch_sigma_slice(sl, s);
         ARC_LAUNCHED();
-        if (pl.exchange && c->comm != nullptr &&
-            c->nccl.allGather(sigma + me * Ms, sigma, static_cast<size_t>(Ms), ncclFloat32, c->comm, s) != ncclSuccess)
-            return ARC_ERR_NCCL;
+        if (pl.exchange && c->xc.any()) {
+            const arc_status ag = c->xc.all_gather_f32(sigma + me * Ms, sigma, static_cast<size_t>(Ms), s);
+            if (ag != ARC_OK) return ag;
+            c->tally[kTallySigma] += Ms;
+            ++c->tally[kTallyCalls];
+        }
     }
     if (sigma_pass && pl.exact) {   // test mode: Sigma from the exact row norms of the node sum
         ExactSigmaLaunch ex{};
@@ -973,7 +1040,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.cand = c->at<unsigned>(pl.o_cand);
         sg.cand_count = c->at<unsigned>(pl.o_cand_count);
         sg.num_blocks = static_cast<int>(pl.sbdev.size());
-        sg.parity = static_cast<int>(c->step_count & 1);
+        sg.parity = status + 1;   // device-side parity word (status[1])
         sg.sel = pl.topk ? reinterpret_cast<int32_t*>(wire) : sel;
         sg.stamps = c->stamps;
         sg.pdl = c->pdl && !c->timing && !(pl.exchange && pl.M > 0) ? 1 : 0;
@@ -1029,8 +1096,10 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         const float* all = wire;
         if (pl.G > 1) {
             float* dst = c->at<float>(pl.o_wire_all);
-            if (c->nccl.allGather(wire, dst, static_cast<size_t>(pl.W) * L, ncclFloat32, c->comm, s) != ncclSuccess)
-                return ARC_ERR_NCCL;
+            const arc_status ag = c->xc.all_gather_f32(wire, dst, static_cast<size_t>(pl.W) * L, s);
+            if (ag != ARC_OK) return ag;
+            c->tally[kTallyValues] += pl.W * L;
+            ++c->tally[kTallyCalls];
             all = dst;
         }
         for (int j = 0; j < c->p.N; ++j) {
@@ -1084,15 +1153,20 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     } else if (pl.exchange) {   // exchange #2 + S6
         const float* reduced = wire;
         if (!ordered) {
-            if (c->comm != nullptr && pl.G > 1) {
-                if (c->nccl.allReduce(wire, wire, static_cast<size_t>(pl.sumKn), ncclFloat32, ncclSum, c->comm, s) != ncclSuccess)
-                    return ARC_ERR_NCCL;
+            if (c->xc.any() && pl.G > 1) {
+                const arc_status ar = c->xc.all_reduce_f32(wire, wire, static_cast<size_t>(pl.sumKn), s);
+                if (ar != ARC_OK) return ar;
+                c->tally[kTallyValues] += pl.sumKn;
+                ++c->tally[kTallyCalls];
             }
         } else {
             float* all = c->at<float>(pl.o_wire_all);
             const size_t cnt = static_cast<size_t>(pl.sumKn) * L;
-            if (c->comm != nullptr) {
-                if (c->nccl.allGather(wire, all, cnt, ncclFloat32, c->comm, s) != ncclSuccess) return ARC_ERR_NCCL;
+            if (c->xc.any()) {
+                const arc_status ag = c->xc.all_gather_f32(wire, all, cnt, s);
+                if (ag != ARC_OK) return ag;
+                c->tally[kTallyValues] += static_cast<int64_t>(cnt);
+                ++c->tally[kTallyCalls];
             } else {
                 ARC_CUDA(cudaMemcpyAsync(all, wire, cnt * sizeof(float), cudaMemcpyDeviceToDevice, s));
             }
@@ -1137,7 +1211,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         ARC_CUDA(cudaMemcpyAsync(sel_out, sel, sizeof(int32_t) * pl.sumK, cudaMemcpyDeviceToDevice, s));
     ARC_MARK(6);
     if (c->timing) ++c->timed_steps;
-    ++c->step_count;
+    ++c->tally[kTallySteps];
     return ARC_OK;
 }
 
@@ -1186,10 +1260,14 @@ arc_status arc_topk_query(arc_topk_ctx* c, int32_t what, void* dst, size_t bytes
             off = pl.o_pnodes;
             need = sizeof(float) * static_cast<size_t>(pl.M) * pl.L * c->p.r;
             break;
-        case ARC_Q_CANDIDATES:   // counters of the last step's parity
-            off = pl.o_cand_count + sizeof(unsigned) * c->p.num_blocks * ((c->step_count + 1) & 1);
-            need = sizeof(unsigned) * c->p.num_blocks;
+        case ARC_Q_CANDIDATES: {   // counters of the last step's parity (device word status[1], toggled per step)
+            unsigned par = 0;
+            ARC_CUDA(cudaStreamSynchronize(c->last));
+            ARC_CUDA(cudaMemcpy(&par, c->ws + pl.o_status + sizeof(unsigned), sizeof par, cudaMemcpyDeviceToHost));
+            off = pl.o_cand_count + sizeof(unsigned) * pl.sbdev.size() * ((par & 1u) ^ 1u);
+            need = sizeof(unsigned) * pl.sbdev.size();
             break;
+        }
         default: return ARC_ERR_INVALID_ARG;
     }
     if (bytes < need) return ARC_ERR_INVALID_ARG;
@@ -1246,6 +1324,12 @@ arc_status arc_topk_read_timing(arc_topk_ctx* c, float* ms, int32_t n_phases, in
     }
     if (steps) *steps = c->timed_steps;
     c->timed_steps = 0;
+    return ARC_OK;
+}
+
+arc_status arc_topk_comm_tally(const arc_topk_ctx* c, int64_t* out, int32_t n) {
+    if (c == nullptr || out == nullptr || n < 1 || n > kTallyN) return ARC_ERR_INVALID_ARG;
+    for (int k = 0; k < n; ++k) out[k] = c->tally[k];
     return ARC_OK;
 }
 

@@ -85,7 +85,9 @@ struct SelectGatherLaunch {
     unsigned* cand;                // [2][num_blocks][2 * kCandCap] boundary-bin candidates (key | row)
     unsigned* cand_count;          // [2][num_blocks]
     int num_blocks;
-    int parity;                    // step parity: selects this step's candidate buffers
+    unsigned* parity;              // device word: bit 0 selects this step's candidate / boundary
+                                   // counters; toggled by the kernel once every CTA has read it, so
+                                   // a CUDA-graph replay of a captured step stays consistent
     int32_t* sel;
     unsigned long long* stamps;    // debug: [grid][8] %globaltimer at phase boundaries, or nullptr
     // speculative S0 of the next step: V for t_next (nullptr: none)

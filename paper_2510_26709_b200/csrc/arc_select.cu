@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     const bool arc = B.kind == ARC_BLOCK_ARC && B.K < B.m;
     const long long bb = it.b;
     const int sidx = B.slice_base + it.c;
-    const int par = s.parity;
+    const int par = static_cast<int>(__ldcg(s.parity) & 1u);   // read by every CTA before barrier 1
     unsigned* ccount = s.cand_count + par * s.num_blocks;                 // this step's counters
     unsigned* cand = s.cand + (static_cast<long long>(par) * s.num_blocks + bb) * (2 * kCandCap);
 
@@ -614,6 +614,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
         grid.sync();                                 // ---------------- barrier 1
     }
     STAMP(2);
+    // every CTA has read this step's parity (before barrier 1): the next step uses the other one
+    if (blockIdx.x == 0 && tid == 0) *s.parity = static_cast<unsigned>(par ^ 1);
     // any block with more candidates than fit takes the digit-by-digit path
     // (uniform across the grid, so every CTA meets the same barriers)
     bool overflow = false;

@@ -1,4 +1,4 @@
-"""EF21M + ARC-Top-K as a PyTorch DDP communication hook.
+"""EF21M + ARC-Top-K as a PyTorch DDP communication hook (SURVEY.md §8(f) row 1).
 
 Every DDP gradient bucket gets its own compression context (per-tensor blocks
 in the bucket's order: each 2-D (or conv) tensor is an ARC block of rows =
@@ -9,13 +9,22 @@ follows applies x <- x - gamma gbar (eq:ef21m-3) — or Adam on gbar, as
 in the paper's experiments.
 
 For the first `warmup_steps` iterations the hook averages the gradients
-densely (the paper starts compression after 1000 iterations); at the
-switch it initialises the EF21M state with h = g = the local gradient and gbar
-= their average (V_0 = 0, the Theorem 1 setting).
+densely (the paper starts compression after 1000 iterations).  The
+EF21M state of a context is initialised at the first compressed iteration it
+sees — h = g = the local gradient, gbar = their average (V_0 = 0, the Theorem 1
+setting) — so a bucket that DDP rebuilds (it re-buckets once after its
+first iteration) restarts from that state instead of from zeros.
 
-Each bucket's step runs on a side stream that first waits for the backward
-stream, so a bucket's compression overlaps the backward pass of the layers
-still to come; the returned future carries the side stream's completion.
+Scaling (one process per GPU):
+  * one library communicator for every bucket (made once per hook state with
+    ``dist.private_nccl_group``) instead of one per bucket context;
+  * two side streams, alternating by bucket index: bucket b+1's streaming pass
+    (S1, HBM-bound) runs while bucket b's exchanges (S2, S5) wait on NVLink.
+    NCCL keeps one communicator's operations in issue order, and every rank
+    issues the buckets in the same order, as NCCL requires.
+Each side stream first waits for the backward stream, so a bucket's
+compression also overlaps the backward pass of the layers still to come; the
+returned future carries the side stream's completion.
 
     from paper_2510_26709_b200.ddp import ArcTopKHookState, arc_topk_hook
     state = ArcTopKHookState(mu_bp=100, eta=0.1, r=4, seed=1234, warmup_steps=1000)
@@ -50,7 +59,10 @@ def bucket_layout(shapes, mu_bp: int, dense_n: int = 1024) -> tuple[int, list[Bl
 
 
 class ArcTopKHookState:
-    """Hook state: compression settings plus one context and EF21M state per bucket."""
+    """Hook state: compression settings, one context and EF21M state per bucket,
+    the shared library communicator and the two side streams."""
+
+    NUM_STREAMS = 2
 
     def __init__(self, mu_bp: int = 100, eta: float = 0.1, r: int = 4, seed: int = 20251030,
                  warmup_steps: int = 0, process_group=None, reduce: str = "nccl"):
@@ -60,32 +72,49 @@ class ArcTopKHookState:
         self.reduce = reduce
         self.iteration = 0
         self.buckets: dict[int, dict] = {}
-        self._stream = None
+        self._streams: list[torch.cuda.Stream] = []
+        self._comm = None
+        self.contexts_created = 0
 
     def world(self) -> int:
         return dist.get_world_size(self.pg) if dist.is_initialized() else 1
 
-    def stream(self, device) -> torch.cuda.Stream:
-        if self._stream is None:
-            self._stream = torch.cuda.Stream(device=device)
-        return self._stream
+    def stream(self, device, index: int) -> torch.cuda.Stream:
+        if not self._streams:
+            self._streams = [torch.cuda.Stream(device=device) for _ in range(self.NUM_STREAMS)]
+        return self._streams[index % len(self._streams)]
 
-    def context(self, index: int, bucket) -> dict:
+    def comm_group(self, pg, device):
+        """The one NCCL group every bucket's context uses (collective on first use:
+        every rank reaches it at the same bucket of the same iteration)."""
+        if self._comm is None:
+            from .dist import private_nccl_group
+            self._comm = private_nccl_group(pg, device)
+        return self._comm
+
+    def context(self, index: int, bucket) -> tuple[dict, bool]:
+        """The bucket's context; fresh = True when it was (re)created now."""
         b = self.buckets.get(index)
         buf = bucket.buffer()
         shapes = [tuple(p.shape) for p in bucket.parameters()]
-        if b is None or b["shapes"] != shapes:   # new bucket (DDP rebuilds its buckets once, early)
-            d, blocks = bucket_layout(shapes, self.mu_bp)
-            assert d == buf.numel(), "bucket buffer does not match its parameters"
-            N = self.world()
-            pg = self.pg if self.pg is not None else (dist.group.WORLD if N > 1 else None)
-            ctx = ArcTopK(d, blocks, N=N, eta=self.eta, r=self.r, seed=self.seed + 7919 * index, nodes_local=1,
-                          pg=pg, rank=dist.get_rank(pg) if pg is not None else 0, reduce=self.reduce,
-                          device=buf.device)
-            b = {"d": d, "ctx": ctx, "h": torch.zeros_like(buf), "g": torch.zeros_like(buf),
-                 "gbar": torch.zeros_like(buf), "shapes": shapes, "blocks": blocks}
-            self.buckets[index] = b
-        return b
+        if b is not None and b["shapes"] == shapes:
+            return b, False
+        # new bucket (DDP rebuilds its buckets once, early)
+        if b is not None:
+            b["ctx"].close()
+        d, blocks = bucket_layout(shapes, self.mu_bp)
+        assert d == buf.numel(), "bucket buffer does not match its parameters"
+        N = self.world()
+        pg = self.pg if self.pg is not None else (dist.group.WORLD if N > 1 else None)
+        comm = self.comm_group(pg, buf.device) if pg is not None and N > 1 else None
+        ctx = ArcTopK(d, blocks, N=N, eta=self.eta, r=self.r, seed=self.seed + 7919 * index, nodes_local=1,
+                      pg=pg, rank=dist.get_rank(pg) if pg is not None else 0, reduce=self.reduce,
+                      device=buf.device, comm_group=comm)
+        b = {"d": d, "ctx": ctx, "h": torch.zeros_like(buf), "g": torch.zeros_like(buf),
+             "gbar": torch.zeros_like(buf), "shapes": shapes, "blocks": blocks}
+        self.buckets[index] = b
+        self.contexts_created += 1
+        return b, True
 
 
 def arc_topk_hook(state: ArcTopKHookState, bucket) -> torch.futures.Future:
@@ -99,7 +128,7 @@ def arc_topk_hook(state: ArcTopKHookState, bucket) -> torch.futures.Future:
         state.iteration += 1
     N = state.world()
     main = torch.cuda.current_stream(device)
-    side = state.stream(device)
+    side = state.stream(device, idx)
     side.wait_stream(main)
     fut = torch.futures.Future(devices=[device])
     with torch.cuda.stream(side):
@@ -109,8 +138,8 @@ def arc_topk_hook(state: ArcTopKHookState, bucket) -> torch.futures.Future:
                 dist.all_reduce(buf, group=state.pg)
                 buf.div_(N)
         else:
-            b = state.context(idx, bucket)
-            if t == state.warmup_steps:          # switch: h = g = local gradient, gbar = average
+            b, fresh = state.context(idx, bucket)
+            if fresh:                             # EF21M start: h = g = local gradient, gbar = average
                 b["h"].copy_(buf)
                 b["g"].copy_(buf)
                 b["gbar"].copy_(buf)

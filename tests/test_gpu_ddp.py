@@ -11,7 +11,11 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def test_ddp_hook_matches_oracle(orc):
+@pytest.mark.parametrize("warmup", [0, 1])
+def test_ddp_hook_matches_oracle(orc, warmup):
+    """warmup = 0: the EF21M state is initialised at each context's first compressed
+    iteration, including the contexts DDP's bucket rebuild (after iteration 0)
+    creates; warmup = 1: dense average first, then the same."""
     import torch.distributed as dist
     import torch.nn as nn
     from torch.nn.parallel import DistributedDataParallel as DDP
@@ -23,13 +27,13 @@ def test_ddp_hook_matches_oracle(orc):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(0)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29531")
+    os.environ["MASTER_PORT"] = str(29531 + warmup)
     if not dist.is_initialized():
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     torch.manual_seed(0)
     model = nn.Sequential(nn.Linear(96, 80), nn.ReLU(), nn.Linear(80, 64), nn.ReLU(), nn.Linear(64, 10)).to(dev)
     ddp = DDP(model, device_ids=[0], bucket_cap_mb=0.02)
-    state = ArcTopKHookState(mu_bp=1000, eta=0.2, r=4, seed=11, warmup_steps=1)
+    state = ArcTopKHookState(mu_bp=1000, eta=0.2, r=4, seed=11, warmup_steps=warmup)
     seen = []
 
     def recording_hook(st, bucket):
@@ -50,19 +54,21 @@ def test_ddp_hook_matches_oracle(orc):
         for (t, idx, shapes, raw) in seen:
             d, blocks = bucket_layout(shapes, 1000)
             buf = raw.cpu().numpy()
-            if t < 1:
+            if t < warmup:
                 expect = buf                                   # dense warm-up (one rank)
-            elif t == 1:
-                oracles[idx] = orc.OracleEF21M(d, blocks, N=1, eta=0.2, r=4, seed=11 + 7919 * idx,
-                                               h0=[buf], g0=[buf], gbar0=buf)
+            elif idx not in oracles or oracles[idx][0] != shapes:
+                # a context's first compressed iteration: h = g = gbar = the gradient
+                oracles[idx] = (shapes, orc.OracleEF21M(d, blocks, N=1, eta=0.2, r=4, seed=11 + 7919 * idx,
+                                                        h0=[buf], g0=[buf], gbar0=buf))
                 expect = buf
             else:
-                oracles[idx].step(t, [buf])
-                expect = oracles[idx].gbar
+                oracles[idx][1].step(t, [buf])
+                expect = oracles[idx][1].gbar
             # the parameters' gradients now hold the hook's output, in bucket order
             got = torch.cat([p.grad.reshape(-1) for p in _in_bucket_order(model, shapes)]).cpu().numpy()
             assert got.tobytes() == np.asarray(expect, np.float32).tobytes(), f"step {step} bucket {idx}"
     assert max_buckets >= 2, "expected several buckets after DDP's rebuild"
+    assert len(oracles) >= 2
     dist.destroy_process_group()
 
 

@@ -301,6 +301,49 @@ def test_determinism_and_graph_capture(orc):
     assert outs[0] == outs[1] == outs[2]
 
 
+@pytest.mark.parametrize("kind", ["normal", "dup_rows"])
+def test_graph_replayed_three_times_equals_three_eager_steps(kind):
+    """A captured step replayed 3x gives exactly what 3 eager steps at the same t give
+    (the selection's double-buffered candidate / boundary counters are switched by a
+    device-side parity word, so replays of one graph never reuse a stale counter).
+    dup_rows (every Sigma equal) overflows the candidate list: the boundary-row path."""
+    from paper_2510_26709_b200 import ArcTopK
+    from synth import adversarial
+    d, N, n = 600_000, 2, 100
+    blocks = flat_blocks(d, n, K=900)
+    grads = [torch.from_numpy(x).to(DEV) for x in adversarial(kind, d, N, seed=4, n=n)]
+    outs = []
+    for mode in ("eager", "graph"):
+        ctx = ArcTopK(d, blocks, N=N, eta=0.5, seed=3)
+        h = [torch.zeros(d, device=DEV) for _ in range(N)]
+        g = [torch.zeros(d, device=DEV) for _ in range(N)]
+        gbar = torch.zeros(d, device=DEV)
+        sel = torch.empty(ctx.sum_K, dtype=torch.int32, device=DEV)
+        sels = []
+        if mode == "graph":
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(graph, stream=s):
+                    ctx.step(7, grads, h, g, gbar, sel, stream=s)
+            for _ in range(3):
+                graph.replay()
+                torch.cuda.synchronize()
+                sels.append(sel.cpu().numpy().copy())
+        else:
+            for _ in range(3):
+                ctx.step(7, grads, h, g, gbar, sel)
+                torch.cuda.synchronize()
+                sels.append(sel.cpu().numpy().copy())
+        outs.append((sels, gbar.cpu().numpy().tobytes() + b"".join(x.cpu().numpy().tobytes() for x in g + h)))
+        ctx.close()
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(a, b)
+        assert np.all(np.diff(a) > 0) and a.min() >= 0 and a.max() < blocks[0].m
+    assert outs[0][1] == outs[1][1]
+
+
 # ------------------------------------------------------------------ full-size configs
 
 @pytest.mark.parametrize("name,N,steps", [("C2", 8, 2), ("C3", 1, 2)])

@@ -643,3 +643,25 @@ def test_noef_rows_outside_selection_only_decay(orc):
     assert np.array_equal(rows[~mask], scaled.reshape(-1, n)[~mask])
     want = (scaled.reshape(-1, n)[mask] + out["values"].reshape(K, n)).astype(np.float32)
     assert np.array_equal(rows[mask], want)
+
+
+def test_threads_are_bit_identical(orc):
+    """The oracle's row-parallel loops (OpenMP) give bit-identical results to one
+    thread: every row's arithmetic is the same sequence whichever thread runs it."""
+    from synth import GradientSource
+    blocks = [Block(0, 5000, 50, 100, 7, 0), Block(5000, 3001, 1001, 3, 40, 0), Block(8001, 999, 1, 1024, 1, 1),
+              Block(9000, 20_000, 10, 2000, 2, 0)]
+    d, N = 29_000, 3
+    src = GradientSource(d, blocks, N, seed=4)
+    outs = []
+    for threads in (1, 8):
+        orc.set_threads(threads)
+        o = orc.OracleEF21M(d, blocks, N=N, eta=0.3, r=4, seed=2)
+        res = [o.step(t, [x.numpy() for x in src.grads(t)], debug=True) for t in range(3)]
+        outs.append((res, [x.copy() for x in o.h + o.g] + [o.gbar.copy()]))
+    orc.set_threads(1)
+    for a, b in zip(outs[0][0], outs[1][0]):
+        for k in a:
+            assert a[k].tobytes() == b[k].tobytes(), k
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert a.tobytes() == b.tobytes()
