@@ -71,7 +71,8 @@ def lib():
         L.orc_apply_adam.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64] + [ctypes.c_float] * 4
         L.orc_set_threads.argtypes = [ctypes.c_int32]
         L.orc_get_threads.restype = ctypes.c_int32
-        L.orc_set_threads(1)          # the plain oracle unless a caller asks for threads
+        # the plain oracle (1 thread) unless a caller asks for threads (bit-identical)
+        L.orc_set_threads(int(os.environ.get("ARC_ORACLE_THREADS", "1")))
         _lib = L
     return _lib
 
