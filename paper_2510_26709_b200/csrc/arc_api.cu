@@ -462,6 +462,7 @@ struct arc_topk_ctx {
     int64_t tally[kTallyN] = {};
     unsigned char* ws = nullptr;
     int grid = 0, num_tiles = 0, shape = 0, vs_cap = 0;
+    int sel_grid = 0;                             // CTAs of the (persistent) selection kernel
     int grid_w = 0, vs_cap_w = 0, tiles_w0 = 0;   // the wide blocks' ranged launch (grid_w == 0: none)
     float ome = 0.f, Nf = 0.f;
     cudaStream_t last = nullptr;
@@ -612,13 +613,24 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void*
                 if (!(c->pl.dense_fast && B.kind == ARC_BLOCK_DENSE)) n += (B.m + rows - 1) / rows;
             return n;
         };
+        // (more slices than co-resident CTAs: the kernel is persistent, every CTA
+        // takes ceil(slices / resident) of them, at most select_max_slices_per_cta())
         int rows = kSliceMin;
         while (rows < select_max_slice_rows() && slices(rows) > resident) rows += 32;
         if (const char* e = std::getenv("ARC_SLICE_ROWS")) {
             const int f = std::atoi(e);
-            if (f >= kSliceMin && f <= select_max_slice_rows() && slices(f) <= resident) rows = f;
+            if (f >= kSliceMin && f <= select_max_slice_rows()) rows = f;
         }
-        if (slices(rows) > resident) { delete c; return ARC_ERR_UNSUPPORTED; }
+        int grid = static_cast<int>(std::min<int64_t>(slices(rows), resident));
+        if (const char* e = std::getenv("ARC_SELECT_GRID")) {   // debug knob: fewer CTAs (several slices each)
+            const int f = std::atoi(e);
+            if (f >= 1 && f < grid) grid = f;
+        }
+        if (grid > 0 && (slices(rows) + grid - 1) / grid > select_max_slices_per_cta()) {
+            delete c;
+            return ARC_ERR_UNSUPPORTED;
+        }
+        c->sel_grid = grid;
         const size_t total = c->pl.total;
         if (rows != kSliceMin) {
             c->pl = Plan();
@@ -1030,6 +1042,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.blocks = sblocks;
         sg.items = c->at<SliceItem>(pl.o_items);
         sg.num_items = static_cast<int>(pl.items.size());
+        sg.grid = std::min(c->sel_grid, sg.num_items);
         sg.slice_rows = pl.slice_rows;
         sg.sigma = sigma;
         sg.hist1 = hist1;
@@ -1349,10 +1362,10 @@ arc_status arc_topk_get_status(arc_topk_ctx* c, uint32_t* flags) {
 
 arc_status arc_topk_debug_stamps(arc_topk_ctx* c, uint64_t* stamps_host, int64_t n, int32_t* grid) {
     if (c == nullptr || c->stamps == nullptr || stamps_host == nullptr) return ARC_ERR_INVALID_ARG;
-    const int64_t all = static_cast<int64_t>(c->pl.items.size()) * 8;
+    const int64_t all = static_cast<int64_t>(c->sel_grid) * 8;
     ARC_CUDA(cudaStreamSynchronize(c->last));
     ARC_CUDA(cudaMemcpy(stamps_host, c->stamps, sizeof(uint64_t) * (n < all ? n : all), cudaMemcpyDeviceToHost));
-    if (grid) *grid = static_cast<int32_t>(c->pl.items.size());
+    if (grid) *grid = static_cast<int32_t>(c->sel_grid);
     return ARC_OK;
 }
 

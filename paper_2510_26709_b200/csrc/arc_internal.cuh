@@ -75,6 +75,7 @@ struct SelectGatherLaunch {
     const BlockDev* blocks;
     const SliceItem* items;        // every slice of every block (one CTA each)
     int num_items;
+    int grid;                      // CTAs (<= num_items, all co-resident); CTA b takes slices b, b + grid, ...
     int slice_rows;                // rows per slice (<= 4096)
     const float* sigma;
     unsigned* hist1;               // [num_blocks][2048] digit key[31:21] (filled by the Sigma pass)
@@ -167,6 +168,7 @@ struct GatherLaunch;
 cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch& ga, cudaStream_t st);
 int select_gather_resident_ctas();
 int select_max_slice_rows();
+int select_max_slices_per_cta();
 
 struct GatherLaunch {
     const BlockDev* blocks;

@@ -4,8 +4,9 @@
 //
 // S3  I_b = argtop_{K_b}(Sigma_b)  (zn28373 P:236-237; ties -> smaller row,
 //     R5; NaN above +Inf, R15): an MSB-first radix select on the 32-bit order
-//     keys, digits key[31:21] | key[20:10] | key[9:0].  Every CTA owns a slice
-//     of consecutive rows of one block and keeps its keys in shared memory.
+//     keys, digits key[31:21] | key[20:10] | key[9:0].  A slice is <= 4096
+//     consecutive rows of one block; the kernel is persistent (CTA b takes slices
+//     b, b + grid, ...), and a CTA with one slice keeps its keys in shared memory.
 //     Digit 1 was histogrammed by the pass that produced Sigma (phase 0 here
 //     when Sigma came from the exchange or several local nodes), so each slice
 //     knows the boundary bin b1 at once: it counts its keys above b1 and appends
@@ -348,6 +349,7 @@ __device__ __forceinline__ void gather_row_warp(const GatherLaunch& a, const Blo
 }
 
 constexpr int kMaxSliceRows = 4096;
+constexpr int kMaxSlicesPerCta = 32;   // slices one CTA of the persistent selection kernel takes at most
 
 // Candidate resolution on a small list in shared memory (every CTA of the block
 // computes the same result): T = the krem-th largest key among the candidates
@@ -409,159 +411,203 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-template <bool kPhase0>
+// One selection slice: rows [lo, hi) of one selection block.
+struct Slice {
+    BlockDev B;
+    long long bb;   // selection block index
+    int c;          // slice index in the block
+    int lo, hi, nk;
+    int sidx;       // global slice index (slice_gt / slice_eq)
+    bool arc;       // a real selection (ARC block with K < m); otherwise identity
+};
+__device__ __forceinline__ Slice slice_of(const SelectGatherLaunch& s, int item) {
+    Slice x;
+    const SliceItem it = s.items[item];
+    x.B = s.blocks[it.b];
+    x.bb = it.b;
+    x.c = it.c;
+    x.lo = it.c * s.slice_rows;
+    x.hi = min(x.B.m, x.lo + s.slice_rows);
+    x.nk = x.hi - x.lo;
+    x.sidx = x.B.slice_base + it.c;
+    x.arc = x.B.kind == ARC_BLOCK_ARC && x.B.K < x.B.m;
+    return x;
+}
+
+// the slice's order keys (R15) from Sigma in global memory into shared memory
+__device__ __forceinline__ void load_keys(const float* __restrict__ sigma, const Slice& x, unsigned* s_keys) {
+    const float* __restrict__ sg = sigma + x.B.row_base + x.lo;
+    for (int i0 = 0; i0 < x.nk; i0 += 4 * kThreads) {
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k * kThreads + static_cast<int>(threadIdx.x);
+            v[k] = i < x.nk ? __ldcg(sg + i) : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k * kThreads + static_cast<int>(threadIdx.x);
+            if (i < x.nk) s_keys[i] = order_key(v[k]);
+        }
+    }
+}
+
+// The selection kernel is PERSISTENT: CTA b handles slices b, b + grid, b + 2 grid,
+// ... (at most kMaxSlicesPerCta), so any block table is accepted whatever the
+// number of co-resident CTAs.  With one slice per CTA (the common case) the
+// slice's keys stay in shared memory across the grid barriers; with several
+// they are re-read from Sigma (L2) for each slice.
+template <bool kPhase0, bool kMulti>
 __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
     cg::grid_group grid = cg::this_grid();
 #define STAMP(k) \
     if (s.stamps != nullptr && threadIdx.x == 0) s.stamps[blockIdx.x * 8 + (k)] = globaltimer()
     STAMP(0);
     __shared__ unsigned sh[2048];                   // histogram
-    __shared__ unsigned s_keys[kMaxSliceRows];      // this slice's order keys
-    __shared__ int s_rows[kMaxSliceRows];           // boundary-bin candidates (keys | rows)
+    __shared__ unsigned s_keys[kMaxSliceRows];      // the current slice's order keys
+    __shared__ int s_rows[kMaxSliceRows];           // boundary-bin candidates (keys | rows) / row lists
     __shared__ int warp_sums[32];
     __shared__ unsigned s_dig;
     __shared__ int s_abv;
     __shared__ int s_nb;                            // early mode: selected boundary-bin rows
+    __shared__ unsigned s_b1[kMaxSlicesPerCta];     // per slice of this CTA: digit-1 boundary bin
+    __shared__ int s_krem[kMaxSlicesPerCta];        //   and the rank still to find inside it
 
-    const SliceItem it = s.items[blockIdx.x];
-    const BlockDev B = s.blocks[it.b];
-    grid_dependency_wait();   // Sigma and the digit-1 histogram are complete
     const int tid = threadIdx.x;
-    const int lo = it.c * s.slice_rows, hi = min(B.m, lo + s.slice_rows), nk = hi - lo;
-    const bool arc = B.kind == ARC_BLOCK_ARC && B.K < B.m;
-    const long long bb = it.b;
-    const int sidx = B.slice_base + it.c;
+    // (kMulti: grid < num_items, some CTAs take several slices; else one slice per CTA)
+    const int nmine = kMulti ? (s.num_items - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                                   static_cast<int>(gridDim.x)
+                             : 1;
+    const bool cached = !kMulti;                    // keys survive in s_keys across the barriers
+    auto item_of = [&](int k) { return static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x); };
+    grid_dependency_wait();   // Sigma and the digit-1 histogram are complete
     const int par = static_cast<int>(__ldcg(s.parity) & 1u);   // read by every CTA before barrier 1
     unsigned* ccount = s.cand_count + par * s.num_blocks;                 // this step's counters
-    unsigned* cand = s.cand + (static_cast<long long>(par) * s.num_blocks + bb) * (2 * kCandCap);
 
     // ------------------------------------------------ phase 0
     // Sigma was not formed by the streaming pass: either the kernel forms it here
     // from this GPU's per-node sketches ([M][L][r], several local nodes, no
     // exchange: S2 summed in node order, R9, R21), or k_sigma_slice + the Sigma
-    // all-gather left it in s.sigma (exchange path).  Then the slice's keys, the
-    // block's digit-1 histogram, and a grid barrier so the histogram is complete.
+    // all-gather left it in s.sigma (exchange path).  Then the slices' keys, the
+    // blocks' digit-1 histograms, and a grid barrier so they are complete.
     if constexpr (kPhase0) {
-        if (B.kind == ARC_BLOCK_ARC && (arc || s.xsk != nullptr)) {   // every ARC block gets its Sigma
-            for (int i = tid; i < kHist1Bins; i += kThreads) sh[i] = 0;
-            __syncthreads();
-            auto finish = [&](int i, float sig) {
-                const unsigned key = order_key(sig);
-                s_keys[i] = key;
-                atomicAdd(&sh[key >> kHist1Shift], 1u);
-            };
-            if (s.xsk == nullptr) {
-                const float* __restrict__ sg = s.sigma + B.row_base + lo;
-                for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {
-                    float v[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int i = i0 + k * kThreads + tid;
-                        v[k] = i < nk ? __ldcg(sg + i) : 0.0f;
-                    }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int i = i0 + k * kThreads + tid;
-                        if (i < nk) finish(i, v[k]);
-                    }
-                }
-            } else {
-                const int L = s.L;
-                auto sigma_of = [&](int i, const float* S) {
-                    float sig = 0.0f;
-                    for (int j = 0; j < s.r; ++j) {
-                        sig = ffma(S[j], S[j], sig);                           // O8, zn28373
-                    }
-                    s.sigma_w[B.row_base + lo + i] = sig;
-                    if (!isfinite(sig)) atomicOr(s.status, kStatusNonfinite);
-                    finish(i, sig);
+        for (int k = 0; k < nmine; ++k) {
+            const Slice x = slice_of(s, item_of(k));
+            const BlockDev& B = x.B;
+            const int lo = x.lo, nk = x.nk;
+            if (B.kind == ARC_BLOCK_ARC && (x.arc || s.xsk != nullptr)) {   // every ARC block gets its Sigma
+                __syncthreads();                                            // (s_keys / sh of the previous slice)
+                for (int i = tid; i < kHist1Bins; i += kThreads) sh[i] = 0;
+                __syncthreads();
+                auto finish = [&](int i, float sig) {
+                    const unsigned key = order_key(sig);
+                    s_keys[i] = key;
+                    atomicAdd(&sh[key >> kHist1Shift], 1u);
                 };
-                if (s.r == 4) {
-                    // 4 rows per thread, 4 nodes per round: 16 float4 loads in flight
+                if (s.xsk == nullptr) {
+                    const float* __restrict__ sg = s.sigma + B.row_base + lo;
                     for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {
-                        float S[4][4];
-                        for (int n0 = 0; n0 < L; n0 += 4) {
-                            float4 v[4][4];
+                        float v[4];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const int i = i0 + u * kThreads + tid;
-                                const long long p = B.row_base + lo + i;
-#pragma unroll
-                                for (int k = 0; k < 4; ++k)
-                                    if (i < nk && n0 + k < L)
-                                        v[u][k] = __ldcg(reinterpret_cast<const float4*>(s.xsk + (p * L + n0 + k) * 4));
-                            }
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                                for (int k = 0; k < 4; ++k) {
-                                    if (n0 + k >= L) continue;
-                                    const float4 w = v[u][k];
-                                    if (n0 + k == 0) { S[u][0] = w.x; S[u][1] = w.y; S[u][2] = w.z; S[u][3] = w.w; }
-                                    else {                                               // R9 node order
-                                        S[u][0] = fadd(S[u][0], w.x); S[u][1] = fadd(S[u][1], w.y);
-                                        S[u][2] = fadd(S[u][2], w.z); S[u][3] = fadd(S[u][3], w.w);
-                                    }
-                                }
+                        for (int q = 0; q < 4; ++q) {
+                            const int i = i0 + q * kThreads + tid;
+                            v[q] = i < nk ? __ldcg(sg + i) : 0.0f;
                         }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int i = i0 + u * kThreads + tid;
-                            if (i < nk) sigma_of(i, S[u]);
+                        for (int q = 0; q < 4; ++q) {
+                            const int i = i0 + q * kThreads + tid;
+                            if (i < nk) finish(i, v[q]);
                         }
                     }
                 } else {
-                    for (int i = tid; i < nk; i += kThreads) {
-                        const long long p = B.row_base + lo + i;
-                        float S[32];
+                    const int L = s.L;
+                    auto sigma_of = [&](int i, const float* S) {
+                        float sig = 0.0f;
                         for (int j = 0; j < s.r; ++j) {
-                            float a = 0.0f;
-                            for (int l = 0; l < L; ++l) {
-                                const float v = __ldcg(s.xsk + (p * L + l) * s.r + j);
-                                a = l == 0 ? v : fadd(a, v);
-                            }
-                            S[j] = a;
+                            sig = ffma(S[j], S[j], sig);                           // O8, zn28373
                         }
-                        sigma_of(i, S);
+                        s.sigma_w[B.row_base + lo + i] = sig;
+                        if (!isfinite(sig)) atomicOr(s.status, kStatusNonfinite);
+                        finish(i, sig);
+                    };
+                    if (s.r == 4) {
+                        // 4 rows per thread, 4 nodes per round: 16 float4 loads in flight
+                        for (int i0 = 0; i0 < nk; i0 += 4 * kThreads) {
+                            float S[4][4];
+                            for (int n0 = 0; n0 < L; n0 += 4) {
+                                float4 v[4][4];
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const int i = i0 + u * kThreads + tid;
+                                    const long long p = B.row_base + lo + i;
+#pragma unroll
+                                    for (int q = 0; q < 4; ++q)
+                                        if (i < nk && n0 + q < L)
+                                            v[u][q] = __ldcg(reinterpret_cast<const float4*>(s.xsk + (p * L + n0 + q) * 4));
+                                }
+#pragma unroll
+                                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                    for (int q = 0; q < 4; ++q) {
+                                        if (n0 + q >= L) continue;
+                                        const float4 w = v[u][q];
+                                        if (n0 + q == 0) { S[u][0] = w.x; S[u][1] = w.y; S[u][2] = w.z; S[u][3] = w.w; }
+                                        else {                                               // R9 node order
+                                            S[u][0] = fadd(S[u][0], w.x); S[u][1] = fadd(S[u][1], w.y);
+                                            S[u][2] = fadd(S[u][2], w.z); S[u][3] = fadd(S[u][3], w.w);
+                                        }
+                                    }
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int i = i0 + u * kThreads + tid;
+                                if (i < nk) sigma_of(i, S[u]);
+                            }
+                        }
+                    } else {
+                        for (int i = tid; i < nk; i += kThreads) {
+                            const long long p = B.row_base + lo + i;
+                            float S[32];
+                            for (int j = 0; j < s.r; ++j) {
+                                float a = 0.0f;
+                                for (int l = 0; l < L; ++l) {
+                                    const float v = __ldcg(s.xsk + (p * L + l) * s.r + j);
+                                    a = l == 0 ? v : fadd(a, v);
+                                }
+                                S[j] = a;
+                            }
+                            sigma_of(i, S);
+                        }
                     }
                 }
+                if (x.arc) flush_hist(sh, s.hist1 + x.bb * kHist1Bins, kHist1Bins);
             }
-            if (arc) flush_hist(sh, s.hist1 + bb * kHist1Bins, kHist1Bins);
         }
         grid.sync();                                 // ---------------- barrier 0
     }
-    // ------------------------------------------------ phase A
-    unsigned b1 = 0;
-    int krem = B.K;
-    int gt_pos = 0, gt_tot = 0;                      // this thread's / the slice's rows above bin b1
-    if (arc) {
-        const float* __restrict__ sg = s.sigma + B.row_base + lo;
+    // ------------------------------------------------ phase A (per slice)
+    // the digit-1 boundary bin b1 of the slice's block, the slice's count of keys
+    // above it, and its keys in b1 appended to the block's candidate list
+    int gt_pos = 0, gt_tot = 0;                      // (one slice per CTA: this thread's / the slice's rows above b1)
+    for (int k = 0; k < nmine; ++k) {
+        const Slice x = slice_of(s, item_of(k));
+        if (!x.arc) continue;
+        const BlockDev& B = x.B;
+        __syncthreads();                             // (s_keys, sh of the previous slice)
         unsigned hv[8];                              // digit-1 histogram, loaded alongside the keys
 #pragma unroll
-        for (int k = 0; k < 8; ++k) hv[k] = __ldcg(s.hist1 + bb * kHist1Bins + tid + k * kThreads);
-        for (int i0 = 0; i0 < nk && !kPhase0; i0 += 4 * kThreads) {
-            float v[4];
+        for (int q = 0; q < 8; ++q) hv[q] = __ldcg(s.hist1 + x.bb * kHist1Bins + tid + q * kThreads);
+        if (!(kPhase0 && cached)) load_keys(s.sigma, x, s_keys);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = i0 + k * kThreads + tid;
-                v[k] = i < nk ? sg[i] : 0.0f;
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = i0 + k * kThreads + tid;
-                if (i < nk) s_keys[i] = order_key(v[k]);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) sh[tid + k * kThreads] = hv[k];
+        for (int q = 0; q < 8; ++q) sh[tid + q * kThreads] = hv[q];
         __syncthreads();
         int above;
-        b1 = top_digit(sh, kHist1Bins, krem, warp_sums, &s_dig, &s_abv, &above);
-        krem -= above;
+        const unsigned b1 = top_digit(sh, kHist1Bins, B.K, warp_sums, &s_dig, &s_abv, &above);
+        const int krem = B.K - above;
         // keys above bin b1 and the candidates (keys in bin b1) of this slice;
         // both counts in one packed scan (each <= 4096)
         int gt1 = 0, nc = 0;
-        for (int i = tid; i < nk; i += kThreads) {
+        for (int i = tid; i < x.nk; i += kThreads) {
             const unsigned d1 = s_keys[i] >> 21;
             gt1 += d1 > b1;
             nc += d1 == b1;
@@ -572,15 +618,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
         gt_pos = packed >> 16;
         gt_tot = packed_tot >> 16;
         if (tid == 0) {
-            s.slice_gt[sidx] = packed_tot >> 16;
-            s_abv = ctot > 0 ? static_cast<int>(atomicAdd(ccount + bb, static_cast<unsigned>(ctot))) : 0;
+            s.slice_gt[x.sidx] = packed_tot >> 16;
+            s_abv = ctot > 0 ? static_cast<int>(atomicAdd(ccount + x.bb, static_cast<unsigned>(ctot))) : 0;
+            s_b1[k] = b1;
+            s_krem[k] = krem;
         }
         __syncthreads();
+        unsigned* cand = s.cand + (static_cast<long long>(par) * s.num_blocks + x.bb) * (2 * kCandCap);
         int cpos = s_abv + (packed & 0xFFFF);
-        for (int i = tid; i < nk && nc > 0; i += kThreads) {
+        for (int i = tid; i < x.nk && nc > 0; i += kThreads) {
             const unsigned key = s_keys[i];
             if ((key >> 21) == b1) {
-                if (cpos < kCandCap) { cand[cpos] = key; cand[kCandCap + cpos] = static_cast<unsigned>(lo + i); }
+                if (cpos < kCandCap) { cand[cpos] = key; cand[kCandCap + cpos] = static_cast<unsigned>(x.lo + i); }
                 ++cpos;
             }
         }
@@ -592,21 +641,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
              i += static_cast<long long>(gridDim.x) * kThreads)
             rng::gen_V_item(s.vblocks, s.num_vblocks, s.r, s.key, s.t_lo, s.t_hi, i, s.V_next);
     STAMP(1);
-    if (it.c == 0)   // next step's candidate counter of this block
-        for (int i = tid; i < 1; i += kThreads) s.cand_count[(par ^ 1) * s.num_blocks + bb] = 0;
+    for (int k = 0; k < nmine; ++k) {                // next step's candidate counter of each block
+        const SliceItem it = s.items[item_of(k)];
+        if (it.c == 0 && tid == 0) s.cand_count[(par ^ 1) * s.num_blocks + it.b] = 0;
+    }
     if (s.early) {
-        // split barrier 1: the rows of this slice above the boundary bin b1 are
+        // split barrier 1: the rows of a slice above the boundary bin b1 are
         // selected whatever the candidates resolve to (fewer than K keys lie above
         // b1), so their S4..S6 runs while the other CTAs reach the barrier
         auto token = grid.barrier_arrive();
-        if (arc) {
-            int pos = gt_pos;
-            for (int i = tid; i < nk; i += kThreads)
-                if ((s_keys[i] >> 21) > b1) s_rows[pos++] = i;
-            __syncthreads();
-            gather_rows_local<4>(ga, B, lo, s_rows, gt_tot);
-        } else {
-            gather_rows_local<4>(ga, B, lo, nullptr, nk);   // K = m: every row
+        for (int k = 0; k < nmine; ++k) {
+            const Slice x = slice_of(s, item_of(k));
+            if (x.arc) {
+                __syncthreads();                     // (s_rows / s_keys of the previous slice)
+                if (!cached) {
+                    load_keys(s.sigma, x, s_keys);
+                    __syncthreads();
+                    int g1 = 0;
+                    for (int i = tid; i < x.nk; i += kThreads) g1 += (s_keys[i] >> 21) > s_b1[k];
+                    gt_pos = cta_exclusive_scan(g1, warp_sums, &gt_tot);
+                }
+                const unsigned b1 = s_b1[k];
+                int pos = gt_pos;
+                for (int i = tid; i < x.nk; i += kThreads)
+                    if ((s_keys[i] >> 21) > b1) s_rows[pos++] = i;
+                __syncthreads();
+                gather_rows_local<4>(ga, x.B, x.lo, s_rows, gt_tot);
+            } else {
+                gather_rows_local<4>(ga, x.B, x.lo, nullptr, x.nk);   // K = m: every row
+            }
         }
         __syncthreads();                             // s_rows is reused below
         grid.barrier_wait(std::move(token));
@@ -620,176 +683,209 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     // (uniform across the grid, so every CTA meets the same barriers)
     bool overflow = false;
     for (int b = tid; b < s.num_blocks; b += kThreads) overflow |= __ldcg(ccount + b) > static_cast<unsigned>(kCandCap);
-    // this block's candidates and the preceding slices' counts, loaded together
-    // this block's candidate slots (all of them: one round, no wait for the count)
-    // and the preceding slices' counts, loaded together
-    const int C = arc ? static_cast<int>(min(__ldcg(ccount + bb), static_cast<unsigned>(kCandCap))) : 0;
-    int before = 0;
-    if (arc) {
-        for (int c = tid; c < it.c; c += kThreads) before += __ldcg(s.slice_gt + B.slice_base + c);
-        unsigned* ck = reinterpret_cast<unsigned*>(s_rows);
-        int* ci = s_rows + kCandCap;
-#pragma unroll
-        for (int k = 0; k < kCandCap / kThreads; ++k) {
-            const int i = tid + k * kThreads;
-            ck[i] = __ldcg(cand + i);
-            ci[i] = static_cast<int>(__ldcg(cand + kCandCap + i));
-        }
-    }
     overflow = __syncthreads_or(overflow);
+    for (int k = 0; k < nmine; ++k) {                // hist1 was read by every slice before barrier 1: reset
+        const Slice x = slice_of(s, item_of(k));
+        if (x.B.kind == ARC_BLOCK_ARC && x.c == 0)
+            for (int i = tid; i < kHist1Bins; i += kThreads) s.hist1[x.bb * kHist1Bins + i] = 0;
+    }
     STAMP(3);
-    unsigned T = 0;
-    int P_eq = 0x7FFFFFFF, need_eq = 0, sel_before = 0;
-    bool use_peq = true;
-    if (B.kind == ARC_BLOCK_ARC && it.c == 0)   // read by every slice before barrier 1: reset
-        for (int i = tid; i < kHist1Bins; i += kThreads) s.hist1[bb * kHist1Bins + i] = 0;
+    int32_t* __restrict__ sel_all = s.sel;
+    // one slice's compaction: its selected rows (key > T, or key == T and
+    // [use_peq] row <= P_eq / [else] within the slice's quota of equal keys) in
+    // ascending order at sel_before; early mode: its selected boundary-bin rows
+    // (still to update) listed in s_rows[0 .. s_nb)
+    auto compact = [&](const Slice& x, unsigned b1, unsigned T, int P_eq, int need_eq, int sel_before, bool use_peq) {
+        int32_t* __restrict__ out = sel_all + x.B.sel_base;
+        const int per = (s.slice_rows + kThreads - 1) / kThreads;   // consecutive rows per thread
+        int my_eq = 0;
+        if (!use_peq)
+            for (int q = 0; q < per; ++q) {
+                const int i = tid * per + q;
+                my_eq += (i < x.nk && s_keys[i] == T);
+            }
+        int eq_tot;
+        int eq_rank = use_peq ? 0 : cta_exclusive_scan(my_eq, warp_sums, &eq_tot);
+        int my_sel = 0;
+        unsigned take_mask = 0;                      // per <= 16
+        for (int q = 0; q < per; ++q) {
+            const int i = tid * per + q;
+            bool t = false;
+            if (i < x.nk) {
+                const unsigned key = s_keys[i];
+                if (key > T) t = true;
+                else if (key == T) {
+                    if (use_peq) t = x.lo + i <= P_eq;
+                    else { t = eq_rank < need_eq; ++eq_rank; }
+                }
+            }
+            if (t) { take_mask |= 1u << q; ++my_sel; }
+        }
+        if (tid == 0) s_nb = 0;
+        int nsel;
+        int pos = cta_exclusive_scan(my_sel, warp_sums, &nsel);
+        for (int q = 0; q < per; ++q) {
+            if (take_mask & (1u << q)) {
+                const int i = tid * per + q;
+                out[sel_before + pos] = x.lo + i;
+                ++pos;
+                // early mode: the selected rows of the boundary bin are still to do
+                if (s.early && (s_keys[i] >> 21) == b1) s_rows[atomicAdd(&s_nb, 1)] = i;
+            }
+        }
+        __syncthreads();
+    };
+    auto identity = [&](const Slice& x) {            // DENSE blocks and K = m
+        int32_t* __restrict__ out = sel_all + x.B.sel_base;
+        for (int p = x.lo + tid; p < x.hi; p += kThreads) out[p] = p;
+    };
+    // early mode after an overflow: this CTA's selected boundary rows, appended to one list
+    auto append_boundary = [&](const Slice& x) {
+        if (tid == 0) s_abv = s_nb > 0 ? static_cast<int>(atomicAdd(ga.bnd_count + par, static_cast<unsigned>(s_nb))) : 0;
+        __syncthreads();
+        for (int i = tid; i < s_nb; i += kThreads) ga.bnd[s_abv + i] = make_int2(static_cast<int>(x.bb), x.lo + s_rows[i]);
+        __syncthreads();
+    };
     if (!overflow) {
-        if (arc) {
+        for (int k = 0; k < nmine; ++k) {
+            const Slice x = slice_of(s, item_of(k));
+            if (!x.arc) { identity(x); continue; }
+            __syncthreads();                         // (s_rows / s_keys of the previous slice)
+            const unsigned* cand = s.cand + (static_cast<long long>(par) * s.num_blocks + x.bb) * (2 * kCandCap);
+            // this block's candidate slots (all of them: one round, no wait for the count)
+            // and the preceding slices' counts, loaded together
+            const int C = static_cast<int>(min(__ldcg(ccount + x.bb), static_cast<unsigned>(kCandCap)));
+            int before = 0;
+            for (int c = tid; c < x.c; c += kThreads) before += __ldcg(s.slice_gt + x.B.slice_base + c);
             unsigned* ck = reinterpret_cast<unsigned*>(s_rows);
             int* ci = s_rows + kCandCap;
-            resolve_candidates(ck, ci, C, b1, krem, sh, warp_sums, &s_dig, &s_abv, &T, &P_eq);
+#pragma unroll
+            for (int q = 0; q < kCandCap / kThreads; ++q) {
+                const int i = tid + q * kThreads;
+                ck[i] = __ldcg(cand + i);
+                ci[i] = static_cast<int>(__ldcg(cand + kCandCap + i));
+            }
+            if (!cached) load_keys(s.sigma, x, s_keys);
+            __syncthreads();
+            unsigned T;
+            int P_eq;
+            const unsigned b1 = s_b1[k];
+            resolve_candidates(ck, ci, C, b1, s_krem[k], sh, warp_sums, &s_dig, &s_abv, &T, &P_eq);
             // rows selected before this slice: keys above bin b1 in earlier slices,
             // plus the selected candidates at earlier rows
             for (int i = tid; i < C; i += kThreads)
-                before += (ci[i] < lo && (ck[i] > T || (ck[i] == T && ci[i] <= P_eq)));
-            int tot;
-            cta_exclusive_scan(before, warp_sums, &tot);
-            sel_before = tot;
+                before += (ci[i] < x.lo && (ck[i] > T || (ck[i] == T && ci[i] <= P_eq)));
+            int sel_before;
+            cta_exclusive_scan(before, warp_sums, &sel_before);
+            STAMP(4);
+            compact(x, b1, T, P_eq, 0, sel_before, true);
+            STAMP(5);
+            if (s.early) gather_rows_local<4>(ga, x.B, x.lo, s_rows, s_nb);
+        }
+        if (s.early) {
+            STAMP(6);
+            STAMP(7);
+            return;
         }
     } else {
         // ---- digit by digit (some block's boundary bin overflowed the candidate
         // list): digit-2 histogram of bin b1, then digit 3, one barrier each
-        unsigned b2 = 0;
-        if (arc) {
+        for (int k = 0; k < nmine; ++k) {
+            const Slice x = slice_of(s, item_of(k));
+            if (!x.arc) continue;
+            __syncthreads();
+            if (!cached) load_keys(s.sigma, x, s_keys);
             for (int i = tid; i < 2048; i += kThreads) sh[i] = 0;
             __syncthreads();
-            for (int i = tid; i < nk; i += kThreads)
+            const unsigned b1 = s_b1[k];
+            for (int i = tid; i < x.nk; i += kThreads)
                 if ((s_keys[i] >> 21) == b1) atomicAdd(&sh[(s_keys[i] >> 10) & 2047u], 1u);
-            flush_hist(sh, s.hist2 + bb * 2048, 2048);
+            flush_hist(sh, s.hist2 + x.bb * 2048, 2048);
         }
         grid.sync();                                 // ---------------- barrier 1b
-        if (arc) {
-            load_hist(sh, s.hist2 + bb * 2048, 2048);
+        for (int k = 0; k < nmine; ++k) {
+            const Slice x = slice_of(s, item_of(k));
+            if (!x.arc) continue;
+            __syncthreads();
+            const unsigned b1 = s_b1[k];
+            const int kr = s_krem[k];
+            if (!cached) load_keys(s.sigma, x, s_keys);
+            load_hist(sh, s.hist2 + x.bb * 2048, 2048);   // (ends with a barrier: b1, kr read by all)
             int above;
-            b2 = top_digit(sh, 2048, krem, warp_sums, &s_dig, &s_abv, &above);
-            krem -= above;
+            const unsigned b2 = top_digit(sh, 2048, kr, warp_sums, &s_dig, &s_abv, &above);
             const unsigned pre = (b1 << 11) | b2;
+            if (tid == 0) { s_b1[k] = pre; s_krem[k] = kr - above; }   // from here on: key[31:10] of the K-th key
             for (int i = tid; i < 1024; i += kThreads) sh[i] = 0;
             __syncthreads();
-            for (int i = tid; i < nk; i += kThreads)
+            for (int i = tid; i < x.nk; i += kThreads)
                 if ((s_keys[i] >> 10) == pre) atomicAdd(&sh[s_keys[i] & 1023u], 1u);
-            flush_hist(sh, s.hist3 + bb * 1024, 1024);
+            flush_hist(sh, s.hist3 + x.bb * 1024, 1024);
         }
         grid.sync();                                 // ---------------- barrier 2
-        if (arc) {
-            if (it.c == 0)
-                for (int i = tid; i < 2048; i += kThreads) s.hist2[bb * 2048 + i] = 0;
-            load_hist(sh, s.hist3 + bb * 1024, 1024);
+        for (int k = 0; k < nmine; ++k) {
+            const Slice x = slice_of(s, item_of(k));
+            if (!x.arc) continue;
+            __syncthreads();
+            if (x.c == 0)
+                for (int i = tid; i < 2048; i += kThreads) s.hist2[x.bb * 2048 + i] = 0;
+            const unsigned pre = s_b1[k];
+            const int kr = s_krem[k];
+            if (!cached) load_keys(s.sigma, x, s_keys);
+            load_hist(sh, s.hist3 + x.bb * 1024, 1024);   // (ends with a barrier: pre, kr read by all)
             int above;
-            const unsigned b3 = top_digit(sh, 1024, krem, warp_sums, &s_dig, &s_abv, &above);
-            T = (b1 << 21) | (b2 << 10) | b3;
-            need_eq = krem - above;
+            const unsigned b3 = top_digit(sh, 1024, kr, warp_sums, &s_dig, &s_abv, &above);
+            const unsigned T = (pre << 10) | b3;
+            if (tid == 0) { s_b1[k] = T; s_krem[k] = kr - above; }   // (T, need_eq) of the block
             int gt = 0, eq = 0;
-            for (int i = tid; i < nk; i += kThreads) {
+            for (int i = tid; i < x.nk; i += kThreads) {
                 gt += s_keys[i] > T;
                 eq += s_keys[i] == T;
             }
             int tg, te;
             cta_exclusive_scan(gt, warp_sums, &tg);
             cta_exclusive_scan(eq, warp_sums, &te);
-            if (tid == 0) { s.slice_gt[sidx] = tg; s.slice_eq[sidx] = te; }
+            if (tid == 0) { s.slice_gt[x.sidx] = tg; s.slice_eq[x.sidx] = te; }
         }
         grid.sync();                                 // ---------------- barrier 3
-        if (arc) {
-            if (it.c == 0)
-                for (int i = tid; i < 1024; i += kThreads) s.hist3[bb * 1024 + i] = 0;
+        if (s.early && blockIdx.x == 0 && tid == 0) ga.bnd_count[par ^ 1] = 0;   // the next step's counter
+        for (int k = 0; k < nmine; ++k) {
+            const Slice x = slice_of(s, item_of(k));
+            if (!x.arc) { identity(x); continue; }
+            __syncthreads();
+            if (x.c == 0)
+                for (int i = tid; i < 1024; i += kThreads) s.hist3[x.bb * 1024 + i] = 0;
+            if (!cached) load_keys(s.sigma, x, s_keys);
             int gb = 0, eb = 0;
-            for (int c = tid; c < it.c; c += kThreads) {
-                gb += __ldcg(s.slice_gt + B.slice_base + c);
-                eb += __ldcg(s.slice_eq + B.slice_base + c);
+            for (int c = tid; c < x.c; c += kThreads) {
+                gb += __ldcg(s.slice_gt + x.B.slice_base + c);
+                eb += __ldcg(s.slice_eq + x.B.slice_base + c);
             }
             int gtot, etot;
             cta_exclusive_scan(gb, warp_sums, &gtot);
             cta_exclusive_scan(eb, warp_sums, &etot);
-            sel_before = gtot + min(etot, need_eq);
-            need_eq = max(0, need_eq - etot);        // quota left for this slice's equal keys
-            use_peq = false;
+            const int need_eq = s_krem[k];
+            const unsigned T = s_b1[k];
+            const int sel_before = gtot + min(etot, need_eq);
+            // b1 of the block = T's top 11 bits (the boundary rows of early mode)
+            compact(x, T >> 21, T, 0x7FFFFFFF, max(0, need_eq - etot), sel_before, false);
+            if (s.early) append_boundary(x);
         }
-    }
-    STAMP(4);
-    // ------------------------------------------------ compaction, S4..S6
-    int32_t* __restrict__ out = s.sel + B.sel_base;
-    if (arc) {
-        const int per = (s.slice_rows + kThreads - 1) / kThreads;   // consecutive rows per thread
-        int my_eq = 0;
-        if (!use_peq)
-            for (int k = 0; k < per; ++k) {
-                const int i = tid * per + k;
-                my_eq += (i < nk && s_keys[i] == T);
+        if (s.early) {
+            // a candidate overflow (massive ties): the selected boundary rows may crowd
+            // a few slices, so every slice appended them to one list and, after a
+            // barrier, the grid's warps take them row by row
+            __threadfence();
+            grid.sync();                             // ---------------- the boundary list is complete
+            const int total = static_cast<int>(__ldcg(ga.bnd_count + par));
+            const int lane = tid & 31, warps = kThreads / 32;
+            for (int j = blockIdx.x * warps + (tid >> 5); j < total; j += gridDim.x * warps) {
+                const int2 br = __ldcg(ga.bnd + j);
+                gather_row_warp(ga, ga.blocks[br.x], br.y, lane);
             }
-        int eq_tot;
-        int eq_rank = use_peq ? 0 : cta_exclusive_scan(my_eq, warp_sums, &eq_tot);
-        int my_sel = 0;
-        unsigned take_mask = 0;                      // per <= 16
-        for (int k = 0; k < per; ++k) {
-            const int i = tid * per + k;
-            bool t = false;
-            if (i < nk) {
-                const unsigned key = s_keys[i];
-                if (key > T) t = true;
-                else if (key == T) {
-                    if (use_peq) t = lo + i <= P_eq;
-                    else { t = eq_rank < need_eq; ++eq_rank; }
-                }
-            }
-            if (t) { take_mask |= 1u << k; ++my_sel; }
+            STAMP(6);
+            STAMP(7);
+            return;
         }
-        if (tid == 0) s_nb = 0;
-        int nsel;
-        int pos = cta_exclusive_scan(my_sel, warp_sums, &nsel);
-        for (int k = 0; k < per; ++k) {
-            if (take_mask & (1u << k)) {
-                const int i = tid * per + k;
-                out[sel_before + pos] = lo + i;
-                ++pos;
-                // early mode: the selected rows of the boundary bin are still to do
-                if (s.early && (s_keys[i] >> 21) == b1) s_rows[atomicAdd(&s_nb, 1)] = i;
-            }
-        }
-    } else {
-        // identity selection: DENSE blocks and K = m
-        for (int p = lo + tid; p < hi; p += kThreads) out[p] = p;
-    }
-    STAMP(5);
-    if (s.early && !overflow) {
-        if (arc) {
-            __syncthreads();
-            gather_rows_local<4>(ga, B, lo, s_rows, s_nb);
-        }
-        STAMP(6);
-        STAMP(7);
-        return;
-    }
-    if (s.early) {
-        // a candidate overflow (massive ties): the selected boundary rows may crowd
-        // a few slices, so every slice appends them to one list and, after a
-        // barrier, the grid's warps take them row by row
-        if (arc && tid == 0) s_abv = s_nb > 0 ? static_cast<int>(atomicAdd(ga.bnd_count + par, static_cast<unsigned>(s_nb))) : 0;
-        if (blockIdx.x == 0 && tid == 0) ga.bnd_count[par ^ 1] = 0;   // the next step's counter
-        __syncthreads();
-        if (arc)
-            for (int i = tid; i < s_nb; i += kThreads) ga.bnd[s_abv + i] = make_int2(static_cast<int>(bb), lo + s_rows[i]);
-        __threadfence();
-        grid.sync();                                 // ---------------- the boundary list is complete
-        const int total = static_cast<int>(__ldcg(ga.bnd_count + par));
-        const int lane = tid & 31, warps = kThreads / 32;
-        for (int j = blockIdx.x * warps + (tid >> 5); j < total; j += gridDim.x * warps) {
-            const int2 br = __ldcg(ga.bnd + j);
-            gather_row_warp(ga, ga.blocks[br.x], br.y, lane);
-        }
-        STAMP(6);
-        STAMP(7);
-        return;
     }
     // S4 (+S5, S6): all selected-row segments spread evenly over the grid; the
     // (static) segment descriptors of this thread's first items are fetched
@@ -820,17 +916,22 @@ int select_gather_resident_ctas() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int per_sm2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_gather<false>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_gather<false, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<true, false>, kThreads, 0);
+    if (per_sm2 < per_sm) per_sm = per_sm2;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<false, true>, kThreads, 0);
+    if (per_sm2 < per_sm) per_sm = per_sm2;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<true, true>, kThreads, 0);
     if (per_sm2 < per_sm) per_sm = per_sm2;
     return sms * (per_sm < 1 ? 1 : per_sm);
 }
 
 int select_max_slice_rows() { return kMaxSliceRows; }
+int select_max_slices_per_cta() { return kMaxSlicesPerCta; }
 
 cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch& ga, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(s.num_items);
+    cfg.gridDim = dim3(s.grid);   // persistent: CTA b takes slices b, b + grid, ...
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
@@ -841,8 +942,12 @@ cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = s.pdl ? 2 : 1;
-    if (s.build_hist) return cudaLaunchKernelEx(&cfg, k_select_gather<true>, s, ga);
-    return cudaLaunchKernelEx(&cfg, k_select_gather<false>, s, ga);
+    const bool multi = s.grid < s.num_items;
+    if (s.build_hist)
+        return multi ? cudaLaunchKernelEx(&cfg, k_select_gather<true, true>, s, ga)
+                     : cudaLaunchKernelEx(&cfg, k_select_gather<true, false>, s, ga);
+    return multi ? cudaLaunchKernelEx(&cfg, k_select_gather<false, true>, s, ga)
+                 : cudaLaunchKernelEx(&cfg, k_select_gather<false, false>, s, ga);
 }
 
 }  // namespace arc

@@ -72,6 +72,28 @@ def llama1b_blocks(mu_bp: int = 10) -> tuple[int, list[Block]]:
     return off, blocks
 
 
+def llama7b_scaled_blocks(mu_bp: int = 10, col_div: int = 512) -> tuple[int, list[Block]]:
+    """A LLaMA-7B-shaped per-tensor table (hidden 4096, FFN 11008, 32 layers,
+    vocab 32000: 226 ARC blocks + one DENSE block) with the true row counts m
+    but every row length divided by `col_div` (scaled down so the CPU oracle
+    finishes in seconds): the selection sees the full 7B block/row structure
+    (1.42M rows, 368 slices of <= 4096 rows), the streaming pass a small d."""
+    H, F, L, Vv = 4096, 11008, 32, 32000
+    shapes = [(Vv, H)]
+    for _ in range(L):
+        shapes += [(H, H), (H, H), (H, H), (H, H), (F, H), (F, H), (H, F)]
+    shapes += [(Vv, H)]
+    blocks, off = [], 0
+    for (m, n) in shapes:
+        n = max(1, n // col_div)
+        blocks.append(Block(off, m * n, m, n, k_from_bp(m, mu_bp), 0))
+        off += m * n
+    dense = (2 * L + 1) * H // col_div
+    blocks.append(Block(off, dense, 1, dense, 1, 1))
+    off += dense
+    return off, blocks
+
+
 # Named configurations (BASELINE.json "configs"; SURVEY.md §8(d1)).
 CONFIGS = {
     # configs[0]: N=4 simulated nodes on one GPU, d=65,536, K=1% -> n=1 (m=d, K=656)

@@ -344,6 +344,62 @@ def test_graph_replayed_three_times_equals_three_eager_steps(kind):
     assert outs[0][1] == outs[1][1]
 
 
+# ------------------------------------------------------------------ persistent selection (several slices per CTA)
+
+@pytest.fixture
+def select_grid(monkeypatch):
+    """Force the selection kernel onto fewer CTAs than slices (ARC_SELECT_GRID,
+    read at create): every CTA then takes several slices (the persistent path)."""
+    def set_grid(grid, slice_rows=256):
+        monkeypatch.setenv("ARC_SELECT_GRID", str(grid))
+        monkeypatch.setenv("ARC_SLICE_ROWS", str(slice_rows))
+    return set_grid
+
+
+@pytest.mark.parametrize("grid", [2, 3, 7])
+def test_persistent_selection_multiblock(orc, select_grid, grid):
+    """Several slices per CTA: mixed ARC blocks (ragged, unaligned, K = m, K = 1)
+    and a DENSE block, early-gather steps and segment-gather steps alternating."""
+    select_grid(grid)
+    shapes = [(3000, 16, 31, 0), (700, 5461 // 43, 3, 0), (64, 64, 64, 0), (1, 1000, 1, 0),
+              (5000, 3, 170, 0), (13, 100, 13, 1), (1300, 20, 2, 0)]
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n, m, n, K, kind))
+        off += m * n
+    run_parity(orc, off, blocks, N=1, steps=4)
+    run_parity(orc, off, blocks, N=3, steps=3)                     # phase 0: Sigma from the node sketches
+    run_parity(orc, off, blocks, N=2, steps=3, force_exchange=True, reduce="ordered")
+
+
+@pytest.mark.parametrize("kind", ["dup_rows", "zeros", "nonfinite"])
+def test_persistent_selection_ties_overflow(orc, select_grid, kind):
+    """Massive ties overflow the candidate list: the digit-by-digit path with
+    several slices per CTA (and the early boundary-row list)."""
+    select_grid(5)
+    d, N, n = 40_000, 2, 4
+    blocks = flat_blocks(d, n, K=700)
+    fixed = adversarial(kind, d, N, n=n)
+    run_parity(orc, d, blocks, N=N, steps=2, grads_fn=lambda t: fixed)
+
+
+def test_persistent_selection_topk_baseline(orc, select_grid):
+    """The All-Gather Top-K baseline (a selection block per node) on 4 CTAs."""
+    select_grid(4)
+    test_topk_allgather_baseline(orc, 4, 60_000, 96, 12)
+
+
+def test_llama7b_shaped_table_creates_and_matches(orc):
+    """A LLaMA-7B-shaped per-tensor table (226 ARC blocks, 1.42M rows: 368 slices of
+    <= 4096 rows, more than the 296 co-resident CTAs) is accepted by create and
+    is bit-exact against the oracle (rows scaled down to keep the oracle fast)."""
+    from synth import llama7b_scaled_blocks
+    d, blocks = llama7b_scaled_blocks()
+    assert sum(1 for b in blocks if b.kind == 0) == 226
+    assert sum(-(-b.m // 4096) for b in blocks if b.kind == 0) == 368
+    run_parity(orc, d, blocks, N=1, steps=2, check_debug=False)
+
+
 # ------------------------------------------------------------------ full-size configs
 
 @pytest.mark.parametrize("name,N,steps", [("C2", 8, 2), ("C3", 1, 2)])
@@ -539,7 +595,8 @@ def test_randomized_configurations(orc, case):
 
 # ------------------------------------------------------------------ selection vs torch.sort
 
-@pytest.mark.parametrize("cfg,mu_bp", [("C5_1e8", 100), ("C5_1e8", 1000), ("C3", 10)])
+@pytest.mark.parametrize("cfg,mu_bp", [("C5_1e8", 100), ("C5_1e8", 1000), ("C3", 10), ("C5_1e9", 100),
+                                        ("C5_1e9", 1000), ("C5_1e9", 10)])
 def test_selection_matches_torch_stable_sort(cfg, mu_bp):
     """the GPU selection against torch.sort(stable) of the same Sigma's
     order keys (larger key first, ties -> smaller row, NaN above +Inf) at full size,
@@ -565,6 +622,75 @@ def test_selection_matches_torch_stable_sort(cfg, mu_bp):
         want = torch.sort(order[:b.K]).values.to(torch.int32)
         assert torch.equal(sel[sum(x.K for x in blocks[:blocks.index(b)]):][:b.K], want)
         base += b.m
+    ctx.close()
+
+
+# ------------------------------------------------------------------ selection valid in binary64
+
+def _gamma(k):
+    u = 2.0 ** -24
+    return k * u / (1 - k * u)
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5_1e9"])
+def test_selection_valid_in_binary64(cfg):
+    """An order-independent check of the GPU selection at full size (not the O6
+    order the oracle shares with the kernel): from the GPU's own residual
+    Delta = h' (-) g_prev (one fp32 subtraction) and V, recompute S = Delta V and
+    Sigma = sum_j S_j^2 in binary64 (zn28373 P:236-237, Alg. 1 l.4-6) with a
+    rounding bound beta_p for ANY fp32 summation order: |S32_j - S64_j| <= E_j =
+    gamma_{n+5} sum_q |Delta_q V_qj| (the dot products), then the squares and
+    the r-term fma chain.  Asserts (a) the kernel's Sigma is within beta of the
+    binary64 value on every row, and (b) every selected row's Sigma64 + beta is
+    >= every unselected row's Sigma64 - beta (the K largest, up to rounding)."""
+    from paper_2510_26709_b200 import ArcTopK
+    from paper_2510_26709_b200 import _lib as L
+    d, blocks = config_blocks(cfg)
+    r = 4
+    src = GradientSource(d, blocks, 1, seed=41, device=DEV)
+    h, g, gbar = [torch.zeros(d, device=DEV)], [torch.zeros(d, device=DEV)], torch.zeros(d, device=DEV)
+    ctx = ArcTopK(d, blocks, N=1, eta=0.1, r=r, seed=41, debug_sketch=True)
+    sel = torch.empty(ctx.sum_K, dtype=torch.int32, device=DEV)
+    for t in range(2):
+        g_prev = g[0].clone()
+        ctx.step(t, src.grads(t), h, g, gbar, sel)
+    torch.cuda.synchronize()
+    sig_gpu = ctx.query(L.Q_SIGMA).double()
+    V_all = ctx.query(L.Q_V)
+    goff = roff = soff = 0
+    checked = 0
+    for b in blocks:
+        if b.kind != 0:
+            soff += b.K
+            continue
+        ldv = -(-b.n // 4) * 4
+        Vb = V_all[goff:goff + r * ldv].view(r, ldv)[:, :b.n].double().t().contiguous()      # n x r
+        goff += r * ldv
+        D = torch.zeros(b.m * b.n, device=DEV)
+        D[:b.len] = h[0][b.offset:b.offset + b.len] - g_prev[b.offset:b.offset + b.len]    # fp32, as the kernel
+        D = D.view(b.m, b.n)
+        sig64 = torch.empty(b.m, dtype=torch.float64, device=DEV)
+        beta = torch.empty(b.m, dtype=torch.float64, device=DEV)
+        step = max(1, (1 << 27) // b.n)
+        for p0 in range(0, b.m, step):
+            D64 = D[p0:p0 + step].double()
+            S = D64 @ Vb
+            E = _gamma(b.n + 5) * (D64.abs() @ Vb.abs())
+            sig64[p0:p0 + step] = (S * S).sum(1)
+            beta[p0:p0 + step] = (2 * S.abs() * E + E * E).sum(1) + _gamma(r + 1) * ((S.abs() + E) ** 2).sum(1)
+        sg = sig_gpu[roff:roff + b.m]
+        assert torch.all((sg - sig64).abs() <= beta + 1e-300), f"{cfg} block at {b.offset}: Sigma outside the bound"
+        chosen = torch.zeros(b.m, dtype=torch.bool, device=DEV)
+        chosen[sel[soff:soff + b.K].long()] = True
+        assert int(chosen.sum()) == b.K
+        if b.K < b.m:
+            lo = (sig64 + beta)[chosen].min()
+            hi = (sig64 - beta)[~chosen].max()
+            assert lo >= hi, f"{cfg} block at {b.offset}: a selected row is below an unselected one ({lo} < {hi})"
+        checked += 1
+        roff += b.m
+        soff += b.K
+    assert checked == sum(1 for b in blocks if b.kind == 0)
     ctx.close()
 
 
