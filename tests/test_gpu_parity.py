@@ -512,6 +512,24 @@ def test_wide_blocks_ranged_launch(orc, r, exchange):
                reduce="ordered" if exchange else "nccl")
 
 
+@pytest.mark.parametrize("layout", [
+    [(3, 5, 3, 0), (40, 4100, 5, 0)],                    # n % 4 == 0, block offset 14: every row s = 2
+    [(1, 1, 1, 0), (33, 5461, 4, 0), (2, 3, 1, 0)],     # n = 5461: s cycles 1, 2, 3, 0 row by row
+    [(2, 2, 2, 0), (9, 13001, 2, 0)],                    # V wider than the stage (ranges), s = 0, 1, 2, ...
+    [(1, 6, 1, 0), (21, 5461, 21, 0)],                   # K = m, last block ends the buffer at d % 4 = 3
+])
+@pytest.mark.parametrize("r", [4, 8])
+def test_wide_unaligned_rows_realigned(orc, layout, r):
+    """Wide-row launch, rows that start off a 16-byte boundary: 16-byte loads of the
+    aligned quads realigned with warp shuffles (arc_sketch.cu load_batch) — bit-exact,
+    including the last row of the buffer (its aligned quad is never read past d)."""
+    blocks, off = [], 0
+    for m, n, K, kind in layout:
+        blocks.append(Block(off, m * n - (n // 3 if m > 1 else 0), m, n, K, kind))
+        off += blocks[-1].len
+    run_parity(orc, off, blocks, N=2, steps=3, r=r)
+
+
 @pytest.mark.parametrize("r", [4, 32])
 def test_wide_blocks_beyond_the_full_stage(orc, r):
     """The second launch stages a wide block's whole V_b^T (up to 196 KB) once per
