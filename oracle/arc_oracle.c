@@ -99,6 +99,27 @@ void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint3
 static float bits_to_float(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
 static uint32_t float_to_bits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 
+/*
+ * bfloat16 wire [R25] (not in the paper, whose precision is
+ * unstated, A10): the binary32 value rounded to the nearest bfloat16 (8
+ * significand bits, binary32's exponent range), ties to even, returned as the
+ * binary32 number it represents.  Written from the definition: the 16 low bits
+ * are dropped, rounding up when they exceed the halfway point 0x8000, or equal
+ * it and the kept part is odd.  Infinities stay; any NaN becomes a NaN.
+ */
+float orc_bf16(float x)
+{
+    uint32_t u = float_to_bits(x);
+    if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu) != 0)
+        return bits_to_float((u | 0x00400000u) & 0xFFFF0000u);     /* quiet NaN, sign kept */
+    uint32_t low = u & 0xFFFFu, keep = u >> 16;
+    if (low > 0x8000u || (low == 0x8000u && (keep & 1u))) keep += 1u;   /* carries into the exponent */
+    return bits_to_float(keep << 16);
+}
+
+/* the value node i puts on the value wire [R25]: x itself, or bf16(x) */
+static float wire_value(float x, int32_t wire) { return wire ? orc_bf16(x) : x; }
+
 /* word -> uniform in (0,1): (x >> 9) * 2^-23 + 2^-24, both operations exact [R8]. */
 float orc_uniform(uint32_t x)
 {
@@ -317,10 +338,11 @@ static float o6_dot(const float* x, const float* y, int64_t ys, int64_t nv)
  *   sigma   [m]       : Sigma_p: s = +0; s <- fma(S_pj, S_pj, s), j = 0..r-1 (O8)
  *   sel     [K]       : I, ascending
  *   C_local [N][K][n] : [G_i]_{I,:}, compact rows in I order, +0 in padding
+ *                       (wire = 1: each entry rounded to bfloat16 [R25])
  *   C_glob  [K][n]    : (1/N) sum_i C_local_i = A / N, A summed in node order
  */
 void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int32_t r,
-                   const float* const* G, const float* V, int32_t exact,
+                   const float* const* G, const float* V, int32_t exact, int32_t wire,
                    float* P_nodes, float* S_out, float* sigma, int32_t* sel,
                    float* C_local, float* C_glob)
 {
@@ -378,7 +400,7 @@ void orc_arc_round(int32_t N, int64_t len, int64_t m, int64_t n, int64_t K, int3
         for (int64_t q = 0; q < n; q++) {
             float a = 0.0f;
             for (int32_t i = 0; i < N; i++) {
-                float c = (q < nv) ? G[i][p * n + q] : 0.0f;
+                float c = wire_value((q < nv) ? G[i][p * n + q] : 0.0f, wire);   /* [R25] */
                 if (C_local) C_local[((size_t)i * K + k) * n + q] = c;
                 a = (i == 0) ? c : a + c;
             }
@@ -428,6 +450,8 @@ typedef struct {
     int32_t num_blocks;
     int32_t pad_;
     const orc_block* blocks;  /* tile [0, d) in order                      */
+    int32_t wire;             /* value wire: 0 binary32, 1 bfloat16 [R25]  */
+    int32_t pad2_;
 } orc_cfg;
 
 /* debug outputs, each optional: V concatenated per ARC block ([n_b][r]);
@@ -474,7 +498,7 @@ int orc_step(const orc_cfg* cfg, int64_t t,
                 for (int64_t q = 0; q < n; q++) {
                     float a = 0.0f;
                     for (int32_t i = 0; i < N; i++) {
-                        float c = (q < nv) ? D[i][p * n + q] : 0.0f;
+                        float c = wire_value((q < nv) ? D[i][p * n + q] : 0.0f, cfg->wire);   /* [R25] */
                         Cl[((size_t)i * K + k) * n + q] = c;
                         a = (i == 0) ? c : a + c;
                     }
@@ -489,7 +513,7 @@ int orc_step(const orc_cfg* cfg, int64_t t,
             float* V = (float*)malloc((size_t)n * cfg->r * sizeof(float));
             orc_gaussian_V(cfg->seed, t, b, n, cfg->r, V);
             float* sg = (float*)malloc((size_t)m * sizeof(float));
-            orc_arc_round(N, len, m, n, K, cfg->r, (const float* const*)D, V, cfg->exact,
+            orc_arc_round(N, len, m, n, K, cfg->r, (const float* const*)D, V, cfg->exact, cfg->wire,
                           NULL, NULL, sg, sel, Cl, Cg);
             if (V_out) memcpy(V_out + V_pos, V, (size_t)n * cfg->r * sizeof(float));
             if (sigma_out) memcpy(sigma_out + sig_pos, sg, (size_t)m * sizeof(float));
@@ -504,7 +528,7 @@ int orc_step(const orc_cfg* cfg, int64_t t,
                 for (int64_t q = 0; q < n; q++) {
                     float a = 0.0f;
                     for (int32_t i = 0; i < N; i++) {
-                        float c = (q < nv) ? D[i][k * n + q] : 0.0f;
+                        float c = wire_value((q < nv) ? D[i][k * n + q] : 0.0f, cfg->wire);   /* [R25] */
                         Cl[((size_t)i * K + k) * n + q] = c;
                         a = (i == 0) ? c : a + c;
                     }
@@ -515,6 +539,9 @@ int orc_step(const orc_cfg* cfg, int64_t t,
 
         /* eq:ef21m-2: g_t = g_{t-1} + C_local(h_t - g_{t-1}); rows outside I
          * receive + 0 and are left as they are [R12].  gbar += C [R13].
+         * With the bfloat16 wire C_local holds what node i sent, bf16(Delta_i),
+         * so g_i moves by exactly that and the rounding error stays in the
+         * residual h_i - g_i for the next steps (error feedback) [R25].
          * (The rows of I are distinct, so rows may run on any thread.) */
 #pragma omp parallel for schedule(static)
         for (int64_t k = 0; k < K; k++) {
@@ -564,7 +591,7 @@ int orc_step_noef(const orc_cfg* cfg, int64_t t, const float* const* grad, float
             float* V = (float*)malloc((size_t)n * cfg->r * sizeof(float));
             orc_gaussian_V(cfg->seed, t, b, n, cfg->r, V);
             float* sg = (float*)malloc((size_t)m * sizeof(float));
-            orc_arc_round(N, len, m, n, K, cfg->r, G, V, 0, NULL, NULL, sg, sel, NULL, Cg);
+            orc_arc_round(N, len, m, n, K, cfg->r, G, V, 0, cfg->wire, NULL, NULL, sg, sel, NULL, Cg);
             if (V_out) memcpy(V_out + V_pos, V, (size_t)n * cfg->r * sizeof(float));
             if (sigma_out) memcpy(sigma_out + sig_pos, sg, (size_t)m * sizeof(float));
             V_pos += n * cfg->r;
@@ -578,7 +605,7 @@ int orc_step_noef(const orc_cfg* cfg, int64_t t, const float* const* grad, float
                 for (int64_t q = 0; q < n; q++) {
                     float a = 0.0f;
                     for (int32_t i = 0; i < N; i++) {
-                        float c = (q < nv) ? G[i][k * n + q] : 0.0f;
+                        float c = wire_value((q < nv) ? G[i][k * n + q] : 0.0f, cfg->wire);   /* [R25] */
                         a = (i == 0) ? c : a + c;
                     }
                     Cg[(size_t)k * n + q] = a / (float)N;

@@ -55,7 +55,9 @@ def lib():
         L.orc_argtop_k.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
         L.orc_arc_round.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
-                                    ctypes.c_int32] + [ctypes.c_void_p] * 6
+                                    ctypes.c_int32, ctypes.c_int32] + [ctypes.c_void_p] * 6
+        L.orc_bf16.argtypes = [ctypes.c_float]
+        L.orc_bf16.restype = ctypes.c_float
         L.orc_randk_keys.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p]
         L.orc_ln_array.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         L.orc_sigma_rows.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
@@ -87,7 +89,7 @@ class _Cfg(ctypes.Structure):
     _fields_ = [("N", ctypes.c_int32), ("r", ctypes.c_int32), ("d", ctypes.c_int64),
                 ("eta", ctypes.c_float), ("exact", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("num_blocks", ctypes.c_int32), ("pad_", ctypes.c_int32),
-                ("blocks", ctypes.POINTER(_Block))]
+                ("blocks", ctypes.POINTER(_Block)), ("wire", ctypes.c_int32), ("pad2_", ctypes.c_int32)]
 
 
 @dataclass(frozen=True)
@@ -200,7 +202,13 @@ def _ptr_array(arrs):
     return (ctypes.c_void_p * len(arrs))(*[_ptr(a) for a in arrs])
 
 
-def arc_round(G_nodes, n: int, K: int, V=None, r: int | None = None, exact: bool = False, m: int | None = None):
+def bf16(x: float) -> float:
+    """The binary32 value rounded to bfloat16 (ties to even) [R25]."""
+    return float(lib().orc_bf16(float(x)))
+
+
+def arc_round(G_nodes, n: int, K: int, V=None, r: int | None = None, exact: bool = False, m: int | None = None,
+              wire: str = "f32"):
     """Algorithm 1 on N local flat blocks (each ``len`` floats viewed as m x n).
 
     Returns dict with P_nodes [N,m,r] (P'_i = G_i V, unscaled), S [m,r] (their
@@ -222,6 +230,7 @@ def arc_round(G_nodes, n: int, K: int, V=None, r: int | None = None, exact: bool
                C_local=np.zeros((N, K, n), np.float32), C=np.zeros((K, n), np.float32))
     Gp = _ptr_array(G)
     lib().orc_arc_round(N, length, m, n, K, r, ctypes.cast(Gp, ctypes.c_void_p), _ptr(V), int(bool(exact)),
+                        {"f32": 0, "bf16": 1}[wire],
                         _ptr(out["P_nodes"]), _ptr(out["S"]), _ptr(out["sigma"]), _ptr(out["sel"]),
                         _ptr(out["C_local"]), _ptr(out["C"]))
     return out
@@ -234,15 +243,16 @@ class OracleEF21M:
     ``h[i]``, ``g[i]`` (per node) and ``gbar`` (the replicated tracker)."""
 
     def __init__(self, d: int, blocks, N: int, eta: float, r: int, seed: int, exact: bool = False,
-                 h0=None, g0=None, gbar0=None, method: str = "arc"):
+                 h0=None, g0=None, gbar0=None, method: str = "arc", wire: str = "f32"):
         self.d, self.N, self.eta, self.r, self.seed, self.exact = int(d), int(N), float(eta), int(r), int(seed), bool(exact)
         self.method = method
         self.blocks = list(blocks)
         self._cblocks = (_Block * len(self.blocks))(*[
             _Block(b.offset, b.len, b.m, b.n, b.K, b.kind, 0) for b in self.blocks])
         mode = 2 if method == "randk" else int(self.exact)
+        self.wire = wire
         self._cfg = _Cfg(self.N, self.r, self.d, self.eta, mode, self.seed & (2**64 - 1),
-                         len(self.blocks), 0, self._cblocks)
+                         len(self.blocks), 0, self._cblocks, {"f32": 0, "bf16": 1}[wire], 0)
         self.h = [np.zeros(d, np.float32) if h0 is None else _f32(h0[i]).copy() for i in range(N)]
         self.g = [np.zeros(d, np.float32) if g0 is None else _f32(g0[i]).copy() for i in range(N)]
         self.gbar = np.zeros(d, np.float32) if gbar0 is None else _f32(gbar0).copy()
@@ -304,7 +314,7 @@ class OracleEF21M:
         return dict(sel=sel.reshape(self.N, self.sum_K), values=vals.reshape(self.N, self.sum_Kn))
 
 
-__all__ = ["Block", "OracleEF21M", "get_threads", "set_threads", "apply_adam", "apply_sgd", "arc_round", "argtop_k", "build", "gaussian_V", "ln", "ln_array", "lib",
+__all__ = ["Block", "OracleEF21M", "bf16", "get_threads", "set_threads", "apply_adam", "apply_sgd", "arc_round", "argtop_k", "build", "gaussian_V", "ln", "ln_array", "lib",
            "momentum", "philox4x32_10", "randk_keys", "sigma_key", "sigma_rows", "sincos2pi", "sincos2pi_array",
            "uniform"]
 
