@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define ARC_TOPK_ABI_VERSION 1u
+#define ARC_TOPK_ABI_VERSION 2u
 #define ARC_MAX_NODES_LOCAL 16
 
 typedef struct arc_topk_ctx arc_topk_ctx;   /* opaque, library-owned */
@@ -114,6 +114,19 @@ typedef enum {
 #define ARC_FLAG_LOOPBACK_COMM  0x8u  /* nccl_comm is an arc_topk_loopback_comm() handle: G ranks   */
                                       /* emulated in one process on one GPU (tests; not with LSA)  */
 
+/* The value wire (exchange #2's payload, R25):
+ * ARC_WIRE_F32 sends the compact rows C_i in binary32; ARC_WIRE_BF16 rounds each
+ * entry to bfloat16 at the source (round to nearest, ties to even), halving the
+ * payload.  The EF update adds what was sent, g_i <- g_i + bf16(C_i), so the
+ * rounding error stays in the residual h_i - g_i (error feedback); every sum
+ * (A = sum_i C_i, gbar += A / N) stays binary32.  The rounding is applied on
+ * every placement (also with every node on one GPU), so I, h, g and, with
+ * ORDERED / LSA, gbar do not depend on G.  With ARC_REDUCE_NCCL the all-reduce
+ * runs in bfloat16 (the rank's local pre-sum and NCCL's partial sums are rounded
+ * to bf16, u = 2^-8 each): gbar within (G + 1) u M (R25).  The sketch exchange (P'_i, Sigma) stays binary32.  Not for
+ * ARC_METHOD_TOPK_ALLGATHER (its payload carries indices): ARC_ERR_UNSUPPORTED. */
+typedef enum { ARC_WIRE_F32 = 0, ARC_WIRE_BF16 = 1 } arc_wire;
+
 /* One block: the m x n row-major view of flat elements [offset, offset+len),
  * (m-1) n < len <= m n (only the last row may be short, R14).  K rows kept,
  * 1 <= K <= m; DENSE blocks require K == m.  Blocks must tile [0, d) in order. */
@@ -132,13 +145,19 @@ typedef struct {
     int32_t  rank;          /* this GPU's rank in the communicator (0 when G == 1)    */
     int64_t  d;             /* per-node vector length in floats                       */
     int32_t  r;             /* sketch width, 1..32 (paper: 4)                         */
-    int32_t  num_blocks;    /* >= 1                                                   */
+    int32_t  num_blocks;    /* >= 1; or 0 with blocks == NULL: the single-block       */
+                            /* shorthand below (one ARC block over [0, d))            */
     const arc_block* blocks;/* host array, copied at create                           */
     float    eta;           /* EF21M momentum, 0 < eta <= 1 (NOEF_MSGD: beta, [0, 1)) */
     int32_t  value_reduce;  /* arc_reduce_mode                                        */
     uint64_t seed;          /* shared base seed (R7), identical on every rank         */
     uint32_t flags;         /* ARC_FLAG_*                                             */
     uint32_t method;        /* arc_method: ARC_METHOD_ARC (0) or the baseline below   */
+    int64_t  n, K;          /* num_blocks == 0: rows of n floats, m = ceil(d / n)     */
+                            /* (the last row short, R14), K rows kept, 1 <= K <= m    */
+                            /* (P:226-228 reshape; Alg. 1 input K); else ignored      */
+    int32_t  wire;          /* arc_wire: exchange #2's payload precision (R25)        */
+    int32_t  reserved;      /* 0                                                      */
 } arc_topk_params;
 
 /* Bytes of device workspace `create` needs for these params (host-only call). */
@@ -184,6 +203,10 @@ typedef enum {
     ARC_Q_SEL = 2,      /* int32 [sum_b K_b]             I_b                                   */
     ARC_Q_P_NODES = 3,  /* float [sum_ARC m_b][nodes_local][r]  P'_i = G_i V, unscaled (needs
                            DEBUG_SKETCH, or G > 1, or nodes_local > 1)                         */
+    ARC_Q_S = 5,        /* float [sum_ARC m_b][r]  S = sum_i P'_i, the node sum in ascending node id
+                           (R9): Alg. 1 l.5 before the 1/(N sqrt r) scaling (R2, R3); every node on
+                           this GPU (G == 1) and P' kept (as ARC_Q_P_NODES), else
+                           ARC_ERR_UNSUPPORTED (with G > 1 each rank holds only its own nodes')  */
     ARC_Q_CANDIDATES = 4 /* uint32 [num_blocks] rows sharing the boundary bin of the last selection
                             ([nodes_local][num_blocks] for ARC_METHOD_TOPK_ALLGATHER, whose
                             nodes select separately); synchronises the step's stream first    */

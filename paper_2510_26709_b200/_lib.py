@@ -13,7 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # ARC_LIB_PATH: an alternative build of the same library (A/B timing experiments)
 LIB_PATH = os.environ.get("ARC_LIB_PATH") or os.path.join(_PKG, "libarctopk.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_NODES_LOCAL = 16
 
 # arc_status
@@ -29,7 +29,9 @@ METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK, METHOD_NOEF_MSGD, METHOD_EXACT 
 # arc_opt_kind
 OPT_SGD, OPT_ADAM = 0, 1
 # arc_query
-Q_V, Q_SIGMA, Q_SEL, Q_P_NODES, Q_CANDIDATES = 0, 1, 2, 3, 4
+Q_V, Q_SIGMA, Q_SEL, Q_P_NODES, Q_CANDIDATES, Q_S = 0, 1, 2, 3, 4, 5
+# arc_wire
+WIRE_F32, WIRE_BF16 = 0, 1
 
 EXPORTED = [
     "arc_topk_workspace_bytes", "arc_topk_create", "arc_topk_step", "arc_topk_step_host",
@@ -54,7 +56,8 @@ class ArcParams(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("d", ctypes.c_int64), ("r", ctypes.c_int32),
                 ("num_blocks", ctypes.c_int32), ("blocks", ctypes.POINTER(ArcBlock)),
                 ("eta", ctypes.c_float), ("value_reduce", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32), ("method", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("method", ctypes.c_uint32),
+                ("n", ctypes.c_int64), ("K", ctypes.c_int64), ("wire", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class ArcOptParams(ctypes.Structure):

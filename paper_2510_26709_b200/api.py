@@ -100,33 +100,46 @@ class ArcTopK:
       comm_group: an NCCL group over pg's ranks for the library's collectives
       (``dist.private_nccl_group(pg, device)``), shared by several contexts;
       default: a private group per context.
+      wire: "f32" or "bf16" — exchange #2's payload precision (R25: each sent
+      entry rounded to bfloat16 at the source, EF keeps the rounding error).
+      blocks=None with n, K: the single-block shorthand (rows of n, K kept).
       loopback: a :class:`LoopbackGroup` of G = N / nodes_local emulated ranks
       (tests on one GPU; this context is rank ``rank`` of it, and must be
       created and stepped from its own host thread, concurrently with the
       other ranks'); no process group is used then.
     """
 
-    def __init__(self, d: int, blocks: Sequence, N: int, eta: float, r: int = 4, seed: int = 20251030,
+    def __init__(self, d: int, blocks: Sequence | None, N: int, eta: float, r: int = 4, seed: int = 20251030,
                  nodes_local: int | None = None, pg=None, rank: int = 0, reduce: str = "nccl",
                  host_staging: bool = False, debug_sketch: bool = False, force_exchange: bool = False,
-                 method: str = "arc", device=None, stream=None, comm_group=None, loopback=None):
+                 method: str = "arc", device=None, stream=None, comm_group=None, loopback=None,
+                 wire: str = "f32", n: int | None = None, K: int | None = None):
         self.lib = L.lib()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.d, self.N = int(d), int(N)
         self.nodes_local = int(nodes_local if nodes_local is not None else N)
         self.G = self.N // self.nodes_local
+        if blocks is None:                       # the ABI's single-block shorthand (n, K)
+            if n is None or K is None:
+                raise ValueError("give blocks, or n and K")
+            blocks = [Block(0, int(d), -(-int(d) // int(n)), int(n), int(K), L.BLOCK_ARC)]
+            nb = 0
+        else:
+            nb = len(blocks)
         self.blocks = list(blocks)
         self._cblocks = (L.ArcBlock * len(self.blocks))(*[
             L.ArcBlock(int(b.offset), int(b.len), int(b.m), int(b.n), int(b.K), int(b.kind), 0) for b in self.blocks])
         flags = (L.FLAG_HOST_STAGING if host_staging else 0) | (L.FLAG_DEBUG_SKETCH if debug_sketch else 0) | \
                 (L.FLAG_FORCE_EXCHANGE if force_exchange else 0) | (L.FLAG_LOOPBACK_COMM if loopback is not None else 0)
         self.params = L.ArcParams(L.ABI_VERSION, self.N, self.nodes_local, int(rank), self.d, int(r),
-                                  len(self.blocks), self._cblocks, float(eta),
+                                  nb, self._cblocks if nb else None, float(eta),
                                   {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED, "lsa": L.REDUCE_LSA}[reduce],
                                   int(seed) & (2**64 - 1), flags,
                                   {"arc": L.METHOD_ARC, "topk_allgather": L.METHOD_TOPK_ALLGATHER,
                                    "randk": L.METHOD_RANDK, "noef_msgd": L.METHOD_NOEF_MSGD,
-                                   "exact": L.METHOD_EXACT}[method])
+                                   "exact": L.METHOD_EXACT}[method],
+                                  int(n or 0), int(K or 0), {"f32": L.WIRE_F32, "bf16": L.WIRE_BF16}[wire], 0)
+        self.wire = wire
         self.method = method
         nbytes = ctypes.c_size_t()
         L.check(self.lib.arc_topk_workspace_bytes(ctypes.byref(self.params), ctypes.byref(nbytes)),
@@ -142,7 +155,8 @@ class ArcTopK:
             if pg is None:
                 raise ValueError("N / nodes_local > 1 needs an NCCL process group")
             from .dist import check_consistent, params_digest, private_nccl_group
-            check_consistent(pg, params_digest(d, self.blocks, self.N, self.nodes_local, r, eta, seed, reduce))
+            check_consistent(pg, params_digest(d, self.blocks, self.N, self.nodes_local, r, eta, seed, reduce,
+                                               method, wire))
             # the library's collectives get a communicator of their own, so they can
             # never interleave with torch's collectives on the caller's group; several
             # contexts (e.g. one per DDP bucket) may share one: comm_group, made once
@@ -212,6 +226,7 @@ class ArcTopK:
         shapes = {L.Q_V: (self.sum_nr_arc, torch.float32), L.Q_SIGMA: (self.sum_m_arc, torch.float32),
                   L.Q_SEL: (self.sum_K, torch.int32),
                   L.Q_P_NODES: (self.sum_m_arc * self.nodes_local * self.r, torch.float32),
+                  L.Q_S: (self.sum_m_arc * self.r, torch.float32),
                   L.Q_CANDIDATES: (len(self.blocks) * (self.nodes_local if self.method == "topk_allgather" else 1),
                                    torch.int32)}
         n, dt = shapes[what]

@@ -97,6 +97,11 @@ struct Comm {
         if (lb) return loopback_all_reduce_f32(lb, send, recv, count, s);
         return nccl->allReduce(send, recv, count, ncclFloat32, ncclSum, nc, s) == ncclSuccess ? ARC_OK : ARC_ERR_NCCL;
     }
+    // the bfloat16 value wire (R25): NCCL sums in bfloat16 (rounded partial sums)
+    arc_status all_reduce_bf16(const void* send, void* recv, size_t count, cudaStream_t s) const {
+        if (lb) return loopback_all_reduce_bf16(lb, send, recv, count, s);
+        return nccl->allReduce(send, recv, count, ncclBfloat16, ncclSum, nc, s) == ncclSuccess ? ARC_OK : ARC_ERR_NCCL;
+    }
     // grouped point-to-point all-to-all (counts / displacements in floats, host arrays [G])
     arc_status all_to_all_f32(const float* send, const size_t* scount, const size_t* sdispl, float* recv,
                               const size_t* rcount, const size_t* rdispl, int G, cudaStream_t s) const {
@@ -166,6 +171,9 @@ arc_status validate(const arc_topk_params* p) {
         return ARC_ERR_INVALID_ARG;
     if (p->value_reduce != ARC_REDUCE_NCCL && p->value_reduce != ARC_REDUCE_ORDERED && p->value_reduce != ARC_REDUCE_LSA)
         return ARC_ERR_INVALID_ARG;
+    if (p->wire != ARC_WIRE_F32 && p->wire != ARC_WIRE_BF16) return ARC_ERR_INVALID_ARG;
+    if (p->reserved != 0) return ARC_ERR_INVALID_ARG;
+    if (p->wire == ARC_WIRE_BF16 && p->method == ARC_METHOD_TOPK_ALLGATHER) return ARC_ERR_UNSUPPORTED;
     if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
     if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE | ARC_FLAG_LOOPBACK_COMM))
         return ARC_ERR_INVALID_ARG;
@@ -192,6 +200,21 @@ arc_status validate(const arc_topk_params* p) {
     if (pos != p->d) return ARC_ERR_INVALID_ARG;
     if (M > INT32_MAX || sumK > INT32_MAX / 64) return ARC_ERR_INVALID_ARG;
     return ARC_OK;
+}
+
+// The single-block shorthand (num_blocks == 0, blocks == NULL): one ARC block
+// of rows of n floats over [0, d), m = ceil(d / n), K rows kept (
+// Alg. 1's K).  `out` is the params with the block table filled in (`one`).
+arc_status normalize(const arc_topk_params* in, arc_topk_params& out, arc_block& one) {
+    if (in == nullptr) return ARC_ERR_INVALID_ARG;
+    out = *in;
+    if (in->num_blocks == 0 && in->blocks == nullptr) {
+        if (in->n < 1 || in->d < 1) return ARC_ERR_INVALID_ARG;
+        one = arc_block{0, in->d, (in->d + in->n - 1) / in->n, in->n, in->K, ARC_BLOCK_ARC, 0};
+        out.num_blocks = 1;
+        out.blocks = &one;
+    }
+    return validate(&out);
 }
 
 void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
@@ -319,8 +342,9 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
         // symmetric window instead of the workspace
         const bool ordered = p->value_reduce == ARC_REDUCE_ORDERED;
         const bool lsa = p->value_reduce == ARC_REDUCE_LSA;
-        pl.o_wire = lsa ? 0 : take(sizeof(float) * sumKn * (ordered ? pl.L : 1));
-        pl.o_wire_all = ordered ? take(sizeof(float) * sumKn * pl.L * pl.G) : 0;
+        const size_t we = p->wire == ARC_WIRE_BF16 ? 2 : sizeof(float);   // payload entry bytes (R25)
+        pl.o_wire = lsa ? 0 : take(we * sumKn * (ordered ? pl.L : 1));
+        pl.o_wire_all = ordered ? take(we * sumKn * pl.L * pl.G) : 0;
     }
     if (p->flags & ARC_FLAG_HOST_STAGING) {
         // each node's staged gradient starts 256-byte aligned (the kernels' 16-byte loads)
@@ -444,6 +468,8 @@ uint64_t params_hash(const arc_topk_params* p) {
     h = fnv1a(h, &p->eta, sizeof p->eta);
     h = fnv1a(h, &p->value_reduce, sizeof p->value_reduce);
     h = fnv1a(h, &p->seed, sizeof p->seed);
+    h = fnv1a(h, &p->method, sizeof p->method);
+    h = fnv1a(h, &p->wire, sizeof p->wire);
     const uint32_t f = p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_LOOPBACK_COMM);
     h = fnv1a(h, &f, sizeof f);
     return h;
@@ -539,7 +565,7 @@ static arc_status lsa_setup(arc_topk_ctx* c, cudaStream_t s) {
     const ncclTeam_t team = n.teamLsa(c->comm);
     if (team.nRanks != pl.G || pl.G > 72) return ARC_ERR_UNSUPPORTED;   // every rank in one NVLink domain
     if (cudaStreamSynchronize(s) != cudaSuccess) return ARC_ERR_CUDA;
-    size_t bytes = sizeof(float) * static_cast<size_t>(std::max<int64_t>(pl.sumKn, 1)) * pl.L;
+    size_t bytes = (c->p.wire == ARC_WIRE_BF16 ? 2 : sizeof(float)) * static_cast<size_t>(std::max<int64_t>(pl.sumKn, 1)) * pl.L;
     bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
     if (n.memAlloc(&c->win_buf, bytes) != ncclSuccess) return ARC_ERR_NCCL;
     if (n.winRegister(c->comm, c->win_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) return ARC_ERR_NCCL;
@@ -579,22 +605,28 @@ const char* arc_topk_status_string(arc_status s) {
     return "unknown status";
 }
 
-arc_status arc_topk_workspace_bytes(const arc_topk_params* params, size_t* bytes) {
+arc_status arc_topk_workspace_bytes(const arc_topk_params* params_in, size_t* bytes) {
     if (bytes == nullptr) return ARC_ERR_INVALID_ARG;
-    const arc_status v = validate(params);
+    arc_topk_params np;
+    arc_block one;
+    const arc_status v = normalize(params_in, np, one);
     if (v != ARC_OK) return v;
+    const arc_topk_params* params = &np;
     Plan pl;
     make_plan(params, pl);
     *bytes = pl.total;
     return ARC_OK;
 }
 
-arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm, void* workspace, size_t workspace_bytes,
+arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, void* workspace, size_t workspace_bytes,
                            void* stream, arc_topk_ctx** out) {
     if (out == nullptr) return ARC_ERR_INVALID_ARG;
     *out = nullptr;
-    const arc_status v = validate(params);
+    arc_topk_params np;
+    arc_block one;
+    const arc_status v = normalize(params_in, np, one);
     if (v != ARC_OK) return v;
+    const arc_topk_params* params = &np;
     if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) % kAlign) != 0) return ARC_ERR_INVALID_ARG;
     arc_topk_ctx* c = new (std::nothrow) arc_topk_ctx();
     if (c == nullptr) return ARC_ERR_INVALID_ARG;
@@ -1021,6 +1053,9 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ga.noef = pl.noef ? 1 : 0;
     ga.bnd = c->at<int2>(pl.o_bnd);
     ga.bnd_count = c->at<unsigned>(pl.o_bnd_count);
+    const int bf16 = c->p.wire == ARC_WIRE_BF16 ? 1 : 0;   // R25
+    const size_t we = bf16 ? 2 : sizeof(float);           // payload entry bytes
+    ga.bf16 = bf16;
     const bool ordered = c->p.value_reduce != ARC_REDUCE_NCCL;   // ORDERED and LSA: per-node payloads
     float* wire = c->lsa ? static_cast<float*>(c->win_buf)
                          : ((pl.exchange || pl.topk) ? c->at<float>(pl.o_wire) : nullptr);
@@ -1099,7 +1134,9 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         dl.sel = sel;
         dl.mode = !pl.exchange ? 0 : (ordered ? 2 : 1);
         dl.noef = pl.noef ? 1 : 0;
-        dl.values = !pl.exchange ? values_out : wire;
+        dl.values = !pl.exchange ? values_out : nullptr;
+        dl.payload = pl.exchange ? static_cast<void*>(wire) : nullptr;
+        dl.bf16 = bf16;
         dl.sum_Kn = pl.sumKn;
         launch_dense(dl, s);
         ARC_LAUNCHED();
@@ -1136,6 +1173,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         x.L = L;
         x.N = c->p.N;
         x.sum_Kn = pl.sumKn;
+        x.bf16 = bf16;
         if (!pl.segs_real.empty()) {
             ScatterLaunch sa{};
             sa.blocks = blocks;
@@ -1164,24 +1202,25 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             ARC_LAUNCHED();
         }
     } else if (pl.exchange) {   // exchange #2 + S6
-        const float* reduced = wire;
+        const void* reduced = wire;
         if (!ordered) {
             if (c->xc.any() && pl.G > 1) {
-                const arc_status ar = c->xc.all_reduce_f32(wire, wire, static_cast<size_t>(pl.sumKn), s);
+                const arc_status ar = bf16 ? c->xc.all_reduce_bf16(wire, wire, static_cast<size_t>(pl.sumKn), s)
+                                           : c->xc.all_reduce_f32(wire, wire, static_cast<size_t>(pl.sumKn), s);
                 if (ar != ARC_OK) return ar;
                 c->tally[kTallyValues] += pl.sumKn;
                 ++c->tally[kTallyCalls];
             }
         } else {
-            float* all = c->at<float>(pl.o_wire_all);
+            void* all = c->ws + pl.o_wire_all;
             const size_t cnt = static_cast<size_t>(pl.sumKn) * L;
             if (c->xc.any()) {
-                const arc_status ag = c->xc.all_gather_f32(wire, all, cnt, s);
+                const arc_status ag = c->xc.all_gather_bytes(wire, all, cnt * we, s);
                 if (ag != ARC_OK) return ag;
                 c->tally[kTallyValues] += static_cast<int64_t>(cnt);
                 ++c->tally[kTallyCalls];
             } else {
-                ARC_CUDA(cudaMemcpyAsync(all, wire, cnt * sizeof(float), cudaMemcpyDeviceToDevice, s));
+                ARC_CUDA(cudaMemcpyAsync(all, wire, cnt * we, cudaMemcpyDeviceToDevice, s));
             }
             reduced = all;
         }
@@ -1191,6 +1230,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sa.num_rows = static_cast<int>(pl.segs_real.size());
         sa.sel = sel;
         sa.wire = reduced;
+        sa.bf16 = bf16;
         sa.mode = ordered ? 1 : 0;
         sa.nodes_total = c->p.N;
         sa.sum_Kn = pl.sumKn;
@@ -1208,6 +1248,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             ds.dense_ids = c->at<int>(pl.o_dense_ids);
             ds.num_dense = static_cast<int>(pl.dense_ids.size());
             ds.wire = reduced;
+            ds.bf16 = bf16;
             ds.mode = ordered ? 1 : 0;
             ds.nodes_total = c->p.N;
             ds.sum_Kn = pl.sumKn;
@@ -1273,6 +1314,15 @@ arc_status arc_topk_query(arc_topk_ctx* c, int32_t what, void* dst, size_t bytes
             off = pl.o_pnodes;
             need = sizeof(float) * static_cast<size_t>(pl.M) * pl.L * c->p.r;
             break;
+        case ARC_Q_S: {   // S = sum_i P'_i (node order), every node on this GPU
+            if (!pl.keep_pnodes || pl.G > 1 || pl.randk || pl.topk) return ARC_ERR_UNSUPPORTED;
+            need = sizeof(float) * static_cast<size_t>(pl.M) * c->p.r;
+            if (bytes < need) return ARC_ERR_INVALID_ARG;
+            if (need == 0) return ARC_OK;
+            launch_node_sum(c->pnodes_ptr(), pl.M, pl.L, c->p.r, static_cast<float*>(dst), static_cast<cudaStream_t>(stream));
+            ARC_LAUNCHED();
+            return ARC_OK;
+        }
         case ARC_Q_CANDIDATES: {   // counters of the last step's parity (device word status[1], toggled per step)
             unsigned par = 0;
             ARC_CUDA(cudaStreamSynchronize(c->last));

@@ -1,6 +1,7 @@
 // arc_device.cuh — device helpers shared by the kernel files of libarctopk.so:
 // explicitly rounded binary32 operations (no contraction, R9) and streaming loads.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace arc {
@@ -36,6 +37,21 @@ static __device__ __forceinline__ float4 ld_na4(const float* p) {
     asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
     return v;
+}
+
+// ---- the value wire (R25): binary32, or bfloat16 rounded at the source --------
+// what a node sends: c itself, or bf16(c) (round to nearest even), as binary32
+static __device__ __forceinline__ float wire_round(float c, int bf16) {
+    return bf16 ? __bfloat162float(__float2bfloat16_rn(c)) : c;
+}
+// element i of a payload buffer of binary32 or bfloat16 entries
+static __device__ __forceinline__ float pay_ld(const void* base, long long i, int bf16) {
+    return bf16 ? __bfloat162float(__ldcg(static_cast<const __nv_bfloat16*>(base) + i))
+                : __ldcg(static_cast<const float*>(base) + i);
+}
+static __device__ __forceinline__ void pay_st(void* base, long long i, float v, int bf16) {
+    if (bf16) static_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(v);
+    else static_cast<float*>(base)[i] = v;
 }
 
 // Order key of a Sigma value (R15): its binary32 bit pattern (Sigma >= +0, so

@@ -186,6 +186,7 @@ struct GatherLaunch {
                         // 3 = Top-K baseline: node B.node only, wire values at B.val_base
     long long sum_Kn;
     int noef;           // without EF: C_i = grad_i rows, no h / g (u = gbar, scaled by the sketch pass)
+    int bf16;           // bfloat16 value wire (R25): C_i rounded at the source; modes 1, 2 payloads in bf16
     int2* bnd;          // early mode after an overflow: selected boundary rows (block, row)
     unsigned* bnd_count;   // [2] by step parity
 };
@@ -195,8 +196,9 @@ struct ScatterLaunch {
     const SelRow* rows;
     int num_rows;
     const int32_t* sel;
-    const float* wire;      // reduced sums (mode 0) or gathered per-node wires (mode 1)
+    const void* wire;       // reduced sums (mode 0) or gathered per-node wires (mode 1); float or bf16 entries
     int mode;               // 0 = already summed; 1 = [G*nodes_local][sumKn], ordered sum
+    int bf16;               // payload entries are bfloat16 (R25)
     int nodes_total;        // N (mode 1)
     long long sum_Kn;
     float Nf;
@@ -230,6 +232,9 @@ struct ExactSigmaLaunch {
 };
 void launch_exact_sigma(const ExactSigmaLaunch& a, cudaStream_t s);
 
+// ARC_Q_S: the node sum S [M][r] of the per-node sketches [M][L][r] (node order)
+void launch_node_sum(const float* pnodes, long long M, int L, int r, float* dst, cudaStream_t s);
+
 // DENSE blocks with every node on this GPU: one streaming pass (identity compressor).
 struct DenseLaunch {
     const BlockDev* blocks;
@@ -240,7 +245,9 @@ struct DenseLaunch {
     float eta, ome, Nf;
     int N_int;
     float* gbar;
-    float* values;              // mode 0: optional A/N; modes 1, 2: the exchange payload
+    float* values;              // mode 0: optional A/N (float)
+    void* payload;              // modes 1, 2: the exchange payload (float or bf16 entries)
+    int bf16;                   // bfloat16 value wire (R25)
     int32_t* sel;               // identity selection written here
     int mode;                   // 0 = fused local; 1 = payload = local node sum; 2 = payload per node
     long long sum_Kn;           // mode 2: per-node payload stride
@@ -254,8 +261,9 @@ struct DenseScatterLaunch {
     const BlockDev* blocks;
     const int* dense_ids;
     int num_dense;
-    const float* wire;
+    const void* wire;           // float or bf16 entries
     int mode;                   // 0 = summed; 1 = [N][sum_Kn] per node, ordered sum
+    int bf16;
     int nodes_total;
     long long sum_Kn;
     float Nf;
@@ -273,6 +281,7 @@ struct LsaScatter {
     ncclWindow_vidmem* win;        // window of [L][sum_Kn] floats per rank
     int G, L, N;                   // ranks (= LSA team), local nodes, global nodes
     long long sum_Kn;
+    int bf16;                      // window entries are bfloat16 (R25)
 };
 void launch_lsa_scatter(const ScatterLaunch& a, const LsaScatter& x, cudaStream_t s);
 // Exchange #1 over peer memory: every rank's per-node sketches P' ([M][L][r])

@@ -88,9 +88,9 @@ __global__ void __launch_bounds__(256) k_scatter(const ScatterLaunch a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (k >= ocnt) continue;
-            float A = a.wire[o0 + q + k];
+            float A = pay_ld(a.wire, o0 + q + k, a.bf16);
             if (a.mode == 1)
-                for (int i = 1; i < a.nodes_total; ++i) A = fadd(A, a.wire[static_cast<long long>(i) * a.sum_Kn + o0 + q + k]);
+                for (int i = 1; i < a.nodes_total; ++i) A = fadd(A, pay_ld(a.wire, static_cast<long long>(i) * a.sum_Kn + o0 + q + k, a.bf16));
             val[k] = k < cnt ? (pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf)) : 0.0f;   // R3; +0 padding
         }
         if (B.vec && cnt == 4) {
@@ -154,9 +154,9 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
         // identity selection
         for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < B.m; p += (long long)gridDim.x * blockDim.x)
             a.sel[B.sel_base + p] = static_cast<int32_t>(p);
-        // payload element (block-relative q) of node i (mode 2) or of the local sum
-        auto out_at = [&](long long q, int i) -> float* {
-            return a.values + (a.mode == 2 ? static_cast<long long>(i) * a.sum_Kn : 0LL) + B.val_base + q;
+        // payload element (block-relative q) of node i (mode 2) or of the local sum (mode 1)
+        auto put = [&](long long q, int i, float v) {
+            pay_st(a.payload, (a.mode == 2 ? static_cast<long long>(i) * a.sum_Kn : 0LL) + B.val_base + q, v, a.bf16);
         };
         // element loop: quads when the block is 16-byte aligned, else scalars
         const bool vec = (B.off % 4) == 0;
@@ -167,12 +167,13 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
             for (int i = 0; i < a.nodes_local; ++i) {
                 const float4 gr = __ldcs(reinterpret_cast<const float4*>(a.nodes.grad[i] + e));
                 if (a.noef) {   // without EF: C_i = grad_i (identity compressor), no h / g
-                    const float r4[4] = {gr.x, gr.y, gr.z, gr.w};
+                    const float r4[4] = {wire_round(gr.x, a.bf16), wire_round(gr.y, a.bf16), wire_round(gr.z, a.bf16),
+                                         wire_round(gr.w, a.bf16)};   // (R25)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) A[k] = (i == 0) ? r4[k] : fadd(A[k], r4[k]);
                     if (a.mode == 2)
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) *out_at(4 * f + k, i) = r4[k];
+                        for (int k = 0; k < 4; ++k) put(4 * f + k, i, r4[k]);
                     continue;
                 }
                 const float4 hv = *reinterpret_cast<const float4*>(a.nodes.h[i] + e);
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     hn[k] = ffma(a.eta, r4[k], fmul(a.ome, h4[k]));   // O2, R11
-                    c4[k] = fsub(hn[k], g4[k]);                              // R4
+                    c4[k] = wire_round(fsub(hn[k], g4[k]), a.bf16);          // R4, R25
                     gn[k] = fadd(g4[k], c4[k]);                              // R12
                     A[k] = (i == 0) ? c4[k] : fadd(A[k], c4[k]);             // R9 node order
                 }
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
                 *reinterpret_cast<float4*>(a.nodes.g[i] + e) = make_float4(gn[0], gn[1], gn[2], gn[3]);
                 if (a.mode == 2)
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) *out_at(4 * f + k, i) = c4[k];
+                    for (int k = 0; k < 4; ++k) put(4 * f + k, i, c4[k]);
             }
             if (a.noef && a.mode != 0) {   // u <- eta u here; the scatter adds A / N
                 const float4 bv = *reinterpret_cast<const float4*>(a.gbar + e);
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
             }
             if (a.mode == 1) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) *out_at(4 * f + k, 0) = A[k];
+                for (int k = 0; k < 4; ++k) put(4 * f + k, 0, A[k]);
                 continue;
             }
             if (a.mode == 2) continue;
@@ -225,9 +226,11 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
              q += (long long)gridDim.x * blockDim.x) {
             if (q >= len) {
                 if (a.mode == 2) {
-                    for (int i = 0; i < a.nodes_local; ++i) *out_at(q, i) = 0.0f;
+                    for (int i = 0; i < a.nodes_local; ++i) put(q, i, 0.0f);
+                } else if (a.mode == 1) {
+                    put(q, 0, 0.0f);
                 } else if (a.values != nullptr) {
-                    *out_at(q, 0) = 0.0f;
+                    a.values[B.val_base + q] = 0.0f;
                 }
                 continue;
             }
@@ -235,12 +238,12 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
             float A = 0.0f;
             if (a.noef) {   // without EF: C_i = grad_i, u <- eta u (+ A / N in mode 0)
                 for (int i = 0; i < a.nodes_local; ++i) {
-                    const float c = a.nodes.grad[i][e];
+                    const float c = wire_round(a.nodes.grad[i][e], a.bf16);   // (R25)
                     A = (i == 0) ? c : fadd(A, c);
-                    if (a.mode == 2) *out_at(q, i) = c;
+                    if (a.mode == 2) put(q, i, c);
                 }
                 const float us = fmul(a.eta, a.gbar[e]);
-                if (a.mode == 1) *out_at(q, 0) = A;
+                if (a.mode == 1) put(q, 0, A);
                 if (a.mode != 0) { a.gbar[e] = us; continue; }
                 const float v = pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf);
                 a.gbar[e] = fadd(us, v);
@@ -251,12 +254,12 @@ __global__ void __launch_bounds__(256) k_dense(const DenseLaunch a) {
                 const float hn = ffma(a.eta, a.nodes.grad[i][e], fmul(a.ome, a.nodes.h[i][e]));   // O2, R11
                 a.nodes.h[i][e] = hn;
                 const float gv = a.nodes.g[i][e];
-                const float c = fsub(hn, gv);
+                const float c = wire_round(fsub(hn, gv), a.bf16);   // (R25)
                 a.nodes.g[i][e] = fadd(gv, c);
                 A = (i == 0) ? c : fadd(A, c);
-                if (a.mode == 2) *out_at(q, i) = c;
+                if (a.mode == 2) put(q, i, c);
             }
-            if (a.mode == 1) { *out_at(q, 0) = A; continue; }
+            if (a.mode == 1) { put(q, 0, A); continue; }
             if (a.mode == 2) continue;
             const float v = pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf);
             a.gbar[e] = fadd(a.gbar[e], v);
@@ -274,9 +277,9 @@ __global__ void __launch_bounds__(256) k_dense_scatter(const DenseScatterLaunch 
         for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
              q += (long long)gridDim.x * blockDim.x) {
             const long long o = B.val_base + q;
-            float A = a.wire[o];
+            float A = pay_ld(a.wire, o, a.bf16);
             if (a.mode == 1)
-                for (int i = 1; i < a.nodes_total; ++i) A = fadd(A, a.wire[static_cast<long long>(i) * a.sum_Kn + o]);
+                for (int i = 1; i < a.nodes_total; ++i) A = fadd(A, pay_ld(a.wire, static_cast<long long>(i) * a.sum_Kn + o, a.bf16));
             const float v = q < B.len ? (pow2 ? fmul(A, invN) : __fdiv_rn(A, a.Nf)) : 0.0f;
             if (q < B.len) a.gbar[B.off + q] = fadd(a.gbar[B.off + q], v);
             if (a.values != nullptr) a.values[o] = v;
@@ -411,6 +414,29 @@ void launch_scatter(const ScatterLaunch& a, cudaStream_t s) {
     if (grid > 148 * 8) grid = 148 * 8;
     if (grid < 1) grid = 1;
     k_scatter<<<static_cast<int>(grid), 256, 0, s>>>(a);
+}
+
+
+// ARC_Q_S (debug): S = P'_0 (+) P'_1 (+) ... of every ARC row, ascending node id
+// (R9), from the per-node sketches [M][L][r] of one GPU holding every node.
+namespace {
+__global__ void __launch_bounds__(256) k_node_sum(const float* __restrict__ pn, long long M, int L, int r,
+                                                  float* __restrict__ dst) {
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < M * r; e += static_cast<long long>(gridDim.x) * 256) {
+        const long long p = e / r;
+        const int j = static_cast<int>(e - p * r);
+        float S = pn[p * L * r + j];
+        for (int l = 1; l < L; ++l) S = dev::fadd(S, pn[(p * L + l) * r + j]);
+        dst[e] = S;
+    }
+}
+}  // namespace
+
+void launch_node_sum(const float* pnodes, long long M, int L, int r, float* dst, cudaStream_t s) {
+    const long long n = M * r;
+    if (n <= 0) return;
+    const int grid = static_cast<int>(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8);
+    k_node_sum<<<grid, 256, 0, s>>>(pnodes, M, L, r, dst);
 }
 
 }  // namespace arc

@@ -22,6 +22,7 @@
 // The all-reduce sums the ranks in DESCENDING rank order — a different order
 // from the oracle's ascending node order, standing in for NCCL's unspecified
 // one, so the ARC_REDUCE_NCCL tolerance contract is exercised.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -58,7 +59,7 @@ struct LoopbackGroup {
     };
     std::vector<Post> posts;
     std::vector<cudaEvent_t> ready, done;
-    std::vector<float*> scratch;                 // all-reduce partial sums, one per rank
+    std::vector<void*> scratch;                  // all-reduce sums, one per rank (bytes: scratch_n)
     std::vector<size_t> scratch_n;
     std::vector<LoopbackComm> handles;
 };
@@ -92,23 +93,25 @@ bool barrier(LoopbackGroup* g) {
 }
 
 struct SumArgs {
-    const float* src[kLoopbackMaxRanks];
+    const void* src[kLoopbackMaxRanks];
     int G;
     long long n;
-    float* dst;
+    void* dst;
 };
 
-// dst[e] = src[G-1][e] + src[G-2][e] + ... + src[0][e], left to right
+// dst[e] = src[G-1][e] + src[G-2][e] + ... + src[0][e], left to right, in
+// binary32; bfloat16 buffers (the R25 wire): the binary32 sum rounded once
+template <class T>
 __global__ void k_loopback_sum(const SumArgs a) {
     for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < a.n;
          e += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float s = a.src[a.G - 1][e];
-        for (int k = a.G - 2; k >= 0; --k) s = __fadd_rn(s, a.src[k][e]);
-        a.dst[e] = s;
+        float s = static_cast<float>(static_cast<const T*>(a.src[a.G - 1])[e]);
+        for (int k = a.G - 2; k >= 0; --k) s = __fadd_rn(s, static_cast<float>(static_cast<const T*>(a.src[k])[e]));
+        static_cast<T*>(a.dst)[e] = static_cast<T>(s);
     }
 }
 
-enum { kAllGather = 0, kAllReduce = 1, kAllToAll = 2 };
+enum { kAllGather = 0, kAllReduce = 1, kAllToAll = 2, kAllReduceBf16 = 3 };
 
 arc_status collective(LoopbackComm* c, int kind, const void* send, void* recv, size_t bytes, const size_t* scount,
                       const size_t* sdispl, const size_t* rcount, const size_t* rdispl, cudaStream_t s) {
@@ -152,24 +155,26 @@ arc_status collective(LoopbackComm* c, int kind, const void* send, void* recv, s
             }
         } else {   // all-reduce (sum): every rank's send buffer summed into this rank's scratch
             const size_t n = bytes;
+            const size_t esz = kind == kAllReduceBf16 ? 2 : sizeof(float);
             for (int k = 0; k < g->G; ++k)
                 if (g->posts[k].bytes != n) st = ARC_ERR_NCCL;
             if (st == ARC_OK && n > 0) {
-                if (g->scratch_n[me] < n) {
+                if (g->scratch_n[me] < n * esz) {
                     if (g->scratch[me]) cudaFree(g->scratch[me]);
                     g->scratch[me] = nullptr;
                     g->scratch_n[me] = 0;
-                    if (cudaMalloc(&g->scratch[me], n * sizeof(float)) != cudaSuccess) st = ARC_ERR_CUDA;
-                    else g->scratch_n[me] = n;
+                    if (cudaMalloc(&g->scratch[me], n * esz) != cudaSuccess) st = ARC_ERR_CUDA;
+                    else g->scratch_n[me] = n * esz;
                 }
                 if (st == ARC_OK) {
                     SumArgs a{};
-                    for (int k = 0; k < g->G; ++k) a.src[k] = static_cast<const float*>(g->posts[k].send);
+                    for (int k = 0; k < g->G; ++k) a.src[k] = g->posts[k].send;
                     a.G = g->G;
                     a.n = static_cast<long long>(n);
                     a.dst = g->scratch[me];
                     const int grid = static_cast<int>(std::min<long long>((a.n + 255) / 256, 148 * 8));
-                    k_loopback_sum<<<grid, 256, 0, s>>>(a);
+                    if (kind == kAllReduceBf16) k_loopback_sum<__nv_bfloat16><<<grid, 256, 0, s>>>(a);
+                    else k_loopback_sum<float><<<grid, 256, 0, s>>>(a);
                     if (cudaPeekAtLastError() != cudaSuccess) { (void)cudaGetLastError(); st = ARC_ERR_CUDA; }
                 }
             }
@@ -179,8 +184,9 @@ arc_status collective(LoopbackComm* c, int kind, const void* send, void* recv, s
     if (!barrier(g)) return ARC_ERR_NCCL;
     for (int k = 0; k < g->G; ++k)
         if (k != me && cudaStreamWaitEvent(s, g->done[k], 0) != cudaSuccess) st = ARC_ERR_CUDA;
-    if (st == ARC_OK && kind == kAllReduce && bytes > 0 &&
-        cudaMemcpyAsync(recv, g->scratch[me], bytes * sizeof(float), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    if (st == ARC_OK && (kind == kAllReduce || kind == kAllReduceBf16) && bytes > 0 &&
+        cudaMemcpyAsync(recv, g->scratch[me], bytes * (kind == kAllReduceBf16 ? 2 : sizeof(float)),
+                        cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         st = ARC_ERR_CUDA;
     return st;
 }
@@ -195,6 +201,9 @@ arc_status loopback_all_gather(LoopbackComm* c, const void* send, void* recv, si
 }
 arc_status loopback_all_reduce_f32(LoopbackComm* c, const float* send, float* recv, size_t count, cudaStream_t s) {
     return collective(c, kAllReduce, send, recv, count, nullptr, nullptr, nullptr, nullptr, s);
+}
+arc_status loopback_all_reduce_bf16(LoopbackComm* c, const void* send, void* recv, size_t count, cudaStream_t s) {
+    return collective(c, kAllReduceBf16, send, recv, count, nullptr, nullptr, nullptr, nullptr, s);
 }
 arc_status loopback_all_to_all_f32(LoopbackComm* c, const float* send, const size_t* scount, const size_t* sdispl,
                                    float* recv, const size_t* rcount, const size_t* rdispl, cudaStream_t s) {
@@ -247,7 +256,7 @@ arc_status arc_topk_loopback_destroy(void* group) {
     cudaDeviceSynchronize();
     for (cudaEvent_t e : g->ready) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : g->done) if (e) cudaEventDestroy(e);
-    for (float* p : g->scratch) if (p) cudaFree(p);
+    for (void* p : g->scratch) if (p) cudaFree(p);
     delete g;
     return ARC_OK;
 }

@@ -17,6 +17,8 @@ int loopback_rank(const LoopbackComm* c);
 arc_status loopback_all_gather(LoopbackComm* c, const void* send, void* recv, size_t bytes, cudaStream_t s);
 // all-reduce(sum) of `count` floats (in place allowed)
 arc_status loopback_all_reduce_f32(LoopbackComm* c, const float* send, float* recv, size_t count, cudaStream_t s);
+// all-reduce(sum) of `count` bfloat16 entries (the R25 wire): binary32 sum rounded once
+arc_status loopback_all_reduce_bf16(LoopbackComm* c, const void* send, void* recv, size_t count, cudaStream_t s);
 // all-to-all: scount[k] floats from send + sdispl[k] go to rank k; rcount[k]
 // floats from rank k land at recv + rdispl[k]  (host arrays of G entries)
 arc_status loopback_all_to_all_f32(LoopbackComm* c, const float* send, const size_t* scount, const size_t* sdispl,

@@ -45,14 +45,17 @@ __device__ __forceinline__ void load_peers(const LsaScatter& x, PeerBase& pb) {
     __syncthreads();
 }
 
+// payload element o of node i = g L + l at peer g (float or bf16 entries, R25)
+__device__ __forceinline__ float peer_ld(const PeerBase& pb, const LsaScatter& x, int i, long long o) {
+    const int g = i / x.L, l = i - g * x.L;
+    return pay_ld(pb.p[g], static_cast<long long>(l) * x.sum_Kn + o, x.bf16);
+}
+
 // A = C_0 ⊕ C_1 ⊕ ... ⊕ C_{N-1} of payload element o, node i = g L + l at
 // peer g, offset l * sum_Kn + o (R9: the order of the ORDERED mode).
 __device__ __forceinline__ float node_sum(const PeerBase& pb, const LsaScatter& x, long long o) {
-    float A = __ldcg(pb.p[0] + o);
-    for (int i = 1; i < x.N; ++i) {
-        const int g = i / x.L, l = i - g * x.L;
-        A = fadd(A, __ldcg(pb.p[g] + static_cast<long long>(l) * x.sum_Kn + o));
-    }
+    float A = peer_ld(pb, x, 0, o);
+    for (int i = 1; i < x.N; ++i) A = fadd(A, peer_ld(pb, x, i, o));
     return A;
 }
 
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(256) k_lsa_scatter(const ScatterLaunch a, cons
         const long long e0 = B.off + static_cast<long long>(p) * B.n;
         const long long o0 = B.val_base + static_cast<long long>(R.k) * B.n;
         const int cnt = max(0, min(4, nv - q)), ocnt = min(4, B.n - q);
-        if (ocnt == 4 && (((o0 + q) | x.sum_Kn) & 3) == 0) {   // 16-byte payload loads
+        if (!x.bf16 && ocnt == 4 && (((o0 + q) | x.sum_Kn) & 3) == 0) {   // 16-byte payload loads
             float4 A = __ldcg(reinterpret_cast<const float4*>(pb.p[0] + o0 + q));
             for (int i = 1; i < x.N; ++i) {
                 const int g = i / x.L, l = i - g * x.L;

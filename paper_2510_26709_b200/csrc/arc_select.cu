@@ -223,14 +223,22 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                 Quad c, gn;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    c.v[kk] = kk < cnt[u] ? (a.noef ? hq[u].v[kk] : fsub(hq[u].v[kk], gq[u].v[kk])) : 0.0f;   // C_i (+0 padding)
+                    c.v[kk] = kk < cnt[u] ? wire_round(a.noef ? hq[u].v[kk] : fsub(hq[u].v[kk], gq[u].v[kk]), a.bf16)
+                                          : 0.0f;   // C_i, what node i sends (R25; +0 padding)
                     gn.v[kk] = a.noef ? 0.0f : fadd(gq[u].v[kk], c.v[kk]);                             // R12
                     A[u].v[kk] = (i == 0 || per_node) ? c.v[kk] : fadd(A[u].v[kk], c.v[kk]);   // R9 node order
                 }
                 if (cnt[u] > 0 && !a.noef) store_quad(pg + e[u], gn, v4[u], cnt[u]);
-                if (a.mode == 2)
-                    store_quad(a.values + static_cast<long long>(i) * a.sum_Kn + o[u], c,
-                               ov4[u] && (a.sum_Kn % 4 == 0), ocnt[u]);
+                if (a.mode == 2) {
+                    if (a.bf16) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            if (kk < ocnt[u]) pay_st(a.values, static_cast<long long>(i) * a.sum_Kn + o[u] + kk, c.v[kk], 1);
+                    } else {
+                        store_quad(a.values + static_cast<long long>(i) * a.sum_Kn + o[u], c,
+                                   ov4[u] && (a.sum_Kn % 4 == 0), ocnt[u]);
+                    }
+                }
             }
         }
 #pragma unroll
@@ -246,6 +254,10 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                     store_quad(a.gbar + e[u], gb[u], v4[u], cnt[u]);
                 }
                 if (a.values != nullptr) store_quad(a.values + o[u], val, ov4[u], ocnt[u]);
+            } else if (a.mode == 1 && a.bf16) {   // the local node sum, rounded for the bf16 all-reduce
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    if (kk < ocnt[u]) pay_st(a.values, o[u] + kk, A[u].v[kk], 1);
             } else if (a.mode == 1 || a.mode == 3) {
                 store_quad(a.values + o[u], A[u], ov4[u] && a.mode == 1, ocnt[u]);
             }
@@ -300,7 +312,7 @@ __device__ void gather_rows_local(const GatherLaunch& a, const BlockDev& B, int 
                 Quad gn;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    const float c = a.noef ? hq[u].v[kk] : fsub(hq[u].v[kk], gq[u].v[kk]);   // C_i
+                    const float c = wire_round(a.noef ? hq[u].v[kk] : fsub(hq[u].v[kk], gq[u].v[kk]), a.bf16);   // C_i (R25)
                     gn.v[kk] = a.noef ? 0.0f : fadd(gq[u].v[kk], c);                       // R12
                     A[u].v[kk] = i == 0 ? c : fadd(A[u].v[kk], c);                 // R9 node order
                 }
@@ -336,7 +348,7 @@ __device__ __forceinline__ void gather_row_warp(const GatherLaunch& a, const Blo
             if (!a.noef) gq = load_quad(pg + e, v4, nv);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                const float c = a.noef ? hq.v[kk] : fsub(hq.v[kk], gq.v[kk]);   // C_i
+                const float c = wire_round(a.noef ? hq.v[kk] : fsub(hq.v[kk], gq.v[kk]), a.bf16);   // C_i (R25)
                 gn.v[kk] = a.noef ? 0.0f : fadd(gq.v[kk], c);                 // R12
                 A.v[kk] = i == 0 ? c : fadd(A.v[kk], c);                      // R9 node order
             }

@@ -20,10 +20,12 @@ def node_ids(rank: int, nodes_local: int) -> list[int]:
 
 
 def params_digest(d: int, blocks: Sequence, N: int, nodes_local: int, r: int, eta: float, seed: int,
-                  reduce: str) -> str:
+                  reduce: str, method: str = "arc", wire: str = "f32") -> str:
     h = hashlib.sha256()
     h.update(struct.pack("<qiiifQ", int(d), int(N), int(nodes_local), int(r), float(eta), int(seed) & (2**64 - 1)))
     h.update(reduce.encode())
+    h.update(method.encode())
+    h.update(wire.encode())
     for b in blocks:
         h.update(struct.pack("<qqqqqi", int(b.offset), int(b.len), int(b.m), int(b.n), int(b.K), int(b.kind)))
     return h.hexdigest()

@@ -199,3 +199,37 @@ def test_missing_library_fails_loudly(tmp_path):
     env = dict(os.environ, ARC_LIB_PATH=str(tmp_path / "absent.so"), PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root)
     assert "RAISED True" in out.stdout, out.stderr
+
+
+def test_single_block_shorthand_and_wire_validation(L):
+    """ABI v2: num_blocks == 0 with blocks == NULL is the single-block shorthand
+    (rows of n, K kept; P:226-228) — the same workspace as the explicit block;
+    the wire field accepts ARC_WIRE_F32 / ARC_WIRE_BF16 only, and the bf16 wire is
+    refused for the Top-K baseline (its payload carries indices); an ABI v1
+    struct version is rejected."""
+    d, n, K = 100_003, 768, 13
+    explicit = _params(L, [(0, d, -(-d // n), n, K, 0)], N=1, nodes_local=1)
+    st1, b1 = _ws(L, explicit)
+    short = L.ArcParams(L.ABI_VERSION, 1, 1, 0, d, 4, 0, None, 0.1, 0, 7, 0, 0, n, K, 0, 0)
+    st2, b2 = _ws(L, short)
+    assert st1 == st2 == L.OK and b1 == b2
+    bad_k = L.ArcParams(L.ABI_VERSION, 1, 1, 0, d, 4, 0, None, 0.1, 0, 7, 0, 0, n, -(-d // n) + 1, 0, 0)
+    assert _ws(L, bad_k)[0] == L.ERR_INVALID_ARG
+    bad_n = L.ArcParams(L.ABI_VERSION, 1, 1, 0, d, 4, 0, None, 0.1, 0, 7, 0, 0, 0, 1, 0, 0)
+    assert _ws(L, bad_n)[0] == L.ERR_INVALID_ARG
+    for wire, want in [(L.WIRE_F32, L.OK), (L.WIRE_BF16, L.OK), (2, L.ERR_INVALID_ARG)]:
+        p = _params(L, [(0, 1000, 10, 100, 3, 0)])
+        p.wire = wire
+        assert _ws(L, p)[0] == want
+    p = _params(L, [(0, 1000, 10, 100, 3, 0)])
+    p.wire, p.method = L.WIRE_BF16, L.METHOD_TOPK_ALLGATHER
+    assert _ws(L, p)[0] == L.ERR_UNSUPPORTED
+    p = _params(L, [(0, 1000, 10, 100, 3, 0)])
+    p.abi_version = 1
+    assert _ws(L, p)[0] == L.ERR_INVALID_ARG
+    # the bf16 wire halves exchange #2's workspace payload (ORDERED: [L][sum Kn] + [G][L][sum Kn])
+    base = _params(L, [(0, 100_000, 1000, 100, 100, 0)], N=4, nodes_local=2, reduce=L.REDUCE_ORDERED)
+    half = _params(L, [(0, 100_000, 1000, 100, 100, 0)], N=4, nodes_local=2, reduce=L.REDUCE_ORDERED)
+    half.wire = L.WIRE_BF16
+    s_f, s_h = _ws(L, base)[1], _ws(L, half)[1]
+    assert s_f - s_h >= (2 * 100 * 100 * 2 + 2 * 2 * 100 * 100 * 2) - 1024

@@ -42,15 +42,16 @@ def assert_same_floats(gpu: np.ndarray, ref: np.ndarray, what: str):
 
 def run_parity(orc, d, blocks, N, steps=3, eta=0.1, r=4, seed=5, grads_fn=None, reduce="nccl",
                force_exchange=False, check_debug=True, host=False, nodes_local=None, pg=None, ts=None,
-               method="arc"):
+               method="arc", wire="f32"):
     from paper_2510_26709_b200 import ArcTopK
     nl = N if nodes_local is None else nodes_local
     assert nl == N, "single-GPU parity: all nodes local"
     src = GradientSource(d, blocks, N, seed=seed) if grads_fn is None else None
     ctx = ArcTopK(d, blocks, N=N, eta=eta, r=r, seed=seed, nodes_local=nl, reduce=reduce,
                   debug_sketch=check_debug, force_exchange=force_exchange, host_staging=host, pg=pg,
-                  method=method)
-    o = orc.OracleEF21M(d, blocks, N=N, eta=eta, r=r, seed=seed, method=method)
+                  method=method, wire=wire)
+    o = orc.OracleEF21M(d, blocks, N=N, eta=eta, r=r, seed=seed, method="arc" if method == "exact" else method,
+                        exact=method == "exact", wire=wire)
     noef = method == "noef_msgd"      # no (h, g) state: gbar is the momentum u
     h = [torch.zeros(d, device=DEV) for _ in range(N)]
     g = [torch.zeros(d, device=DEV) for _ in range(N)]
@@ -191,8 +192,9 @@ def test_exchange_kernels_single_gpu(orc, reduce):
     run_parity(orc, 50_000, flat_blocks(50_000, 96, K=40), N=4, steps=3, reduce=reduce, force_exchange=True)
 
 
+@pytest.mark.parametrize("wire", ["f32", "bf16"])
 @pytest.mark.parametrize("reduce", ["nccl", "ordered", "lsa"])
-def test_exchange_through_nccl_one_rank(orc, reduce):
+def test_exchange_through_nccl_one_rank(orc, reduce, wire):
     """The exchange path with a real NCCL communicator borrowed from a 1-rank torch
     ProcessGroupNCCL (dlopen'd libnccl, ncclAllGather of the per-node sketches and
     of the ordered wire): bit-exact against the oracle."""
@@ -203,8 +205,12 @@ def test_exchange_through_nccl_one_rank(orc, reduce):
     if not dist.is_initialized():
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
     try:
-        run_parity(orc, 30_000, flat_blocks(30_000, 128, K=21), N=2, steps=3, reduce=reduce, force_exchange=True,
-                   pg=dist.group.WORLD)
+        # (NCCL reduce + bf16 wire rounds the local pre-sum of several nodes to bf16 —
+        # within the R25 tolerance, tested across emulated ranks in test_gpu_loopback.py;
+        # with one node per rank the payload is each node's own bf16 rows: bit-exact)
+        N = 1 if (reduce == "nccl" and wire == "bf16") else 2
+        run_parity(orc, 30_000, flat_blocks(30_000, 128, K=21), N=N, steps=3, reduce=reduce, force_exchange=True,
+                   pg=dist.group.WORLD, wire=wire)
     finally:
         pass
 
@@ -342,6 +348,67 @@ def test_graph_replayed_three_times_equals_three_eager_steps(kind):
         assert np.array_equal(a, b)
         assert np.all(np.diff(a) > 0) and a.min() >= 0 and a.max() < blocks[0].m
     assert outs[0][1] == outs[1][1]
+
+
+# ------------------------------------------------------------------ bfloat16 value wire (R25)
+
+@pytest.mark.parametrize("method", ["arc", "randk", "noef_msgd", "exact"])
+@pytest.mark.parametrize("N", [1, 3])
+def test_bf16_wire(orc, method, N):
+    """The bf16 value wire (R25) with every node on one GPU: each sent entry
+    rounded at the source, EF keeps the rest — bit-exact against the oracle's
+    wire="bf16" (selection, values, h, g, gbar), early-gather and segment steps,
+    mixed ARC (ragged, unaligned, K = m) and DENSE blocks."""
+    shapes = [(300, 96, 5, 0), (77, 127, 3, 0), (64, 64, 64, 0), (13, 100, 13, 1), (1000, 3, 17, 0)]
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n - (n // 2 if kind == 0 and m > 1 else 0), m, n, K, kind))
+        off += blocks[-1].len
+    eta = 0.9 if method == "noef_msgd" else 0.1
+    run_parity(orc, off, blocks, N=N, steps=4, method=method, wire="bf16", eta=eta, check_debug=method == "arc")
+
+
+@pytest.mark.parametrize("reduce", ["nccl", "ordered"])
+def test_bf16_wire_exchange_kernels(orc, reduce):
+    """The G > 1 kernel sequence on one GPU (no comm: collectives are copies) with
+    bf16 payloads: k_dense payload, the gather's bf16 stores, k_scatter's reads."""
+    shapes = [(300, 96, 5, 0), (13, 100, 13, 1), (1000, 3, 17, 0)]
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n, m, n, K, kind))
+        off += m * n
+    # (NCCL + bf16 with several local nodes rounds their pre-sum: tolerance, test_gpu_loopback.py)
+    run_parity(orc, off, blocks, N=3 if reduce == "ordered" else 1, steps=3, force_exchange=True, reduce=reduce,
+               wire="bf16")
+
+
+def test_bf16_wire_full_size_c3(orc):
+    d, blocks = config_blocks("C3")
+    run_parity(orc, d, blocks, N=1, steps=2, seed=20251030, wire="bf16", check_debug=False)
+
+
+def test_query_node_sum_S(orc):
+    """ARC_Q_S: S = P'_0 + P'_1 + ... (node order) equals the sum of the queried
+    per-node sketches; Sigma = fma chain of S_j^2 (O8) equals the queried Sigma."""
+    from paper_2510_26709_b200 import ArcTopK
+    from paper_2510_26709_b200 import _lib as L
+    d, N = 30_000, 3
+    blocks = flat_blocks(d, 100, K=9)
+    src = GradientSource(d, blocks, N, seed=8)
+    ctx = ArcTopK(d, blocks, N=N, eta=0.1, r=4, seed=8, debug_sketch=True)
+    h = [torch.zeros(d, device=DEV) for _ in range(N)]
+    g = [torch.zeros(d, device=DEV) for _ in range(N)]
+    gbar = torch.zeros(d, device=DEV)
+    ctx.step(0, [x.to(DEV) for x in src.grads(0)], h, g, gbar)
+    S = ctx.query(L.Q_S).cpu().numpy().reshape(-1, 4)
+    Pn = ctx.query(L.Q_P_NODES).cpu().numpy().reshape(-1, N, 4)
+    want = Pn[:, 0, :].copy()
+    for i in range(1, N):
+        want = (want + Pn[:, i, :]).astype(np.float32)
+    assert S.tobytes() == want.tobytes()
+    sig = ctx.query(L.Q_SIGMA).cpu().numpy()
+    assert sig.tobytes() == orc.sigma_rows(S).tobytes()
+    ctx.close()
 
 
 # ------------------------------------------------------------------ persistent selection (several slices per CTA)
