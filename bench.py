@@ -407,7 +407,8 @@ def measure(run: Runner, args, config: str, mu_bp, steps: int, warmup: int, *, e
     g = [torch.zeros(d, device=dev) for _ in range(L)]
     gbar = torch.zeros(d, device=dev)
     ctx = ArcTopK(d, blocks, N=N, eta=0.1, r=4, seed=20251030, nodes_local=L, pg=run.pg, rank=run.rank,
-                  reduce=args.reduce, host_staging=e2e_steps > 0, force_exchange=args.force_exchange)
+                  reduce=args.reduce, host_staging=e2e_steps > 0, force_exchange=args.force_exchange,
+                  wire=args.wire)
     stream = torch.cuda.current_stream()
 
     # ---------------------------------------------------------------- device-timed steps
@@ -511,6 +512,10 @@ def measure(run: Runner, args, config: str, mu_bp, steps: int, warmup: int, *, e
                        "nominal_peak": 7700.0, "nominal_frac": achieved / 7700.0}
     out["step_roofline"] = {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms, "hbm_bytes": ab["total"],
                             "nvlink_bus_bytes": bus["total"], "nvlink_peak_GBps": NVLINK_PEAK}
+    # what each rank hands to the two exchanges per step (Table I's payloads)
+    we = 2 if args.wire == "bf16" else 4
+    out["wire"] = {"dtype": args.wire, "value_payload_bytes": we * kn * (L if args.reduce != "nccl" else 1),
+                   "sketch_payload_bytes": 4 * M * L * 4, "sent_at_this_G": run.world > 1 or args.force_exchange}
     # the two exchanges: bytes this GPU moves over NVLink per step and the bus
     # rate over their phase time (phase = collective + the kernel it feeds)
     if run.world > 1:
@@ -531,6 +536,84 @@ def measure(run: Runner, args, config: str, mu_bp, steps: int, warmup: int, *, e
     return out
 
 
+def measure_bucketed(run: Runner, args, config: str, steps: int, warmup: int, bucket_elems: int = 25 * 2**20,
+                     pool_max: int = 4):
+    """The per-layer bucketed variant: the
+    config's block table cut into DDP-style buckets of <= bucket_elems elements
+    (whole tensors, in order), one context per bucket (sharing one communicator
+    at G > 1, as paper_2510_26709_b200.ddp does), each bucket's step on one of two
+    alternating streams.  Timed like the single-call step; same gradients."""
+    torch = run.torch
+    from paper_2510_26709_b200 import ArcTopK, Block
+    from synth import GradientSource
+    L = args.nodes_per_gpu
+    d, blocks = workload(config, None)
+    N = L * run.world
+    dev = run.dev
+    buckets, cur, size = [], [], 0
+    for b in blocks:
+        if cur and size + b.len > bucket_elems:
+            buckets.append(cur)
+            cur, size = [], 0
+        cur.append(b)
+        size += b.len
+    if cur:
+        buckets.append(cur)
+    src = GradientSource(d, blocks, N, seed=20251030, device=dev)
+    nodes = list(range(run.rank * L, (run.rank + 1) * L))
+    free = torch.cuda.mem_get_info(dev)[0]
+    pool_n = max(1, min(pool_max, int((free * 0.5 - 16 * d * L) // (4 * d * L))))
+    pool = [src.grads(t, nodes) for t in range(pool_n)]
+    h = [torch.zeros(d, device=dev) for _ in range(L)]
+    g = [torch.zeros(d, device=dev) for _ in range(L)]
+    gbar = torch.zeros(d, device=dev)
+    comm = None
+    if run.world > 1:
+        from paper_2510_26709_b200.dist import private_nccl_group
+        comm = private_nccl_group(run.pg, dev)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    ctxs = []
+    for bk in buckets:
+        off0 = bk[0].offset
+        lb = [Block(b.offset - off0, b.len, b.m, b.n, b.K, b.kind) for b in bk]
+        dl = sum(b.len for b in bk)
+        ctxs.append((ArcTopK(dl, lb, N=N, eta=0.1, r=4, seed=20251030, nodes_local=L, pg=run.pg, rank=run.rank,
+                             reduce=args.reduce, comm_group=comm), off0, dl))
+    main = torch.cuda.current_stream()
+
+    def one_step(t):
+        gr = pool[t % pool_n]
+        for k, (ctx, off0, dl) in enumerate(ctxs):
+            st = streams[k % 2]
+            st.wait_stream(main)
+            ctx.step(t, [x[off0:off0 + dl] for x in gr], [x[off0:off0 + dl] for x in h],
+                     [x[off0:off0 + dl] for x in g], gbar[off0:off0 + dl], stream=st)
+        for st in streams:
+            main.wait_stream(st)
+
+    for t in range(warmup):
+        one_step(t)
+    torch.cuda.synchronize()
+    run.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for k in range(steps):
+        one_step(warmup + k)
+    e1.record(main)
+    e1.synchronize()
+    run.barrier()
+    ms = run.max_over_ranks(e0.elapsed_time(e1) / steps)
+    out = {"config": config, "buckets": len(buckets), "bucket_elems_max": bucket_elems, "ms_per_step": ms,
+           "value": 4.0 * d * N / (ms * 1e-3) / 1e9, "unit": "GB/s", "steps": steps,
+           "kernels_per_step": sum(c[0].kernels_per_step for c in ctxs),
+           "note": "one context per DDP-style bucket (whole tensors, <= 25 Mi elements), two alternating streams"}
+    for c in ctxs:
+        c[0].close()
+    del pool, h, g, gbar
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -540,6 +623,7 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--nodes-per-gpu", type=int, default=1)
     ap.add_argument("--reduce", default="nccl", choices=["nccl", "ordered", "lsa"])
+    ap.add_argument("--wire", default="f32", choices=["f32", "bf16"], help="exchange #2 payload precision (R25)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--pool", type=int, default=8, help="distinct gradient sets cycled in the timed loop")
@@ -597,6 +681,15 @@ def main():
                 extras[name]["clocks"] = ex.get("clocks")
             except Exception as e:
                 extras[name] = {"unavailable": f"{type(e).__name__}: {str(e)[:200]}"}
+        try:   # the per-layer bucketed C4 against its single call
+            bk = measure_bucketed(run, args, "C4", max(10, min(args.steps, 50)), args.warmup)
+            single = extras.get("C4", {}).get("ms_per_step")
+            if single:
+                bk["single_call_ms_per_step"] = single
+                bk["bucketed_over_single"] = bk["ms_per_step"] / single
+            extras["C4_bucketed"] = bk
+        except Exception as e:
+            extras["C4_bucketed"] = {"unavailable": f"{type(e).__name__}: {str(e)[:200]}"}
 
     cpu = None
     if run.rank == 0 and not args.no_cpu_baseline:
@@ -623,12 +716,14 @@ def main():
                                    f"{args.config}: d={d}, {head['blocks']} block(s), sum K={head['sum_K']}, "
                                    f"mu_bp={args.mu_bp}, r=4, eta=0.1, {L} node(s) per GPU",
                        "d": d, "N_nodes": head["N_nodes"], "nodes_per_gpu": L, "reduce": args.reduce,
+                       "wire": args.wire,
                        "parallelism": f"dp{run.world}",
                        "l2": "no flush: per-step inputs (16 B x d = %.1f GB) exceed the 126 MB L2" % (16 * d / 1e9),
                        "gradient_pool": head["gradient_pool"]},
             "roofline": head["roofline"],
             "step_roofline": head["step_roofline"],
             "phases_ms": head["phases_ms"],
+            "wire": head["wire"],
             "collectives": head.get("collectives"),
             "comm_tally_per_rank0": head["comm_tally"],
             "nccl": {"version": nccl_ver, "NCCL_ALGO": os.environ.get("NCCL_ALGO"),
