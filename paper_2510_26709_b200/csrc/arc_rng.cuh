@@ -111,6 +111,10 @@ static __device__ __forceinline__ void box_muller(unsigned xa, unsigned xb, floa
 
 // Entries of V for step t: item it (in [0, sum_b n_b ceil(r/4)) over the ARC
 // blocks in order) is Philox block (q, jj) of the block it falls in.
+// item `it` of block b (b = the last ARC block whose first item is <= it)
+static __device__ __forceinline__ void gen_V_item_in(const BlockDev* __restrict__ blocks, int b, int r, uint2 key,
+                                                     unsigned t_lo, unsigned t_hi, long long it, float* __restrict__ V);
+
 static __device__ __forceinline__ void gen_V_item(const BlockDev* __restrict__ blocks, int num_blocks, int r,
                                                   uint2 key, unsigned t_lo, unsigned t_hi, long long it,
                                                   float* __restrict__ V) {
@@ -121,6 +125,25 @@ static __device__ __forceinline__ void gen_V_item(const BlockDev* __restrict__ b
         const long long first = (blocks[mid].v_off / r) * R4;   // (v_off = sum of r * ldv)
         if (first <= it) { b = mid; lo = mid + 1; } else hi = mid - 1;
     }
+    gen_V_item_in(blocks, b, r, key, t_lo, t_hi, it, V);
+}
+
+// the same with the blocks' first items in a (shared-memory) table: first[b] =
+// (v_off_b / r) * ceil(r / 4) — no dependent global loads in the search
+static __device__ __forceinline__ void gen_V_item_tab(const BlockDev* __restrict__ blocks, const long long* first,
+                                                      int num_blocks, int r, uint2 key, unsigned t_lo, unsigned t_hi,
+                                                      long long it, float* __restrict__ V) {
+    int lo = 0, hi = num_blocks - 1, b = -1;
+    while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        if (first[mid] <= it) { b = mid; lo = mid + 1; } else hi = mid - 1;
+    }
+    gen_V_item_in(blocks, b, r, key, t_lo, t_hi, it, V);
+}
+
+static __device__ __forceinline__ void gen_V_item_in(const BlockDev* __restrict__ blocks, int b, int r, uint2 key,
+                                                     unsigned t_lo, unsigned t_hi, long long it, float* __restrict__ V) {
+    const int R4 = (r + 3) >> 2;
     while (b >= 0 && blocks[b].kind != ARC_BLOCK_ARC) --b;   // DENSE blocks own no items
     if (b < 0) return;
     const long long local = it - (blocks[b].v_off / r) * R4;

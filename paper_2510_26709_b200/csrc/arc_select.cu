@@ -134,6 +134,26 @@ __device__ __forceinline__ Quad load_quad(const float* p, bool vec4, int nvalid)
     }
     return x;
 }
+// Two-step loads for the segment gather's batch of quads: issue_quad issues the
+// 16-byte load unconditionally (from a zero quad when the quad is not 16-byte
+// loadable), so the batch's loads are all in flight before the first result is
+// used; patch_quad then fills the quads that are not (unaligned rows, the short
+// last row) with scalar loads.  (With the load inside a vector/scalar branch the
+// compiler merged each result right after its LDG, serialising the batch: ncu
+// source page; C5 d = 1e9 at 10 %: 772 -> 564 us.  The early-gather path keeps
+// load_quad: this form measured no faster there and slower on unaligned rows.)
+__device__ const float4 k_zero_quad = {0.f, 0.f, 0.f, 0.f};
+__device__ __forceinline__ Quad issue_quad(const float* p, bool vec4) {
+    const float4 t = *(vec4 ? reinterpret_cast<const float4*>(p) : &k_zero_quad);
+    Quad x;
+    x.v[0] = t.x; x.v[1] = t.y; x.v[2] = t.z; x.v[3] = t.w;
+    return x;
+}
+__device__ __forceinline__ void patch_quad(Quad& x, const float* p, bool vec4, int nvalid) {
+    if (!vec4)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x.v[k] = k < nvalid ? p[k] : 0.0f;
+}
 __device__ __forceinline__ void store_quad(float* p, const Quad& x, bool vec4, int nvalid) {
     if (vec4) {
         *reinterpret_cast<float4*>(p) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
@@ -152,6 +172,10 @@ __device__ __forceinline__ int row_valid_cols(const BlockDev& B, int p) {
 // Balanced S4 (+S5, S6): the selected rows of every block cut into segments of
 // kSegQuads quads (host table), CTA b processes segments [seg0, seg1); every
 // (segment, quad) pair is one item, kThreads * UN items in flight per pass.
+// The segments' descriptors and selected rows are staged in shared memory first
+// (`cap` at a time: one round of independent loads), so an item's data loads do
+// not wait on a chain of descriptor -> block -> selection loads (that chain cost
+// the unstaged version ~2.5 x its bandwidth at K n = 1e8, C5 d = 1e9, 10 %).
 // A / N: for N a power of two the product with the exact reciprocal is the
 // same correctly rounded value as the quotient (R3), and much cheaper.
 __device__ __forceinline__ float div_N(float A, float Nf, float invN, bool pow2) {
@@ -159,10 +183,18 @@ __device__ __forceinline__ float div_N(float A, float Nf, float invN, bool pow2)
 }
 
 template <int UN>
-__device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const SelRow* pre) {
-    const int items = (seg1 - seg0) * kSegQuads;
+__device__ void gather_segments(const GatherLaunch& a, int seg_begin, int seg_end, int4* stage, int cap) {
     const bool pow2 = (a.N_int & (a.N_int - 1)) == 0;
     const float invN = 1.0f / a.Nf;
+    for (int seg0 = seg_begin; seg0 < seg_end; seg0 += cap) {
+    const int seg1 = min(seg_end, seg0 + cap);
+    __syncthreads();                                 // (the previous round's stage is consumed)
+    for (int sg = seg0 + static_cast<int>(threadIdx.x); sg < seg1; sg += kThreads) {
+        const SelRow R = a.rows[sg];
+        stage[sg - seg0] = make_int4(R.b, R.k, R.q0, __ldcg(a.sel + a.blocks[R.b].sel_base + R.k));
+    }
+    __syncthreads();
+    const int items = (seg1 - seg0) * kSegQuads;
     for (int base = 0; base < items; base += kThreads * UN) {
         int cnt[UN], ocnt[UN], nd[UN];
         long long e[UN], o[UN];
@@ -175,17 +207,17 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
             e[u] = o[u] = 0;
             v4[u] = ov4[u] = dense[u] = false;
             if (item < items) {
-                const SelRow R = (base == 0 && pre != nullptr) ? pre[u] : a.rows[seg0 + item / kSegQuads];
-                const BlockDev& B = a.blocks[R.b];
-                const int f = R.q0 + item % kSegQuads;
+                const int4 R = stage[item / kSegQuads];      // (block, k, q0, selected row)
+                const BlockDev& B = a.blocks[R.x];
+                const int f = R.z + item % kSegQuads;
                 const int q = 4 * f;
                 if (q < B.n) {
-                    const int p = __ldcg(a.sel + B.sel_base + R.k);
+                    const int p = R.w;
                     const int nv = row_valid_cols(B, p);
                     cnt[u] = max(0, min(4, nv - q));
                     ocnt[u] = min(4, B.n - q);
                     e[u] = B.off + static_cast<long long>(p) * B.n + q;
-                    o[u] = B.val_base + static_cast<long long>(R.k) * B.n + q;
+                    o[u] = B.val_base + static_cast<long long>(R.y) * B.n + q;
                     v4[u] = B.vec && cnt[u] == 4;
                     ov4[u] = B.vec && (o[u] % 4 == 0) && ocnt[u] == 4;
                     dense[u] = B.kind == ARC_BLOCK_DENSE;
@@ -201,20 +233,27 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
             float* __restrict__ ph = a.noef ? const_cast<float*>(a.nodes.grad[i]) : a.nodes.h[i];
             float* __restrict__ pg = a.nodes.g[i];
             Quad hq[UN], gq[UN];
+            bool act[UN];
 #pragma unroll
-            for (int u = 0; u < UN; ++u) {
-                if (i == 0 && a.mode == 0 && cnt[u] > 0) gb[u] = load_quad(a.gbar + e[u], v4[u], cnt[u]);
-                if (cnt[u] > 0 && (!per_node || nd[u] == i)) {
-                    if (!a.noef) gq[u] = load_quad(pg + e[u], v4[u], cnt[u]);
-                    if (dense[u]) {   // DENSE block: eq:ef21m-1 here (R11, R20)
-                        const Quad hv = load_quad(ph + e[u], v4[u], cnt[u]);
-                        const Quad gr = load_quad(a.nodes.grad[i] + e[u], v4[u], cnt[u]);
+            for (int u = 0; u < UN; ++u) {   // issue every load of the batch ...
+                act[u] = cnt[u] > 0 && (!per_node || nd[u] == i);
+                const bool gbl = i == 0 && a.mode == 0 && cnt[u] > 0;
+                if (i == 0) gb[u] = issue_quad(a.gbar + e[u], v4[u] && gbl);
+                gq[u] = issue_quad(pg + e[u], v4[u] && act[u] && !a.noef);
+                hq[u] = issue_quad(ph + e[u], v4[u] && act[u]);
+            }
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) hq[u].v[kk] = ffma(a.eta, gr.v[kk], fmul(a.ome, hv.v[kk]));   // O2
-                        store_quad(ph + e[u], hq[u], v4[u], cnt[u]);
-                    } else {
-                        hq[u] = load_quad(ph + e[u], v4[u], cnt[u]);
-                    }
+            for (int u = 0; u < UN; ++u) {   // ... then the scalar quads and DENSE rows
+                if (i == 0 && a.mode == 0 && cnt[u] > 0) patch_quad(gb[u], a.gbar + e[u], v4[u], cnt[u]);
+                if (!act[u]) continue;
+                if (!a.noef) patch_quad(gq[u], pg + e[u], v4[u], cnt[u]);
+                patch_quad(hq[u], ph + e[u], v4[u], cnt[u]);
+                if (dense[u]) {   // DENSE block: eq:ef21m-1 here (R11, R20); hq held h
+                    Quad gr = issue_quad(a.nodes.grad[i] + e[u], v4[u]);
+                    patch_quad(gr, a.nodes.grad[i] + e[u], v4[u], cnt[u]);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) hq[u].v[kk] = ffma(a.eta, gr.v[kk], fmul(a.ome, hq[u].v[kk]));   // O2
+                    store_quad(ph + e[u], hq[u], v4[u], cnt[u]);
                 }
             }
 #pragma unroll
@@ -262,6 +301,7 @@ __device__ void gather_segments(const GatherLaunch& a, int seg0, int seg1, const
                 store_quad(a.values + o[u], A[u], ov4[u] && a.mode == 1, ocnt[u]);
             }
         }
+    }
     }
 }
 
@@ -476,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     if (s.stamps != nullptr && threadIdx.x == 0) s.stamps[blockIdx.x * 8 + (k)] = globaltimer()
     STAMP(0);
     __shared__ unsigned sh[2048];                   // histogram
-    __shared__ unsigned s_keys[kMaxSliceRows];      // the current slice's order keys
+    __shared__ __align__(16) unsigned s_keys[kMaxSliceRows];   // the current slice's order keys
     __shared__ int s_rows[kMaxSliceRows];           // boundary-bin candidates (keys | rows) / row lists
     __shared__ int warp_sums[32];
     __shared__ unsigned s_dig;
@@ -648,10 +688,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     }
     // S0 of the next step, generated here speculatively (V depends only on
     // (seed, t, b)); the host uses it only if the next step's t matches
-    if (s.V_next != nullptr)
+    // (the blocks' first items staged in shared memory — s_rows is free here — so
+    // the per-item block search makes no dependent global loads: with C4's 171
+    // blocks the global search cost ~20 us of this phase)
+    if (s.V_next != nullptr) {
+        const int R4 = (s.r + 3) >> 2;
+        long long* first = reinterpret_cast<long long*>(s_rows);
+        const bool tab = s.num_vblocks <= kMaxSliceRows / 2;
+        __syncthreads();
+        if (tab)
+            for (int b = tid; b < s.num_vblocks; b += kThreads) first[b] = (s.vblocks[b].v_off / s.r) * R4;
+        __syncthreads();
         for (long long i = blockIdx.x * static_cast<long long>(kThreads) + tid; i < s.v_items;
-             i += static_cast<long long>(gridDim.x) * kThreads)
-            rng::gen_V_item(s.vblocks, s.num_vblocks, s.r, s.key, s.t_lo, s.t_hi, i, s.V_next);
+             i += static_cast<long long>(gridDim.x) * kThreads) {
+            if (tab) rng::gen_V_item_tab(s.vblocks, first, s.num_vblocks, s.r, s.key, s.t_lo, s.t_hi, i, s.V_next);
+            else rng::gen_V_item(s.vblocks, s.num_vblocks, s.r, s.key, s.t_lo, s.t_hi, i, s.V_next);
+        }
+        __syncthreads();   // (s_rows is reused below)
+    }
     STAMP(1);
     for (int k = 0; k < nmine; ++k) {                // next step's candidate counter of each block
         const SliceItem it = s.items[item_of(k)];
@@ -899,23 +953,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
             return;
         }
     }
-    // S4 (+S5, S6): all selected-row segments spread evenly over the grid; the
-    // (static) segment descriptors of this thread's first items are fetched
-    // before the barrier
+    // S4 (+S5, S6): all selected-row segments spread evenly over the grid
     constexpr int UN = 4;
     const long long S = ga.num_rows;
     const int seg0 = static_cast<int>(S * blockIdx.x / gridDim.x);
     const int seg1 = static_cast<int>(S * (blockIdx.x + 1) / gridDim.x);
-    SelRow pre[UN];
-#pragma unroll
-    for (int u = 0; u < UN; ++u) {
-        const int item = u * kThreads + tid;
-        pre[u] = item < (seg1 - seg0) * kSegQuads ? ga.rows[seg0 + item / kSegQuads] : SelRow{0, 0, 0};
-    }
     __threadfence();
     grid.sync();                                     // ---------------- the selection is complete
     STAMP(6);
-    gather_segments<UN>(ga, seg0, seg1, pre);
+    // (s_keys, 16 KB, is free now: the segment stage)
+    gather_segments<UN>(ga, seg0, seg1, reinterpret_cast<int4*>(s_keys), kMaxSliceRows / 4);
     __syncthreads();
     STAMP(7);
 #undef STAMP

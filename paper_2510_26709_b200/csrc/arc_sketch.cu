@@ -45,6 +45,53 @@ __device__ __forceinline__ int row_cols(long long len, int n, int p) {
     return rest < n ? static_cast<int>(rest) : n;
 }
 
+// Cache policy of the streaming pass's loads (build-time knobs for A/B runs):
+// ARC_SK_LDG for the gradient (read once), ARC_SK_LDS for the state h, g;
+// 0 = streaming (evict-first), 1 = cache global (L2, normal eviction),
+// 4 = cache global + 256-byte L2 prefetch.  ARC_SK_ST: the h' store.
+// Measured (profiles/r02_cache_policy.txt): the state through L2 with normal
+// eviction and the gradient evict-first is within 0.6 % of the best on every
+// layout tried (C3 -2.3 % step time against all-streaming); the gradient through
+// L2 as well gains 0.5 % on C3 but costs 16 % on C2 (d = 11.7M: h and g then no
+// longer stay in the 126 MB L2 between steps).
+#ifndef ARC_SK_LDG
+#define ARC_SK_LDG 0
+#endif
+#ifndef ARC_SK_LDS
+#define ARC_SK_LDS 1
+#endif
+#ifndef ARC_SK_ST
+#define ARC_SK_ST 0
+#endif
+template <int POL>
+__device__ __forceinline__ float4 sk_ld4p(const float* p) {
+    if constexpr (POL == 1) {
+        return __ldcg(reinterpret_cast<const float4*>(p));
+    } else if constexpr (POL == 4) {
+        float4 v;
+        asm volatile("ld.global.cg.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+        return v;
+    } else {
+        return __ldcs(reinterpret_cast<const float4*>(p));
+    }
+}
+__device__ __forceinline__ float4 sk_ld4(const float* p) { return sk_ld4p<ARC_SK_LDS>(p); }    // h, g
+__device__ __forceinline__ float4 sk_ld4g(const float* p) { return sk_ld4p<ARC_SK_LDG>(p); }   // grad
+// scalar loads (rows that are not 16-byte aligned): streaming, so the 4 loads of a
+// quad meet in L1 (cache-global scalar loads measured 23 % slower on n = 5461 rows)
+__device__ __forceinline__ float sk_ld1(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ void sk_st4(float* p, float4 v) {
+#if ARC_SK_ST == 1      // write-back (default policy)
+    *reinterpret_cast<float4*>(p) = v;
+#elif ARC_SK_ST == 2    // no L1 allocation, default L2 policy
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+#else                   // streaming store, the measured default
+    __stcs(reinterpret_cast<float4*>(p), v);
+#endif
+}
+
 // sum over the 32 lanes, butterfly order of O6 (every lane ends with the same value)
 __device__ __forceinline__ float butterfly(float a) {
 #pragma unroll
@@ -92,7 +139,7 @@ __device__ __forceinline__ void segment(const SketchLaunch& a, int k, int nseg, 
     }
     if (NOEF && ph == nullptr) {
     } else if (q + 3 < nv && vec) {
-        __stcs(reinterpret_cast<float4*>(ph + e), make_float4(hn[0], hn[1], hn[2], hn[3]));
+        sk_st4(ph + e, make_float4(hn[0], hn[1], hn[2], hn[3]));
     } else {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
@@ -349,23 +396,23 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
                             const long long e = base + q;
                             float tg[4] = {0.f, 0.f, 0.f, 0.f}, th[4] = {0.f, 0.f, 0.f, 0.f}, td[4] = {0.f, 0.f, 0.f, 0.f};
                             if (k0 + u < ke && q + 3 < nv && T_vec) {
-                                const float4 g4 = __ldcs(reinterpret_cast<const float4*>(pg + e));
+                                const float4 g4 = sk_ld4g(pg + e);
                                 tg[0] = g4.x; tg[1] = g4.y; tg[2] = g4.z; tg[3] = g4.w;
                                 if (!NOEF || ph != nullptr) {
-                                    const float4 h4 = __ldcs(reinterpret_cast<const float4*>(ph + e));
+                                    const float4 h4 = sk_ld4(ph + e);
                                     th[0] = h4.x; th[1] = h4.y; th[2] = h4.z; th[3] = h4.w;
                                 }
                                 if (!NOEF) {
-                                    const float4 d4 = __ldcs(reinterpret_cast<const float4*>(pgg + e));
+                                    const float4 d4 = sk_ld4(pgg + e);
                                     td[0] = d4.x; td[1] = d4.y; td[2] = d4.z; td[3] = d4.w;
                                 }
                             } else if (k0 + u < ke) {
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
                                     if (q + k < nv) {
-                                        tg[k] = __ldcs(pg + e + k);
-                                        if (!NOEF || ph != nullptr) th[k] = __ldcs(ph + e + k);
-                                        if (!NOEF) td[k] = __ldcs(pgg + e + k);
+                                        tg[k] = sk_ld1(pg + e + k);
+                                        if (!NOEF || ph != nullptr) th[k] = sk_ld1(ph + e + k);
+                                        if (!NOEF) td[k] = sk_ld1(pgg + e + k);
                                     }
                             }
                             xg[u] = make_float4(tg[0], tg[1], tg[2], tg[3]);
@@ -413,18 +460,17 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
                     const int q = 128 * (k0 + u) + 4 * lane;
                     const long long e = base + q;
                     if (q + 3 < nv && T_vec) {
-                        xg[u] = __ldcs(reinterpret_cast<const float4*>(pg + e));
-                        xh[u] = (!NOEF || ph != nullptr) ? __ldcs(reinterpret_cast<const float4*>(ph + e))
-                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-                        xd[u] = !NOEF ? __ldcs(reinterpret_cast<const float4*>(pgg + e)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        xg[u] = sk_ld4g(pg + e);
+                        xh[u] = (!NOEF || ph != nullptr) ? sk_ld4(ph + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        xd[u] = !NOEF ? sk_ld4(pgg + e) : make_float4(0.f, 0.f, 0.f, 0.f);
                     } else {
                         float tg[4] = {0.f, 0.f, 0.f, 0.f}, th[4] = {0.f, 0.f, 0.f, 0.f}, td[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             if (q + k < nv) {
-                                tg[k] = __ldcs(pg + e + k);
-                                if (!NOEF || ph != nullptr) th[k] = __ldcs(ph + e + k);
-                                if (!NOEF) td[k] = __ldcs(pgg + e + k);
+                                tg[k] = sk_ld1(pg + e + k);
+                                if (!NOEF || ph != nullptr) th[k] = sk_ld1(ph + e + k);
+                                if (!NOEF) td[k] = sk_ld1(pgg + e + k);
                             }
                         xg[u] = make_float4(tg[0], tg[1], tg[2], tg[3]);
                         xh[u] = make_float4(th[0], th[1], th[2], th[3]);

@@ -8,7 +8,7 @@ import __graft_entry__
 __graft_entry__.build()
 from paper_2510_26709_b200 import ArcTopK
 from synth import GradientSource, config_blocks
-d, blocks = config_blocks(sys.argv[1] if len(sys.argv) > 1 else "C3")
+d, blocks = config_blocks(sys.argv[1] if len(sys.argv) > 1 else "C3", int(sys.argv[2]) if len(sys.argv) > 2 else None)
 dev = torch.device("cuda", 0)
 src = GradientSource(d, blocks, 1, seed=20251030, device=dev)
 pool = [src.grads(t) for t in range(4)]
