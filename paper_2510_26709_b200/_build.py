@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libarctopk.so")
-SOURCES = [os.path.join(CSRC, "arc_kernels.cu"), os.path.join(CSRC, "arc_sketch.cu"),
+SOURCES = [os.path.join(CSRC, "arc_kernels.cu"), os.path.join(CSRC, "arc_sketch.cu"), os.path.join(CSRC, "arc_sketch_tma.cu"),
            os.path.join(CSRC, "arc_select.cu"), os.path.join(CSRC, "arc_lsa.cu"),
            os.path.join(CSRC, "arc_optim.cu"), os.path.join(CSRC, "arc_loopback.cu"),
            os.path.join(CSRC, "arc_api.cu")]
@@ -54,19 +54,45 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
+    """extra / out: additional nvcc flags and another output path (A/B variants, tools/build_variant.sh)."""
+    target = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(),
-           *SOURCES, "-o", tmp, "-ldl"]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    tmp = target + f".tmp{os.getpid()}"
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
+    objdir = os.path.join(PKG, "build_obj", str(os.getpid()))
+    os.makedirs(objdir, exist_ok=True)
+    # one nvcc per source, in parallel (the kernel files take minutes each), then one link
+    jobs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [_nvcc(), *compile_flags, *(extra or []), *(["-Xptxas=-v"] if verbose else []), *inc, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        jobs.append((obj, subprocess.Popen(cmd)))
+    failed = [obj for obj, pr in jobs if pr.wait() != 0]
+    try:
+        if failed:
+            raise subprocess.CalledProcessError(1, f"nvcc ({len(failed)} source(s) failed)")
+        subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                        "-Xcompiler", "-fPIC", *[obj for obj, _ in jobs], "-o", tmp, "-ldl"], check=True)
+    finally:
+        for obj, _ in jobs:
+            if os.path.exists(obj):
+                os.remove(obj)
+        try:
+            os.rmdir(objdir)
+        except OSError:
+            pass
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--out" in sys.argv:   # python -m paper_2510_26709_b200._build --out PATH [nvcc flags ...]
+        i = sys.argv.index("--out")
+        print(build(extra=sys.argv[i + 2:], out=os.path.abspath(sys.argv[i + 1])))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -150,7 +150,7 @@ struct Plan {
     bool dense_fast = false;         // DENSE blocks handled by the streaming k_dense (not Top-K)
     std::vector<int> dense_ids;
     // workspace offsets (bytes)
-    size_t o_cta_w = 0;
+    size_t o_cta_w = 0, o_cta_t = 0;
     size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
            o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
            o_vals = 0, o_hash = 0, o_hist1 = 0, o_hist2 = 0, o_hist3 = 0, o_slice_gt = 0, o_slice_eq = 0,
@@ -313,6 +313,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_tiles = take(sizeof(TileDesc) * pl.max_tiles);
     pl.o_cta = take(sizeof(int) * (kMaxGrid + 1));
     pl.o_cta_w = take(sizeof(int) * (kMaxGrid + 1));
+    pl.o_cta_t = take(sizeof(int) * (kMaxGrid + 1));
     pl.o_selrows = take(sizeof(SelRow) * pl.num_segs);
     pl.o_V = take(sizeof(float) * sum_nr * 2);   // double-buffered by t parity
     pl.Ms = (M + pl.G - 1) / pl.G;
@@ -490,6 +491,7 @@ struct arc_topk_ctx {
     int grid = 0, num_tiles = 0, shape = 0, vs_cap = 0;
     int sel_grid = 0;                             // CTAs of the (persistent) selection kernel
     int grid_w = 0, vs_cap_w = 0, tiles_w0 = 0;   // the wide blocks' ranged launch (grid_w == 0: none)
+    int grid_t = 0, vs_cap_t = 0;                 // the bulk-copy fed launch (grid_t == 0: none)
     float ome = 0.f, Nf = 0.f;
     cudaStream_t last = nullptr;
     // per-phase timing
@@ -706,7 +708,7 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
 
     // static tables
     std::vector<Tile> tiles;
-    std::vector<int> cta_begin, cta_begin_w;
+    std::vector<int> cta_begin, cta_begin_w, cta_begin_t;
     {   // streaming-pass variant: 0 = 4 row segments per batch (>= 3 CTAs/SM),
         // 1 = 2 segments per batch at 4 CTAs/SM, 2 = 4 segments at 2 CTAs/SM
         // (ARC_SKETCH_SHAPE, experiments).  A row of n columns is ceil(n/128)
@@ -730,15 +732,31 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
         // blocks whose V_b^T fits the shared-memory stage stream in one launch; the
         // wider ones (methods with a sketch) and blocks of rows of <= 4 columns (one
         // row per thread) in a second launch, so the main kernel carries neither path
+        //
+        // Blocks of the sketch methods (EF21M) whose rows are not 16-byte aligned
+        // (n >= 256) go to a third launch fed by bulk copies (arc_sketch_tma.cu)
+        // when their V_b^T fits next to its rings: the main launch would read them
+        // with scalar loads (ARC_SKETCH_TMA: 0 = off, 2 = every ARC block of more
+        // than 4 columns, for A/B runs)
         const bool sketches = !c->pl.topk && !c->pl.randk;
-        std::vector<char> narrow(c->pl.bdev.size(), 1), wide(c->pl.bdev.size(), 0);
+        int tma_mode = 1;
+        if (const char* e = getenv("ARC_SKETCH_TMA")) tma_mode = atoi(e);
+        const int tma_cap = sketches && !c->pl.noef && tma_mode > 0 ? sketch_tma_vs_cap(c->p.r) : 0;
+        std::vector<char> narrow(c->pl.bdev.size(), 1), wide(c->pl.bdev.size(), 0), viatma(c->pl.bdev.size(), 0);
         c->vs_cap = 0;
-        bool any_wide = false;
+        c->vs_cap_t = 0;
+        bool any_wide = false, any_tma = false;
         for (size_t b = 0; b < c->pl.bdev.size(); ++b) {
             const BlockDev& B = c->pl.bdev[b];
             if (B.kind != ARC_BLOCK_ARC) continue;
             const int cap = sketch_vs_cap(c->p.r, B.n);
-            if (((cap == 0 && sketches) || B.n <= 4) && sketch_ranged_cap(c->p.r) > 0) {
+            const int64_t need = static_cast<int64_t>(c->p.r) * ((B.n + 3) / 4 * 4);
+            if (B.n > 4 && need <= tma_cap && (tma_mode >= 2 || (!B.vec && B.n >= 256))) {
+                narrow[b] = 0;
+                viatma[b] = 1;
+                any_tma = true;
+                c->vs_cap_t = std::max<int>(c->vs_cap_t, static_cast<int>(need));
+            } else if (((cap == 0 && sketches) || B.n <= 4) && sketch_ranged_cap(c->p.r) > 0) {
                 narrow[b] = 0;
                 wide[b] = 1;
                 any_wide = true;
@@ -767,6 +785,19 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
             for (int& x : cbw) x += c->tiles_w0;
             tiles.insert(tiles.end(), tw.begin(), tw.end());
             cta_begin_w = std::move(cbw);
+        }
+        c->grid_t = 0;
+        if (any_tma) {
+            std::vector<Tile> tt;
+            std::vector<int> cbt;
+            int sms = 0, dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            plan_tiles(c->pl, viatma, std::max(sms, 1), 32, sketch_tile_cols(c->shape), tt, cbt, c->grid_t);
+            const int t0 = static_cast<int>(tiles.size());
+            for (int& x : cbt) x += t0;
+            tiles.insert(tiles.end(), tt.begin(), tt.end());
+            cta_begin_t = std::move(cbt);
         }
     }
     c->num_tiles = static_cast<int>(tiles.size());
@@ -802,6 +833,7 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
             UPLOAD(c->pl.o_tiles, tdesc);
             UPLOAD(c->pl.o_cta, cta_begin);
             UPLOAD(c->pl.o_cta_w, cta_begin_w);
+            UPLOAD(c->pl.o_cta_t, cta_begin_t);
             UPLOAD(c->pl.o_selrows, rows);
             UPLOAD(c->pl.o_items, c->pl.items);
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_cand_count, 0, sizeof(unsigned) * 2 * c->pl.sbdev.size(), s));
@@ -952,6 +984,14 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             a.vs_cap = c->vs_cap_w;
             a.ranged = 1;
             launch_ef_sketch(a, s);
+            ARC_LAUNCHED();
+        }
+        if (c->grid_t > 0) {   // unaligned rows / wide V through the bulk-copy rings
+            a.cta_begin = c->at<int>(pl.o_cta_t);
+            a.grid = c->grid_t;
+            a.vs_cap = c->vs_cap_t;
+            a.ranged = 0;
+            launch_ef_sketch_tma(a, s);
             ARC_LAUNCHED();
         }
     } else {
@@ -1357,7 +1397,7 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     // steady state with consecutive t: V comes from the previous step's select
     // kernel (k_vgen only when there is none)
     const Plan& pl = c->pl;
-    const int sketch = pl.M > 0 ? (c->grid > 0 ? 1 : 0) + (c->grid_w > 0 ? 1 : 0) : 0;
+    const int sketch = pl.M > 0 ? (c->grid > 0 ? 1 : 0) + (c->grid_w > 0 ? 1 : 0) + (c->grid_t > 0 ? 1 : 0) : 0;
     const int sel = pl.items.empty() ? 0 : 1;
     if (pl.topk) return sketch + sel + c->p.N;   // + N ordered merges
     const int vgen = (pl.M > 0 && pl.items.empty() && !pl.randk) ? 1 : 0;

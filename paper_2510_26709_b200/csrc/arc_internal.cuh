@@ -158,6 +158,10 @@ int sketch_vs_cap(int r, int max_n);   // floats of V_b^T the streaming pass sta
 int sketch_ranged_cap(int r);          // floats staged per range by the wide blocks' launch
 int ef_sketch_resident_ctas_ranged(int r, int vs_cap);
 int sketch_wide_threads(int r);        // threads per CTA of that launch (tiles of <= 4-column rows: one row per thread)
+// the bulk-copy (TMA) fed launch for unaligned rows and wide V (arc_sketch_tma.cu): one CTA per SM
+void launch_ef_sketch_tma(const SketchLaunch& a, cudaStream_t s);
+int sketch_tma_vs_cap(int r);          // floats of V_b^T it stages next to its rings
+int sketch_tma_threads();
 int sketch_tile_rows(int shape);
 int sketch_tile_cols(int shape);
 int sketch_shape_ok(int shape, int r);
