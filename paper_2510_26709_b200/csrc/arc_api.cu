@@ -490,6 +490,7 @@ struct arc_topk_ctx {
     unsigned char* ws = nullptr;
     int grid = 0, num_tiles = 0, shape = 0, vs_cap = 0;
     int sel_grid = 0;                             // CTAs of the (persistent) selection kernel
+    bool sel_cluster = false;                     // ... launched as one thread-block cluster
     int grid_w = 0, vs_cap_w = 0, tiles_w0 = 0;   // the wide blocks' ranged launch (grid_w == 0: none)
     int grid_t = 0, vs_cap_t = 0;                 // the bulk-copy fed launch (grid_t == 0: none)
     float ome = 0.f, Nf = 0.f;
@@ -651,14 +652,33 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
         // takes ceil(slices / resident) of them, at most select_max_slices_per_cta())
         int rows = kSliceMin;
         while (rows < select_max_slice_rows() && slices(rows) > resident) rows += 32;
+        // a small selection (<= 16 slices of the smallest height, one per CTA) runs
+        // as one thread-block cluster: hardware barriers instead of grid barriers
+        // through global memory and no cooperative launch (C5 d = 1e6: step 25.0 ->
+        // 21.1 us).  Taller slices to fit a cluster measured slower (C1: 16 CTAs of
+        // 4096 rows instead of 256 of 256: 20.9 -> 22.2 us), so only selections that
+        // are small anyway take it (ARC_SELECT_CLUSTER: the largest cluster, 0 = off)
+        c->sel_cluster = false;
+        {
+            int cl = 16;
+            if (const char* e = std::getenv("ARC_SELECT_CLUSTER")) cl = std::atoi(e);
+            const int64_t ns = slices(rows);
+            if (cl > 0 && ns >= 1 && ns <= cl && select_cluster_max(static_cast<int>(ns)) == ns) c->sel_cluster = true;
+        }
         if (const char* e = std::getenv("ARC_SLICE_ROWS")) {
             const int f = std::atoi(e);
-            if (f >= kSliceMin && f <= select_max_slice_rows()) rows = f;
+            if (f >= kSliceMin && f <= select_max_slice_rows()) {
+                rows = f;
+                c->sel_cluster = false;
+            }
         }
         int grid = static_cast<int>(std::min<int64_t>(slices(rows), resident));
         if (const char* e = std::getenv("ARC_SELECT_GRID")) {   // debug knob: fewer CTAs (several slices each)
             const int f = std::atoi(e);
-            if (f >= 1 && f < grid) grid = f;
+            if (f >= 1 && f < grid) {
+                grid = f;
+                c->sel_cluster = false;
+            }
         }
         if (grid > 0 && (slices(rows) + grid - 1) / grid > select_max_slices_per_cta()) {
             delete c;
@@ -1133,6 +1153,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         sg.stamps = c->stamps;
         sg.pdl = c->pdl && !c->timing && !(pl.exchange && pl.M > 0) ? 1 : 0;
         sg.early = c->early && ga.mode == 0 && ga.values == nullptr ? 1 : 0;
+        sg.cluster = c->sel_cluster && sg.grid == sg.num_items ? 1 : 0;
         sg.build_hist = sigma_pass ? 1 : 0;
         if (sigma_pass && !pl.exchange && !pl.exact) {
             sg.xsk = c->pnodes_ptr();

@@ -100,6 +100,7 @@ struct SelectGatherLaunch {
     uint2 key;
     unsigned t_lo, t_hi;
     int pdl;                       // launch with programmatic stream serialization
+    int cluster;                   // the grid is one thread-block cluster (<= 16 CTAs, one slice each)
     int early;                     // mode 0 without values: gather the certainly selected rows
                                    // (digit 1 above the boundary bin) before barrier 1 completes
     // Sigma not formed by the streaming pass: the kernel builds the digit-1
@@ -173,6 +174,7 @@ cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch
 int select_gather_resident_ctas();
 int select_max_slice_rows();
 int select_max_slices_per_cta();
+int select_cluster_max(int want);      // largest one-cluster grid <= want the selection kernel can launch
 
 struct GatherLaunch {
     const BlockDev* blocks;

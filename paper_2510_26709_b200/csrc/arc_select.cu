@@ -504,14 +504,31 @@ __device__ __forceinline__ void load_keys(const float* __restrict__ sigma, const
     }
 }
 
+// Grid-wide barriers.  The kernel normally runs as a cooperative grid (cg grid
+// barriers through global memory).  A small selection (at most 16 slices) runs
+// as ONE thread-block cluster instead: the cluster's hardware barrier
+// (barrier.cluster arrive.release / wait.acquire, memory-ordered at cluster
+// scope, which here is every thread of the grid) replaces the grid barrier, and
+// the launch is an ordinary one — no cooperative launch.
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire;" ::: "memory"); }
+
 // The selection kernel is PERSISTENT: CTA b handles slices b, b + grid, b + 2 grid,
 // ... (at most kMaxSlicesPerCta), so any block table is accepted whatever the
 // number of co-resident CTAs.  With one slice per CTA (the common case) the
 // slice's keys stay in shared memory across the grid barriers; with several
 // they are re-read from Sigma (L2) for each slice.
-template <bool kPhase0, bool kMulti>
+template <bool kPhase0, bool kMulti, bool kCluster>
 __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGatherLaunch s, const GatherLaunch ga) {
     cg::grid_group grid = cg::this_grid();
+    auto grid_sync = [&]() {
+        if constexpr (kCluster) {
+            cluster_arrive();
+            cluster_wait();
+        } else {
+            grid.sync();
+        }
+    };
 #define STAMP(k) \
     if (s.stamps != nullptr && threadIdx.x == 0) s.stamps[blockIdx.x * 8 + (k)] = globaltimer()
     STAMP(0);
@@ -635,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
                 if (x.arc) flush_hist(sh, s.hist1 + x.bb * kHist1Bins, kHist1Bins);
             }
         }
-        grid.sync();                                 // ---------------- barrier 0
+        grid_sync();                                 // ---------------- barrier 0
     }
     // ------------------------------------------------ phase A (per slice)
     // the digit-1 boundary bin b1 of the slice's block, the slice's count of keys
@@ -715,32 +732,41 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
         // split barrier 1: the rows of a slice above the boundary bin b1 are
         // selected whatever the candidates resolve to (fewer than K keys lie above
         // b1), so their S4..S6 runs while the other CTAs reach the barrier
-        auto token = grid.barrier_arrive();
-        for (int k = 0; k < nmine; ++k) {
-            const Slice x = slice_of(s, item_of(k));
-            if (x.arc) {
-                __syncthreads();                     // (s_rows / s_keys of the previous slice)
-                if (!cached) {
-                    load_keys(s.sigma, x, s_keys);
+        auto early_gather = [&]() {
+            for (int k = 0; k < nmine; ++k) {
+                const Slice x = slice_of(s, item_of(k));
+                if (x.arc) {
+                    __syncthreads();                     // (s_rows / s_keys of the previous slice)
+                    if (!cached) {
+                        load_keys(s.sigma, x, s_keys);
+                        __syncthreads();
+                        int g1 = 0;
+                        for (int i = tid; i < x.nk; i += kThreads) g1 += (s_keys[i] >> 21) > s_b1[k];
+                        gt_pos = cta_exclusive_scan(g1, warp_sums, &gt_tot);
+                    }
+                    const unsigned b1 = s_b1[k];
+                    int pos = gt_pos;
+                    for (int i = tid; i < x.nk; i += kThreads)
+                        if ((s_keys[i] >> 21) > b1) s_rows[pos++] = i;
                     __syncthreads();
-                    int g1 = 0;
-                    for (int i = tid; i < x.nk; i += kThreads) g1 += (s_keys[i] >> 21) > s_b1[k];
-                    gt_pos = cta_exclusive_scan(g1, warp_sums, &gt_tot);
+                    gather_rows_local<4>(ga, x.B, x.lo, s_rows, gt_tot);
+                } else {
+                    gather_rows_local<4>(ga, x.B, x.lo, nullptr, x.nk);   // K = m: every row
                 }
-                const unsigned b1 = s_b1[k];
-                int pos = gt_pos;
-                for (int i = tid; i < x.nk; i += kThreads)
-                    if ((s_keys[i] >> 21) > b1) s_rows[pos++] = i;
-                __syncthreads();
-                gather_rows_local<4>(ga, x.B, x.lo, s_rows, gt_tot);
-            } else {
-                gather_rows_local<4>(ga, x.B, x.lo, nullptr, x.nk);   // K = m: every row
             }
+            __syncthreads();                             // s_rows is reused below
+        };
+        if constexpr (kCluster) {
+            cluster_arrive();
+            early_gather();
+            cluster_wait();
+        } else {
+            auto token = grid.barrier_arrive();
+            early_gather();
+            grid.barrier_wait(std::move(token));
         }
-        __syncthreads();                             // s_rows is reused below
-        grid.barrier_wait(std::move(token));
     } else {
-        grid.sync();                                 // ---------------- barrier 1
+        grid_sync();                                 // ---------------- barrier 1
     }
     STAMP(2);
     // every CTA has read this step's parity (before barrier 1): the next step uses the other one
@@ -868,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
                 if ((s_keys[i] >> 21) == b1) atomicAdd(&sh[(s_keys[i] >> 10) & 2047u], 1u);
             flush_hist(sh, s.hist2 + x.bb * 2048, 2048);
         }
-        grid.sync();                                 // ---------------- barrier 1b
+        grid_sync();                                 // ---------------- barrier 1b
         for (int k = 0; k < nmine; ++k) {
             const Slice x = slice_of(s, item_of(k));
             if (!x.arc) continue;
@@ -887,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
                 if ((s_keys[i] >> 10) == pre) atomicAdd(&sh[s_keys[i] & 1023u], 1u);
             flush_hist(sh, s.hist3 + x.bb * 1024, 1024);
         }
-        grid.sync();                                 // ---------------- barrier 2
+        grid_sync();                                 // ---------------- barrier 2
         for (int k = 0; k < nmine; ++k) {
             const Slice x = slice_of(s, item_of(k));
             if (!x.arc) continue;
@@ -912,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
             cta_exclusive_scan(eq, warp_sums, &te);
             if (tid == 0) { s.slice_gt[x.sidx] = tg; s.slice_eq[x.sidx] = te; }
         }
-        grid.sync();                                 // ---------------- barrier 3
+        grid_sync();                                 // ---------------- barrier 3
         if (s.early && blockIdx.x == 0 && tid == 0) ga.bnd_count[par ^ 1] = 0;   // the next step's counter
         for (int k = 0; k < nmine; ++k) {
             const Slice x = slice_of(s, item_of(k));
@@ -941,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
             // a few slices, so every slice appended them to one list and, after a
             // barrier, the grid's warps take them row by row
             __threadfence();
-            grid.sync();                             // ---------------- the boundary list is complete
+            grid_sync();                             // ---------------- the boundary list is complete
             const int total = static_cast<int>(__ldcg(ga.bnd_count + par));
             const int lane = tid & 31, warps = kThreads / 32;
             for (int j = blockIdx.x * warps + (tid >> 5); j < total; j += gridDim.x * warps) {
@@ -959,7 +985,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     const int seg0 = static_cast<int>(S * blockIdx.x / gridDim.x);
     const int seg1 = static_cast<int>(S * (blockIdx.x + 1) / gridDim.x);
     __threadfence();
-    grid.sync();                                     // ---------------- the selection is complete
+    grid_sync();                                     // ---------------- the selection is complete
     STAMP(6);
     // (s_keys, 16 KB, is free now: the segment stage)
     gather_segments<UN>(ga, seg0, seg1, reinterpret_cast<int4*>(s_keys), kMaxSliceRows / 4);
@@ -975,12 +1001,12 @@ int select_gather_resident_ctas() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int per_sm2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_gather<false, false>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<true, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_gather<false, false, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<true, false, false>, kThreads, 0);
     if (per_sm2 < per_sm) per_sm = per_sm2;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<false, true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<false, true, false>, kThreads, 0);
     if (per_sm2 < per_sm) per_sm = per_sm2;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<true, true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_select_gather<true, true, false>, kThreads, 0);
     if (per_sm2 < per_sm) per_sm = per_sm2;
     return sms * (per_sm < 1 ? 1 : per_sm);
 }
@@ -997,16 +1023,53 @@ cudaError_t launch_select_gather(const SelectGatherLaunch& s, const GatherLaunch
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    if (s.cluster) {   // the whole grid is one cluster (its hardware barrier is the grid barrier)
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(s.grid);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+    }
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = s.pdl ? 2 : 1;
+    if (s.cluster)
+        return s.build_hist ? cudaLaunchKernelEx(&cfg, k_select_gather<true, false, true>, s, ga)
+                            : cudaLaunchKernelEx(&cfg, k_select_gather<false, false, true>, s, ga);
     const bool multi = s.grid < s.num_items;
     if (s.build_hist)
-        return multi ? cudaLaunchKernelEx(&cfg, k_select_gather<true, true>, s, ga)
-                     : cudaLaunchKernelEx(&cfg, k_select_gather<true, false>, s, ga);
-    return multi ? cudaLaunchKernelEx(&cfg, k_select_gather<false, true>, s, ga)
-                 : cudaLaunchKernelEx(&cfg, k_select_gather<false, false>, s, ga);
+        return multi ? cudaLaunchKernelEx(&cfg, k_select_gather<true, true, false>, s, ga)
+                     : cudaLaunchKernelEx(&cfg, k_select_gather<true, false, false>, s, ga);
+    return multi ? cudaLaunchKernelEx(&cfg, k_select_gather<false, true, false>, s, ga)
+                 : cudaLaunchKernelEx(&cfg, k_select_gather<false, false, false>, s, ga);
+}
+
+// the largest grid (<= want) the selection kernel can run as one thread-block cluster (0: none)
+int select_cluster_max(int want) {
+    const void* fns[2] = {reinterpret_cast<const void*>(k_select_gather<false, false, true>),
+                          reinterpret_cast<const void*>(k_select_gather<true, false, true>)};
+    int best = want;
+    for (const void* f : fns) {
+        cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        int c = best;
+        for (; c >= 1; --c) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(c);
+            cfg.blockDim = dim3(kThreads);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = static_cast<unsigned>(c);
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, f, &cfg) == cudaSuccess && n >= 1) break;
+            cudaGetLastError();
+        }
+        best = c;
+    }
+    return best;
 }
 
 }  // namespace arc
