@@ -537,12 +537,17 @@ def measure(run: Runner, args, config: str, mu_bp, steps: int, warmup: int, *, e
 
 
 def measure_bucketed(run: Runner, args, config: str, steps: int, warmup: int, bucket_elems: int = 25 * 2**20,
-                     pool_max: int = 4):
+                     pool_max: int = 4, graphs: bool = False):
     """The per-layer bucketed variant: the
     config's block table cut into DDP-style buckets of <= bucket_elems elements
     (whole tensors, in order), one context per bucket (sharing one communicator
     at G > 1, as paper_2510_26709_b200.ddp does), each bucket's step on one of two
-    alternating streams.  Timed like the single-call step; same gradients."""
+    alternating streams.  Timed like the single-call step; same gradients.
+    graphs=True: every bucket's step captured once per gradient set into a CUDA
+    graph (device-side iteration counter, ARC_FLAG_DEVICE_T) and replayed, as the
+    DDP hook's cuda_graphs option does.  host_ms_per_step: CPU time to enqueue a
+    step (the launches and the ctypes marshalling the graphs replace)."""
+    import time
     torch = run.torch
     from paper_2510_26709_b200 import ArcTopK, Block
     from synth import GradientSource
@@ -578,16 +583,28 @@ def measure_bucketed(run: Runner, args, config: str, steps: int, warmup: int, bu
         lb = [Block(b.offset - off0, b.len, b.m, b.n, b.K, b.kind) for b in bk]
         dl = sum(b.len for b in bk)
         ctxs.append((ArcTopK(dl, lb, N=N, eta=0.1, r=4, seed=20251030, nodes_local=L, pg=run.pg, rank=run.rank,
-                             reduce=args.reduce, comm_group=comm), off0, dl))
+                             reduce=args.reduce, comm_group=comm, device_t=graphs), off0, dl))
     main = torch.cuda.current_stream()
+    cgraphs = []
+    if graphs:   # one graph per (bucket, gradient set): the inputs are fixed per graph
+        for k, (ctx, off0, dl) in enumerate(ctxs):
+            ctx.set_iteration(0, stream=streams[k % 2])
+            cgraphs.append([ctx.capture([x[off0:off0 + dl] for x in pool[j]], [x[off0:off0 + dl] for x in h],
+                                        [x[off0:off0 + dl] for x in g], gbar[off0:off0 + dl], stream=streams[k % 2])
+                            for j in range(pool_n)])
+        torch.cuda.synchronize()
 
     def one_step(t):
         gr = pool[t % pool_n]
         for k, (ctx, off0, dl) in enumerate(ctxs):
             st = streams[k % 2]
             st.wait_stream(main)
-            ctx.step(t, [x[off0:off0 + dl] for x in gr], [x[off0:off0 + dl] for x in h],
-                     [x[off0:off0 + dl] for x in g], gbar[off0:off0 + dl], stream=st)
+            if graphs:
+                with torch.cuda.stream(st):
+                    cgraphs[k][t % pool_n].replay()
+            else:
+                ctx.step(t, [x[off0:off0 + dl] for x in gr], [x[off0:off0 + dl] for x in h],
+                         [x[off0:off0 + dl] for x in g], gbar[off0:off0 + dl], stream=st)
         for st in streams:
             main.wait_stream(st)
 
@@ -597,16 +614,21 @@ def measure_bucketed(run: Runner, args, config: str, steps: int, warmup: int, bu
     run.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(main)
+    host_s = 0.0
     for k in range(steps):
+        c0 = time.perf_counter()
         one_step(warmup + k)
+        host_s += time.perf_counter() - c0
     e1.record(main)
     e1.synchronize()
     run.barrier()
     ms = run.max_over_ranks(e0.elapsed_time(e1) / steps)
     out = {"config": config, "buckets": len(buckets), "bucket_elems_max": bucket_elems, "ms_per_step": ms,
+           "host_ms_per_step": 1e3 * host_s / steps, "cuda_graphs": graphs,
            "value": 4.0 * d * N / (ms * 1e-3) / 1e9, "unit": "GB/s", "steps": steps,
            "kernels_per_step": sum(c[0].kernels_per_step for c in ctxs),
            "note": "one context per DDP-style bucket (whole tensors, <= 25 Mi elements), two alternating streams"}
+    del cgraphs
     for c in ctxs:
         c[0].close()
     del pool, h, g, gbar
@@ -688,6 +710,10 @@ def main():
                 bk["single_call_ms_per_step"] = single
                 bk["bucketed_over_single"] = bk["ms_per_step"] / single
             extras["C4_bucketed"] = bk
+            bg = measure_bucketed(run, args, "C4", max(10, min(args.steps, 50)), args.warmup, graphs=True)
+            if single:
+                bg["bucketed_over_single"] = bg["ms_per_step"] / single
+            extras["C4_bucketed_graphs"] = bg
         except Exception as e:
             extras["C4_bucketed"] = {"unavailable": f"{type(e).__name__}: {str(e)[:200]}"}
 

@@ -113,6 +113,13 @@ typedef enum {
 #define ARC_FLAG_FORCE_EXCHANGE 0x4u  /* G == 1: run the G > 1 kernel sequence (tests)           */
 #define ARC_FLAG_LOOPBACK_COMM  0x8u  /* nccl_comm is an arc_topk_loopback_comm() handle: G ranks   */
                                       /* emulated in one process on one GPU (tests; not with LSA)  */
+#define ARC_FLAG_DEVICE_T       0x10u /* the iteration t lives in device memory (the workspace):    */
+                                      /* arc_topk_step ignores its t argument, its kernels read the */
+                                      /* counter and the step advances it by one, so a CUDA graph   */
+                                      /* of one captured step replays iterations t, t + 1, ...      */
+                                      /* (R7: V and the Rand-K keys depend on t).  Every step draws */
+                                      /* its own V (no speculative V for t + 1).  The counter starts */
+                                      /* at 0; arc_topk_set_iteration sets it.                      */
 
 /* The value wire (exchange #2's payload, R25):
  * ARC_WIRE_F32 sends the compact rows C_i in binary32; ARC_WIRE_BF16 rounds each
@@ -183,6 +190,11 @@ arc_status arc_topk_create(const arc_topk_params* params, void* nccl_comm,
 arc_status arc_topk_step(arc_topk_ctx* ctx, int64_t t,
                          const float* const* grad, float* const* h, float* const* g,
                          float* gbar, int32_t* sel_out, float* values_out, void* stream);
+
+/* ARC_FLAG_DEVICE_T contexts: enqueue (on `stream`, async) the write of t into
+ * the context's device iteration counter, which the next step uses (and
+ * advances).  ARC_ERR_INVALID_ARG for a context without the flag or t < 0. */
+arc_status arc_topk_set_iteration(arc_topk_ctx* ctx, int64_t t, void* stream);
 
 /* Same step with the gradients in HOST memory (pinned for async copies): the
  * call enqueues host->device copies of grad_host[i] (d floats each) into the

@@ -23,7 +23,7 @@ BLOCK_ARC, BLOCK_DENSE = 0, 1
 # arc_reduce_mode
 REDUCE_NCCL, REDUCE_ORDERED, REDUCE_LSA = 0, 1, 2
 # flags
-FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE, FLAG_LOOPBACK_COMM = 0x1, 0x2, 0x4, 0x8
+FLAG_HOST_STAGING, FLAG_DEBUG_SKETCH, FLAG_FORCE_EXCHANGE, FLAG_LOOPBACK_COMM, FLAG_DEVICE_T = 0x1, 0x2, 0x4, 0x8, 0x10
 # arc_method
 METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK, METHOD_NOEF_MSGD, METHOD_EXACT = 0, 1, 2, 3, 4
 # arc_opt_kind
@@ -35,7 +35,7 @@ WIRE_F32, WIRE_BF16 = 0, 1
 
 EXPORTED = [
     "arc_topk_workspace_bytes", "arc_topk_create", "arc_topk_step", "arc_topk_step_host",
-    "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_kernels_per_step",
+    "arc_topk_set_iteration", "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_kernels_per_step",
     "arc_topk_destroy", "arc_topk_status_string", "arc_topk_set_timing", "arc_topk_read_timing",
     "arc_topk_debug_stamps", "arc_topk_apply_update", "arc_topk_comm_tally",
     "arc_topk_loopback_create", "arc_topk_loopback_comm", "arc_topk_loopback_destroy",
@@ -88,6 +88,7 @@ def lib():
         L.arc_topk_create.argtypes = [P(ArcParams), vp, vp, ctypes.c_size_t, vp, P(vp)]
         L.arc_topk_step.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp]
         L.arc_topk_step_host.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp]
+        L.arc_topk_set_iteration.argtypes = [vp, i64, vp]
         L.arc_topk_query.argtypes = [vp, i32, vp, ctypes.c_size_t, vp]
         L.arc_topk_sizes.argtypes = [vp, P(i64), P(i64), P(i64), P(i64)]
         L.arc_topk_get_status.argtypes = [vp, P(ctypes.c_uint32)]
@@ -106,7 +107,7 @@ def lib():
         L.arc_topk_status_string.argtypes = [ctypes.c_int]
         L.arc_topk_status_string.restype = ctypes.c_char_p
         for name in ["arc_topk_workspace_bytes", "arc_topk_create", "arc_topk_step", "arc_topk_step_host",
-                     "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_destroy",
+                     "arc_topk_set_iteration", "arc_topk_query", "arc_topk_sizes", "arc_topk_get_status", "arc_topk_destroy",
                      "arc_topk_set_timing", "arc_topk_read_timing", "arc_topk_apply_update",
                      "arc_topk_comm_tally", "arc_topk_loopback_create", "arc_topk_loopback_comm",
                      "arc_topk_loopback_destroy"]:

@@ -113,7 +113,7 @@ class ArcTopK:
                  nodes_local: int | None = None, pg=None, rank: int = 0, reduce: str = "nccl",
                  host_staging: bool = False, debug_sketch: bool = False, force_exchange: bool = False,
                  method: str = "arc", device=None, stream=None, comm_group=None, loopback=None,
-                 wire: str = "f32", n: int | None = None, K: int | None = None):
+                 wire: str = "f32", n: int | None = None, K: int | None = None, device_t: bool = False):
         self.lib = L.lib()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.d, self.N = int(d), int(N)
@@ -130,7 +130,9 @@ class ArcTopK:
         self._cblocks = (L.ArcBlock * len(self.blocks))(*[
             L.ArcBlock(int(b.offset), int(b.len), int(b.m), int(b.n), int(b.K), int(b.kind), 0) for b in self.blocks])
         flags = (L.FLAG_HOST_STAGING if host_staging else 0) | (L.FLAG_DEBUG_SKETCH if debug_sketch else 0) | \
-                (L.FLAG_FORCE_EXCHANGE if force_exchange else 0) | (L.FLAG_LOOPBACK_COMM if loopback is not None else 0)
+                (L.FLAG_FORCE_EXCHANGE if force_exchange else 0) | (L.FLAG_LOOPBACK_COMM if loopback is not None else 0) | \
+                (L.FLAG_DEVICE_T if device_t else 0)
+        self.device_t = bool(device_t)
         self.params = L.ArcParams(L.ABI_VERSION, self.N, self.nodes_local, int(rank), self.d, int(r),
                                   nb, self._cblocks if nb else None, float(eta),
                                   {"nccl": L.REDUCE_NCCL, "ordered": L.REDUCE_ORDERED, "lsa": L.REDUCE_LSA}[reduce],
@@ -206,6 +208,28 @@ class ArcTopK:
                                        sel_out.data_ptr() if sel_out is not None else None,
                                        values_out.data_ptr() if values_out is not None else None,
                                        _stream_handle(stream)), "arc_topk_step")
+
+    def set_iteration(self, t: int, stream=None) -> None:
+        """device_t contexts: the iteration the next step uses (async on the stream);
+        every step then advances the device counter by one."""
+        L.check(self.lib.arc_topk_set_iteration(self.ctx, int(t), _stream_handle(stream)), "arc_topk_set_iteration")
+
+    def capture(self, grads, h, g, gbar, sel_out: torch.Tensor | None = None,
+                values_out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
+                pool=None) -> torch.cuda.CUDAGraph:
+        """device_t contexts: capture one step on these tensors into a CUDA graph.
+        Each ``replay()`` runs one whole step (one launch from the host) at the
+        device iteration counter and advances it, so replays continue t, t + 1, ...
+        Capturing enqueues no work; call :meth:`set_iteration` before the first
+        replay."""
+        if not self.device_t:
+            raise ValueError("capture needs a context created with device_t=True")
+        graph = torch.cuda.CUDAGraph()
+        s = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.graph(graph, stream=s, pool=pool, capture_error_mode="relaxed"):
+            self.step(0, grads, h, g, gbar, sel_out, values_out, stream=s)
+        return graph
 
     def step_host(self, t: int, grads_host, h, g, gbar, sel_host: torch.Tensor | None = None,
                   values_host: torch.Tensor | None = None, stream=None) -> None:

@@ -150,7 +150,7 @@ struct Plan {
     bool dense_fast = false;         // DENSE blocks handled by the streaming k_dense (not Top-K)
     std::vector<int> dense_ids;
     // workspace offsets (bytes)
-    size_t o_cta_w = 0, o_cta_t = 0;
+    size_t o_cta_w = 0, o_cta_t = 0, o_tdev = 0;
     size_t o_blocks = 0, o_tiles = 0, o_cta = 0, o_selrows = 0, o_V = 0, o_sigma = 0, o_sel = 0,
            o_status = 0, o_pnodes = 0, o_xrecv = 0, o_wire = 0, o_wire_all = 0, o_staging = 0,
            o_vals = 0, o_hash = 0, o_hist1 = 0, o_hist2 = 0, o_hist3 = 0, o_slice_gt = 0, o_slice_eq = 0,
@@ -175,7 +175,8 @@ arc_status validate(const arc_topk_params* p) {
     if (p->reserved != 0) return ARC_ERR_INVALID_ARG;
     if (p->wire == ARC_WIRE_BF16 && p->method == ARC_METHOD_TOPK_ALLGATHER) return ARC_ERR_UNSUPPORTED;
     if (p->num_blocks < 1 || p->blocks == nullptr) return ARC_ERR_INVALID_ARG;
-    if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE | ARC_FLAG_LOOPBACK_COMM))
+    if (p->flags & ~(ARC_FLAG_HOST_STAGING | ARC_FLAG_DEBUG_SKETCH | ARC_FLAG_FORCE_EXCHANGE | ARC_FLAG_LOOPBACK_COMM |
+                     ARC_FLAG_DEVICE_T))
         return ARC_ERR_INVALID_ARG;
     if (p->method != ARC_METHOD_ARC && p->method != ARC_METHOD_TOPK_ALLGATHER && p->method != ARC_METHOD_RANDK &&
         p->method != ARC_METHOD_NOEF_MSGD && p->method != ARC_METHOD_EXACT)
@@ -320,6 +321,7 @@ void make_plan(const arc_topk_params* p, Plan& pl, int slice_rows = kSliceMin) {
     pl.o_sigma = take(sizeof(float) * std::max<int64_t>(std::max<int64_t>(M * nl, pl.G * pl.Ms), 1));
     pl.o_sel = take(sizeof(int32_t) * sumK);
     pl.o_status = take(16);
+    pl.o_tdev = take(16);
     pl.o_hist1 = take(sizeof(unsigned) * kHist1Bins * nsb);
     pl.o_hist2 = take(sizeof(unsigned) * 2048 * nsb);
     pl.o_hist3 = take(sizeof(unsigned) * 1024 * nsb);
@@ -861,6 +863,7 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist2, 0, sizeof(unsigned) * 2048 * c->pl.sbdev.size(), s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist3, 0, sizeof(unsigned) * 1024 * c->pl.sbdev.size(), s));
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_status, 0, 16, s));
+            ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_tdev, 0, 16, s));   // ARC_FLAG_DEVICE_T: t = 0
             ARC_CUDA(cudaMemsetAsync(c->ws + c->pl.o_hist1, 0, sizeof(unsigned) * kHist1Bins * c->pl.sbdev.size(), s));
             ARC_CUDA(cudaStreamSynchronize(s));
             return ARC_OK;
@@ -951,14 +954,19 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     if (pl.topk && (sel_out != nullptr || values_out != nullptr)) return ARC_ERR_INVALID_ARG;
 
     ARC_MARK(0);
+    // ARC_FLAG_DEVICE_T: t is the device counter (read by the kernels, advanced by
+    // the selection kernel); V single-buffered and drawn by every step
+    const bool dev_t = (c->p.flags & ARC_FLAG_DEVICE_T) != 0;
+    unsigned long long* t_dev = dev_t ? c->at<unsigned long long>(pl.o_tdev) : nullptr;
+    if (dev_t) t = 0;
     // S0 (skipped when the previous step already generated V for this t)
-    float* V_t = V + static_cast<size_t>(t & 1) * pl.sum_nr;
+    float* V_t = V + static_cast<size_t>(dev_t ? 0 : (t & 1)) * pl.sum_nr;
     // (a captured step always draws its own V: a replay must not depend on what
     // eager steps between capture and replay left in the double buffer)
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return ARC_ERR_CUDA;
-    if (pl.M > 0 && !pl.topk && !pl.randk && (c->v_ready != t || cap != cudaStreamCaptureStatusNone)) {
-        launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V_t, s);
+    if (pl.M > 0 && !pl.topk && !pl.randk && (dev_t || c->v_ready != t || cap != cudaStreamCaptureStatusNone)) {
+        launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V_t, s, t_dev);
         ARC_LAUNCHED();
     }
     c->last_t = t;
@@ -978,6 +986,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         a.ome = c->ome;
         a.Nf = c->Nf;
         a.V = V_t;
+        a.t_dev = t_dev;
         a.sigma = sigma;
         a.hist1 = hist1;
         a.pnodes = pl.keep_pnodes ? c->pnodes_ptr() : nullptr;
@@ -1162,7 +1171,9 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             sg.Nf = c->Nf;
             sg.status = status;
         }
-        const bool spec = pl.M > 0 && !pl.topk && !pl.randk && t < INT64_MAX;
+        const bool spec = pl.M > 0 && !pl.topk && !pl.randk && t < INT64_MAX && !dev_t;
+        sg.t_advance = t_dev;
+        sg.r = c->p.r;   // (phase 0 forms Sigma over r sketch columns)
         if (spec) {
             const uint64_t tn = static_cast<uint64_t>(t + 1);
             sg.vblocks = blocks;
@@ -1179,6 +1190,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             (void)cudaGetLastError();
             return ARC_ERR_CUDA;
         }
+        if (sg.num_items > 0) t_dev = nullptr;   // (advanced by the selection kernel)
     }
     if (!pl.dense_ids.empty()) {   // DENSE blocks: identity compressor, streaming
         DenseLaunch dl{};
@@ -1324,6 +1336,10 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     ARC_MARK(5);
     if (sel_out != nullptr)
         ARC_CUDA(cudaMemcpyAsync(sel_out, sel, sizeof(int32_t) * pl.sumK, cudaMemcpyDeviceToDevice, s));
+    if (t_dev != nullptr) {   // ARC_FLAG_DEVICE_T and no selection kernel ran: advance t here
+        launch_advance_t(t_dev, s);
+        ARC_LAUNCHED();
+    }
     ARC_MARK(6);
     if (c->timing) ++c->timed_steps;
     ++c->tally[kTallySteps];
@@ -1334,6 +1350,18 @@ arc_status arc_topk_step(arc_topk_ctx* c, int64_t t, const float* const* grad, f
                          float* gbar, int32_t* sel_out, float* values_out, void* stream) {
     if (c == nullptr || grad == nullptr || gbar == nullptr) return ARC_ERR_INVALID_ARG;   // (h, g: checked per method)
     return run_step(c, t, grad, h, g, gbar, sel_out, values_out, static_cast<cudaStream_t>(stream));
+}
+
+arc_status arc_topk_set_iteration(arc_topk_ctx* c, int64_t t, void* stream) {
+    if (c == nullptr || t < 0 || !(c->p.flags & ARC_FLAG_DEVICE_T)) return ARC_ERR_INVALID_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned long long v = static_cast<unsigned long long>(t);
+    // (a kernel, not a host copy: the value travels as an argument, so the call is
+    // also legal inside a stream capture)
+    launch_set_u64(c->at<unsigned long long>(c->pl.o_tdev), v, s);
+    if (cudaGetLastError() != cudaSuccess) return ARC_ERR_CUDA;
+    c->last = s;
+    return ARC_OK;
 }
 
 arc_status arc_topk_step_host(arc_topk_ctx* c, int64_t t, const float* const* grad_host, float* const* h,
@@ -1421,7 +1449,7 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     const int sketch = pl.M > 0 ? (c->grid > 0 ? 1 : 0) + (c->grid_w > 0 ? 1 : 0) + (c->grid_t > 0 ? 1 : 0) : 0;
     const int sel = pl.items.empty() ? 0 : 1;
     if (pl.topk) return sketch + sel + c->p.N;   // + N ordered merges
-    const int vgen = (pl.M > 0 && pl.items.empty() && !pl.randk) ? 1 : 0;
+    const int vgen = (pl.M > 0 && !pl.topk && !pl.randk && (pl.items.empty() || (c->p.flags & ARC_FLAG_DEVICE_T))) ? 1 : 0;
     const int sigma = (pl.exchange || pl.exact) && !pl.randk && pl.M > 0 ? 1 : 0;
     const int dense = pl.dense_ids.empty() ? 0 : 1;
     const int scatter = pl.exchange ? (pl.segs_real.empty() ? 0 : 1) + dense : 0;

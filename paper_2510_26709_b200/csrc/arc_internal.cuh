@@ -101,6 +101,7 @@ struct SelectGatherLaunch {
     unsigned t_lo, t_hi;
     int pdl;                       // launch with programmatic stream serialization
     int cluster;                   // the grid is one thread-block cluster (<= 16 CTAs, one slice each)
+    unsigned long long* t_advance; // ARC_FLAG_DEVICE_T: the device iteration counter, += 1 at the end
     int early;                     // mode 0 without values: gather the certainly selected rows
                                    // (digit 1 above the boundary bin) before barrier 1 completes
     // Sigma not formed by the streaming pass: the kernel builds the digit-1
@@ -123,7 +124,9 @@ struct NodePtrs {
 
 // ---- launchers (arc_kernels.cu) ---------------------------------------------
 void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r, uint64_t seed,
-                 int64_t t, float* V, cudaStream_t s);
+                 int64_t t, float* V, cudaStream_t s, const unsigned long long* t_dev = nullptr);
+void launch_advance_t(unsigned long long* t_dev, cudaStream_t s);   // t_dev += 1 (one thread)
+void launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);   // *p = v (one thread)
 
 struct SketchLaunch {
     const BlockDev* blocks;
@@ -150,6 +153,7 @@ struct SketchLaunch {
     int noef;          // compressed MSGD without EF: sketch the gradient, u = gbar <- eta u
     int ranged;        // the launch over blocks whose V_b^T exceeds the stage (ranges of vs_cap / r columns)
     float* gbar;       // (noef) the replicated momentum u
+    const unsigned long long* t_dev;   // ARC_FLAG_DEVICE_T: t in device memory (Rand-K keys), else nullptr
     int pdl;           // launch with programmatic stream serialization (overlap the launch)
     unsigned* status;
 };

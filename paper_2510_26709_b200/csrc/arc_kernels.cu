@@ -34,8 +34,14 @@ using namespace rng;
 // (q*R4 + jj, b, lo32 t, hi32 t), key (lo32 seed, hi32 seed).  V_b is stored
 // transposed ([r][n_b], column j contiguous: the streaming pass reads it so).
 __global__ void __launch_bounds__(256) k_vgen(const BlockDev* __restrict__ blocks, int r, uint2 key,
-                                              unsigned t_lo, unsigned t_hi, float* __restrict__ V) {
+                                              unsigned t_lo, unsigned t_hi, float* __restrict__ V,
+                                              const unsigned long long* __restrict__ t_dev) {
     const int b = blockIdx.y;
+    if (t_dev != nullptr) {   // ARC_FLAG_DEVICE_T: this step's t from the device counter
+        const unsigned long long t = __ldcg(t_dev);
+        t_lo = static_cast<unsigned>(t);
+        t_hi = static_cast<unsigned>(t >> 32);
+    }
     if (blocks[b].kind != ARC_BLOCK_ARC) return;
     const int n = blocks[b].n;
     const long long v_off = blocks[b].v_off;
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(256) k_exact_sigma(const ExactSigmaLaunch a) {
 // ---- launchers ---------------------------------------------------------------
 
 void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r, uint64_t seed, int64_t t,
-                 float* V, cudaStream_t s) {
+                 float* V, cudaStream_t s, const unsigned long long* t_dev) {
     const int threads = 256;
     int gx = (max_nR4 + threads - 1) / threads;
     if (gx < 1) gx = 1;
@@ -437,8 +443,13 @@ void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r,
     dim3 grid(gx, num_blocks);
     const uint2 key = make_uint2(static_cast<unsigned>(seed), static_cast<unsigned>(seed >> 32));
     k_vgen<<<grid, threads, 0, s>>>(blocks_dev, r, key, static_cast<unsigned>(static_cast<uint64_t>(t)),
-                                    static_cast<unsigned>(static_cast<uint64_t>(t) >> 32), V);
+                                    static_cast<unsigned>(static_cast<uint64_t>(t) >> 32), V, t_dev);
 }
+
+__global__ void k_advance_t(unsigned long long* t_dev) { *t_dev += 1ull; }
+void launch_advance_t(unsigned long long* t_dev, cudaStream_t s) { k_advance_t<<<1, 1, 0, s>>>(t_dev); }
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+void launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) { k_set_u64<<<1, 1, 0, s>>>(p, v); }
 
 static int rows_grid(int num_rows) {
     int grid = (num_rows + 7) / 8;   // 8 warps per CTA, one warp per row segment

@@ -771,6 +771,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     STAMP(2);
     // every CTA has read this step's parity (before barrier 1): the next step uses the other one
     if (blockIdx.x == 0 && tid == 0) *s.parity = static_cast<unsigned>(par ^ 1);
+    // ARC_FLAG_DEVICE_T: the step's kernels that read t (V, Rand-K keys) ran before this one
+    if (s.t_advance != nullptr && blockIdx.x == 0 && tid == 0) *s.t_advance += 1ull;
     // any block with more candidates than fit takes the digit-by-digit path
     // (uniform across the grid, so every CTA meets the same barriers)
     bool overflow = false;
@@ -991,6 +993,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_select_gather(const SelectGathe
     gather_segments<UN>(ga, seg0, seg1, reinterpret_cast<int4*>(s_keys), kMaxSliceRows / 4);
     __syncthreads();
     STAMP(7);
+
 #undef STAMP
 }
 

@@ -181,12 +181,12 @@ __device__ __forceinline__ void segment(const SketchLaunch& a, int k, int nseg, 
 // Per-row epilogue (P[j] is the same in every lane).
 template <int RJ>
 __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int row_base, int b, int node, int lane, int r,
-                                             const float (&P)[RJ], unsigned* s_hist) {
+                                             const float (&P)[RJ], unsigned* s_hist, unsigned t_lo, unsigned t_hi) {
     if (a.mode == 3) {
         // Rand-K: row p's shared key (R16), written once (node-0 tiles)
         if (lane == 0 && node == 0) {
             const uint4 x = rng::philox4x32_10(
-                make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(b) | 0x80000000u, a.t_lo, a.t_hi), a.key);
+                make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(b) | 0x80000000u, t_lo, t_hi), a.key);
             const float sig = __uint_as_float(x.x >> 2);
             a.sigma[row_base + p] = sig;
             atomicAdd(&s_hist[order_key_dev(sig) >> kHist1Shift], 1u);
@@ -247,6 +247,12 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
     const int r = a.r;
     const float eta = a.eta, ome = a.ome;
     const int mode = a.mode;
+    unsigned t_lo = a.t_lo, t_hi = a.t_hi;   // (Rand-K keys)
+    if (mode == 3 && a.t_dev != nullptr) {   // ARC_FLAG_DEVICE_T: this step's t from the device counter
+        const unsigned long long t = __ldcg(a.t_dev);
+        t_lo = static_cast<unsigned>(t);
+        t_hi = static_cast<unsigned>(t >> 32);
+    }
     const bool sketch = mode <= 1;
     const bool cta_hist = true;                 // every mode histograms its keys in shared memory first
     auto flush_hist = [&](int b) {
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
                 if (mode == 3) {
                     if (node == 0) {
                         const uint4 x = rng::philox4x32_10(
-                            make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(T_b) | 0x80000000u, a.t_lo, a.t_hi),
+                            make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(T_b) | 0x80000000u, t_lo, t_hi),
                             a.key);
                         const float sig = __uint_as_float(x.x >> 2);
                         a.sigma[T_row_base + p] = sig;
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
                             for (int j = 0; j < RJ; ++j) s_P[rr][j] = P[j];
                         continue;
                     }
-                    row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
+                    row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist, t_lo, t_hi);
                 }
             }
           }
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
                                 gx, hx, dx, eta, ome, r, acc, P);
                 }
             }
-            row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
+            row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist, t_lo, t_hi);
         }
         if constexpr (RANGED) carry = rr - T_rows;
         }

@@ -26,6 +26,11 @@ Each side stream first waits for the backward stream, so a bucket's
 compression also overlaps the backward pass of the layers still to come; the
 returned future carries the side stream's completion.
 
+With ``cuda_graphs=True`` each bucket's step is captured once into a CUDA graph
+and replayed every iteration (one host launch per bucket instead of the step's
+kernel launches and argument marshalling); the iteration t lives in device
+memory and advances with each replay (the library's ARC_FLAG_DEVICE_T).
+
     from paper_2510_26709_b200.ddp import ArcTopKHookState, arc_topk_hook
     state = ArcTopKHookState(mu_bp=100, eta=0.1, r=4, seed=1234, warmup_steps=1000)
     ddp_model.register_comm_hook(state, arc_topk_hook)
@@ -65,8 +70,9 @@ class ArcTopKHookState:
     NUM_STREAMS = 2
 
     def __init__(self, mu_bp: int = 100, eta: float = 0.1, r: int = 4, seed: int = 20251030,
-                 warmup_steps: int = 0, process_group=None, reduce: str = "nccl"):
+                 warmup_steps: int = 0, process_group=None, reduce: str = "nccl", cuda_graphs: bool = False):
         self.mu_bp, self.eta, self.r, self.seed = int(mu_bp), float(eta), int(r), int(seed)
+        self.cuda_graphs = bool(cuda_graphs)
         self.warmup_steps = int(warmup_steps)
         self.pg = process_group
         self.reduce = reduce
@@ -109,7 +115,7 @@ class ArcTopKHookState:
         comm = self.comm_group(pg, buf.device) if pg is not None and N > 1 else None
         ctx = ArcTopK(d, blocks, N=N, eta=self.eta, r=self.r, seed=self.seed + 7919 * index, nodes_local=1,
                       pg=pg, rank=dist.get_rank(pg) if pg is not None else 0, reduce=self.reduce,
-                      device=buf.device, comm_group=comm)
+                      device=buf.device, comm_group=comm, device_t=self.cuda_graphs)
         b = {"d": d, "ctx": ctx, "h": torch.zeros_like(buf), "g": torch.zeros_like(buf),
              "gbar": torch.zeros_like(buf), "shapes": shapes, "blocks": blocks}
         self.buckets[index] = b
@@ -146,6 +152,16 @@ def arc_topk_hook(state: ArcTopKHookState, bucket) -> torch.futures.Future:
                 if N > 1:
                     dist.all_reduce(b["gbar"], group=state.pg)
                     b["gbar"].div_(N)
+            elif state.cuda_graphs:
+                # one CUDA graph per bucket: the step is captured once (on the bucket's
+                # buffer, which DDP keeps from iteration to iteration) and replayed, one
+                # host launch per bucket; the context's device iteration counter advances
+                # with every replay (ARC_FLAG_DEVICE_T)
+                if b.get("graph_buf") != buf.data_ptr():
+                    b["ctx"].set_iteration(t, stream=side)
+                    b["graph"] = b["ctx"].capture([buf], [b["h"]], [b["g"]], b["gbar"], stream=side)
+                    b["graph_buf"] = buf.data_ptr()
+                b["graph"].replay()
             else:
                 b["ctx"].step(t, [buf], [b["h"]], [b["g"]], b["gbar"], stream=side)
             buf.copy_(b["gbar"])

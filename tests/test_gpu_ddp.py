@@ -11,8 +11,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("warmup", [0, 1])
-def test_ddp_hook_matches_oracle(orc, warmup):
+@pytest.mark.parametrize("warmup,graphs", [(0, False), (1, False), (0, True), (1, True)])
+def test_ddp_hook_matches_oracle(orc, warmup, graphs):
     """warmup = 0: the EF21M state is initialised at each context's first compressed
     iteration, including the contexts DDP's bucket rebuild (after iteration 0)
     creates; warmup = 1: dense average first, then the same."""
@@ -27,13 +27,13 @@ def test_ddp_hook_matches_oracle(orc, warmup):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(0)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ["MASTER_PORT"] = str(29531 + warmup)
+    os.environ["MASTER_PORT"] = str(29531 + warmup + 2 * graphs)
     if not dist.is_initialized():
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     torch.manual_seed(0)
     model = nn.Sequential(nn.Linear(96, 80), nn.ReLU(), nn.Linear(80, 64), nn.ReLU(), nn.Linear(64, 10)).to(dev)
     ddp = DDP(model, device_ids=[0], bucket_cap_mb=0.02)
-    state = ArcTopKHookState(mu_bp=1000, eta=0.2, r=4, seed=11, warmup_steps=warmup)
+    state = ArcTopKHookState(mu_bp=1000, eta=0.2, r=4, seed=11, warmup_steps=warmup, cuda_graphs=graphs)
     seen = []
 
     def recording_hook(st, bucket):
