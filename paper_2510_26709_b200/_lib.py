@@ -88,7 +88,8 @@ def lib():
         L.arc_topk_create.argtypes = [P(ArcParams), vp, vp, ctypes.c_size_t, vp, P(vp)]
         L.arc_topk_step.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp]
         L.arc_topk_step_host.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp]
-        L.arc_topk_set_iteration.argtypes = [vp, i64, vp]
+        if hasattr(L, "arc_topk_set_iteration"):   # (absent from older builds used in A/B runs)
+            L.arc_topk_set_iteration.argtypes = [vp, i64, vp]
         L.arc_topk_query.argtypes = [vp, i32, vp, ctypes.c_size_t, vp]
         L.arc_topk_sizes.argtypes = [vp, P(i64), P(i64), P(i64), P(i64)]
         L.arc_topk_get_status.argtypes = [vp, P(ctypes.c_uint32)]
@@ -111,7 +112,8 @@ def lib():
                      "arc_topk_set_timing", "arc_topk_read_timing", "arc_topk_apply_update",
                      "arc_topk_comm_tally", "arc_topk_loopback_create", "arc_topk_loopback_comm",
                      "arc_topk_loopback_destroy"]:
-            getattr(L, name).restype = ctypes.c_int
+            if hasattr(L, name):
+                getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
 

@@ -179,15 +179,29 @@ __device__ __forceinline__ void segment(const SketchLaunch& a, int k, int nseg, 
 }
 
 // Per-row epilogue (P[j] is the same in every lane).
+// Rand-K key of row p of block b at this step's t (R16; ARC_FLAG_DEVICE_T: t from the device counter)
+__device__ __forceinline__ float randk_key_t(const unsigned long long* t_dev, unsigned t_lo, unsigned t_hi, uint2 key, int p,
+                                           int b) {
+    if (t_dev != nullptr) {
+        const unsigned long long t = __ldcg(t_dev);
+        t_lo = static_cast<unsigned>(t);
+        t_hi = static_cast<unsigned>(t >> 32);
+    }
+    const uint4 x = rng::philox4x32_10(make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(b) | 0x80000000u, t_lo, t_hi),
+                                       key);
+    return __uint_as_float(x.x >> 2);
+}
+__device__ __forceinline__ float randk_key(const SketchLaunch& a, int p, int b) {
+    return randk_key_t(a.t_dev, a.t_lo, a.t_hi, a.key, p, b);
+}
+
 template <int RJ>
 __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int row_base, int b, int node, int lane, int r,
-                                             const float (&P)[RJ], unsigned* s_hist, unsigned t_lo, unsigned t_hi) {
+                                             const float (&P)[RJ], unsigned* s_hist) {
     if (a.mode == 3) {
         // Rand-K: row p's shared key (R16), written once (node-0 tiles)
         if (lane == 0 && node == 0) {
-            const uint4 x = rng::philox4x32_10(
-                make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(b) | 0x80000000u, t_lo, t_hi), a.key);
-            const float sig = __uint_as_float(x.x >> 2);
+            const float sig = randk_key(a, p, b);
             a.sigma[row_base + p] = sig;
             atomicAdd(&s_hist[order_key_dev(sig) >> kHist1Shift], 1u);
         }
@@ -247,12 +261,6 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
     const int r = a.r;
     const float eta = a.eta, ome = a.ome;
     const int mode = a.mode;
-    unsigned t_lo = a.t_lo, t_hi = a.t_hi;   // (Rand-K keys)
-    if (mode == 3 && a.t_dev != nullptr) {   // ARC_FLAG_DEVICE_T: this step's t from the device counter
-        const unsigned long long t = __ldcg(a.t_dev);
-        t_lo = static_cast<unsigned>(t);
-        t_hi = static_cast<unsigned>(t >> 32);
-    }
     const bool sketch = mode <= 1;
     const bool cta_hist = true;                 // every mode histograms its keys in shared memory first
     auto flush_hist = [&](int b) {
@@ -340,10 +348,7 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
                 for (int j = 0; j < RJ; ++j) P[j] = fadd(P[j], 0.0f);    // the butterfly with idle lanes
                 if (mode == 3) {
                     if (node == 0) {
-                        const uint4 x = rng::philox4x32_10(
-                            make_uint4(static_cast<unsigned>(p), static_cast<unsigned>(T_b) | 0x80000000u, t_lo, t_hi),
-                            a.key);
-                        const float sig = __uint_as_float(x.x >> 2);
+                        const float sig = randk_key(a, p, T_b);
                         a.sigma[T_row_base + p] = sig;
                         atomicAdd(&s_hist[order_key_dev(sig) >> kHist1Shift], 1u);
                     }
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
                             for (int j = 0; j < RJ; ++j) s_P[rr][j] = P[j];
                         continue;
                     }
-                    row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist, t_lo, t_hi);
+                    row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
                 }
             }
           }
@@ -494,7 +499,7 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
                                 gx, hx, dx, eta, ome, r, acc, P);
                 }
             }
-            row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist, t_lo, t_hi);
+            row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
         }
         if constexpr (RANGED) carry = rr - T_rows;
         }

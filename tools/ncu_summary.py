@@ -35,7 +35,7 @@ SCALE = {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0, "byte": 1, "Kbyte": 1e3, 
 
 
 def short(name):
-    for k in ["k_ef_sketch", "k_select_gather", "k_vgen", "k_sigma_slice", "k_scatter", "k_gather_ef",
+    for k in ["k_ef_sketch_tma", "k_ef_sketch", "k_select_gather", "k_vgen", "k_sigma_slice", "k_scatter", "k_gather_ef",
               "k_select", "k_sel_scan", "k_sel_write"]:
         if k in name:
             return k
