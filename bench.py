@@ -536,6 +536,52 @@ def measure(run: Runner, args, config: str, mu_bp, steps: int, warmup: int, *, e
     return out
 
 
+def measure_graph(run: Runner, config: str, steps: int, S: int = 8, **ctx_kw):
+    """Device time of a step with the host out of the loop (one GPU): S consecutive
+    steps, one per gradient set, captured in ONE CUDA graph (device iteration
+    counter, ARC_FLAG_DEVICE_T; the public ArcTopK.step inside torch.cuda.graph)
+    and replayed; ms per step = elapsed / (replays * S).  For small workloads the
+    eager loop is bound by the host's launch + marshalling time instead."""
+    torch = run.torch
+    from paper_2510_26709_b200 import ArcTopK, _lib
+    from synth import GradientSource
+    d, blocks = workload(config, None)
+    dev = run.dev
+    src = GradientSource(d, blocks, 1, seed=20251030, device=dev)
+    pool = [src.grads(t) for t in range(S)]
+    h, g = [torch.zeros(d, device=dev)], [torch.zeros(d, device=dev)]
+    gbar = torch.zeros(d, device=dev)
+    ctx = ArcTopK(d, blocks, N=1, eta=0.1, r=4, seed=20251030, nodes_local=1, device_t=True, **ctx_kw)
+    plan = ctx.query(_lib.Q_PLAN).cpu().tolist()
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    for j in range(S):
+        ctx.step(0, pool[j], h, g, gbar, stream=s)
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s, capture_error_mode="relaxed"):
+        for j in range(S):
+            ctx.step(0, pool[j], h, g, gbar, stream=s)
+    ctx.set_iteration(S)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    reps = max(1, steps // S)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        graph.replay()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / (reps * S)
+    ctx.close()
+    del pool, h, g, gbar, graph
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "steps": reps * S, "value": 4.0 * d / (ms * 1e-3) / 1e9, "unit": "GB/s",
+            "selection_form": ["cooperative grid", "one cluster", "fused tail", "none"][plan[0]],
+            "kernels_per_step": plan[3]}
+
+
 def measure_bucketed(run: Runner, args, config: str, steps: int, warmup: int, bucket_elems: int = 25 * 2**20,
                      pool_max: int = 4, graphs: bool = False):
     """The per-layer bucketed variant: the
@@ -703,6 +749,20 @@ def main():
                 extras[name]["clocks"] = ex.get("clocks")
             except Exception as e:
                 extras[name] = {"unavailable": f"{type(e).__name__}: {str(e)[:200]}"}
+        # the small single-GPU configs, eager and with the host out of the loop
+        # (configs[4]'s d = 1e6 point: the fused tail; C2 with one node)
+        if run.world == 1:
+            for name in ("C5_1e6", "C2"):
+                try:
+                    ex = measure(run, args, name, None, max(50, min(args.steps, 300)), args.warmup, pool_max=8,
+                                 clocks=False)
+                    gr = measure_graph(run, name, max(80, min(args.steps, 400)))
+                    extras[name] = {"d": ex["d"], "sum_K": ex["sum_K"], "ms_per_step": ex["ms_per_step"],
+                                    "graph": gr, "step_roofline_frac_graph":
+                                        ex["step_roofline"]["t_roof_ms"] / gr["ms_per_step"],
+                                    "t_roof_ms": ex["step_roofline"]["t_roof_ms"], "phases_ms": ex["phases_ms"]}
+                except Exception as e:
+                    extras[name] = {"unavailable": f"{type(e).__name__}: {str(e)[:200]}"}
         try:   # the per-layer bucketed C4 against its single call
             bk = measure_bucketed(run, args, "C4", max(10, min(args.steps, 50)), args.warmup)
             single = extras.get("C4", {}).get("ms_per_step")

@@ -219,9 +219,15 @@ typedef enum {
                            (R9): Alg. 1 l.5 before the 1/(N sqrt r) scaling (R2, R3); every node on
                            this GPU (G == 1) and P' kept (as ARC_Q_P_NODES), else
                            ARC_ERR_UNSUPPORTED (with G > 1 each rank holds only its own nodes')  */
-    ARC_Q_CANDIDATES = 4 /* uint32 [num_blocks] rows sharing the boundary bin of the last selection
+    ARC_Q_CANDIDATES = 4, /* uint32 [num_blocks] rows sharing the boundary bin of the last selection
                             ([nodes_local][num_blocks] for ARC_METHOD_TOPK_ALLGATHER, whose
                             nodes select separately); synchronises the step's stream first    */
+    ARC_Q_PLAN = 6      /* int32 [4] how the context runs a step (fixed at create): [0] selection
+                           form: 0 cooperative grid, 1 one thread-block cluster, 2 the fused tail
+                           (S3 in the streaming launch's last CTA + a small update kernel: one node
+                           on this GPU, no exchange, a small selection), 3 none; [1] selection
+                           CTAs (1 for the tail); [2] streaming (S1) launches; [3] kernels per
+                           step (arc_topk_kernels_per_step)                                     */
 } arc_query;
 arc_status arc_topk_query(arc_topk_ctx* ctx, int32_t what, void* dst, size_t bytes, void* stream);
 
@@ -251,7 +257,12 @@ arc_status arc_topk_read_timing(arc_topk_ctx* ctx, float* ms, int32_t n_phases, 
 /* Debug: per-CTA %globaltimer stamps (ns) at the phase boundaries of the last
  * step's select/gather kernel, when the context was created with the
  * environment variable ARC_DEBUG_STAMPS=1 (else ARC_ERR_INVALID_ARG).  Copies
- * min(n, grid * 8) uint64 values into host memory (synchronises). */
+ * min(n, grid * 8) uint64 values into host memory (synchronises).  When the
+ * step ran the fused small-problem tail (S3..S6 in the streaming launch's last
+ * CTA; no selection kernel) *grid = 1 and the row holds: [0] streaming launch
+ * start (CTA 0), [1] tail start (the last CTA's arrival), [2] keys and
+ * histogram loaded, [3] digits resolved (last ARC block), [4] selection
+ * written, [5] S4..S6 done. */
 arc_status arc_topk_debug_stamps(arc_topk_ctx* ctx, uint64_t* stamps_host, int64_t n, int32_t* grid);
 
 /* The model update that consumes gbar (R23,

@@ -29,7 +29,7 @@ METHOD_ARC, METHOD_TOPK_ALLGATHER, METHOD_RANDK, METHOD_NOEF_MSGD, METHOD_EXACT 
 # arc_opt_kind
 OPT_SGD, OPT_ADAM = 0, 1
 # arc_query
-Q_V, Q_SIGMA, Q_SEL, Q_P_NODES, Q_CANDIDATES, Q_S = 0, 1, 2, 3, 4, 5
+Q_V, Q_SIGMA, Q_SEL, Q_P_NODES, Q_CANDIDATES, Q_S, Q_PLAN = 0, 1, 2, 3, 4, 5, 6
 # arc_wire
 WIRE_F32, WIRE_BF16 = 0, 1
 

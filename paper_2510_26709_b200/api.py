@@ -252,7 +252,8 @@ class ArcTopK:
                   L.Q_P_NODES: (self.sum_m_arc * self.nodes_local * self.r, torch.float32),
                   L.Q_S: (self.sum_m_arc * self.r, torch.float32),
                   L.Q_CANDIDATES: (len(self.blocks) * (self.nodes_local if self.method == "topk_allgather" else 1),
-                                   torch.int32)}
+                                   torch.int32),
+                  L.Q_PLAN: (4, torch.int32)}
         n, dt = shapes[what]
         out = torch.empty(max(n, 1), dtype=dt, device=self.device)
         L.check(self.lib.arc_topk_query(self.ctx, int(what), int(out.data_ptr()), out.numel() * out.element_size(),

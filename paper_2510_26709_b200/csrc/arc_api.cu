@@ -505,6 +505,8 @@ struct arc_topk_ctx {
     int64_t v_ready = -1;        // t whose V the previous step generated speculatively
     bool pdl = true;             // programmatic dependent launch between the step's kernels (ARC_PDL=0: off)
     bool early = true;           // early gather of the certain rows in the select kernel (ARC_EARLY=0: off)
+    bool tail = false;           // S3..S6 in the streaming launch's last CTA (small single-node selections)
+    int tail_keys = 0;           // the largest ARC block's rows (keys staged in shared memory by the tail)
     int64_t last_t = 0;
     int64_t v_items = 0;
     // ARC_REDUCE_LSA: library-owned symmetric window and device communicator
@@ -839,7 +841,26 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
         D.b = tiles[i].b;
         D.node = tiles[i].node;
     }
-    {
+    {   // the fused small-problem tail (arc_sketch.cu): S3..S6 in the streaming launch's
+        // last CTA when the GPU holds the one node, there is no exchange and the
+        // selection is small (ARC_TAIL=0: off, the selection kernel instead)
+        const Plan& P = c->pl;
+        int arc_blocks = 0, max_m = 0;
+        int64_t sk = 0, skn = 0;
+        for (const BlockDev& B : P.bdev)
+            if (B.kind == ARC_BLOCK_ARC) {
+                ++arc_blocks;
+                max_m = std::max(max_m, B.m);
+                sk += B.K;
+                skn += static_cast<int64_t>(B.K) * B.n;
+            }
+        bool on = true;
+        if (const char* e = getenv("ARC_TAIL")) on = e[0] != '0';
+        const int r_eff = P.randk ? 1 : c->p.r;
+        c->tail = on && !P.exchange && P.L == 1 && c->p.N == 1 && !P.topk && !P.exact && c->grid > 0 &&
+                  c->grid_w == 0 && c->grid_t == 0 && r_eff <= 8 && arc_blocks >= 1 &&
+                  arc_blocks <= kTailMaxBlocks && P.M <= kTailMaxRows && sk <= kTailMaxK && skn <= kTailMaxKn;
+        c->tail_keys = max_m;
     }
     const std::vector<SelRow>& rows = c->pl.segs;
 
@@ -1003,9 +1024,47 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
         ARC_MARK(1);
         a.noef = pl.noef ? 1 : 0;
         a.gbar = gbar;
+        if (c->tail) {   // S3..S6 in the last CTA (no selection kernel this step)
+            TailArgs& ta = a.tail;
+            ta.done = status + 2;
+            ta.sel = sel;
+            ta.values = values_out;
+            ta.bf16 = c->p.wire == ARC_WIRE_BF16 ? 1 : 0;
+            ta.N_int = c->p.N;
+            ta.t_advance = t_dev;
+            ta.key_cap = c->tail_keys;
+            ta.stamps = c->stamps;
+            ta.nblk = 0;
+            ta.quads = 0;
+            for (const BlockDev& B : pl.bdev) {
+                if (B.kind != ARC_BLOCK_ARC) continue;
+                TailBlk& tb = ta.blk[ta.nblk++];
+                tb.off = B.off;
+                tb.len = B.len;
+                tb.val_base = B.val_base;
+                tb.q_begin = ta.quads;
+                tb.n = B.n;
+                tb.K = B.K;
+                tb.sel_base = B.sel_base;
+                tb.vec = B.vec;
+                ta.quads += static_cast<long long>(B.K) * ((B.n + 3) / 4);
+            }
+            const bool spec = !pl.randk && t < INT64_MAX && !dev_t;
+            if (spec) {
+                const uint64_t tn = static_cast<uint64_t>(t + 1);
+                ta.V_next = V + static_cast<size_t>((t + 1) & 1) * pl.sum_nr;
+                ta.v_items = c->v_items;
+                ta.tn_lo = static_cast<unsigned>(tn);
+                ta.tn_hi = static_cast<unsigned>(tn >> 32);
+            }
+        }
         if (c->grid > 0) {
             launch_ef_sketch(a, s);
             ARC_LAUNCHED();
+            if (c->tail) {   // S4..S6 of the tail's selection
+                launch_tail_update(a, s);
+                ARC_LAUNCHED();
+            }
         }
         if (c->grid_w > 0) {   // blocks with V_b^T wider than the stage
             a.cta_begin = c->at<int>(pl.o_cta_w);
@@ -1185,12 +1244,17 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
             sg.t_lo = static_cast<unsigned>(tn);
             sg.t_hi = static_cast<unsigned>(tn >> 32);
         }
-        c->v_ready = (spec && sg.num_items > 0) ? t + 1 : -1;
-        if (sg.num_items > 0 && launch_select_gather(sg, ga, s) != cudaSuccess) {
-            (void)cudaGetLastError();
-            return ARC_ERR_CUDA;
+        if (c->tail && pl.M > 0) {   // (S3..S6, the next V and the t advance ran in the streaming launch)
+            c->v_ready = (!pl.randk && t < INT64_MAX && !dev_t) ? t + 1 : -1;
+            t_dev = nullptr;
+        } else {
+            c->v_ready = (spec && sg.num_items > 0) ? t + 1 : -1;
+            if (sg.num_items > 0 && launch_select_gather(sg, ga, s) != cudaSuccess) {
+                (void)cudaGetLastError();
+                return ARC_ERR_CUDA;
+            }
+            if (sg.num_items > 0) t_dev = nullptr;   // (advanced by the selection kernel)
         }
-        if (sg.num_items > 0) t_dev = nullptr;   // (advanced by the selection kernel)
     }
     if (!pl.dense_ids.empty()) {   // DENSE blocks: identity compressor, streaming
         DenseLaunch dl{};
@@ -1420,6 +1484,15 @@ arc_status arc_topk_query(arc_topk_ctx* c, int32_t what, void* dst, size_t bytes
             need = sizeof(unsigned) * pl.sbdev.size();
             break;
         }
+        case ARC_Q_PLAN: {   // host-side facts, copied synchronously
+            const int32_t plan[4] = {pl.items.empty() ? 3 : c->tail ? 2 : c->sel_cluster ? 1 : 0,
+                                     pl.items.empty() ? 0 : c->tail ? 1 : c->sel_grid,
+                                     pl.M > 0 ? (c->grid > 0) + (c->grid_w > 0) + (c->grid_t > 0) : 0,
+                                     arc_topk_kernels_per_step(c)};
+            if (bytes < sizeof plan) return ARC_ERR_INVALID_ARG;
+            ARC_CUDA(cudaMemcpy(dst, plan, sizeof plan, cudaMemcpyDefault));
+            return ARC_OK;
+        }
         default: return ARC_ERR_INVALID_ARG;
     }
     if (bytes < need) return ARC_ERR_INVALID_ARG;
@@ -1447,7 +1520,7 @@ int32_t arc_topk_kernels_per_step(const arc_topk_ctx* c) {
     // kernel (k_vgen only when there is none)
     const Plan& pl = c->pl;
     const int sketch = pl.M > 0 ? (c->grid > 0 ? 1 : 0) + (c->grid_w > 0 ? 1 : 0) + (c->grid_t > 0 ? 1 : 0) : 0;
-    const int sel = pl.items.empty() ? 0 : 1;
+    const int sel = pl.items.empty() ? 0 : 1;   // (the fused tail: S3 in the sketch launch + the update kernel)
     if (pl.topk) return sketch + sel + c->p.N;   // + N ordered merges
     const int vgen = (pl.M > 0 && !pl.topk && !pl.randk && (pl.items.empty() || (c->p.flags & ARC_FLAG_DEVICE_T))) ? 1 : 0;
     const int sigma = (pl.exchange || pl.exact) && !pl.randk && pl.M > 0 ? 1 : 0;
@@ -1501,10 +1574,10 @@ arc_status arc_topk_get_status(arc_topk_ctx* c, uint32_t* flags) {
 
 arc_status arc_topk_debug_stamps(arc_topk_ctx* c, uint64_t* stamps_host, int64_t n, int32_t* grid) {
     if (c == nullptr || c->stamps == nullptr || stamps_host == nullptr) return ARC_ERR_INVALID_ARG;
-    const int64_t all = static_cast<int64_t>(c->sel_grid) * 8;
+    const int64_t all = static_cast<int64_t>(c->tail ? 1 : c->sel_grid) * 8;   // (the fused tail: one row)
     ARC_CUDA(cudaStreamSynchronize(c->last));
     ARC_CUDA(cudaMemcpy(stamps_host, c->stamps, sizeof(uint64_t) * (n < all ? n : all), cudaMemcpyDeviceToHost));
-    if (grid) *grid = static_cast<int32_t>(c->sel_grid);
+    if (grid) *grid = static_cast<int32_t>(c->tail ? 1 : c->sel_grid);
     return ARC_OK;
 }
 

@@ -128,6 +128,37 @@ void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r,
 void launch_advance_t(unsigned long long* t_dev, cudaStream_t s);   // t_dev += 1 (one thread)
 void launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);   // *p = v (one thread)
 
+// The fused small-problem tail of the streaming pass (arc_sketch.cu): with one
+// node on the GPU, no exchange and a small selection, the LAST CTA of the
+// streaming launch to finish (a done counter) runs S3..S6 itself — no second
+// launch, no grid barrier ("fused tail").
+constexpr int kTailMaxRows = 8192;      // M = sum m_b over the ARC blocks, at most
+constexpr int kTailMaxK = 2048;         // sum K_b (the selected rows, listed in shared memory)
+constexpr long long kTailMaxKn = 32768; // sum K_b n_b (the rows one CTA updates)
+constexpr int kTailMaxBlocks = 8;       // ARC blocks
+struct TailBlk {                    // an ARC block as the tail's update kernel reads it (kernel parameter)
+    long long off, len, val_base;
+    long long q_begin;              // first quad of the block's selected rows in the update's item space
+    int n, K, sel_base, vec;
+};
+struct TailArgs {
+    unsigned* done;                 // CTAs finished (workspace word, zero between steps); nullptr: no tail
+    int32_t* sel;                   // the selection (sum K_b entries, block sel_base offsets)
+    float* values;                  // optional A / N (val_base offsets)
+    int bf16;                       // R25: C rounded at the source
+    int N_int;
+    unsigned long long* t_advance;  // ARC_FLAG_DEVICE_T: += 1 once the step's t readers are done
+    float* V_next;                  // speculative S0 of the next step (nullptr: none), drawn by every CTA
+    long long v_items;
+    unsigned tn_lo, tn_hi;
+    int key_cap;                    // floats of dynamic shared memory (keys of one block, m_b <= key_cap)
+    unsigned long long* stamps;     // debug (ARC_DEBUG_STAMPS=1): %globaltimer at the tail's phases, or nullptr
+    int nblk;                       // ARC blocks (<= kTailMaxBlocks) and their update table
+    long long quads;                // sum over them of K_b ceil(n_b / 4): the update's items
+    TailBlk blk[kTailMaxBlocks];
+};
+
+
 struct SketchLaunch {
     const BlockDev* blocks;
     const TileDesc* tiles;  // all tiles, grouped by CTA
@@ -156,8 +187,12 @@ struct SketchLaunch {
     const unsigned long long* t_dev;   // ARC_FLAG_DEVICE_T: t in device memory (Rand-K keys), else nullptr
     int pdl;           // launch with programmatic stream serialization (overlap the launch)
     unsigned* status;
+    TailArgs tail;     // (mode 0 / 3, one node, no exchange) the fused S3..S6 tail, or tail.done == nullptr
 };
 void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s);
+// S4..S6 of the tail's selection: a small grid launched right behind the streaming
+// launch (programmatic dependent launch when a.pdl), waiting for it to complete.
+void launch_tail_update(const SketchLaunch& a, cudaStream_t s);
 int ef_sketch_resident_ctas(int r, int shape, int vs_cap);   // SMs x occupancy
 int sketch_vs_cap(int r, int max_n);   // floats of V_b^T the streaming pass stages in shared memory (0: too wide)
 int sketch_ranged_cap(int r);          // floats staged per range by the wide blocks' launch

@@ -31,6 +31,7 @@
 #include "arc_device.cuh"
 #include "arc_internal.cuh"
 #include "arc_rng.cuh"
+#include "arc_select_common.cuh"
 
 namespace arc {
 namespace {
@@ -233,13 +234,295 @@ __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int r
     }
 }
 
+// ---- the fused small-problem tail: S3..S6 in the last CTA ------
+// Every CTA, after its tiles, draws its share of the next step's V (S0,
+// speculative; V depends only on (seed, t, b)), fences its writes and
+// increments the done counter once.  The CTA that brings the counter to the
+// grid size has every other CTA's Sigma rows and digit-1 histogram bins
+// visible, and runs the selection of k_select_gather on keys held in shared
+// memory: per ARC block, the boundary digit 1 from the complete histogram,
+// digits 2 and 3 (key[20:10], key[9:0]) by two shared-memory histogram passes
+// over the keys whose higher digits match, so T = the K_b-th largest key and
+// need_eq = how many keys equal to T are taken; then ONE ordered pass writes
+// I_b ascending (key > T, or key == T among the need_eq smallest rows: ties
+// -> smaller row, R5; NaN keys largest, R15).  S4..S6 follow on the selected
+// rows with the arithmetic of gather_rows_local (one node on this GPU, N = 1:
+// C = h' - g [R25 rounding], g <- g + C, gbar <- gbar + C / N, R3, R12, R13).
+// No grid barrier, no second launch: nothing waits on another CTA.
+__device__ const float4 k_tail_zero4 = {0.f, 0.f, 0.f, 0.f};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int NT>
+__device__ __forceinline__ bool tail_arrive(const SketchLaunch& a) {
+    __shared__ unsigned s_last;
+    const TailArgs& T = a.tail;
+    if (T.V_next != nullptr)   // (item i on CTA i mod grid: a few items per CTA, none on the critical path)
+        for (long long i = threadIdx.x * static_cast<long long>(gridDim.x) + blockIdx.x; i < T.v_items;
+             i += static_cast<long long>(gridDim.x) * NT)
+            rng::gen_V_item(a.blocks, a.num_blocks, a.r, a.key, T.tn_lo, T.tn_hi, i, T.V_next);
+    __threadfence();   // this thread's Sigma, histogram, h' and V writes, before the CTA's increment
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(T.done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last != 0;
+}
+
+template <int NT>
+__device__ void tail_select_update(const SketchLaunch& a, unsigned* sh, int* s_list, unsigned* s_keys) {
+    __shared__ int warp_sums[32];
+    __shared__ unsigned s_dig;
+    __shared__ int s_abv, s_cnt;
+    constexpr int kTailCand = kHist1Bins / 2;   // boundary-bin keys ranked directly (sh holds keys | rows)
+    const int tid = threadIdx.x;
+    const TailArgs& T = a.tail;
+#define TAIL_STAMP(k) \
+    if (T.stamps != nullptr && tid == 0) T.stamps[k] = globaltimer_ns()
+    TAIL_STAMP(1);
+    // the update kernel behind this launch may become resident now (it waits for this grid)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // ---- S3 per ARC block
+    for (int b = 0; b < a.num_blocks; ++b) {
+        const BlockDev& B = a.blocks[b];
+        if (B.kind != ARC_BLOCK_ARC) continue;
+        const int m = B.m, K = B.K, sel_base = B.sel_base;
+        __syncthreads();                                     // (sh, s_keys of the previous block)
+        // the block's digit-1 histogram and order keys (R15): every load of a
+        // batch in flight before the first is used (one L2 round trip per batch)
+        const float* __restrict__ sg = a.sigma + B.row_base;
+        unsigned* gh = a.hist1 + static_cast<long long>(b) * kHist1Bins;
+        {
+            constexpr int HB = kHist1Bins / NT;
+            unsigned hv[HB];
+#pragma unroll
+            for (int k = 0; k < HB; ++k) hv[k] = __ldcg(gh + tid + k * NT);
+            for (int i0 = 0; i0 < m; i0 += 8 * NT) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * NT + tid;
+                    v[u] = i < m ? __ldcg(sg + i) : 0.0f;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * NT + tid;
+                    if (i < m) s_keys[i] = order_key_dev(v[u]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < HB; ++k) {
+                sh[tid + k * NT] = hv[k];
+                gh[tid + k * NT] = 0u;                       // (the next step's histogram starts empty)
+            }
+        }
+        __syncthreads();
+        TAIL_STAMP(2);
+        // T = the K-th largest key; selected: key > T, or key == T and (use_peq)
+        // row <= P_eq / (else) among the need_eq smallest rows with key T
+        unsigned Tk = 0u;   // K = m: every row (key >= +0, P_eq = m - 1)
+        int Peq = m - 1, need_eq = m;
+        bool use_peq = true;
+        if (K < m) {
+            int above;
+            const unsigned b1 = selc::top_digit<NT>(sh, kHist1Bins, K, warp_sums, &s_dig, &s_abv, &above);
+            int krem = K - above;
+            // the keys of the boundary bin b1 (usually a handful) listed in sh, then
+            // ranked in the order (key desc, row asc): the krem-th is (T, P_eq)
+            unsigned* ck = sh;
+            int* ci = reinterpret_cast<int*>(sh + kTailCand);
+            if (tid == 0) s_cnt = 0;
+            __syncthreads();
+            for (int i = tid; i < m; i += NT) {
+                const unsigned k = s_keys[i];
+                if ((k >> 21) == b1) {
+                    const int slot = atomicAdd(&s_cnt, 1);
+                    if (slot < kTailCand) { ck[slot] = k; ci[slot] = i; }
+                }
+            }
+            __syncthreads();
+            const int E = s_cnt;
+            if (E <= kTailCand) {
+                for (int c = tid; c < E; c += NT) {
+                    const unsigned key = ck[c];
+                    const int row = ci[c];
+                    int rank = 0;
+#pragma unroll 4
+                    for (int j = 0; j < E; ++j) rank += ck[j] > key || (ck[j] == key && ci[j] < row);
+                    if (rank == krem - 1) { s_dig = key; s_abv = row; }
+                }
+                __syncthreads();
+                Tk = s_dig;
+                Peq = s_abv;
+                __syncthreads();
+            } else {   // a crowded boundary bin (massive ties): digits 2 and 3 by histogram passes
+                use_peq = false;
+                for (int i = tid; i < 2048; i += NT) sh[i] = 0u;
+                __syncthreads();
+                for (int i = tid; i < m; i += NT) {
+                    const unsigned k = s_keys[i];
+                    if ((k >> 21) == b1) atomicAdd(&sh[(k >> 10) & 2047u], 1u);
+                }
+                __syncthreads();
+                const unsigned b2 = selc::top_digit<NT>(sh, 2048, krem, warp_sums, &s_dig, &s_abv, &above);
+                krem -= above;
+                const unsigned pre = (b1 << 11) | b2;        // key[31:10] of the K-th key
+                for (int i = tid; i < 1024; i += NT) sh[i] = 0u;
+                __syncthreads();
+                for (int i = tid; i < m; i += NT) {
+                    const unsigned k = s_keys[i];
+                    if ((k >> 10) == pre) atomicAdd(&sh[k & 1023u], 1u);
+                }
+                __syncthreads();
+                const unsigned b3 = selc::top_digit<NT>(sh, 1024, krem, warp_sums, &s_dig, &s_abv, &above);
+                krem -= above;
+                Tk = (pre << 10) | b3;
+                need_eq = krem;                              // >= 1 keys equal to T are taken
+            }
+        }
+        TAIL_STAMP(3);
+        // ordered pass: thread tid owns rows [r0, r1); I_b written ascending
+        const int R = (m + NT - 1) / NT;
+        const int r0 = min(m, tid * R), r1 = min(m, r0 + R);
+        int tot, pos;
+        if (use_peq) {
+            int cnt = 0;
+            for (int i = r0; i < r1; ++i) {
+                const unsigned k = s_keys[i];
+                cnt += k > Tk || (k == Tk && i <= Peq);
+            }
+            pos = selc::cta_exclusive_scan(cnt, warp_sums, &tot);
+            for (int i = r0; i < r1; ++i) {
+                const unsigned k = s_keys[i];
+                if (k > Tk || (k == Tk && i <= Peq)) {
+                    T.sel[sel_base + pos] = i;
+                    s_list[sel_base + pos] = i;
+                    ++pos;
+                }
+            }
+        } else {
+            int gt = 0, eq = 0;
+            for (int i = r0; i < r1; ++i) {
+                const unsigned k = s_keys[i];
+                gt += k > Tk;
+                eq += k == Tk;
+            }
+            int eq_seen = selc::cta_exclusive_scan(eq, warp_sums, &tot);
+            const int take_eq = max(0, min(eq, need_eq - eq_seen));
+            pos = selc::cta_exclusive_scan(gt + take_eq, warp_sums, &tot);
+            for (int i = r0; i < r1; ++i) {
+                const unsigned k = s_keys[i];
+                bool take = k > Tk;
+                if (k == Tk) take = eq_seen++ < need_eq;
+                if (take) {
+                    T.sel[sel_base + pos] = i;
+                    s_list[sel_base + pos] = i;
+                    ++pos;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    TAIL_STAMP(4);
+    if (tid == 0) {
+        if (T.t_advance != nullptr) *T.t_advance += 1ull;   // (every reader of this step's t is done)
+        *T.done = 0u;                                       // (the next launch counts from zero)
+    }
+#undef TAIL_STAMP
+}
+
+// S4..S6 on the tail's selected rows (one node on this GPU, N = 1 here): one
+// quad (4 columns of one selected row) per thread, the arithmetic of
+// gather_rows_local — C = h' - g [R25 rounding], g <- g + C, gbar <- gbar + C / N
+// (R3, R12, R13), A / N into the values when requested.  Launched right behind
+// the streaming launch: with programmatic dependent launch its CTAs are resident
+// while the last CTA selects (that CTA triggers its dependents first) and wait
+// here for the streaming grid to complete; the selection is then visible.  (One
+// CTA updating the rows itself measured 9-14 us for 10 rows of 1024 columns.)
+__global__ void __launch_bounds__(256) k_tail_update(const SketchLaunch a) {
+    // the next kernel (the next step's streaming launch) may become resident and run
+    // its prologue now; it waits for this grid before touching the state
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    grid_dependency_wait();
+    const TailArgs& T = a.tail;
+    const bool pow2 = (T.N_int & (T.N_int - 1)) == 0;
+    const float invN = 1.0f / a.Nf;
+    const bool noef = a.noef != 0;
+    const float* __restrict__ ph = noef ? a.nodes.grad[0] : a.nodes.h[0];   // (without EF: C = the gradient rows)
+    float* __restrict__ pg = a.nodes.g[0];
+    float* __restrict__ gbar = a.gbar;
+    for (long long item = blockIdx.x * 256ll + threadIdx.x; item < T.quads; item += gridDim.x * 256ll) {
+        int b = 0;
+        while (b + 1 < T.nblk && item >= T.blk[b + 1].q_begin) ++b;
+        const TailBlk& B = T.blk[b];
+        const int nq = (B.n + 3) >> 2;
+        const long long rel = item - B.q_begin;
+        const int j = static_cast<int>(rel / nq), q = 4 * static_cast<int>(rel - static_cast<long long>(j) * nq);
+        const int p = __ldcg(T.sel + B.sel_base + j);
+        const int cnt = max(0, min(4, row_cols(B.len, B.n, p) - q)), ocnt = min(4, B.n - q);
+        const long long e = B.off + static_cast<long long>(p) * B.n + q;
+        const long long o = B.val_base + static_cast<long long>(j) * B.n + q;
+        const bool v4 = cnt == 4 && B.vec;
+        float hq[4] = {0.f, 0.f, 0.f, 0.f}, gq[4] = {0.f, 0.f, 0.f, 0.f}, bq[4] = {0.f, 0.f, 0.f, 0.f};
+        if (v4) {
+            const float4 h4 = __ldcg(reinterpret_cast<const float4*>(ph + e));
+            const float4 b4 = __ldcg(reinterpret_cast<const float4*>(gbar + e));
+            const float4 g4 = noef ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldcg(reinterpret_cast<const float4*>(pg + e));
+            hq[0] = h4.x; hq[1] = h4.y; hq[2] = h4.z; hq[3] = h4.w;
+            bq[0] = b4.x; bq[1] = b4.y; bq[2] = b4.z; bq[3] = b4.w;
+            gq[0] = g4.x; gq[1] = g4.y; gq[2] = g4.z; gq[3] = g4.w;
+        } else {   // unaligned rows, the short last row
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                if (kk < cnt) {
+                    hq[kk] = __ldcg(ph + e + kk);
+                    bq[kk] = __ldcg(gbar + e + kk);
+                    if (!noef) gq[kk] = __ldcg(pg + e + kk);
+                }
+        }
+        float gn[4], val[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const float c = kk < cnt ? wire_round(noef ? hq[kk] : fsub(hq[kk], gq[kk]), T.bf16) : 0.0f;   // C (R25; +0 padding)
+            gn[kk] = fadd(gq[kk], c);                                                          // R12
+            val[kk] = kk < cnt ? (pow2 ? fmul(c, invN) : __fdiv_rn(c, a.Nf)) : 0.0f;           // A / N, R3
+            bq[kk] = fadd(bq[kk], val[kk]);                                                    // R13
+        }
+        if (v4) {
+            if (!noef) *reinterpret_cast<float4*>(pg + e) = make_float4(gn[0], gn[1], gn[2], gn[3]);
+            *reinterpret_cast<float4*>(gbar + e) = make_float4(bq[0], bq[1], bq[2], bq[3]);
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                if (kk < cnt) {
+                    if (!noef) pg[e + kk] = gn[kk];
+                    gbar[e + kk] = bq[kk];
+                }
+        }
+        if (T.values != nullptr) {
+            if (B.vec && ocnt == 4 && (o & 3) == 0) {
+                *reinterpret_cast<float4*>(T.values + o) = make_float4(val[0], val[1], val[2], val[3]);
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    if (kk < ocnt) T.values[o + kk] = val[kk];
+            }
+        }
+    }
+    if (T.stamps != nullptr && blockIdx.x == 0 && threadIdx.x == 0) T.stamps[5] = globaltimer_ns();
+}
+
 // The register path: the same per-segment arithmetic with the batch loaded
 // straight into registers (UN segments, 3 UN float4 per lane), warps streaming
 // their rows independently; V_b^T staged in shared memory as above.
 // RANGED: the launch over the blocks whose V_b^T does not fit the stage; V is
 // staged in ranges of whole 1024-column chunks and every row carries its P'
 // across ranges in shared memory (the O6 order is unchanged)
-template <int RJ, int UN, int MINB, bool NOEF, bool RANGED>
+template <int RJ, int UN, int MINB, bool NOEF, bool RANGED, bool TAIL>
 __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_ef_sketch(const SketchLaunch a) {
     constexpr int NT = RANGED ? wide_threads(RJ) : kThreads, NW = NT / 32;
     __shared__ TileDesc s_tile[kTileCache];
@@ -250,13 +533,23 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int list_begin = a.cta_begin[blockIdx.x], list_end = a.cta_begin[blockIdx.x + 1];
-    if (list_begin >= list_end) return;
+    if (list_begin >= list_end) {
+        if constexpr (TAIL) {   // (an idle CTA still counts, and draws its share of V)
+            grid_dependency_wait();
+            if (tail_arrive<NT>(a))
+                tail_select_update<NT>(a, s_hist, reinterpret_cast<int*>(s_tile), reinterpret_cast<unsigned*>(dyn));
+        }
+        return;
+    }
     const int ntile = list_end - list_begin;
     for (int i = tid; i < min(ntile, kTileCache) * 4; i += NT)
         reinterpret_cast<uint4*>(s_tile)[i] = __ldg(reinterpret_cast<const uint4*>(a.tiles + list_begin) + i);
     for (int i = tid; i < kHist1Bins; i += NT) s_hist[i] = 0;
     __syncthreads();
     grid_dependency_wait();   // the previous kernel (g, V, histogram reset) is complete
+    if constexpr (TAIL) {
+        if (a.tail.stamps != nullptr && blockIdx.x == 0 && tid == 0) a.tail.stamps[0] = globaltimer_ns();
+    }
 
     const int r = a.r;
     const float eta = a.eta, ome = a.ome;
@@ -508,18 +801,22 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
         __syncthreads();
         flush_hist(cur_b);
     }
+    if constexpr (TAIL) {
+        if (tail_arrive<NT>(a))
+            tail_select_update<NT>(a, s_hist, reinterpret_cast<int*>(s_tile), reinterpret_cast<unsigned*>(dyn));
+    }
 }
 
-template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false>
+template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false, bool TAIL = false>
 void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(a.grid);
     cfg.blockDim = dim3(RANGED ? wide_threads(RJ) : kThreads);
-    cfg.dynamicSmemBytes = sizeof(float) * a.vs_cap;
+    cfg.dynamicSmemBytes = sizeof(float) * (TAIL && a.tail.key_cap > a.vs_cap ? a.tail.key_cap : a.vs_cap);
     cfg.stream = s;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sizeof(float) * (RANGED ? kVsBig : kVsMax)));
         attr_set = true;
     }
@@ -528,14 +825,14 @@ void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, a);
+    cudaLaunchKernelEx(&cfg, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED, TAIL>, a);
 }
-template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false>
+template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false, bool TAIL = false>
 int occupancy_reg(int vs_cap) {
-    cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(float) * (RANGED ? kVsBig : kVsMax)));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED, TAIL>,
                                                   RANGED ? wide_threads(RJ) : kThreads, sizeof(float) * vs_cap);
     return per_sm;
 }
@@ -549,6 +846,14 @@ void launch_rj(const SketchLaunch& a, cudaStream_t s) {
         if (a.noef) launch_reg<RJ, wide_un(RJ), 1, true, true>(a, s);
         else launch_reg<RJ, wide_un(RJ), 1, false, true>(a, s);
         return;
+    }
+    if constexpr (RJ <= 8) {   // the fused small-problem tail (r <= 8): shapes 0 and 2 (the chosen ones)
+        if (a.tail.done != nullptr) {
+            if (a.noef) launch_reg<RJ, 3, 3, true, false, true>(a, s);
+            else if (a.shape == 2) launch_reg<RJ, 4, 2, false, false, true>(a, s);
+            else launch_reg<RJ, 3, 3, false, false, true>(a, s);
+            return;
+        }
     }
     if (a.noef) {   // (the without-EF baseline: one variant)
         launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2), true>(a, s);
@@ -572,6 +877,21 @@ int occupancy_rj(int shape, int vs_cap) {
 }
 
 }  // namespace
+
+void launch_tail_update(const SketchLaunch& a, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    const long long ctas = (a.tail.quads + 255) / 256;
+    cfg.gridDim = dim3(static_cast<unsigned>(ctas < 1 ? 1 : ctas > 1184 ? 1184 : ctas));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k_tail_update, a);
+}
 
 int sketch_tile_rows(int) { return 32; }   // (plan_tiles takes 8 for small single-block layouts)
 int sketch_tile_cols(int) { return 128; }

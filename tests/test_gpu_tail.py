@@ -1,0 +1,140 @@
+"""GPU parity of the fused small-problem tail (arc_sketch.cu).
+
+With one node on the GPU, no exchange and a small selection (M <= 8192 ARC
+rows, sum K <= 2048, sum K n <= 32768, <= 8 ARC blocks, r <= 8), the LAST CTA
+of the streaming launch runs S3..S6 itself (a done counter, no grid barrier,
+no selection kernel).  ARC_TAIL (read at create) = 0 forces the selection
+kernel.  Both must give the oracle's result bit for bit: selection, values,
+h, g, gbar, V and Sigma over several steps (values requested on alternate
+steps), with ties, K = m blocks, DENSE blocks, ragged rows, the Rand-K and
+without-EF methods and the bf16 wire; at and just past the size limits.
+"""
+import numpy as np
+import pytest
+import torch
+
+from synth import Block, adversarial
+
+from test_gpu_parity import DEV, run_parity, _built  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+
+def _layout(shapes):
+    blocks, off = [], 0
+    for m, n, K, kind in shapes:
+        blocks.append(Block(off, m * n, m, n, K, kind))
+        off += m * n
+    return off, blocks
+
+
+LAYOUTS = {
+    "c5_1e6": [(977, 1024, 10, 0)],                              # C5 d = 1e6 shape (shape-2 launch)
+    "c3_rows": [(131, 768, 13, 0)],                              # n = 768 (shape-0 launch)
+    "one_row": [(1, 64, 1, 0)],
+    "k_eq_m": [(64, 16, 64, 0)],                                 # identity block
+    "blocks_and_dense": [(300, 33, 9, 0), (40, 100, 40, 1), (700, 8, 3, 0), (513, 5, 512, 0)],
+    "eight_blocks": [(100 + 37 * i, 16 + 8 * i, 3 + i, 0) for i in range(8)],
+    "max_rows": [(8192, 4 * 8, 1024, 0)],                        # M and sum K n at the limits
+    "past_rows": [(8193, 8, 100, 0)],                            # M past the limit: selection kernel
+    "past_kn": [(600, 64, 513, 0)],                              # sum K n past the limit: selection kernel
+}
+TAILED = {"c5_1e6", "c3_rows", "one_row", "k_eq_m", "blocks_and_dense", "eight_blocks", "max_rows"}
+
+
+def _plan(d, blocks):
+    """ARC_Q_PLAN: [selection form (2 = the fused tail), selection CTAs, S1 launches, kernels per step]."""
+    from paper_2510_26709_b200 import ArcTopK, _lib
+    ctx = ArcTopK(d, blocks, N=1, eta=0.1, r=4, seed=5, nodes_local=1)
+    plan = ctx.query(_lib.Q_PLAN).cpu().tolist()
+    ctx.close()
+    return plan
+
+
+@pytest.mark.parametrize("name", sorted(LAYOUTS))
+@pytest.mark.parametrize("tail", ["1", "0"])
+def test_tail_parity(orc, monkeypatch, name, tail):
+    monkeypatch.setenv("ARC_TAIL", tail)
+    d, blocks = _layout(LAYOUTS[name])
+    run_parity(orc, d, blocks, N=1, steps=5)
+
+
+def test_tail_is_taken_exactly_where_eligible(monkeypatch):
+    """ARC_TAIL=1 takes the tail exactly on the eligible layouts; ARC_TAIL=0 never.  The tail's
+    step is the streaming launch + the update kernel (the same count as with the selection kernel)."""
+    for name, shapes in LAYOUTS.items():
+        d, blocks = _layout(shapes)
+        monkeypatch.setenv("ARC_TAIL", "1")
+        on = _plan(d, blocks)
+        monkeypatch.setenv("ARC_TAIL", "0")
+        off = _plan(d, blocks)
+        assert (on[0] == 2) == (name in TAILED), (name, on)
+        assert off[0] in (0, 1), (name, off)
+        assert on[3] == off[3], (name, on, off)
+        if name in TAILED:
+            assert on[1] == 1 and on[2] == 1, (name, on)
+
+
+@pytest.mark.parametrize("kind", ["dup_rows", "zeros", "nonfinite", "huge", "small_int", "subnormal"])
+def test_tail_ties_and_nonfinite(orc, monkeypatch, kind):
+    monkeypatch.setenv("ARC_TAIL", "1")
+    d, blocks = _layout([(2000, 32, 300, 0)])
+    run_parity(orc, d, blocks, N=1, steps=3, grads_fn=lambda t: adversarial(kind, d, 1, seed=t, n=32))
+
+
+@pytest.mark.parametrize("method", ["randk", "noef_msgd"])
+@pytest.mark.parametrize("name", ["c5_1e6", "blocks_and_dense"])
+def test_tail_methods(orc, monkeypatch, method, name):
+    monkeypatch.setenv("ARC_TAIL", "1")
+    d, blocks = _layout(LAYOUTS[name])
+    run_parity(orc, d, blocks, N=1, steps=4, method=method, check_debug=False)
+
+
+@pytest.mark.parametrize("name", ["c5_1e6", "blocks_and_dense"])
+def test_tail_bf16_wire(orc, monkeypatch, name):
+    monkeypatch.setenv("ARC_TAIL", "1")
+    d, blocks = _layout(LAYOUTS[name])
+    run_parity(orc, d, blocks, N=1, steps=4, wire="bf16")
+
+
+def test_tail_non_consecutive_t(orc, monkeypatch):
+    """The speculative V of t + 1 drawn by the streaming launch is used only when the next t matches."""
+    monkeypatch.setenv("ARC_TAIL", "1")
+    d, blocks = _layout(LAYOUTS["c5_1e6"])
+    run_parity(orc, d, blocks, N=1, ts=[0, 1, 2, 5, 6, 9, 3])
+
+
+@pytest.mark.parametrize("r", [1, 3, 8])
+def test_tail_sketch_widths(orc, monkeypatch, r):
+    monkeypatch.setenv("ARC_TAIL", "1")
+    d, blocks = _layout(LAYOUTS["blocks_and_dense"])
+    run_parity(orc, d, blocks, N=1, steps=3, r=r)
+
+
+def test_tail_graph_replays(orc, monkeypatch):
+    """A captured step (device iteration counter) replayed 4 times equals 4 oracle steps: the
+    done counter returns to zero and t advances inside the tail."""
+    from paper_2510_26709_b200 import ArcTopK
+    from synth import GradientSource
+    monkeypatch.setenv("ARC_TAIL", "1")
+    d, blocks = _layout(LAYOUTS["c5_1e6"])
+    src = GradientSource(d, blocks, 1, seed=9)
+    ctx = ArcTopK(d, blocks, N=1, eta=0.1, r=4, seed=9, nodes_local=1, device_t=True)
+    o = orc.OracleEF21M(d, blocks, N=1, eta=0.1, r=4, seed=9)
+    h, g, gbar = (torch.zeros(d, device=DEV) for _ in range(3))
+    grad = torch.zeros(d, device=DEV)
+    sel = torch.empty(ctx.sum_K, dtype=torch.int32, device=DEV)
+    graph = ctx.capture([grad], [h], [g], gbar, sel, None)
+    ctx.set_iteration(0)
+    torch.cuda.synchronize()
+    for t in range(4):
+        gr = src.grads(t)[0]
+        grad.copy_(gr.to(DEV))
+        graph.replay()
+        ref = o.step(t, [gr.numpy()])
+        torch.cuda.synchronize()
+        assert np.array_equal(sel.cpu().numpy(), ref["sel"]), t
+    assert h.cpu().numpy().tobytes() == o.h[0].tobytes()
+    assert g.cpu().numpy().tobytes() == o.g[0].tobytes()
+    assert gbar.cpu().numpy().tobytes() == o.gbar.tobytes()
+    ctx.close()
