@@ -64,6 +64,9 @@ __device__ __forceinline__ int row_cols(long long len, int n, int p) {
 #ifndef ARC_SK_ST
 #define ARC_SK_ST 0
 #endif
+#ifndef ARC_SK_FAST   // predicate-free loop for full aligned rows in the 4-segment variant (A/B knob)
+#define ARC_SK_FAST 1
+#endif
 template <int POL>
 __device__ __forceinline__ float4 sk_ld4p(const float* p) {
     if constexpr (POL == 1) {
@@ -757,6 +760,58 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
             float acc[RJ], P[RJ];
 #pragma unroll
             for (int j = 0; j < RJ; ++j) { acc[j] = 0.0f; P[j] = 0.0f; }
+            // Full rows of whole 128-column segments, 16-byte aligned, V_b^T staged,
+            // r == RJ: the same O6 arithmetic with no per-element predicates.  Only in
+            // the 4-segment / 2-CTA variant (128 registers): C2 sketch 36.9 -> 33.4 us,
+            // C5 d = 1e8 -1 %; in the 80-register variant (C3) it spilled: +3 % (fast
+            // path alone) / +32 % (both paths) (profiles/r02_sketch_fastpath.txt)
+            if constexpr (ARC_SK_FAST && !NOEF && !RANGED && !TAIL && RJ == 4 && UN == 4 && MINB == 2) {
+            if (sketch && v_smem && T_vec && r == RJ && nv == T_n && (T_n & 127) == 0) {
+                const int ldv4 = T_n >> 2;
+                const float4* __restrict__ V4 = reinterpret_cast<const float4*>(Vs);
+                for (int k0 = 0; k0 < nseg; k0 += UN) {
+                    float4 xg[UN], xh[UN], xd[UN];
+#pragma unroll
+                    for (int u = 0; u < UN; ++u) {
+                        if (k0 + u < nseg) {
+                            const long long e = base + 128 * (k0 + u) + 4 * lane;
+                            xg[u] = sk_ld4g(pg + e);
+                            xh[u] = sk_ld4(ph + e);
+                            xd[u] = sk_ld4(pgg + e);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < UN; ++u) {
+                        const int k = k0 + u;
+                        if (k >= nseg) break;
+                        const int q4 = 32 * k + lane;   // quad index of columns q .. q + 3
+                        const float hn0 = ffma(eta, xg[u].x, fmul(ome, xh[u].x)), hn1 = ffma(eta, xg[u].y, fmul(ome, xh[u].y));
+                        const float hn2 = ffma(eta, xg[u].z, fmul(ome, xh[u].z)), hn3 = ffma(eta, xg[u].w, fmul(ome, xh[u].w));
+                        sk_st4(ph + base + 4 * q4, make_float4(hn0, hn1, hn2, hn3));                  // O2, R11
+                        const float d0 = fsub(hn0, xd[u].x), d1 = fsub(hn1, xd[u].y);                // O3, R4
+                        const float d2 = fsub(hn2, xd[u].z), d3 = fsub(hn3, xd[u].w);
+#pragma unroll
+                        for (int j = 0; j < RJ; ++j) {
+                            const float4 v = V4[j * ldv4 + q4];
+                            acc[j] = ffma(d0, v.x, acc[j]);                                      // O6
+                            acc[j] = ffma(d1, v.y, acc[j]);
+                            acc[j] = ffma(d2, v.z, acc[j]);
+                            acc[j] = ffma(d3, v.w, acc[j]);
+                        }
+                        if ((k & 7) == 7 || k == nseg - 1) {                                       // end of a 1024-column chunk
+#pragma unroll
+                            for (int j = 0; j < RJ; ++j) {
+                                const float w = butterfly(acc[j]);
+                                P[j] = (k < 8) ? w : fadd(P[j], w);
+                                acc[j] = 0.0f;
+                            }
+                        }
+                    }
+                }
+                row_epilogue<RJ>(a, p, T_row_base, T_b, node, lane, r, P, s_hist);
+                continue;
+            }
+            }
             for (int k0 = 0; k0 < nseg; k0 += UN) {
                 float4 xg[UN], xh[UN], xd[UN];
 #pragma unroll
