@@ -788,8 +788,31 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
                 c->vs_cap = std::max(c->vs_cap, cap);
             }
         }
-        plan_tiles(c->pl, narrow, ef_sketch_resident_ctas(c->p.r, c->shape, c->vs_cap), sketch_tile_rows(c->shape),
-                   sketch_tile_cols(c->shape), tiles, cta_begin, c->grid);
+        {   // the fused small-problem tail (arc_sketch.cu): S3 in the streaming launch's
+            // last CTA (+ S4..S6 in a small update kernel) when the GPU holds the one node,
+            // there is no exchange and every ARC block's keys fit that CTA's shared memory
+            // (ARC_TAIL=0: off, the selection kernel instead)
+            const Plan& P = c->pl;
+            int arc_blocks = 0, max_m = 0;
+            for (const BlockDev& B : P.bdev)
+                if (B.kind == ARC_BLOCK_ARC) {
+                    ++arc_blocks;
+                    max_m = std::max(max_m, B.m);
+                }
+            bool on = true;
+            if (const char* e = getenv("ARC_TAIL")) on = e[0] != '0';
+            const int r_eff = P.randk ? 1 : c->p.r;
+            c->tail = on && !P.exchange && P.L == 1 && c->p.N == 1 && !P.topk && !P.exact && !any_wide && !any_tma &&
+                      r_eff <= 8 && arc_blocks >= 1 && arc_blocks <= kTailMaxBlocks && max_m <= kTailMaxRows;
+            c->tail_keys = max_m;
+        }
+        // (the tail's launch may stage more shared memory than V_b^T: its keys)
+        const int resident = c->tail ? ef_sketch_resident_ctas_tail(c->p.r, c->shape, c->pl.noef,
+                                                                    std::max(c->vs_cap, c->tail_keys))
+                                     : ef_sketch_resident_ctas(c->p.r, c->shape, c->vs_cap);
+        plan_tiles(c->pl, narrow, resident, sketch_tile_rows(c->shape), sketch_tile_cols(c->shape), tiles, cta_begin,
+                   c->grid);
+        if (c->grid <= 0) c->tail = false;
         c->grid_w = 0;
         if (any_wide) {
             // shared memory: the widest fully staged V_b^T, or the range stage
@@ -840,27 +863,6 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
         D.row_base = B.row_base;
         D.b = tiles[i].b;
         D.node = tiles[i].node;
-    }
-    {   // the fused small-problem tail (arc_sketch.cu): S3..S6 in the streaming launch's
-        // last CTA when the GPU holds the one node, there is no exchange and the
-        // selection is small (ARC_TAIL=0: off, the selection kernel instead)
-        const Plan& P = c->pl;
-        int arc_blocks = 0, max_m = 0;
-        int64_t sk = 0, skn = 0;
-        for (const BlockDev& B : P.bdev)
-            if (B.kind == ARC_BLOCK_ARC) {
-                ++arc_blocks;
-                max_m = std::max(max_m, B.m);
-                sk += B.K;
-                skn += static_cast<int64_t>(B.K) * B.n;
-            }
-        bool on = true;
-        if (const char* e = getenv("ARC_TAIL")) on = e[0] != '0';
-        const int r_eff = P.randk ? 1 : c->p.r;
-        c->tail = on && !P.exchange && P.L == 1 && c->p.N == 1 && !P.topk && !P.exact && c->grid > 0 &&
-                  c->grid_w == 0 && c->grid_t == 0 && r_eff <= 8 && arc_blocks >= 1 &&
-                  arc_blocks <= kTailMaxBlocks && P.M <= kTailMaxRows && sk <= kTailMaxK && skn <= kTailMaxKn;
-        c->tail_keys = max_m;
     }
     const std::vector<SelRow>& rows = c->pl.segs;
 

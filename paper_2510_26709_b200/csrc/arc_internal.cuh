@@ -132,9 +132,9 @@ void launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s)
 // node on the GPU, no exchange and a small selection, the LAST CTA of the
 // streaming launch to finish (a done counter) runs S3..S6 itself — no second
 // launch, no grid barrier ("fused tail").
-constexpr int kTailMaxRows = 8192;      // M = sum m_b over the ARC blocks, at most
-constexpr int kTailMaxK = 2048;         // sum K_b (the selected rows, listed in shared memory)
-constexpr long long kTailMaxKn = 32768; // sum K_b n_b (the rows one CTA updates)
+constexpr int kTailMaxRows = 8192;      // the largest ARC block's rows: its keys in shared memory (32 KB)
+                                        // (C2 with one node, 22,831 rows, measured slower through the tail:
+                                        // 59.8 against 46.7 us per step, profiles/r02_tail.txt)
 constexpr int kTailMaxBlocks = 8;       // ARC blocks
 struct TailBlk {                    // an ARC block as the tail's update kernel reads it (kernel parameter)
     long long off, len, val_base;
@@ -194,6 +194,7 @@ void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s);
 // launch (programmatic dependent launch when a.pdl), waiting for it to complete.
 void launch_tail_update(const SketchLaunch& a, cudaStream_t s);
 int ef_sketch_resident_ctas(int r, int shape, int vs_cap);   // SMs x occupancy
+int ef_sketch_resident_ctas_tail(int r, int shape, bool noef, int dyn_floats);   // (the fused-tail variant)
 int sketch_vs_cap(int r, int max_n);   // floats of V_b^T the streaming pass stages in shared memory (0: too wide)
 int sketch_ranged_cap(int r);          // floats staged per range by the wide blocks' launch
 int ef_sketch_resident_ctas_ranged(int r, int vs_cap);

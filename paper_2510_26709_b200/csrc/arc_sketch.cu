@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "arc_device.cuh"
 #include "arc_internal.cuh"
@@ -252,8 +253,6 @@ __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int r
 // rows with the arithmetic of gather_rows_local (one node on this GPU, N = 1:
 // C = h' - g [R25 rounding], g <- g + C, gbar <- gbar + C / N, R3, R12, R13).
 // No grid barrier, no second launch: nothing waits on another CTA.
-__device__ const float4 k_tail_zero4 = {0.f, 0.f, 0.f, 0.f};
-
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -277,11 +276,12 @@ __device__ __forceinline__ bool tail_arrive(const SketchLaunch& a) {
 }
 
 template <int NT>
-__device__ void tail_select_update(const SketchLaunch& a, unsigned* sh, int* s_list, unsigned* s_keys) {
+__device__ void tail_select(const SketchLaunch& a, unsigned* sh, unsigned* s_keys) {
     __shared__ int warp_sums[32];
     __shared__ unsigned s_dig;
     __shared__ int s_abv, s_cnt;
-    constexpr int kTailCand = kHist1Bins / 2;   // boundary-bin keys ranked directly (sh holds keys | rows)
+    constexpr int kTailCand = 256;   // boundary-bin keys ranked directly, O(E^2) (sh holds keys | rows);
+                                     // a more crowded bin takes the two histogram passes
     const int tid = threadIdx.x;
     const TailArgs& T = a.tail;
 #define TAIL_STAMP(k) \
@@ -297,24 +297,31 @@ __device__ void tail_select_update(const SketchLaunch& a, unsigned* sh, int* s_l
         __syncthreads();                                     // (sh, s_keys of the previous block)
         // the block's digit-1 histogram and order keys (R15): every load of a
         // batch in flight before the first is used (one L2 round trip per batch)
-        const float* __restrict__ sg = a.sigma + B.row_base;
         unsigned* gh = a.hist1 + static_cast<long long>(b) * kHist1Bins;
         {
             constexpr int HB = kHist1Bins / NT;
             unsigned hv[HB];
 #pragma unroll
             for (int k = 0; k < HB; ++k) hv[k] = __ldcg(gh + tid + k * NT);
-            for (int i0 = 0; i0 < m; i0 += 8 * NT) {
-                float v[8];
+            // 16-byte loads of the aligned superset [row_base & ~3, row_base + m) (the
+            // Sigma buffer is 256-byte aligned and padded), 8 per thread per round trip
+            const int a0 = B.row_base & 3;
+            const float4* __restrict__ s4 = reinterpret_cast<const float4*>(a.sigma + (B.row_base - a0));
+            const int nq = (m + a0 + 3) >> 2;
+            for (int i0 = 0; i0 < nq; i0 += 8 * NT) {
+                float4 v[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int i = i0 + u * NT + tid;
-                    v[u] = i < m ? __ldcg(sg + i) : 0.0f;
+                    v[u] = i < nq ? __ldcg(s4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int i = i0 + u * NT + tid;
-                    if (i < m) s_keys[i] = order_key_dev(v[u]);
+                    const int i = 4 * (i0 + u * NT + tid) - a0;   // block row of v[u].x
+                    const float w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (i + k >= 0 && i + k < m) s_keys[i + k] = order_key_dev(w[k]);   // R15
                 }
             }
 #pragma unroll
@@ -403,7 +410,6 @@ __device__ void tail_select_update(const SketchLaunch& a, unsigned* sh, int* s_l
                 const unsigned k = s_keys[i];
                 if (k > Tk || (k == Tk && i <= Peq)) {
                     T.sel[sel_base + pos] = i;
-                    s_list[sel_base + pos] = i;
                     ++pos;
                 }
             }
@@ -423,7 +429,6 @@ __device__ void tail_select_update(const SketchLaunch& a, unsigned* sh, int* s_l
                 if (k == Tk) take = eq_seen++ < need_eq;
                 if (take) {
                     T.sel[sel_base + pos] = i;
-                    s_list[sel_base + pos] = i;
                     ++pos;
                 }
             }
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
         if constexpr (TAIL) {   // (an idle CTA still counts, and draws its share of V)
             grid_dependency_wait();
             if (tail_arrive<NT>(a))
-                tail_select_update<NT>(a, s_hist, reinterpret_cast<int*>(s_tile), reinterpret_cast<unsigned*>(dyn));
+                tail_select<NT>(a, s_hist, reinterpret_cast<unsigned*>(dyn));
         }
         return;
     }
@@ -858,8 +863,15 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
     }
     if constexpr (TAIL) {
         if (tail_arrive<NT>(a))
-            tail_select_update<NT>(a, s_hist, reinterpret_cast<int*>(s_tile), reinterpret_cast<unsigned*>(dyn));
+            tail_select<NT>(a, s_hist, reinterpret_cast<unsigned*>(dyn));
     }
+}
+
+// dynamic shared memory (floats) a variant may request: V_b^T (RANGED: the wide stage), or
+// for the fused tail also the keys of one ARC block
+template <bool RANGED, bool TAIL>
+constexpr int dyn_max() {
+    return RANGED ? kVsBig : (TAIL && kTailMaxRows > kVsMax ? kTailMaxRows : kVsMax);
 }
 
 template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false, bool TAIL = false>
@@ -872,7 +884,7 @@ void launch_reg(const SketchLaunch& a, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sizeof(float) * (RANGED ? kVsBig : kVsMax)));
+                             static_cast<int>(sizeof(float) * dyn_max<RANGED, TAIL>()));
         attr_set = true;
     }
     cudaLaunchAttribute attr[1];
@@ -885,7 +897,7 @@ void launch_reg(const SketchLaunch& a, cudaStream_t s) {
 template <int RJ, int UN, int MINB, bool NOEF = false, bool RANGED = false, bool TAIL = false>
 int occupancy_reg(int vs_cap) {
     cudaFuncSetAttribute(k_ef_sketch<RJ, UN, MINB, NOEF, RANGED, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(float) * (RANGED ? kVsBig : kVsMax)));
+                         static_cast<int>(sizeof(float) * dyn_max<RANGED, TAIL>()));
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ef_sketch<RJ, UN, MINB, NOEF, RANGED, TAIL>,
                                                   RANGED ? wide_threads(RJ) : kThreads, sizeof(float) * vs_cap);
@@ -977,6 +989,20 @@ int ef_sketch_resident_ctas_ranged(int r, int vs_cap) {
                        : r <= 8 ? occupancy_reg<8, wide_un(8), 1, false, true>(vs_cap)
                        : r <= 16 ? occupancy_reg<16, wide_un(16), 1, false, true>(vs_cap)
                                  : occupancy_reg<32, wide_un(32), 1, false, true>(vs_cap);
+    return sms * (per_sm < 1 ? 1 : per_sm);
+}
+
+int ef_sketch_resident_ctas_tail(int r, int shape, bool noef, int dyn_floats) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    auto occ = [&](auto rj) {   // the instantiation launch_rj takes for the tail
+        constexpr int RJ = decltype(rj)::value;
+        if (noef) return occupancy_reg<RJ, 3, 3, true, false, true>(dyn_floats);
+        if (shape == 2) return occupancy_reg<RJ, 4, 2, false, false, true>(dyn_floats);
+        return occupancy_reg<RJ, 3, 3, false, false, true>(dyn_floats);
+    };
+    const int per_sm = r <= 4 ? occ(std::integral_constant<int, 4>{}) : occ(std::integral_constant<int, 8>{});
     return sms * (per_sm < 1 ? 1 : per_sm);
 }
 

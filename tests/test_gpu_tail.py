@@ -1,9 +1,9 @@
 """GPU parity of the fused small-problem tail (arc_sketch.cu).
 
-With one node on the GPU, no exchange and a small selection (M <= 8192 ARC
-rows, sum K <= 2048, sum K n <= 32768, <= 8 ARC blocks, r <= 8), the LAST CTA
-of the streaming launch runs S3..S6 itself (a done counter, no grid barrier,
-no selection kernel).  ARC_TAIL (read at create) = 0 forces the selection
+With one node on the GPU, no exchange and a small selection (every ARC block
+of at most 8,192 rows, at most 8 ARC blocks, r <= 8), the LAST CTA of the
+streaming launch runs S3 itself (a done counter, no grid barrier, no selection
+kernel) and a small kernel launched behind it runs S4..S6.  ARC_TAIL (read at create) = 0 forces the selection
 kernel.  Both must give the oracle's result bit for bit: selection, values,
 h, g, gbar, V and Sigma over several steps (values requested on alternate
 steps), with ties, K = m blocks, DENSE blocks, ragged rows, the Rand-K and
@@ -31,15 +31,20 @@ def _layout(shapes):
 LAYOUTS = {
     "c5_1e6": [(977, 1024, 10, 0)],                              # C5 d = 1e6 shape (shape-2 launch)
     "c3_rows": [(131, 768, 13, 0)],                              # n = 768 (shape-0 launch)
+    "c2_one_node": [(22831, 512, 229, 0)],                       # C2 with one node: selection kernel
     "one_row": [(1, 64, 1, 0)],
     "k_eq_m": [(64, 16, 64, 0)],                                 # identity block
     "blocks_and_dense": [(300, 33, 9, 0), (40, 100, 40, 1), (700, 8, 3, 0), (513, 5, 512, 0)],
     "eight_blocks": [(100 + 37 * i, 16 + 8 * i, 3 + i, 0) for i in range(8)],
-    "max_rows": [(8192, 4 * 8, 1024, 0)],                        # M and sum K n at the limits
-    "past_rows": [(8193, 8, 100, 0)],                            # M past the limit: selection kernel
-    "past_kn": [(600, 64, 513, 0)],                              # sum K n past the limit: selection kernel
+    "nine_blocks": [(50 + 11 * i, 8, 2 + i, 0) for i in range(9)],   # one block too many: selection kernel
+    "max_rows": [(8192, 16, 1024, 0)],                           # the largest block at the key limit (32 KB)
+    "past_rows": [(8193, 8, 100, 0)],                            # one row more: selection kernel
+    "crowded_bin": [(8000, 8, 4000, 0)],                         # K = m / 2: a crowded boundary bin
+    "big_kn": [(600, 64, 513, 0)],                               # many selected rows (the update kernel)
+    "unaligned_base": [(37, 12, 5, 0), (301, 20, 30, 0)],        # second block's Sigma not 16-byte aligned
 }
-TAILED = {"c5_1e6", "c3_rows", "one_row", "k_eq_m", "blocks_and_dense", "eight_blocks", "max_rows"}
+TAILED = {"c5_1e6", "c3_rows", "crowded_bin", "one_row", "k_eq_m", "blocks_and_dense", "eight_blocks", "max_rows",
+          "big_kn", "unaligned_base"}
 
 
 def _plan(d, blocks):
