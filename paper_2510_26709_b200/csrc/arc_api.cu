@@ -747,6 +747,22 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
             waste4 += static_cast<double>(B.len) * (1.0 - nseg / (std::ceil(nseg / 4.0) * 4.0));
         }
         c->shape = waste4 <= waste3 ? 2 : 0;
+        {   // one node on this GPU, r <= 4, a few ARC blocks of full 16-byte-aligned rows of
+            // whole 128-column segments: 3 segments per batch at 2 CTAs/SM (128 registers)
+            // with the predicate-free loop (profiles/r02_sketch_shape5.txt: C3 step -1.6 %,
+            // sketch at the measured HBM peak; C5 d = 1e9 -1.8 %; C2 one node equal; C4's
+            // 171 blocks +1.4 % and several local nodes +7 % keep the rule above)
+            // (layouts small enough for the fused tail keep its measured variant)
+            int nb = 0, max_m = 0;
+            bool full = c->pl.L == 1 && c->p.r <= 4 && !c->pl.topk && !c->pl.randk && !c->pl.noef;
+            for (const BlockDev& B : c->pl.bdev) {
+                if (B.kind != ARC_BLOCK_ARC) continue;
+                ++nb;
+                max_m = std::max(max_m, B.m);
+                full = full && B.vec && B.n % 128 == 0;
+            }
+            if (full && nb >= 1 && nb <= 8 && max_m > kTailMaxRows) c->shape = 5;
+        }
         if (const char* e = getenv("ARC_SKETCH_SHAPE")) {
             const int v = atoi(e);
             if (sketch_shape_ok(v, c->p.r)) c->shape = v;

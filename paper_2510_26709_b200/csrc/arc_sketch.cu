@@ -770,7 +770,7 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
             // the 4-segment / 2-CTA variant (128 registers): C2 sketch 36.9 -> 33.4 us,
             // C5 d = 1e8 -1 %; in the 80-register variant (C3) it spilled: +3 % (fast
             // path alone) / +32 % (both paths) (profiles/r02_sketch_fastpath.txt)
-            if constexpr (ARC_SK_FAST && !NOEF && !RANGED && !TAIL && RJ == 4 && UN == 4 && MINB == 2) {
+            if constexpr (ARC_SK_FAST && !NOEF && !RANGED && !TAIL && RJ == 4 && (UN == 4 || UN == 3) && MINB == 2) {
             if (sketch && v_smem && T_vec && r == RJ && nv == T_n && (T_n & 127) == 0) {
                 const int ldv4 = T_n >> 2;
                 const float4* __restrict__ V4 = reinterpret_cast<const float4*>(Vs);
@@ -905,8 +905,9 @@ int occupancy_reg(int vs_cap) {
 }
 
 // variant (a.shape): UN segments per batch / CTAs per SM: 0 = 3 / 3, 1 = 2 / 4,
-// 2 = 4 / 2, 3 = 6 / 2 (r <= 8; wider sketches get fewer CTAs).  0 and 2 are chosen per
-// layout (arc_api.cu); 1 and 3 measured no better (C3: 3 / 3 325.7 us, 6 / 2 326.3 us)
+// 2 = 4 / 2, 3 = 6 / 2 (r <= 8; wider sketches get fewer CTAs), 5 = 3 / 2 (with the
+// predicate-free loop).  0, 2 and 5 are chosen per layout (arc_api.cu); 1 and 3 measured
+// no better (C3: 3 / 3 325.7 us, 6 / 2 326.3 us)
 template <int RJ>
 void launch_rj(const SketchLaunch& a, cudaStream_t s) {
     if (a.ranged) {   // the wide blocks' launch (one variant)
@@ -928,6 +929,7 @@ void launch_rj(const SketchLaunch& a, cudaStream_t s) {
     }
     switch (a.shape) {
         case 1: launch_reg<RJ, 2, (RJ <= 8 ? 4 : 2)>(a, s); break;
+        case 5: launch_reg<RJ, 3, 2>(a, s); break;
         case 2: launch_reg<RJ, 4, 2>(a, s); break;
         case 3: launch_reg<RJ, (RJ <= 8 ? 6 : 2), 2>(a, s); break;
         default: launch_reg<RJ, 3, (RJ <= 8 ? 3 : 2)>(a, s); break;
@@ -937,6 +939,7 @@ template <int RJ>
 int occupancy_rj(int shape, int vs_cap) {
     switch (shape) {
         case 1: return occupancy_reg<RJ, 2, (RJ <= 8 ? 4 : 2)>(vs_cap);
+        case 5: return occupancy_reg<RJ, 3, 2>(vs_cap);
         case 2: return occupancy_reg<RJ, 4, 2>(vs_cap);
         case 3: return occupancy_reg<RJ, (RJ <= 8 ? 6 : 2), 2>(vs_cap);
         default: return occupancy_reg<RJ, 3, (RJ <= 8 ? 3 : 2)>(vs_cap);
@@ -962,7 +965,7 @@ void launch_tail_update(const SketchLaunch& a, cudaStream_t s) {
 
 int sketch_tile_rows(int) { return 32; }   // (plan_tiles takes 8 for small single-block layouts)
 int sketch_tile_cols(int) { return 128; }
-int sketch_shape_ok(int shape, int) { return shape >= 0 && shape <= 3; }
+int sketch_shape_ok(int shape, int) { return shape >= 0 && shape <= 3 || shape == 5; }
 
 void launch_ef_sketch(const SketchLaunch& a, cudaStream_t s) {
     // Top-K baseline and Rand-K need no sketch columns
