@@ -829,6 +829,7 @@ arc_status arc_topk_create(const arc_topk_params* params_in, void* nccl_comm, vo
         plan_tiles(c->pl, narrow, resident, sketch_tile_rows(c->shape), sketch_tile_cols(c->shape), tiles, cta_begin,
                    c->grid);
         if (c->grid <= 0) c->tail = false;
+
         c->grid_w = 0;
         if (any_wide) {
             // shared memory: the widest fully staged V_b^T, or the range stage
@@ -1075,6 +1076,8 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
                 ta.tn_lo = static_cast<unsigned>(tn);
                 ta.tn_hi = static_cast<unsigned>(tn >> 32);
             }
+            ta.last_cta = status + 3;
+            ta.sk_grid = c->grid;
         }
         if (c->grid > 0) {
             launch_ef_sketch(a, s);

@@ -151,6 +151,8 @@ struct TailArgs {
     float* V_next;                  // speculative S0 of the next step (nullptr: none), drawn by every CTA
     long long v_items;
     unsigned tn_lo, tn_hi;
+    unsigned* last_cta;             // the last CTA's index (its V_next items are drawn by k_tail_update)
+    int sk_grid;                    // the streaming launch's grid
     int key_cap;                    // floats of dynamic shared memory (keys of one block, m_b <= key_cap)
     unsigned long long* stamps;     // debug (ARC_DEBUG_STAMPS=1): %globaltimer at the tail's phases, or nullptr
     int nblk;                       // ARC blocks (<= kTailMaxBlocks) and their update table

@@ -239,9 +239,9 @@ __device__ __forceinline__ void row_epilogue(const SketchLaunch& a, int p, int r
 }
 
 // ---- the fused small-problem tail: S3..S6 in the last CTA ------
-// Every CTA, after its tiles, draws its share of the next step's V (S0,
-// speculative; V depends only on (seed, t, b)), fences its writes and
-// increments the done counter once.  The CTA that brings the counter to the
+// Every CTA, after its tiles, fences its writes and increments the done
+// counter once (then draws its share of the next step's V, off the critical
+// path).  The CTA that brings the counter to the
 // grid size has every other CTA's Sigma rows and digit-1 histogram bins
 // visible, and runs the selection of k_select_gather on keys held in shared
 // memory: per ARC block, the boundary digit 1 from the complete histogram,
@@ -263,16 +263,30 @@ template <int NT>
 __device__ __forceinline__ bool tail_arrive(const SketchLaunch& a) {
     __shared__ unsigned s_last;
     const TailArgs& T = a.tail;
-    if (T.V_next != nullptr)   // (item i on CTA i mod grid: a few items per CTA, none on the critical path)
-        for (long long i = threadIdx.x * static_cast<long long>(gridDim.x) + blockIdx.x; i < T.v_items;
-             i += static_cast<long long>(gridDim.x) * NT)
-            rng::gen_V_item(a.blocks, a.num_blocks, a.r, a.key, T.tn_lo, T.tn_hi, i, T.V_next);
-    __threadfence();   // this thread's Sigma, histogram, h' and V writes, before the CTA's increment
+    __threadfence();   // this thread's Sigma, histogram and h' writes, before the CTA's increment
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(T.done, 1u) == gridDim.x - 1 ? 1u : 0u;
     __syncthreads();
     if (s_last) __threadfence();
     return s_last != 0;
+}
+
+// The CTA's share of the next step's V (S0, speculative: V depends only on (seed, t, b)):
+// item i on CTA i mod grid, drawn AFTER the CTA's increment, off the path to the last
+// arrival.  The last CTA leaves its items to k_tail_update (it records its index), so
+// they do not delay the grid's completion either; the kernels that read V_next wait
+// for both grids.
+template <int NT>
+__device__ __forceinline__ void tail_next_V(const SketchLaunch& a, bool last) {
+    const TailArgs& T = a.tail;
+    if (T.V_next == nullptr) return;
+    if (last) {
+        if (threadIdx.x == 0) *T.last_cta = blockIdx.x;
+        return;
+    }
+    for (long long i = threadIdx.x * static_cast<long long>(gridDim.x) + blockIdx.x; i < T.v_items;
+         i += static_cast<long long>(gridDim.x) * NT)
+        rng::gen_V_item(a.blocks, a.num_blocks, a.r, a.key, T.tn_lo, T.tn_hi, i, T.V_next);
 }
 
 template <int NT>
@@ -463,6 +477,11 @@ __global__ void __launch_bounds__(256) k_tail_update(const SketchLaunch a) {
     const float* __restrict__ ph = noef ? a.nodes.grad[0] : a.nodes.h[0];   // (without EF: C = the gradient rows)
     float* __restrict__ pg = a.nodes.g[0];
     float* __restrict__ gbar = a.gbar;
+    if (T.V_next != nullptr) {   // the streaming launch's last CTA's share of V_next (see tail_next_V)
+        const long long g = T.sk_grid, last = __ldcg(T.last_cta), nt = gridDim.x * 256ll;
+        for (long long i = last + (nt - 1 - (blockIdx.x * 256ll + threadIdx.x)) * g; i < T.v_items; i += nt * g)
+            rng::gen_V_item(a.blocks, a.num_blocks, a.r, a.key, T.tn_lo, T.tn_hi, i, T.V_next);
+    }
     for (long long item = blockIdx.x * 256ll + threadIdx.x; item < T.quads; item += gridDim.x * 256ll) {
         int b = 0;
         while (b + 1 < T.nblk && item >= T.blk[b + 1].q_begin) ++b;
@@ -544,8 +563,9 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
     if (list_begin >= list_end) {
         if constexpr (TAIL) {   // (an idle CTA still counts, and draws its share of V)
             grid_dependency_wait();
-            if (tail_arrive<NT>(a))
-                tail_select<NT>(a, s_hist, reinterpret_cast<unsigned*>(dyn));
+            const bool last = tail_arrive<NT>(a);
+            if (last) tail_select<NT>(a, s_hist, reinterpret_cast<unsigned*>(dyn));
+            tail_next_V<NT>(a, last);
         }
         return;
     }
@@ -862,8 +882,9 @@ __global__ void __launch_bounds__(RANGED ? wide_threads(RJ) : kThreads, MINB) k_
         flush_hist(cur_b);
     }
     if constexpr (TAIL) {
-        if (tail_arrive<NT>(a))
-            tail_select<NT>(a, s_hist, reinterpret_cast<unsigned*>(dyn));
+        const bool last = tail_arrive<NT>(a);
+        if (last) tail_select<NT>(a, s_hist, reinterpret_cast<unsigned*>(dyn));
+        tail_next_V<NT>(a, last);
     }
 }
 
