@@ -233,3 +233,14 @@ def test_single_block_shorthand_and_wire_validation(L):
     half.wire = L.WIRE_BF16
     s_f, s_h = _ws(L, base)[1], _ws(L, half)[1]
     assert s_f - s_h >= (2 * 100 * 100 * 2 + 2 * 2 * 100 * 100 * 2) - 1024
+
+
+def test_query_kinds_match_the_header():
+    """The binding's query constants are the header's arc_query values (ARC_Q_PLAN included)."""
+    import re
+    from paper_2510_26709_b200 import _lib
+    hdr = open(os.path.join(ROOT, "include", "arc_topk.h")).read()
+    vals = {m.group(1): int(m.group(2)) for m in re.finditer(r"\bARC_Q_([A-Z_]+)\s*=\s*(\d+)", hdr)}
+    assert set(vals) >= {"V", "SIGMA", "SEL", "P_NODES", "S", "CANDIDATES", "PLAN"}
+    for name, v in vals.items():
+        assert getattr(_lib, "Q_" + name) == v, name
