@@ -42,6 +42,14 @@ LAYOUTS = {
     "crowded_bin": [(8000, 8, 4000, 0)],                         # K = m / 2: a crowded boundary bin
     "big_kn": [(600, 64, 513, 0)],                               # many selected rows (the update kernel)
     "unaligned_base": [(37, 12, 5, 0), (301, 20, 30, 0)],        # second block's Sigma not 16-byte aligned
+    # blocks streamed by the other launches -- the TMA-fed launch (unaligned rows, n >= 256),
+    # the ranged launch (V_b^T wider than the stage; n <= 4) -- take the selection kernel
+    # (a tail behind those launches measured no faster on C4's DDP buckets: profiles/r02_tail.txt)
+    "with_tma": [(300, 64, 9, 0), (200, 300, 5, 0)],
+    "with_wide": [(300, 64, 9, 0), (40, 4100, 3, 0)],
+    "with_n1": [(300, 64, 9, 0), (5000, 1, 50, 0)],
+    "llama_bucket": [(5461, 2048, 6, 0), (2048, 5461, 3, 0), (2048, 2048, 3, 0)],   # a C4 DDP bucket
+    "only_wide": [(40, 4100, 3, 0)],                             # no main-launch tile: selection kernel
 }
 TAILED = {"c5_1e6", "c3_rows", "crowded_bin", "one_row", "k_eq_m", "blocks_and_dense", "eight_blocks", "max_rows",
           "big_kn", "unaligned_base"}
