@@ -510,6 +510,14 @@ def measure(run: Runner, args, config: str, mu_bp, steps: int, warmup: int, *, e
                        "peak_source": peak_src, "launch_ms": sk_ms,
                        # also against the nominal HBM3e figure (HGX B200, 7.7 TB/s)
                        "nominal_peak": 7700.0, "nominal_frac": achieved / 7700.0}
+    # the selection kernel (the verdict's kernel furthest below its roofline): latency-bound;
+    # its algorithmic bytes are the selected rows' S4..S6 traffic plus its Sigma key reads
+    sel_ms = phase_ms.get("select_gather", 0.0)
+    if sel_ms > 0:
+        sel_bytes = ab["gather_ef"] + 4 * M
+        out["roofline_select"] = {"bound": "latency", "kernel": "k_select_gather", "algorithmic_bytes_per_launch": sel_bytes,
+                                  "launch_ms": sel_ms, "achieved": sel_bytes / (sel_ms * 1e-3) / 1e9, "peak": peak,
+                                  "unit": "GB/s", "frac": sel_bytes / (sel_ms * 1e-3) / 1e9 / peak}
     out["step_roofline"] = {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms, "hbm_bytes": ab["total"],
                             "nvlink_bus_bytes": bus["total"], "nvlink_peak_GBps": NVLINK_PEAK}
     # what each rank hands to the two exchanges per step (Table I's payloads)
@@ -807,6 +815,7 @@ def main():
                        "l2": "no flush: per-step inputs (16 B x d = %.1f GB) exceed the 126 MB L2" % (16 * d / 1e9),
                        "gradient_pool": head["gradient_pool"]},
             "roofline": head["roofline"],
+            "roofline_select": head.get("roofline_select"),
             "step_roofline": head["step_roofline"],
             "phases_ms": head["phases_ms"],
             "wire": head["wire"],
