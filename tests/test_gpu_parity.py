@@ -851,3 +851,24 @@ def test_exact_sketch_needs_all_nodes_local():
     blocks = flat_blocks(4096, 64, K=4)
     with pytest.raises(ArcError):
         ArcTopK(4096, blocks, N=2, eta=0.1, nodes_local=2, method="exact", force_exchange=True, device=DEV)
+
+
+# ------------------------------------------------------------------ streaming-pass variants (round 2)
+
+@pytest.mark.parametrize("shape", [None, "0", "2", "5"])
+@pytest.mark.parametrize("layout", [
+    [(9001, 768, 90)],                         # C3 row length, M past the fused tail's limit
+    [(8300, 1024, 83), (300, 512, 9)],         # two blocks of full 128-column segments
+])
+def test_streaming_variants_with_ragged_rows(orc, monkeypatch, shape, layout):
+    """Every streaming variant, including the predicate-free loop of variants 2 and 5 (full
+    aligned rows) next to the generic loop (the short last row of each block), bit-exact;
+    None = the variant the planner picks (5 for these one-node layouts)."""
+    if shape is not None:
+        monkeypatch.setenv("ARC_SKETCH_SHAPE", shape)
+    blocks, off = [], 0
+    for m, n, K in layout:
+        ln = m * n - 36                        # a short last row (block offsets stay 16-byte aligned)
+        blocks.append(Block(off, ln, m, n, K, 0))
+        off += ln
+    run_parity(orc, off, blocks, N=1, steps=3)
