@@ -221,7 +221,8 @@ typedef enum {
                            ARC_ERR_UNSUPPORTED (with G > 1 each rank holds only its own nodes')  */
     ARC_Q_CANDIDATES = 4, /* uint32 [num_blocks] rows sharing the boundary bin of the last selection
                             ([nodes_local][num_blocks] for ARC_METHOD_TOPK_ALLGATHER, whose
-                            nodes select separately); synchronises the step's stream first    */
+                            nodes select separately); synchronises the step's stream first;
+                            not maintained by the fused tail (ARC_Q_PLAN[0] == 2)             */
     ARC_Q_PLAN = 6      /* int32 [4] how the context runs a step (fixed at create): [0] selection
                            form: 0 cooperative grid, 1 one thread-block cluster, 2 the fused tail
                            (S3 in the streaming launch's last CTA + a small update kernel: one node
