@@ -45,7 +45,7 @@ LAYOUTS = {
     # blocks streamed by the other launches -- the TMA-fed launch (unaligned rows, n >= 256),
     # the ranged launch (V_b^T wider than the stage; n <= 4) -- take the selection kernel
     # (a tail behind those launches measured no faster on C4's DDP buckets: profiles/r02_tail.txt)
-    "with_tma": [(300, 64, 9, 0), (200, 300, 5, 0)],
+    "with_tma": [(300, 64, 9, 0), (200, 301, 5, 0)],               # n = 301: rows not 16-byte aligned
     "with_wide": [(300, 64, 9, 0), (40, 4100, 3, 0)],
     "with_n1": [(300, 64, 9, 0), (5000, 1, 50, 0)],
     "llama_bucket": [(5461, 2048, 6, 0), (2048, 5461, 3, 0), (2048, 2048, 3, 0)],   # a C4 DDP bucket
