@@ -1006,7 +1006,7 @@ static arc_status run_step(arc_topk_ctx* c, int64_t t, const float* const* grad,
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return ARC_ERR_CUDA;
     if (pl.M > 0 && !pl.topk && !pl.randk && (dev_t || c->v_ready != t || cap != cudaStreamCaptureStatusNone)) {
-        launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V_t, s, t_dev);
+        launch_vgen(blocks, c->p.num_blocks, pl.max_nR4, c->p.r, c->p.seed, t, V_t, s, t_dev, c->pdl && !c->timing ? 1 : 0);
         ARC_LAUNCHED();
     }
     c->last_t = t;

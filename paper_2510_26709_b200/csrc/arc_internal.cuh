@@ -124,7 +124,7 @@ struct NodePtrs {
 
 // ---- launchers (arc_kernels.cu) ---------------------------------------------
 void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r, uint64_t seed,
-                 int64_t t, float* V, cudaStream_t s, const unsigned long long* t_dev = nullptr);
+                 int64_t t, float* V, cudaStream_t s, const unsigned long long* t_dev = nullptr, int pdl = 0);
 void launch_advance_t(unsigned long long* t_dev, cudaStream_t s);   // t_dev += 1 (one thread)
 void launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);   // *p = v (one thread)
 

@@ -37,6 +37,10 @@ __global__ void __launch_bounds__(256) k_vgen(const BlockDev* __restrict__ block
                                               unsigned t_lo, unsigned t_hi, float* __restrict__ V,
                                               const unsigned long long* __restrict__ t_dev) {
     const int b = blockIdx.y;
+    // (programmatic dependent launch: the streaming pass behind may become resident now;
+    // this kernel waits for the previous step's kernels -- they read V, advanced t_dev)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    grid_dependency_wait();
     if (t_dev != nullptr) {   // ARC_FLAG_DEVICE_T: this step's t from the device counter
         const unsigned long long t = __ldcg(t_dev);
         t_lo = static_cast<unsigned>(t);
@@ -435,15 +439,23 @@ __global__ void __launch_bounds__(256) k_exact_sigma(const ExactSigmaLaunch a) {
 // ---- launchers ---------------------------------------------------------------
 
 void launch_vgen(const BlockDev* blocks_dev, int num_blocks, int max_nR4, int r, uint64_t seed, int64_t t,
-                 float* V, cudaStream_t s, const unsigned long long* t_dev) {
+                 float* V, cudaStream_t s, const unsigned long long* t_dev, int pdl) {
     const int threads = 256;
     int gx = (max_nR4 + threads - 1) / threads;
     if (gx < 1) gx = 1;
     if (gx > 64) gx = 64;
-    dim3 grid(gx, num_blocks);
     const uint2 key = make_uint2(static_cast<unsigned>(seed), static_cast<unsigned>(seed >> 32));
-    k_vgen<<<grid, threads, 0, s>>>(blocks_dev, r, key, static_cast<unsigned>(static_cast<uint64_t>(t)),
-                                    static_cast<unsigned>(static_cast<uint64_t>(t) >> 32), V, t_dev);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(gx, num_blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k_vgen, blocks_dev, r, key, static_cast<unsigned>(static_cast<uint64_t>(t)),
+                       static_cast<unsigned>(static_cast<uint64_t>(t) >> 32), V, t_dev);
 }
 
 __global__ void k_advance_t(unsigned long long* t_dev) { *t_dev += 1ull; }
