@@ -125,8 +125,9 @@ def test_tail_sketch_widths(orc, monkeypatch, r):
 
 
 def test_tail_graph_replays(orc, monkeypatch):
-    """A captured step (device iteration counter) replayed 4 times equals 4 oracle steps: the
-    done counter returns to zero and t advances inside the tail."""
+    """A captured step (device iteration counter) replayed at t = 0, 1, 2, 7, 8, 3, 4 equals
+    the oracle's steps: the done counter returns to zero, t advances inside the tail, and
+    the V drawn ahead by k_tail_update for the next t is used only when the counter matches."""
     from paper_2510_26709_b200 import ArcTopK
     from synth import GradientSource
     monkeypatch.setenv("ARC_TAIL", "1")
@@ -138,9 +139,10 @@ def test_tail_graph_replays(orc, monkeypatch):
     grad = torch.zeros(d, device=DEV)
     sel = torch.empty(ctx.sum_K, dtype=torch.int32, device=DEV)
     graph = ctx.capture([grad], [h], [g], gbar, sel, None)
-    ctx.set_iteration(0)
-    torch.cuda.synchronize()
-    for t in range(4):
+    ts = [0, 1, 2, 7, 8, 3, 4]   # jumps: the V drawn for the counter's next t is reused only when it matches
+    for k, t in enumerate(ts):
+        if k == 0 or t != ts[k - 1] + 1:
+            ctx.set_iteration(t)
         gr = src.grads(t)[0]
         grad.copy_(gr.to(DEV))
         graph.replay()
